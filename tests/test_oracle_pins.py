@@ -1,0 +1,440 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix (-m "not gpu").
+
+Each test names the pin and the passage it follows. None of
+these re-types an oracle formula: they compare against closed forms, printed values
+(tests/golden/), published known-answer vectors, special cases and brute force.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy.linalg import expm
+
+import oracle
+import synth
+from tests.analytic import exact_covariances, shear_frame_10dof
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _rows(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return [ln.split() for ln in f if ln.strip() and not ln.startswith("#")]
+
+
+# ---------------------------------------------------------------- P1 Toeplitz (Eq. 6)
+def test_p1_toeplitz_l1_example():
+    """l=1, j_b=2, R=(r1,r2,r3) → [[r2, r1],[r3, r2]] (structure of Eq. 6)."""
+    R = np.array([[[1.5]], [[-2.25]], [[3.125]]])
+    T = oracle.toeplitz(R, 2)
+    assert np.array_equal(T, np.array([[-2.25, 1.5], [3.125, -2.25]]))
+
+
+def test_p1_toeplitz_block_rule_and_corners():
+    """top-left R_i, top-right R_1, bottom-left R_{2i-1}; block (r,c) =
+    R_{i+r-c}, bit-exact copies."""
+    rng = np.random.default_rng(0)
+    l, i = 3, 5
+    R = rng.standard_normal((2 * i - 1, l, l))
+    T = oracle.toeplitz(R, i)
+    blk = lambda r, c: T[r * l:(r + 1) * l, c * l:(c + 1) * l]
+    assert np.array_equal(blk(0, 0), R[i - 1])
+    assert np.array_equal(blk(0, i - 1), R[0])
+    assert np.array_equal(blk(i - 1, 0), R[2 * i - 2])
+    for r in range(i):
+        for c in range(i):
+            assert np.array_equal(blk(r, c), R[i + r - c - 1])
+
+
+# ---------------------------------------------------------------- P2 covariance orientation
+def test_p2_covariance_brute_force_and_transpose():
+    """PAPER.md:126 with 1/(N−k): direct double-loop sum on a tiny record; R_{−k}
+    computed by brute force over the negative lag equals R_kᵀ."""
+    rng = np.random.default_rng(1)
+    N, l, L = 37, 3, 5
+    Y = rng.standard_normal((N, l))
+    R = oracle.covariances(Y, L)
+    for k in range(1, L + 1):
+        bf = np.zeros((l, l))
+        neg = np.zeros((l, l))
+        for t in range(N - k):
+            for a in range(l):
+                for b in range(l):
+                    bf[a, b] += Y[t + k, a] * Y[t, b]
+        for t in range(k, N):                    # R_{−k} = Σ_t y_{t−k} y_tᵀ / (N−k)
+            neg += np.outer(Y[t - k], Y[t])
+        np.testing.assert_allclose(R[k - 1], bf / (N - k), rtol=1e-13, atol=1e-15)
+        np.testing.assert_allclose(neg / (N - k), R[k - 1].T, rtol=1e-13, atol=1e-15)
+
+
+def test_p2_delayed_channel_orientation():
+    """Channel 1 is channel 0 delayed by one sample (white noise): R_1[a=1][b=0] =
+    E[y_{t+1}[1] y_t[0]] = E[y_t[0]^2] ≈ 1 while R_1[0][1] ≈ 0 (R_k[a][b] = Σ Y[t+k][a] Y[t][b])."""
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal(200001)
+    Y = np.stack([x[1:], x[:-1]], axis=1)        # Y[t][1] = x[t] = Y[t-1][0]
+    R = oracle.covariances(Y, 1)
+    assert abs(R[0, 1, 0] - 1.0) < 0.02
+    assert abs(R[0, 0, 1]) < 0.02
+
+
+def test_p2_channel_permutation_commutes():
+    """R(P y) = P R(y) Pᵀ (to rounding: BLAS may reorder the sum)."""
+    rng = np.random.default_rng(3)
+    Y = rng.standard_normal((500, 6))
+    perm = rng.permutation(6)
+    R = oracle.covariances(Y, 4)
+    Rp = oracle.covariances(Y[:, perm], 4)
+    np.testing.assert_allclose(Rp, R[:, perm][:, :, perm], rtol=1e-13, atol=1e-16)
+
+
+def test_partial_sums_shards_add_up():
+    """Time shards of the sum in PAPER.md:126 add up to the full sum (multi-GPU split)."""
+    rng = np.random.default_rng(4)
+    Y = rng.standard_normal((1000, 4))
+    full = oracle.covariance_partial_sums(Y, 1, 9)
+    parts = sum(oracle.covariance_partial_sums(Y, 1, 9, a, b)
+                for a, b in ((0, 333), (333, 700), (700, 1000)))
+    np.testing.assert_allclose(parts, full, rtol=1e-13, atol=1e-12)
+
+
+# ---------------------------------------------------------------- P3 analytic rank / convergence
+def test_p3_analytic_toeplitz_rank_2M():
+    """North star: "in the noise-free limit T has rank 2·(number of modes)"."""
+    cfg = synth.config("c1")
+    modes = synth.make_modes(cfg)
+    T = oracle.toeplitz(exact_covariances(modes, 2 * cfg.i - 1), cfg.i)
+    _, S = oracle.full_svd(T)
+    M = len(modes.f)
+    assert S[2 * M - 1] / S[0] > 1e-3
+    assert S[2 * M] / S[0] < 1e-13
+
+
+def test_p3_sampled_covariances_converge_to_analytic():
+    """Sample covariances of the generator approach the closed form as 1/sqrt(N)
+    (mean over seeds: single realizations of narrow-band modes are too noisy)."""
+    mean_err = []
+    for N in (12000, 192000):
+        errs = []
+        for seed in (11, 12, 13, 14):
+            cfg = synth.config("c1", seed=seed)
+            Y, modes = synth.make_record(cfg, N=N)
+            R = oracle.covariances(Y, 2 * cfg.i - 1)
+            Re = exact_covariances(modes, 2 * cfg.i - 1)
+            errs.append(np.linalg.norm(R - Re) / np.linalg.norm(Re))
+        mean_err.append(np.mean(errs))
+    assert mean_err[1] < 0.1
+    assert mean_err[1] < mean_err[0] / 2.5      # 1/4 expected for 16x more samples
+
+
+# ---------------------------------------------------------------- P4 exact identification
+@pytest.mark.parametrize("use_rsvd", [False, True])
+def test_p4_analytic_identification_exact(use_rsvd):
+    """Eqs. (9)-(12) on the exact T at n = 2M return the generating poles."""
+    cfg = synth.config("c1")
+    modes = synth.make_modes(cfg)
+    T = oracle.toeplitz(exact_covariances(modes, 2 * cfg.i - 1), cfg.i)
+    if use_rsvd:
+        U, S, _ = oracle.rsvd(T, cfg.k, 2, 7, 1, n_keep=cfg.n_max)
+    else:
+        U, S = oracle.full_svd(T)
+    M = len(modes.f)
+    cell = oracle.modal_sweep(U, S, cfg.l, cfg.i, [2 * M], cfg.dt)[0]
+    assert cell.count == M
+    f, xi = synth.exact_poles(modes)
+    for j, p in enumerate(cell.poles):
+        assert abs(p.f - f[j]) / f[j] < 1e-11
+        assert abs(p.xi - xi[j]) < 1e-11
+        assert oracle.mac(p.shape, modes.phi[np.argsort(modes.f)[j]]) > 1 - 1e-12
+
+
+# ---------------------------------------------------------------- P5-P7 RSVD
+def test_p5_rsvd_exact_range_capture_and_negative_control():
+    cfg = synth.config("c1")
+    modes = synth.make_modes(cfg)
+    T = oracle.toeplitz(exact_covariances(modes, 2 * cfg.i - 1), cfg.i)
+    _, Sf = oracle.full_svd(T)
+    r = 2 * len(modes.f)
+    for q in (0, 2):
+        _, S, _ = oracle.rsvd(T, r, q, 11, 3)
+        np.testing.assert_allclose(S[:r], Sf[:r], rtol=1e-13)
+    _, S, _ = oracle.rsvd(T, 4, 0, 11, 3)        # k < rank: must miss
+    assert np.max(np.abs(S - Sf[:4]) / Sf[:4]) > 1e-3
+
+
+def test_p6_rsvd_sampled_leading_sigmas():
+    """North star: RSVD σ converge to full-SVD ones for the signal subspace (q = 2)."""
+    cfg = synth.config("c1")
+    Y, modes = synth.make_record(cfg)
+    T = oracle.toeplitz(oracle.covariances(Y, 2 * cfg.i - 1), cfg.i)
+    _, Sf = oracle.full_svd(T)
+    _, S, _ = oracle.rsvd(T, cfg.k, cfg.q, cfg.philox_key, cfg.i)
+    r = 2 * len(modes.f)
+    np.testing.assert_allclose(S[:r], Sf[:r], rtol=1e-12)
+    assert np.all(S <= Sf[:cfg.k] * (1 + 1e-12))   # projected σ never exceed the true ones
+
+
+def test_p7_algorithm1_special_cases():
+    """SPEC.md:165-166 examples of Algorithm 1 (q = p = 0): diag(3,2,1) in 5×5 → S=(3,2,1);
+    rank one u vᵀ → S1 = ‖u‖‖v‖; U orthonormal."""
+    A = np.zeros((5, 5))
+    A[:3, :3] = np.diag([3.0, 2.0, 1.0])
+    U, S, _ = oracle.rsvd(A, 3, 0, 5, 0)
+    np.testing.assert_allclose(S, [3, 2, 1], rtol=1e-12)
+    np.testing.assert_allclose(U.T @ U, np.eye(3), atol=1e-12)
+    rng = np.random.default_rng(5)
+    u, v = rng.standard_normal(20), rng.standard_normal(20)
+    U, S, _ = oracle.rsvd(np.outer(u, v), 1, 0, 5, 0)
+    assert abs(S[0] - np.linalg.norm(u) * np.linalg.norm(v)) < 1e-10 * S[0]
+    rec = U[:, :1] * S[0] @ (U[:, :1].T @ np.outer(u, v)) / S[0]
+    assert np.linalg.norm(rec - np.outer(u, v)) < 1e-10 * np.linalg.norm(np.outer(u, v))
+
+
+def test_householder_qr_sign_and_orthonormal():
+    rng = np.random.default_rng(6)
+    Y = rng.standard_normal((50, 7))
+    Q, R = oracle.householder_qr(Y)
+    assert np.all(np.diag(R) > 0)
+    np.testing.assert_allclose(Q @ R, Y, atol=1e-13)
+    np.testing.assert_allclose(Q.T @ Q, np.eye(7), atol=1e-14)
+    np.testing.assert_allclose(np.tril(R, -1), 0, atol=0)
+
+
+# ---------------------------------------------------------------- P8-P9 conversions (Table 1)
+def test_p8_table1_10dof_through_discrete_conversion():
+    """PAPER.md:329-334 Table 1, through A_d = expm(A_c Δt) → eig → Eq. (12) conversion
+    in oracle.poles_from_eigs (reading A-1: f = |λ|/2π, ξ = −Re λ/|λ|)."""
+    M, K, C, w, (a, b) = shear_frame_10dof()
+    assert abs(a - 0.58150) < 5e-5 and abs(b - 7.7813e-5) < 5e-9     # SURVEY.md P8 anchors
+    n = 10
+    Ac = np.block([[np.zeros((n, n)), np.eye(n)],
+                   [-np.linalg.solve(M, K), -np.linalg.solve(M, C)]])
+    dt = 1 / 200.0
+    mu, Psi = np.linalg.eig(expm(Ac * dt))
+    poles = oracle.poles_from_eigs(mu, Psi[:n], dt)
+    gold = np.array([[float(x) for x in r[1:]] for r in _rows("table1_10dof.txt")])
+    assert len(poles) == 10
+    got = np.array([[p.f, 100 * p.xi] for p in poles])
+    np.testing.assert_allclose(got, gold, atol=5.01e-4)     # printed to 3 decimals
+
+
+def test_p9_conversion_round_trip():
+    """μ = exp(λΔt) → (f, ξ) recovers the inputs to 1e-12."""
+    rng = np.random.default_rng(7)
+    f = rng.uniform(0.3, 20, 50)
+    xi = rng.uniform(0.001, 0.5, 50)
+    w = 2 * np.pi * f
+    lam = -xi * w + 1j * w * np.sqrt(1 - xi ** 2)
+    dt = 0.01
+    poles = oracle.poles_from_eigs(np.exp(lam * dt), np.ones((3, 50), complex), dt)
+    o = np.argsort(f)
+    np.testing.assert_allclose([p.f for p in poles], f[o], rtol=1e-12)
+    np.testing.assert_allclose([p.xi for p in poles], xi[o], rtol=1e-10, atol=1e-13)
+
+
+def test_pole_selection_rules():
+    """Reading A-14: only Im μ > 0 kept; |μ| ≥ 1 (ξ ≤ 0) and real μ dropped."""
+    mu = np.array([0.9 + 0.1j, 0.9 - 0.1j, 0.5 + 0j, 1.01 + 0.2j, -0.7 + 1e-3j])
+    poles = oracle.poles_from_eigs(mu, np.ones((2, 5), complex), 0.01)
+    assert [round(p.mu.real, 3) for p in poles] == [0.9, -0.7]
+
+
+# ---------------------------------------------------------------- P10-P11
+def test_p10_nested_form_equals_literal_pinv():
+    """The S-free nested form (QR of U↑, W = Q↑ᵀU↓, eig(R↑⁻¹W), Φ = U[:l]ψ) equals
+    the literal pinv(O↑)O↓ of Eq. (10) — the algebra the GPU path relies on."""
+    cfg = synth.config("c1")
+    Y, _ = synth.make_record(cfg)
+    T = oracle.toeplitz(oracle.covariances(Y, 2 * cfg.i - 1), cfg.i)
+    U, S, _ = oracle.rsvd(T, cfg.k, cfg.q, cfg.philox_key, cfg.i, cfg.n_max)
+    l, i = cfg.l, cfg.i
+    lit = oracle.modal_sweep(U, S, l, i, cfg.orders, cfg.dt)
+    Qu, Ru = np.linalg.qr(U[: l * (i - 1)])
+    W = Qu.T @ U[l:]
+    for cell in lit:
+        n = cell.n
+        Mn = np.linalg.solve(Ru[:n, :n], W[:n, :n])
+        mu, psi = np.linalg.eig(Mn)
+        nested = oracle.poles_from_eigs(mu, U[:l, :n] @ psi, cfg.dt)
+        assert len(nested) == cell.count
+        for p, q in zip(cell.poles, nested):
+            assert abs(p.f - q.f) / p.f < 1e-9 and abs(p.xi - q.xi) < 1e-9
+            assert oracle.mac(p.shape, q.shape) > 1 - 1e-9
+
+
+def test_p11_scale_invariance():
+    """scaling T by c > 0 leaves the poles unchanged."""
+    cfg = synth.config("c1")
+    Y, _ = synth.make_record(cfg)
+    T = oracle.toeplitz(oracle.covariances(Y, 2 * cfg.i - 1), cfg.i)
+    cells = []
+    for c in (1.0, 37.5):
+        U, S, _ = oracle.rsvd(c * T, cfg.k, cfg.q, cfg.philox_key, cfg.i, cfg.n_max)
+        cells.append(oracle.modal_sweep(U, S, cfg.l, cfg.i, [6, 10], cfg.dt))
+    for a, b in zip(*cells):
+        assert a.count == b.count
+        for p, q in zip(a.poles, b.poles):
+            assert abs(p.f - q.f) / p.f < 1e-9 and abs(p.xi - q.xi) < 1e-9
+
+
+# ---------------------------------------------------------------- P12 parameter anchors
+def test_p12_parameter_anchors():
+    for kind, args, val, *_ in _rows("param_anchors.txt"):
+        kw = dict(a.split("=") for a in args.split(","))
+        kw = {k: float(v) for k, v in kw.items()}
+        val = float(val)
+        if kind == "time_lag_step":
+            assert oracle.time_lag_step(kw["fs"], kw["f0"]) == val
+        elif kind == "lag_of_step":
+            assert abs(oracle.lag_of_step(int(kw["jb"]), kw["fs"]) - val) < 1e-12
+        elif kind.startswith("lag_grid"):
+            grid, jmin, jmax = oracle.lag_grid(kw["fs"], kw["f0"], kw["beta"], int(kw.get("G", 8)))
+            got = {"lag_grid_min": jmin, "lag_grid_max": jmax, "lag_grid_last": grid[-1]}[kind]
+            assert got == val, (kind, got, val)
+        elif kind == "min_rank_percent":
+            assert abs(oracle.min_rank_percent(kw["T"]) - val) < 1e-4
+        elif kind == "sample_count":
+            assert oracle.sample_count(oracle.min_rank_percent(kw["T"]), int(kw["T"])) == val
+
+
+# ---------------------------------------------------------------- P13 Philox
+def test_p13_philox_known_answers():
+    for r in _rows("philox_kat.txt"):
+        v = [int(x, 16) for x in r]
+        out = oracle.philox4x32_10(np.array(v[:4], np.uint32), np.array(v[4:6], np.uint32))
+        assert [int(x) for x in out] == v[6:]
+
+
+def test_p13_sketch_layout_and_moments():
+    m, k, seed, sid = 101, 13, 0x1234_5678_9ABC, 77
+    Om = oracle.gaussian_sketch(m, k, seed, sid)
+    # element e = col·m + row uses pair e//2, even e → cos branch, odd e → sin branch
+    for (row, col) in ((0, 0), (1, 0), (100, 0), (0, 1), (57, 9), (100, 12)):
+        e = col * m + row
+        w = oracle.philox_words(np.array([e // 2]), seed, sid)
+        u1, u2 = oracle.uniforms_from_words(w)
+        r = math.sqrt(-2 * math.log(u1[0]))
+        ref = r * (math.cos(2 * math.pi * u2[0]) if e % 2 == 0 else math.sin(2 * math.pi * u2[0]))
+        assert abs(Om[row, col] - ref) <= 4 * np.spacing(abs(ref)) + 1e-300
+    big = oracle.gaussian_sketch(4000, 50, 3, 4)
+    assert abs(big.mean()) < 0.01 and abs(big.var() - 1) < 0.01
+    w = oracle.philox_words(np.arange(100000), 9, 9)
+    u1, u2 = oracle.uniforms_from_words(w)
+    assert u1.min() > 0 and u1.max() < 1 and abs(u2.mean() - 0.5) < 0.005
+
+
+# ---------------------------------------------------------------- P14 indicators
+def test_p14_mac_mpc_mpd_special_cases():
+    rng = np.random.default_rng(8)
+    phi = rng.standard_normal(12) + 1j * rng.standard_normal(12)
+    assert abs(oracle.mac(phi, (2 - 3j) * phi) - 1) < 1e-14
+    assert oracle.mac([1, 0], [0, 1]) == 0
+    real = rng.standard_normal(12)
+    assert abs(oracle.mpc(real) - 1) < 1e-14 and oracle.mpd(real) < 1e-12
+    assert oracle.mpc([1, 1j, -1, -1j]) < 1e-14
+    assert oracle.mpc([1, 1j]) < 1e-14                    # uncentered reading A-16
+    assert abs(oracle.mpd([1, 1j]) - 1) < 1e-12            # π/4 normalization, A-16
+    pert = real + 0.01j * rng.standard_normal(12)
+    assert oracle.mpd(pert) < 0.05
+    for th in (0.3, 2.0, -1.1):
+        rot = np.exp(1j * th) * pert * 2.5
+        assert abs(oracle.mpc(rot) - oracle.mpc(pert)) < 1e-10
+        assert abs(oracle.mpd(rot) - oracle.mpd(pert)) < 1e-10
+    assert abs(oracle.mac(phi, real) - oracle.mac(real, phi)) < 1e-14
+    n = oracle.normalize_shape(phi)
+    j = np.argmax(np.abs(n))
+    assert abs(np.linalg.norm(n) - 1) < 1e-14 and abs(n[j].imag) < 1e-15 and n[j].real > 0
+
+
+# ---------------------------------------------------------------- P15-P16 covariance statistics
+def test_p15_cosine_autocorrelation():
+    """y_h = cos(ω h Δt) → R_j ≈ 0.5 cos(ω j Δt) within O(1/N)."""
+    N, dt, w = 20000, 0.01, 2 * np.pi * 1.7
+    Y = np.cos(w * np.arange(N) * dt)[:, None]
+    R = oracle.covariances(Y, 30)[:, 0, 0]
+    j = np.arange(1, 31)
+    assert np.max(np.abs(R - 0.5 * np.cos(w * j * dt))) < 10.0 / N
+
+
+def test_p16_white_noise_decay():
+    """off-lag covariances of white noise are O(1/sqrt(N−j))."""
+    rng = np.random.default_rng(9)
+    N = 40000
+    R = oracle.covariances(rng.standard_normal((N, 4)), 10)
+    assert np.max(np.abs(R)) < 4.5 / math.sqrt(N - 10)
+
+
+# ---------------------------------------------------------------- P17 end-to-end statistical
+def test_p17_c1_identifies_generator_poles():
+    cfg = synth.config("c1")
+    Y, modes = synth.make_record(cfg)
+    T = oracle.toeplitz(oracle.covariances(Y, 2 * cfg.i - 1), cfg.i)
+    U, S, _ = oracle.rsvd(T, cfg.k, cfg.q, cfg.philox_key, cfg.i, cfg.n_max)
+    cell = oracle.modal_sweep(U, S, cfg.l, cfg.i, [6], cfg.dt)[0]
+    f, xi = synth.exact_poles(modes)
+    assert cell.count == 3
+    for p, ft, xt in zip(cell.poles, f, xi):
+        assert abs(p.f - ft) / ft < 0.02 and abs(p.xi - xt) < 0.01
+
+
+# ---------------------------------------------------------------- P18 + stab3d semantics
+def _flags_2d_bruteforce(cells, crit):
+    """Order-axis-only soft criteria written from PAPER.md:208 (consecutive orders)."""
+    out = []
+    for o, cell in enumerate(cells):
+        row = []
+        for p in cell.poles:
+            ok = p.xi <= crit.xi_max and p.mpc > crit.mpc_min and p.mpd < crit.mpd_max
+            if not ok:
+                row.append(0)
+                continue
+            st = False
+            if o > 0:
+                for qq in cells[o - 1].poles:
+                    okq = qq.xi <= crit.xi_max and qq.mpc > crit.mpc_min and qq.mpd < crit.mpd_max
+                    if not okq:
+                        continue
+                    df = abs(p.f - qq.f) / max(p.f, qq.f)
+                    dx = abs(p.xi - qq.xi) / max(p.xi, qq.xi)
+                    m = abs(np.vdot(p.shape, qq.shape)) ** 2 / (np.vdot(p.shape, p.shape).real * np.vdot(qq.shape, qq.shape).real)
+                    if df <= crit.alpha_f and dx <= crit.alpha_xi and 1 - m <= crit.alpha_mac:
+                        st = True
+            row.append(2 if st else 1)
+        out.append(row)
+    return out
+
+
+def test_p18_one_lag_stab3d_equals_2d():
+    cfg = synth.config("c1")
+    Y, _ = synth.make_record(cfg)
+    T = oracle.toeplitz(oracle.covariances(Y, 2 * cfg.i - 1), cfg.i)
+    U, S, _ = oracle.rsvd(T, cfg.k, cfg.q, cfg.philox_key, cfg.i, cfg.n_max)
+    cells = oracle.modal_sweep(U, S, cfg.l, cfg.i, cfg.orders, cfg.dt)
+    flags, counts = oracle.stab3d([cells], oracle.SC_10DOF_3D, cfg.n_max // 2)
+    ref = _flags_2d_bruteforce(cells, oracle.SC_10DOF_3D)
+    for o, row in enumerate(ref):
+        assert list(flags[0, o, :len(row)]) == row
+        assert counts[0, o] == row.count(2)
+    assert counts.sum() > 0
+
+
+def _pole(f, xi, shape, mpc=0.99, mpd=0.01):
+    return oracle.Pole(f, xi, complex(0.9, 0.1), oracle.normalize_shape(np.asarray(shape, complex)), mpc, mpd)
+
+
+def test_stab3d_axis_disjunction_and_hard_criteria():
+    """matched along order only → stable; along lag only → stable;
+    SPEC.md:381-383 hard criteria boundaries (MPC = 0.60 exactly rejected)."""
+    C = oracle.SC_10DOF_3D
+    s = [1.0, 0.5, 0.2]
+    cell = lambda n, ps: oracle.OrderCell(n, len(ps), ps)
+    g0 = [cell(2, [_pole(2.00, 0.020, s)]), cell(4, [_pole(5.0, 0.02, s)])]
+    g1 = [cell(2, [_pole(2.01, 0.0201, s), _pole(3.0, 0.12, s), _pole(4.0, 0.02, s, mpc=0.60)]),
+          cell(4, [_pole(2.0, 0.02, s), _pole(5.01, 0.0205, s)])]
+    flags, counts = oracle.stab3d([g0, g1], C, 3)
+    assert list(flags[0, 0]) == [1, 0, 0]          # lowest order of first lag: never stable
+    assert list(flags[0, 1]) == [1, 0, 0]          # 5 Hz vs 2 Hz at order 2: no match
+    assert list(flags[1, 0]) == [2, 0, 0]          # lag axis match; ξ>10% and MPC=0.6 rejected
+    assert list(flags[1, 1]) == [2, 2, 0]          # order axis (2.0 ↔ 2.01) and lag axis (5.01 ↔ 5.0)
+    assert counts.tolist() == [[0, 0], [1, 2]]
