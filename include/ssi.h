@@ -1,0 +1,206 @@
+/*
+ * ssi.h — C ABI of libssi.so, the B200 (sm_100a) hot path of covariance-driven
+ * Stochastic Subspace Identification with Randomized SVD (arXiv 2411.05510,
+ * Tomassini, García-Macías, Ubertini). Citations are /root/reference/PAPER.md line
+ * numbers followed by the paper section / equation.
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ *  - Every array pointer is DEVICE memory owned by the caller (in Python: torch CUDA
+ *    tensors). The library never allocates or frees caller memory and keeps no
+ *    pointer past the completion of the enqueued work. Scratch comes from the caller's
+ *    workspace `ws` of `ws_bytes` bytes, sized by the matching *_ws() query.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream). All
+ *    work is enqueued on it; a call returns once enqueued. Outputs are valid after the
+ *    stream orders past them. The caller selects the device (cudaSetDevice).
+ *  - No global mutable state: calls are reentrant across host threads and devices.
+ *  - Matrices are FP64. "col-major" means element (r, c) at ptr[r + c*ld];
+ *    "row-major" means ptr[r*ld + c].
+ *  - Synchronous argument checks run before any launch and leave outputs untouched:
+ *    NULL pointers / bad sizes -> SSI_ERR_INVALID_ARG, leading dimension too small ->
+ *    SSI_ERR_SHAPE, unsupported dtype / mode -> SSI_ERR_DTYPE, workspace too small ->
+ *    SSI_ERR_WORKSPACE, a failed launch -> SSI_ERR_CUDA (detail in ssi_last_error()).
+ *  - Asynchronous numeric failures (Cholesky breakdown in CholeskyQR2 after its
+ *    shifted retry, Jacobi or Francis-QR non-convergence, non-finite input) are
+ *    recorded in a device status word at the start of `ws`; read it with
+ *    ssi_fetch_device_status() after synchronizing the stream.
+ *  - Determinism: fixed inputs, seed and launch configuration give bit-identical
+ *    outputs run to run (fixed reduction orders, no floating-point atomics).
+ */
+#ifndef SSI_H_
+#define SSI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SSI_API __attribute__((visibility("default")))
+#else
+#define SSI_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t ssi_status;
+enum {
+  SSI_OK = 0,
+  SSI_ERR_INVALID_ARG = 1,
+  SSI_ERR_SHAPE = 2,
+  SSI_ERR_DTYPE = 3,
+  SSI_ERR_WORKSPACE = 4,
+  SSI_ERR_CUDA = 5,
+  SSI_ERR_NONFINITE = 6,
+  SSI_ERR_NUMERIC = 7
+};
+
+/* Record storage types. */
+enum { SSI_F32 = 0, SSI_F64 = 1 };
+
+/* Covariance arithmetic (ssi_covariances cov_mode).
+ *  SSI_COV_FP64   : FP64 products and sums (DMMA tensor-core path).
+ *  SSI_COV_INT8X3 : each sample is cut into three int8 slices against a per-channel
+ *                   power-of-two scale; the six leading slice products are summed
+ *                   EXACTLY in int32 on the 5th-gen tensor cores (tcgen05 kind::i8)
+ *                   and promoted to FP64. Error is the slicing rounding only
+ *                   (<= 2^-22 of the channel's max |y| per sample); see DESIGN.md. */
+enum { SSI_COV_FP64 = 0, SSI_COV_INT8X3 = 1 };
+
+/* ------------------------------------------------------------------------------
+ * A1. Lagged output covariances (§2.1; normalization 1/(N-k), reading
+ * A-6 of DESIGN.md):
+ *     R_k[a][b] = (1/(N-k)) * sum_{t=0}^{N-k-1} Y[t+k][a] * Y[t][b],  k = lag_lo..lag_hi
+ *  Y       : record, time-major [N][ldY] (channel a of sample t at Y[t*ldY + a]),
+ *            dtype SSI_F32 or SSI_F64, ldY >= l. Must be finite.
+ *  R       : output [(lag_hi-lag_lo+1)][l][l] row-major FP64, R_k at block k-lag_lo.
+ *  t_begin, t_end : time shard of the sum, 0 <= t_begin <= t_end <= N: only terms with
+ *            t in [t_begin, t_end) and t+k < N are summed (the kernel reads the halo
+ *            rows t_end .. t_end+lag_hi-1 itself). Used by time-sharded multi-GPU runs.
+ *  normalize : 1 = divide by (N-k) (requires t_begin = 0, t_end = N);
+ *            0 = raw FP64 sums (to be all-reduced across shards, then divided).
+ *  Errors: lag_lo < 1, lag_hi < lag_lo or lag_hi >= N -> INVALID_ARG ("record too
+ *  short"); bad shard -> INVALID_ARG; dtype/mode pairs not supported ->
+ *  DTYPE. Non-finite samples set SSI_ERR_NONFINITE in the device status word.
+ * ---------------------------------------------------------------------------- */
+SSI_API ssi_status ssi_covariances(const void* Y, int32_t dtype, int64_t N, int32_t l, int64_t ldY,
+                           int32_t lag_lo, int32_t lag_hi, int32_t cov_mode,
+                           int64_t t_begin, int64_t t_end, int32_t normalize,
+                           double* R, void* ws, size_t ws_bytes, void* stream);
+SSI_API ssi_status ssi_covariances_ws(int64_t N, int32_t l, int32_t lag_lo, int32_t lag_hi,
+                              int32_t cov_mode, size_t* bytes);
+
+/* ------------------------------------------------------------------------------
+ * A2. Block-Toeplitz matrix T_{1|i}, Eq. (6) (§2.1):
+ *     T[r*l + a][c*l + b] = R_{i+r-c}[a][b],   r, c in [0, i)
+ *  R : [2i-1][l][l] row-major FP64 holding R_1..R_{2i-1} (R_k at block k-1), e.g. the
+ *      output of ssi_covariances with lag_lo = 1, lag_hi >= 2i-1.
+ *  T : output, row-major, m = l*i rows and columns, ldT >= m. Pure copy (bit-exact).
+ * ---------------------------------------------------------------------------- */
+SSI_API ssi_status ssi_toeplitz(const double* R, int32_t l, int32_t i, double* T, int64_t ldT,
+                        void* stream);
+
+/* ------------------------------------------------------------------------------
+ * A3-A8. Randomized SVD of T (§2.2, Algorithm 1 at PAPER.md:255-268,
+ * Eqs. 13-18) with q power iterations (north star; reading A-12):
+ *   Omega = N(0,1) m x k sketch from Philox4x32-10 (key = seed, counter = (element
+ *           pair index, stream_id); reading A-11), generated on the device;
+ *   Y = T Omega; Q = qr(Y) (CholeskyQR2, diag(R) > 0);
+ *   q times: Z = qr(T^T Q); Q = qr(T Z);
+ *   B = Q^T T; small SVD B = U~ S V^T (CholeskyQR2 of B^T + one-sided Jacobi);
+ *   U = Q U~.
+ *  T : m x m row-major FP64, ldT >= m.   k : sketch width (n_max + p), 1 <= k <= m.
+ *  U : output m x n_keep col-major FP64 (leading left singular vectors), ldU >= m,
+ *      1 <= n_keep <= k. Column signs are arbitrary (reading A-13).
+ *  S : output [k] FP64, descending.
+ *  Errors: k or n_keep out of range -> INVALID_ARG. CholeskyQR2 breakdown or Jacobi
+ *  non-convergence -> SSI_ERR_NUMERIC in the device status word.
+ * ---------------------------------------------------------------------------- */
+SSI_API ssi_status ssi_rsvd(const double* T, int64_t ldT, int32_t m, int32_t k, int32_t q,
+                    uint64_t seed, uint64_t stream_id, int32_t n_keep,
+                    double* U, int64_t ldU, double* S, void* ws, size_t ws_bytes,
+                    void* stream);
+SSI_API ssi_status ssi_rsvd_ws(int32_t m, int32_t k, int32_t n_keep, size_t* bytes);
+
+/* Raw Philox words and the Gaussian sketch, exposed for bit-exact verification
+ * (P13). words: [n_pairs][4] uint32 for pairs 0..n_pairs-1; omega: m x k col-major. */
+SSI_API ssi_status ssi_philox_words(uint64_t seed, uint64_t stream_id, int64_t n_pairs,
+                            uint32_t* words, void* stream);
+SSI_API ssi_status ssi_gaussian_sketch(int32_t m, int32_t k, uint64_t seed, uint64_t stream_id,
+                               double* omega, int64_t ldo, void* stream);
+
+/* ------------------------------------------------------------------------------
+ * A9-A11. Modal sweep over model orders n = n_min, n_min+n_step, ..., <= n_max (even),
+ * PAPER.md:156-206 (§2.1, Eqs. 9-12):
+ *   O_n = U_n S_n^{1/2}; A_n = pinv(O_n^up) O_n^down (first / last l(i-1) rows,
+ *   reading A-2); C_n = first l rows; A_n = Psi M Psi^{-1} (reading A-4);
+ *   lambda = ln(mu)/dt, f = |lambda|/(2 pi), xi = -Re(lambda)/|lambda| (reading A-1);
+ *   Phi = C_n Psi. Computed in the S-free nested form: thin QR U^up = Q R, W = Q^T U^down,
+ *   M_n = R[:n,:n]^{-1} W[:n,:n] has the eigenvalues of A_n and Phi = U[0:l,:n] psi_M.
+ *   Poles: Im(mu) > 0, 0 < xi < 1 (reading A-14), shapes unit-norm with the largest
+ *   component real positive (A-15), MPC / MPD (A-16), sorted by (f, xi).
+ *  U : m x n_max col-major (m = l*i, ldU >= m), S : [>= n_max] descending (ssi_rsvd).
+ *  out : caller-allocated pole table (device arrays) with n_orders = number of orders,
+ *        cap >= n_max/2, l = channels. count[o] = number of poles, or -1 when
+ *        S[n-1] < 1e-12 S[0] (order above the numerical rank) or when the
+ *        order's eigen-solve did not converge.
+ * ---------------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_orders;  /* number of model orders (rows) */
+  int32_t cap;       /* pole slots per order (>= n_max/2) */
+  int32_t l;         /* channels (mode-shape length) */
+  int32_t n_min;     /* first order */
+  int32_t n_step;    /* order step (2) */
+  int32_t* count;    /* [n_orders] */
+  double* f;         /* [n_orders][cap] Hz */
+  double* xi;        /* [n_orders][cap] damping ratio */
+  double* mu_re;     /* [n_orders][cap] discrete pole, real part */
+  double* mu_im;     /* [n_orders][cap] discrete pole, imaginary part */
+  double* mpc;       /* [n_orders][cap] */
+  double* mpd;       /* [n_orders][cap] */
+  double* shape;     /* [n_orders][cap][l][2] (re, im) */
+} ssi_pole_table;
+
+SSI_API ssi_status ssi_modal_sweep(const double* U, int64_t ldU, const double* S, int32_t l,
+                           int32_t i, int32_t n_min, int32_t n_max, int32_t n_step,
+                           double dt, const ssi_pole_table* out, void* ws, size_t ws_bytes,
+                           void* stream);
+SSI_API ssi_status ssi_modal_sweep_ws(int32_t l, int32_t i, int32_t n_min, int32_t n_max,
+                              int32_t n_step, size_t* bytes);
+
+/* ------------------------------------------------------------------------------
+ * A13. Hard + 3D soft stability criteria (§2.1 and Eq.
+ * (stabcriteria3D), §2.3 step ii):
+ *   HC: keep iff xi <= xi_max && mpc > mpc_min && mpd < mpd_max (reading A-17).
+ *   SC: a kept pole at (lag g, order o) is stable iff one kept pole at (g, o-1) OR at
+ *       (g-1, o) has d_f <= alpha_f && d_xi <= alpha_xi && 1-MAC <= alpha_mac
+ *       (readings A-18..A-21).
+ *  tables : host array of n_lags pole tables (device arrays inside), lags in increasing
+ *           i, all with equal n_orders, cap, l, n_min, n_step.
+ *  flags  : output [n_lags][n_orders][cap] uint8: 0 rejected / empty, 1 new, 2 stable.
+ *  stable_count : output [n_lags][n_orders] int32 (number of flag-2 poles).
+ * ---------------------------------------------------------------------------- */
+typedef struct {
+  double xi_max, mpc_min, mpd_max;     /* hard criteria */
+  double alpha_f, alpha_xi, alpha_mac; /* soft criteria */
+} ssi_criteria;
+
+SSI_API ssi_status ssi_stab3d(const ssi_pole_table* tables, int32_t n_lags, const ssi_criteria* crit,
+                      uint8_t* flags, int32_t* stable_count, void* stream);
+
+/* ------------------------------------------------------------------------------
+ * Status helpers.
+ * ---------------------------------------------------------------------------- */
+/* Reads the device status word at the start of ws (synchronous copy; call after the
+ * stream finished the work that used ws). */
+SSI_API ssi_status ssi_fetch_device_status(const void* ws, ssi_status* code);
+SSI_API const char* ssi_status_string(ssi_status s);
+/* Thread-local detail of the last synchronous failure on this host thread. */
+SSI_API const char* ssi_last_error(void);
+/* Library version string and the compiled target ("sm_100a"). */
+SSI_API const char* ssi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSI_H_ */

@@ -1,0 +1,81 @@
+"""ctypes loader for libssi.so (include/ssi.h). Argument marshalling only.
+
+The product path has no CPU fallback: if the shared library is missing or was built for
+another target, every entry point raises.
+"""
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libssi.so")
+
+SSI_OK = 0
+SSI_F32, SSI_F64 = 0, 1
+SSI_COV_FP64, SSI_COV_INT8X3 = 0, 1
+
+
+class PoleTableC(C.Structure):
+    _fields_ = [("n_orders", C.c_int32), ("cap", C.c_int32), ("l", C.c_int32),
+                ("n_min", C.c_int32), ("n_step", C.c_int32),
+                ("count", C.c_void_p), ("f", C.c_void_p), ("xi", C.c_void_p),
+                ("mu_re", C.c_void_p), ("mu_im", C.c_void_p), ("mpc", C.c_void_p),
+                ("mpd", C.c_void_p), ("shape", C.c_void_p)]
+
+
+class CriteriaC(C.Structure):
+    _fields_ = [("xi_max", C.c_double), ("mpc_min", C.c_double), ("mpd_max", C.c_double),
+                ("alpha_f", C.c_double), ("alpha_xi", C.c_double), ("alpha_mac", C.c_double)]
+
+
+# name -> (restype, argtypes)
+P, I32, I64, U64, SZ, D = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t, C.c_double
+SIGNATURES = {
+    "ssi_covariances": (I32, [P, I32, I64, I32, I64, I32, I32, I32, I64, I64, I32, P, P, SZ, P]),
+    "ssi_covariances_ws": (I32, [I64, I32, I32, I32, I32, C.POINTER(SZ)]),
+    "ssi_toeplitz": (I32, [P, I32, I32, P, I64, P]),
+    "ssi_rsvd": (I32, [P, I64, I32, I32, I32, U64, U64, I32, P, I64, P, P, SZ, P]),
+    "ssi_rsvd_ws": (I32, [I32, I32, I32, C.POINTER(SZ)]),
+    "ssi_philox_words": (I32, [U64, U64, I64, P, P]),
+    "ssi_gaussian_sketch": (I32, [I32, I32, U64, U64, P, I64, P]),
+    "ssi_modal_sweep": (I32, [P, I64, P, I32, I32, I32, I32, I32, D, C.POINTER(PoleTableC), P, SZ, P]),
+    "ssi_modal_sweep_ws": (I32, [I32, I32, I32, I32, I32, C.POINTER(SZ)]),
+    "ssi_stab3d": (I32, [C.POINTER(PoleTableC), I32, C.POINTER(CriteriaC), P, P, P]),
+    "ssi_fetch_device_status": (I32, [P, C.POINTER(I32)]),
+    "ssi_status_string": (C.c_char_p, [I32]),
+    "ssi_last_error": (C.c_char_p, []),
+    "ssi_version": (C.c_char_p, []),
+}
+
+_lib = None
+
+
+class SSIError(RuntimeError):
+    def __init__(self, fn, code):
+        lib = get()
+        msg = lib.ssi_status_string(code).decode()
+        detail = lib.ssi_last_error().decode()
+        super().__init__(f"{fn}: status {code} ({msg}) {detail}")
+        self.code = code
+
+
+def get():
+    """Load libssi.so once; raise if it is absent (no fallback by design)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not found: run `python -m paper_2411_05510_b200.build` "
+                              "(nvcc, sm_100a). There is no CPU fallback.")
+        lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def call(name, *args):
+    code = getattr(get(), name)(*args)
+    if code != SSI_OK:
+        raise SSIError(name, code)
+    return code

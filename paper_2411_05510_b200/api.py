@@ -1,0 +1,221 @@
+"""Thin torch-facing binding over the libssi.so C ABI (include/ssi.h).
+
+PyTorch supplies device memory and the current CUDA stream; every step of the method
+runs in the library's sm_100a kernels. Functions mirror the C entry points:
+
+    covariances(Y, lag_hi, ...)      -> R [L][l][l] FP64            (A1)
+    toeplitz(R, i)                   -> T [m][m] FP64 row-major     (A2, Eq. 6)
+    rsvd(T, k, q, seed, stream_id)   -> U [m][n_keep] (col-major), S [k]   (A3-A8, Alg. 1)
+    modal_sweep(U, S, l, i, ...)     -> PoleTable                   (A9-A11, Eqs. 9-12)
+    stab3d(tables, criteria)         -> flags, stable_count         (A13)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import PoleTableC, CriteriaC, call, SSI_F32, SSI_F64, SSI_COV_FP64, SSI_COV_INT8X3
+
+COV_MODES = {"fp64": SSI_COV_FP64, "int8x3": SSI_COV_INT8X3}
+
+
+def _ptr(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if not (isinstance(t, torch.Tensor) and t.is_cuda):
+            raise TypeError("libssi operates on CUDA tensors only (no CPU fallback)")
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def device_status(ws: torch.Tensor) -> int:
+    """Status word of the last call that used `ws` (synchronizes the stream)."""
+    torch.cuda.current_stream().synchronize()
+    v = C.c_int32(0)
+    call("ssi_fetch_device_status", _ptr(ws), C.byref(v))
+    return v.value
+
+
+def _check_device(fn, ws, check):
+    if check:
+        code = device_status(ws)
+        if code != 0:
+            raise _lib.SSIError(fn + " (device status)", code)
+
+
+def covariances_ws_bytes(N, l, lag_hi, lag_lo=1, mode="fp64") -> int:
+    b = C.c_size_t(0)
+    call("ssi_covariances_ws", N, l, lag_lo, lag_hi, COV_MODES[mode], C.byref(b))
+    return b.value
+
+
+def covariances(Y: torch.Tensor, lag_hi: int, lag_lo: int = 1, mode: str = "fp64",
+                t_begin: int = 0, t_end: int | None = None, normalize: bool = True,
+                out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
+                check: bool = False) -> torch.Tensor:
+    _require_cuda(Y)
+    if Y.dim() != 2 or Y.stride(1) != 1:
+        raise ValueError("Y must be [N][l] with unit channel stride")
+    dtype = {torch.float32: SSI_F32, torch.float64: SSI_F64}.get(Y.dtype)
+    if dtype is None:
+        raise TypeError("Y must be float32 or float64")
+    N, l = Y.shape
+    t_end = N if t_end is None else t_end
+    L = lag_hi - lag_lo + 1
+    R = out if out is not None else torch.empty((L, l, l), dtype=torch.float64, device=Y.device)
+    if ws is None:
+        ws = _workspace(covariances_ws_bytes(N, l, lag_hi, lag_lo, mode), Y.device)
+    call("ssi_covariances", _ptr(Y), dtype, N, l, Y.stride(0), lag_lo, lag_hi, COV_MODES[mode],
+         t_begin, t_end, 1 if normalize else 0, _ptr(R), _ptr(ws), ws.numel(), _stream())
+    _check_device("ssi_covariances", ws, check)
+    return R
+
+
+def toeplitz(R: torch.Tensor, i: int, out: torch.Tensor | None = None) -> torch.Tensor:
+    _require_cuda(R)
+    l = R.shape[1]
+    if R.shape[0] < 2 * i - 1 or not R.is_contiguous() or R.dtype != torch.float64:
+        raise ValueError("R must be contiguous FP64 [>= 2i-1][l][l]")
+    m = l * i
+    T = out if out is not None else torch.empty((m, m), dtype=torch.float64, device=R.device)
+    call("ssi_toeplitz", _ptr(R), l, i, _ptr(T), T.stride(0), _stream())
+    return T
+
+
+def rsvd_ws_bytes(m, k, n_keep) -> int:
+    b = C.c_size_t(0)
+    call("ssi_rsvd_ws", m, k, n_keep, C.byref(b))
+    return b.value
+
+
+def rsvd(T: torch.Tensor, k: int, q: int, seed: int, stream_id: int, n_keep: int | None = None,
+         ws: torch.Tensor | None = None, check: bool = False):
+    """Returns (U, S): U is an (m, n_keep) column-major view, S has k entries."""
+    _require_cuda(T)
+    m = T.shape[0]
+    n_keep = k if n_keep is None else n_keep
+    if T.dtype != torch.float64 or T.stride(1) != 1:
+        raise ValueError("T must be FP64 row-major")
+    Ucm = torch.empty((n_keep, m), dtype=torch.float64, device=T.device)   # col-major storage
+    S = torch.empty(k, dtype=torch.float64, device=T.device)
+    if ws is None:
+        ws = _workspace(rsvd_ws_bytes(m, k, n_keep), T.device)
+    call("ssi_rsvd", _ptr(T), T.stride(0), m, k, q, C.c_uint64(seed), C.c_uint64(stream_id),
+         n_keep, _ptr(Ucm), m, _ptr(S), _ptr(ws), ws.numel(), _stream())
+    _check_device("ssi_rsvd", ws, check)
+    return Ucm.t(), S
+
+
+def philox_words(seed: int, stream_id: int, n_pairs: int, device="cuda") -> torch.Tensor:
+    w = torch.empty((n_pairs, 4), dtype=torch.int32, device=device)
+    call("ssi_philox_words", C.c_uint64(seed), C.c_uint64(stream_id), n_pairs, _ptr(w), _stream())
+    return w
+
+
+def gaussian_sketch(m: int, k: int, seed: int, stream_id: int, device="cuda") -> torch.Tensor:
+    om = torch.empty((k, m), dtype=torch.float64, device=device)
+    call("ssi_gaussian_sketch", m, k, C.c_uint64(seed), C.c_uint64(stream_id), _ptr(om), m, _stream())
+    return om.t()
+
+
+@dataclass
+class PoleTable:
+    """Device pole table of one (record, lag): rows = model orders n_min..n_max."""
+    n_min: int
+    n_step: int
+    l: int
+    cap: int
+    count: torch.Tensor      # [O] int32 (-1 = order not solved)
+    f: torch.Tensor          # [O][cap] f64
+    xi: torch.Tensor
+    mu_re: torch.Tensor
+    mu_im: torch.Tensor
+    mpc: torch.Tensor
+    mpd: torch.Tensor
+    shape: torch.Tensor      # [O][cap][l][2] f64
+
+    @classmethod
+    def empty(cls, n_min, n_max, n_step, l, device, cap=None):
+        O = (n_max - n_min) // n_step + 1
+        cap = cap or n_max // 2
+        z = lambda *s, dt=torch.float64: torch.zeros(s, dtype=dt, device=device)
+        return cls(n_min, n_step, l, cap, z(O, dt=torch.int32), z(O, cap), z(O, cap), z(O, cap),
+                   z(O, cap), z(O, cap), z(O, cap), z(O, cap, l, 2))
+
+    @property
+    def n_orders(self):
+        return self.count.shape[0]
+
+    @property
+    def orders(self):
+        return [self.n_min + j * self.n_step for j in range(self.n_orders)]
+
+    def as_c(self) -> PoleTableC:
+        return PoleTableC(self.n_orders, self.cap, self.l, self.n_min, self.n_step,
+                          self.count.data_ptr(), self.f.data_ptr(), self.xi.data_ptr(),
+                          self.mu_re.data_ptr(), self.mu_im.data_ptr(), self.mpc.data_ptr(),
+                          self.mpd.data_ptr(), self.shape.data_ptr())
+
+    def tensors(self):
+        return [self.count, self.f, self.xi, self.mu_re, self.mu_im, self.mpc, self.mpd, self.shape]
+
+    def to(self, device):
+        return PoleTable(self.n_min, self.n_step, self.l, self.cap,
+                         *[t.to(device) for t in self.tensors()])
+
+
+def modal_sweep_ws_bytes(l, i, n_min, n_max, n_step) -> int:
+    b = C.c_size_t(0)
+    call("ssi_modal_sweep_ws", l, i, n_min, n_max, n_step, C.byref(b))
+    return b.value
+
+
+def modal_sweep(U: torch.Tensor, S: torch.Tensor, l: int, i: int, n_min: int, n_max: int,
+                n_step: int, dt: float, out: PoleTable | None = None,
+                ws: torch.Tensor | None = None, check: bool = False) -> PoleTable:
+    _require_cuda(U, S)
+    if U.stride(0) != 1:
+        raise ValueError("U must be column-major (as returned by rsvd)")
+    tab = out if out is not None else PoleTable.empty(n_min, n_max, n_step, l, U.device)
+    if ws is None:
+        ws = _workspace(modal_sweep_ws_bytes(l, i, n_min, n_max, n_step), U.device)
+    ct = tab.as_c()
+    call("ssi_modal_sweep", _ptr(U), U.stride(1), _ptr(S), l, i, n_min, n_max, n_step, float(dt),
+         C.byref(ct), _ptr(ws), ws.numel(), _stream())
+    _check_device("ssi_modal_sweep", ws, check)
+    return tab
+
+
+@dataclass(frozen=True)
+class Criteria:
+    xi_max: float = 0.10
+    mpc_min: float = 0.60
+    mpd_max: float = 0.50
+    alpha_f: float = 0.01
+    alpha_xi: float = 0.03
+    alpha_mac: float = 0.02
+
+
+def stab3d(tables: list, crit: Criteria):
+    """flags [G][O][cap] uint8 (0 rejected, 1 new, 2 stable) and stable_count [G][O]."""
+    G = len(tables)
+    t0 = tables[0]
+    dev = t0.count.device
+    flags = torch.zeros((G, t0.n_orders, t0.cap), dtype=torch.uint8, device=dev)
+    counts = torch.zeros((G, t0.n_orders), dtype=torch.int32, device=dev)
+    arr = (PoleTableC * G)(*[t.as_c() for t in tables])
+    cc = CriteriaC(crit.xi_max, crit.mpc_min, crit.mpd_max, crit.alpha_f, crit.alpha_xi, crit.alpha_mac)
+    call("ssi_stab3d", arr, G, C.byref(cc), _ptr(flags), _ptr(counts), _stream())
+    return flags, counts

@@ -1,0 +1,222 @@
+// libssi.so C ABI (include/ssi.h): synchronous argument checks, workspace carving and
+// stream plumbing around the device kernels. No arithmetic of the method runs here.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+
+#include "covariance.cuh"
+#include "cov_i8.cuh"
+#include "linalg.cuh"
+#include "rsvd.cuh"
+
+namespace ssi {
+
+static thread_local char g_err[512] = "";
+
+void set_last_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+ssi_status launch_check(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_last_error("%s: %s", what, cudaGetErrorString(e));
+    return SSI_ERR_CUDA;
+  }
+  return SSI_OK;
+}
+
+static cudaStream_t S(void* p) { return static_cast<cudaStream_t>(p); }
+
+static ssi_status reset_status(void* ws, cudaStream_t s) {
+  if (cudaMemsetAsync(ws, 0, kWsHeader, s) != cudaSuccess) return launch_check("status reset");
+  return SSI_OK;
+}
+
+static size_t cov_ws(int64_t N, int l, int lag_lo, int lag_hi, int mode, int64_t span) {
+  Carver c(nullptr);
+  const int rows = (lag_hi - lag_lo + 1) * l;
+  if (mode == SSI_COV_FP64) c.take<double>(cov_fp64_partial_elems(span, rows, l));
+  else cov_i8_carve(c, N, l, lag_lo, lag_hi);
+  return c.bytes();
+}
+
+}  // namespace ssi
+
+using namespace ssi;
+
+extern "C" {
+
+const char* ssi_last_error(void) { return g_err; }
+
+const char* ssi_version(void) { return "ssi 0.1 (sm_100a)"; }
+
+const char* ssi_status_string(ssi_status s) {
+  switch (s) {
+    case SSI_OK: return "ok";
+    case SSI_ERR_INVALID_ARG: return "invalid argument";
+    case SSI_ERR_SHAPE: return "leading dimension too small";
+    case SSI_ERR_DTYPE: return "unsupported dtype or mode";
+    case SSI_ERR_WORKSPACE: return "workspace too small";
+    case SSI_ERR_CUDA: return "CUDA error";
+    case SSI_ERR_NONFINITE: return "non-finite input";
+    case SSI_ERR_NUMERIC: return "numerical failure (CholeskyQR2 breakdown or non-convergence)";
+    default: return "unknown status";
+  }
+}
+
+ssi_status ssi_fetch_device_status(const void* ws, ssi_status* code) {
+  SSI_REQUIRE(ws && code, SSI_ERR_INVALID_ARG, "ssi_fetch_device_status: NULL pointer");
+  int32_t v = 0;
+  if (cudaMemcpy(&v, ws, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return launch_check("ssi_fetch_device_status");
+  *code = v;
+  return SSI_OK;
+}
+
+ssi_status ssi_covariances_ws(int64_t N, int32_t l, int32_t lag_lo, int32_t lag_hi,
+                              int32_t cov_mode, size_t* bytes) {
+  SSI_REQUIRE(bytes, SSI_ERR_INVALID_ARG, "ssi_covariances_ws: NULL bytes");
+  SSI_REQUIRE(N > 0 && l > 0 && lag_lo >= 1 && lag_hi >= lag_lo, SSI_ERR_INVALID_ARG,
+              "ssi_covariances_ws: bad sizes");
+  SSI_REQUIRE(cov_mode == SSI_COV_FP64 || cov_mode == SSI_COV_INT8X3, SSI_ERR_DTYPE,
+              "ssi_covariances_ws: unknown cov_mode %d", cov_mode);
+  *bytes = cov_ws(N, l, lag_lo, lag_hi, cov_mode, N);
+  return SSI_OK;
+}
+
+ssi_status ssi_covariances(const void* Y, int32_t dtype, int64_t N, int32_t l, int64_t ldY,
+                           int32_t lag_lo, int32_t lag_hi, int32_t cov_mode, int64_t t_begin,
+                           int64_t t_end, int32_t normalize, double* R, void* ws,
+                           size_t ws_bytes, void* stream) {
+  SSI_REQUIRE(Y && R && ws, SSI_ERR_INVALID_ARG, "ssi_covariances: NULL pointer");
+  SSI_REQUIRE(N > 0 && l > 0, SSI_ERR_INVALID_ARG, "ssi_covariances: N and l must be positive");
+  SSI_REQUIRE(lag_lo >= 1 && lag_hi >= lag_lo, SSI_ERR_INVALID_ARG,
+              "ssi_covariances: need 1 <= lag_lo <= lag_hi");
+  SSI_REQUIRE(lag_hi < N, SSI_ERR_INVALID_ARG, "ssi_covariances: record too short (N=%lld, lag %d)",
+              (long long)N, lag_hi);
+  SSI_REQUIRE(0 <= t_begin && t_begin <= t_end && t_end <= N, SSI_ERR_INVALID_ARG,
+              "ssi_covariances: bad time shard [%lld, %lld)", (long long)t_begin, (long long)t_end);
+  SSI_REQUIRE(!normalize || (t_begin == 0 && t_end == N), SSI_ERR_INVALID_ARG,
+              "ssi_covariances: normalize=1 requires the full record");
+  SSI_REQUIRE(ldY >= l, SSI_ERR_SHAPE, "ssi_covariances: ldY < l");
+  SSI_REQUIRE(dtype == SSI_F32 || dtype == SSI_F64, SSI_ERR_DTYPE, "ssi_covariances: bad dtype");
+  SSI_REQUIRE(cov_mode == SSI_COV_FP64 || cov_mode == SSI_COV_INT8X3, SSI_ERR_DTYPE,
+              "ssi_covariances: unknown cov_mode %d", cov_mode);
+  SSI_REQUIRE(cov_mode != SSI_COV_INT8X3 || cov_i8_supported(l, lag_hi - lag_lo + 1, ldY, dtype),
+              SSI_ERR_DTYPE, "ssi_covariances: SSI_COV_INT8X3 needs l %% 32 == 0 and l <= 256");
+  const size_t need = cov_ws(N, l, lag_lo, lag_hi, cov_mode, t_end - t_begin);
+  SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_covariances: workspace %zu < %zu",
+              ws_bytes, need);
+  cudaStream_t s = S(stream);
+  SSI_TRY(reset_status(ws, s));
+  int32_t* st = static_cast<int32_t*>(ws);
+  if (cov_mode == SSI_COV_FP64) {
+    Carver c(ws);
+    const int rows = (lag_hi - lag_lo + 1) * l;
+    double* part = c.take<double>(cov_fp64_partial_elems(t_end - t_begin, rows, l));
+    return cov_fp64(Y, dtype, N, l, ldY, lag_lo, lag_hi, t_begin, t_end, normalize, R, part, st, s);
+  }
+  return cov_i8(Y, dtype, N, l, ldY, lag_lo, lag_hi, t_begin, t_end, normalize, R, ws, st, s);
+}
+
+ssi_status ssi_toeplitz(const double* R, int32_t l, int32_t i, double* T, int64_t ldT, void* stream) {
+  SSI_REQUIRE(R && T, SSI_ERR_INVALID_ARG, "ssi_toeplitz: NULL pointer");
+  SSI_REQUIRE(l > 0 && i > 0, SSI_ERR_INVALID_ARG, "ssi_toeplitz: l and i must be positive");
+  SSI_REQUIRE(ldT >= int64_t(l) * i, SSI_ERR_SHAPE, "ssi_toeplitz: ldT < l*i");
+  return toeplitz_launch(R, l, i, T, ldT, S(stream));
+}
+
+ssi_status ssi_rsvd_ws(int32_t m, int32_t k, int32_t n_keep, size_t* bytes) {
+  SSI_REQUIRE(bytes, SSI_ERR_INVALID_ARG, "ssi_rsvd_ws: NULL bytes");
+  SSI_REQUIRE(m > 0 && k >= 1 && k <= m && n_keep >= 1 && n_keep <= k, SSI_ERR_INVALID_ARG,
+              "ssi_rsvd_ws: bad sizes");
+  *bytes = rsvd_ws_bytes(m, k);
+  return SSI_OK;
+}
+
+ssi_status ssi_rsvd(const double* T, int64_t ldT, int32_t m, int32_t k, int32_t q, uint64_t seed,
+                    uint64_t stream_id, int32_t n_keep, double* U, int64_t ldU, double* S_,
+                    void* ws, size_t ws_bytes, void* stream) {
+  SSI_REQUIRE(T && U && S_ && ws, SSI_ERR_INVALID_ARG, "ssi_rsvd: NULL pointer");
+  SSI_REQUIRE(m > 0 && k >= 1 && k <= m, SSI_ERR_INVALID_ARG, "ssi_rsvd: need 1 <= k <= m");
+  SSI_REQUIRE(n_keep >= 1 && n_keep <= k, SSI_ERR_INVALID_ARG, "ssi_rsvd: need 1 <= n_keep <= k");
+  SSI_REQUIRE(q >= 0, SSI_ERR_INVALID_ARG, "ssi_rsvd: q < 0");
+  SSI_REQUIRE(ldT >= m && ldU >= m, SSI_ERR_SHAPE, "ssi_rsvd: ldT or ldU < m");
+  const size_t need = rsvd_ws_bytes(m, k);
+  SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_rsvd: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = S(stream);
+  SSI_TRY(reset_status(ws, s));
+  return rsvd_run(T, ldT, m, k, q, seed, stream_id, n_keep, U, ldU, S_, ws,
+                  static_cast<int32_t*>(ws), s);
+}
+
+ssi_status ssi_philox_words(uint64_t seed, uint64_t stream_id, int64_t n_pairs, uint32_t* words,
+                            void* stream) {
+  SSI_REQUIRE(words && n_pairs > 0, SSI_ERR_INVALID_ARG, "ssi_philox_words: bad arguments");
+  return philox_words_launch(seed, stream_id, n_pairs, words, S(stream));
+}
+
+ssi_status ssi_gaussian_sketch(int32_t m, int32_t k, uint64_t seed, uint64_t stream_id,
+                               double* omega, int64_t ldo, void* stream) {
+  SSI_REQUIRE(omega && m > 0 && k > 0, SSI_ERR_INVALID_ARG, "ssi_gaussian_sketch: bad arguments");
+  SSI_REQUIRE(ldo >= m, SSI_ERR_SHAPE, "ssi_gaussian_sketch: ldo < m");
+  return sketch_launch(m, k, seed, stream_id, omega, ldo, S(stream));
+}
+
+static ssi_status check_orders(int32_t n_min, int32_t n_max, int32_t n_step) {
+  SSI_REQUIRE(n_min >= 2 && n_min % 2 == 0 && n_step >= 2 && n_step % 2 == 0 && n_max >= n_min,
+              SSI_ERR_INVALID_ARG,
+              "orders must be even: n_min >= 2, n_step >= 2 even, n_max >= n_min (SPEC.md:312)");
+  return SSI_OK;
+}
+
+ssi_status ssi_modal_sweep_ws(int32_t l, int32_t i, int32_t n_min, int32_t n_max, int32_t n_step,
+                              size_t* bytes) {
+  SSI_REQUIRE(bytes && l > 0 && i >= 2, SSI_ERR_INVALID_ARG, "ssi_modal_sweep_ws: bad sizes");
+  SSI_TRY(check_orders(n_min, n_max, n_step));
+  *bytes = modal_ws_bytes(l, i, n_min, n_max, n_step);
+  return SSI_OK;
+}
+
+ssi_status ssi_modal_sweep(const double* U, int64_t ldU, const double* S_, int32_t l, int32_t i,
+                           int32_t n_min, int32_t n_max, int32_t n_step, double dt,
+                           const ssi_pole_table* out, void* ws, size_t ws_bytes, void* stream) {
+  SSI_REQUIRE(U && S_ && out && ws, SSI_ERR_INVALID_ARG, "ssi_modal_sweep: NULL pointer");
+  SSI_REQUIRE(l > 0 && i >= 2 && dt > 0.0, SSI_ERR_INVALID_ARG, "ssi_modal_sweep: need l > 0, i >= 2, dt > 0");
+  SSI_TRY(check_orders(n_min, n_max, n_step));
+  const int64_t m = int64_t(l) * i;
+  SSI_REQUIRE(n_max <= m - l, SSI_ERR_INVALID_ARG, "ssi_modal_sweep: n_max > l(i-1)");
+  SSI_REQUIRE(ldU >= m, SSI_ERR_SHAPE, "ssi_modal_sweep: ldU < l*i");
+  const int no = (n_max - n_min) / n_step + 1;
+  SSI_REQUIRE(out->n_orders == no && out->cap >= n_max / 2 && out->l == l &&
+                  out->n_min == n_min && out->n_step == n_step,
+              SSI_ERR_INVALID_ARG, "ssi_modal_sweep: pole table header does not match the sweep");
+  SSI_REQUIRE(out->count && out->f && out->xi && out->mu_re && out->mu_im && out->mpc && out->mpd &&
+                  out->shape,
+              SSI_ERR_INVALID_ARG, "ssi_modal_sweep: NULL pole-table array");
+  SSI_REQUIRE(modal_smem_bytes(n_max, out->cap) <= 227 * 1024, SSI_ERR_INVALID_ARG,
+              "ssi_modal_sweep: n_max %d too large for the one-CTA eigen-solver", n_max);
+  const size_t need = modal_ws_bytes(l, i, n_min, n_max, n_step);
+  SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_modal_sweep: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = S(stream);
+  SSI_TRY(reset_status(ws, s));
+  return modal_run(U, ldU, S_, l, i, n_min, n_max, n_step, dt, *out, ws, static_cast<int32_t*>(ws), s);
+}
+
+ssi_status ssi_stab3d(const ssi_pole_table* tables, int32_t n_lags, const ssi_criteria* crit,
+                      uint8_t* flags, int32_t* stable_count, void* stream) {
+  SSI_REQUIRE(tables && crit && flags && stable_count && n_lags >= 1, SSI_ERR_INVALID_ARG,
+              "ssi_stab3d: bad arguments");
+  for (int g = 1; g < n_lags; ++g)
+    SSI_REQUIRE(tables[g].n_orders == tables[0].n_orders && tables[g].cap == tables[0].cap &&
+                    tables[g].l == tables[0].l && tables[g].n_min == tables[0].n_min &&
+                    tables[g].n_step == tables[0].n_step,
+                SSI_ERR_INVALID_ARG, "ssi_stab3d: pole tables differ in shape");
+  return stab3d_run(tables, n_lags, *crit, flags, stable_count, S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,33 @@
+// FP64 tensor-core GEMM (mma.sync m8n8k4 -> SASS DMMA) used by the RSVD passes
+// T*Omega, T^T*Q, T*Z (Eqs. 14-15), the CholeskyQR2 Gram products
+// and triangular multiplies, and U = Q*U~ (Eq. 18). FP64 is required for parity
+// (a BF16x3 sketch moves physical poles by 1.6e-4).
+#pragma once
+#include "common.cuh"
+
+namespace ssi {
+
+// Strided operand: element (r, c) at p[r*s_r + c*s_c].
+struct Operand {
+  const double* p;
+  int64_t s_r, s_c;
+};
+
+// C (M x N, col-major, ldc) = alpha * A (M x K) * B (K x N).
+// A is "k-contiguous" when s_c == 1 (row-major), otherwise s_r must be 1 (col-major);
+// likewise B is k-contiguous when s_r == 1. splits > 1 partitions K, writes partials to
+// `partial` ([splits][M*N]) and reduces them in fixed order (deterministic).
+ssi_status gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, Operand A, Operand B,
+                    double* C, int64_t ldc, int splits, double* partial, cudaStream_t s);
+
+// Heuristic split count so that tiles*splits fills the 148 SMs a few times over.
+int gemm_pick_splits(int64_t M, int64_t N, int64_t K);
+size_t gemm_partial_elems(int64_t M, int64_t N, int splits);
+
+// Batched "order" GEMM for the modal sweep: for b in [0, nb), n_b = n0 + b*dn,
+// C_b (n_b x n_b col-major, at Cbase + off_b, off_b = sum_{b'<b} n_b'^2) =
+//   A[:n_b, :n_b] * B[:n_b, :n_b] with A, B col-major (ld lda, ldb).
+ssi_status gemm_f64_orders(int nb, int n0, int dn, const double* A, int64_t lda,
+                           const double* B, int64_t ldb, double* Cbase, cudaStream_t s);
+
+}  // namespace ssi

@@ -1,0 +1,34 @@
+#pragma once
+#include "common.cuh"
+#include "gemm_f64.cuh"
+
+namespace ssi {
+
+// Scratch for one CholeskyQR2 of an m x k matrix.
+struct CholQRWork {
+  double* W;        // k x k Gram
+  double* L1;       // k x k lower, first Cholesky factor
+  double* Linv1;    // k x k lower, its inverse
+  double* L2;
+  double* Linv2;
+  double* Q1;       // m x k intermediate
+  double* chol_g;   // packed triangle when k is too large for shared memory
+  double* partial;  // split-K partials
+};
+size_t cholqr_partial_elems(int64_t m, int k);
+void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w);
+
+// CholeskyQR2 (A5; "qr(Y,0)"): Y = Q R, R = L2^T L1^T upper with
+// positive diagonal. Y: m x k col-major (ldy); Q: m x k col-major (ld m).
+ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, CholQRWork& w,
+                   int32_t* status, cudaStream_t s);
+
+// Single-CTA Cholesky W = L L^T and L^{-1} (lower, col-major ld k).
+ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* gscratch,
+                    int32_t* status, cudaStream_t s);
+
+// One-sided (Hestenes) Jacobi SVD of a k x k matrix G (col-major, overwritten):
+// G V = U Sigma; Ut = U sorted by descending sigma (col-major k x k), S = sigma.
+ssi_status jacobi_svd(double* G, int k, double* Ut, double* S, int32_t* status, cudaStream_t s);
+
+}  // namespace ssi

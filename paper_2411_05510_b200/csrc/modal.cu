@@ -1,0 +1,602 @@
+// A9-A11: per-order modal sweep (§2.1, Eqs. 9-12), one CTA per order.
+//
+// S-free nested form (pin P10): with U^up = U[0:l(i-1), :n_max] = Q R
+// (CholeskyQR2, diag R > 0) and W = Q^T U[l:li, :n_max],
+//     A_n = S_n^{-1/2} (R_n^{-1} W_n) S_n^{1/2},   M_n := R_n^{-1} W_n = Rinv[:n,:n] W[:n,:n]
+// (Rinv upper triangular, so its leading block is R_n^{-1}). eig(A_n) = eig(M_n) and
+// Phi = C_n psi_A = U[0:l, :n] psi_M. Per order the CTA then runs
+//   Householder Hessenberg reduction (global, L2-resident) with C <- C Q_H,
+//   Francis double-shift QR on a banded copy in shared memory (real Schur form T,
+//   LAPACK dlahqr/dlanv2 structure) with C <- C Z,
+//   complex back substitution on T for every pole (Im mu > 0, 0 < xi < 1),
+//   Phi = C x, normalization (reading A-15), MPC / MPD (A-16), f / xi (A-1),
+// and writes the poles sorted by (f, xi).
+#include "linalg.cuh"
+#include "rsvd.cuh"
+
+namespace ssi {
+namespace {
+
+constexpr int NT = 256;
+constexpr int NW = NT / 32;
+constexpr double kUlp = 2.220446049250313e-16;
+constexpr double kSafeMin = 2.2250738585072014e-308;
+
+__host__ __device__ inline int band_lo(int i) { return i > 3 ? i - 3 : 0; }
+__host__ __device__ inline size_t band_elems(int n) {
+  size_t s = 0;
+  for (int i = 0; i < n; ++i) s += size_t(n - band_lo(i));
+  return s;
+}
+__host__ __device__ inline int64_t order_off_sq(int n0, int dn, int b) {
+  int64_t off = 0;
+  for (int bb = 0; bb < b; ++bb) { const int64_t nb = n0 + int64_t(bb) * dn; off += nb * nb; }
+  return off;
+}
+
+struct EigArgs {
+  double* M;            // order slabs (col-major n x n), overwritten
+  double* C;            // order slabs l x n
+  const double* U;
+  int64_t ldU;
+  const double* S;
+  int l, n_min, n_step, n_orders, n_max, cap;
+  double dt;
+  ssi_pole_table tab;
+};
+
+struct Smem {
+  double* H;      // banded Hessenberg / Schur
+  int* rowoff;    // n+1
+  double* v;      // n: Householder vector (Hessenberg phase)
+  double* refl;   // 3 n: (v1, v2, tau) per bulge step
+  double* x;      // NW * 2 * n: per-warp complex eigenvector
+  int* cj;        // cap: block start of candidate
+  double* cre; double* cim; double* cf; double* cxi;  // cap each
+};
+
+__device__ __forceinline__ double& Hat(const Smem& s, int i, int c) {
+  return s.H[s.rowoff[i] + c - band_lo(i)];
+}
+
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int w = 0; w < NW; ++w) t += red[w];
+  return t;
+}
+
+// LAPACK dlanv2: Schur factorization of a real 2x2 nonsymmetric matrix in standardized
+// form. Returns rotation (cs, sn) with [a b; c d]_in = [cs -sn; sn cs][a b; c d]_out[cs sn; -sn cs].
+__device__ void dlanv2(double& a, double& b, double& c, double& d, double& cs, double& sn) {
+  const double eps = kUlp * 0.5;
+  if (c == 0.0) {
+    cs = 1.0; sn = 0.0;
+  } else if (b == 0.0) {
+    cs = 0.0; sn = 1.0;
+    const double t = d; d = a; a = t; b = -c; c = 0.0;
+  } else if ((a - d) == 0.0 && (copysign(1.0, b) != copysign(1.0, c))) {
+    cs = 1.0; sn = 0.0;
+  } else {
+    const double temp = a - d;
+    double p = 0.5 * temp;
+    const double bcmax = fmax(fabs(b), fabs(c));
+    const double bcmis = fmin(fabs(b), fabs(c)) * copysign(1.0, b) * copysign(1.0, c);
+    const double scale = fmax(fabs(p), bcmax);
+    double z = (p / scale) * p + (bcmax / scale) * bcmis;
+    if (z >= 4.0 * eps) {
+      z = p + copysign(sqrt(scale) * sqrt(z), p);
+      a = d + z;
+      d = d - (bcmax / z) * bcmis;
+      const double tau = hypot(c, z);
+      cs = z / tau; sn = c / tau;
+      b = b - c; c = 0.0;
+    } else {
+      const double sigma = b + c;
+      const double tau = hypot(sigma, temp);
+      cs = sqrt(0.5 * (1.0 + fabs(sigma) / tau));
+      sn = -(p / (tau * cs)) * copysign(1.0, sigma);
+      const double aa = a * cs + b * sn, bb = -a * sn + b * cs;
+      const double cc = c * cs + d * sn, dd = -c * sn + d * cs;
+      a = aa * cs + cc * sn; b = bb * cs + dd * sn;
+      c = -aa * sn + cc * cs; d = -bb * sn + dd * cs;
+      const double t2 = 0.5 * (a + d);
+      a = t2; d = t2;
+      if (c != 0.0) {
+        if (b != 0.0) {
+          if (copysign(1.0, b) == copysign(1.0, c)) {
+            const double sab = sqrt(fabs(b)), sac = sqrt(fabs(c));
+            p = copysign(sab * sac, c);
+            const double tt = 1.0 / sqrt(fabs(b + c));
+            a = t2 + p; d = t2 - p;
+            b = b - c; c = 0.0;
+            const double cs1 = sab * tt, sn1 = sac * tt;
+            const double t3 = cs * cs1 - sn * sn1;
+            sn = cs * sn1 + sn * cs1;
+            cs = t3;
+          }
+        } else {
+          b = -c; c = 0.0;
+          const double t3 = cs; cs = -sn; sn = t3;
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ double red[NW];
+  __shared__ double sh_tau, sh_scal, sh_beta, sh_cs, sh_sn, sh_v1, sh_v2;
+  __shared__ int sh_l, sh_fail, sh_nr, sh_ncand;
+
+  const int o = blockIdx.x;
+  const int n = g.n_min + o * g.n_step;
+  const int l = g.l;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  ssi_pole_table T = g.tab;
+  const int cap = T.cap;
+
+  // scalar outputs default to zero for every slot
+  for (int sidx = tid; sidx < cap; sidx += NT) {
+    const int64_t e = int64_t(o) * cap + sidx;
+    T.f[e] = 0.0; T.xi[e] = 0.0; T.mu_re[e] = 0.0; T.mu_im[e] = 0.0; T.mpc[e] = 0.0; T.mpd[e] = 0.0;
+  }
+  // orders above the numerical rank are reported, not solved
+  if (!(g.S[n - 1] >= 1e-12 * g.S[0])) {
+    if (tid == 0) T.count[o] = -1;
+    return;
+  }
+
+  // ---------------- shared memory carve (sized for n_max on the host)
+  Smem s;
+  {
+    char* p = reinterpret_cast<char*>(dsm);
+    const int nm = g.n_max;
+    s.H = reinterpret_cast<double*>(p);      p += sizeof(double) * band_elems(nm);
+    s.v = reinterpret_cast<double*>(p);      p += sizeof(double) * nm;
+    s.refl = reinterpret_cast<double*>(p);   p += sizeof(double) * 3 * nm;
+    s.x = reinterpret_cast<double*>(p);      p += sizeof(double) * NW * 2 * nm;
+    s.cre = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
+    s.cim = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
+    s.cf = reinterpret_cast<double*>(p);     p += sizeof(double) * cap;
+    s.cxi = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
+    s.rowoff = reinterpret_cast<int*>(p);    p += sizeof(int) * (nm + 1);
+    s.cj = reinterpret_cast<int*>(p);
+  }
+  if (tid == 0) {
+    int off = 0;
+    for (int i = 0; i < n; ++i) { s.rowoff[i] = off; off += n - band_lo(i); }
+    s.rowoff[n] = off;
+    sh_fail = 0;
+  }
+
+  double* A = g.M + order_off_sq(g.n_min, g.n_step, o);      // n x n col-major
+  double* C = g.C + int64_t(l) * (int64_t(o) * g.n_min + int64_t(g.n_step) * (int64_t(o) * (o - 1) / 2));
+  // C <- U[0:l, 0:n]
+  for (int64_t e = tid; e < int64_t(l) * n; e += NT) {
+    const int64_t a = e % l, c = e / l;
+    C[e] = g.U[a + c * g.ldU];
+  }
+  __syncthreads();
+
+  // ---------------- Householder Hessenberg reduction, A <- Q^T A Q, C <- C Q
+  for (int j = 0; j + 2 < n; ++j) {
+    const int L = n - j - 1;   // rows j+1..n-1
+    double part = 0.0;
+    for (int r = j + 2 + tid; r < n; r += NT) { const double t = A[r + int64_t(j) * n]; part += t * t; }
+    const double xn2 = block_sum(part, red);
+    if (tid == 0) {
+      const double alpha = A[j + 1 + int64_t(j) * n];
+      if (xn2 == 0.0) {
+        sh_tau = 0.0;
+      } else {
+        const double beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        sh_tau = (beta - alpha) / beta;
+        sh_scal = 1.0 / (alpha - beta);
+        sh_beta = beta;
+      }
+    }
+    __syncthreads();
+    const double tau = sh_tau;
+    if (tau == 0.0) continue;
+    const double scal = sh_scal;
+    for (int r = tid; r < L; r += NT) {
+      double* col = A + int64_t(j) * n;
+      if (r == 0) { s.v[0] = 1.0; col[j + 1] = sh_beta; }
+      else { s.v[r] = col[j + 1 + r] * scal; col[j + 1 + r] = 0.0; }
+    }
+    __syncthreads();
+    // left: columns j+1..n-1
+    for (int c = j + 1 + warp; c < n; c += NW) {
+      double* col = A + int64_t(c) * n + j + 1;
+      double w = 0.0;
+      for (int r = lane; r < L; r += 32) w += s.v[r] * col[r];
+      w = warp_sum(w) * tau;
+      for (int r = lane; r < L; r += 32) col[r] -= w * s.v[r];
+    }
+    __syncthreads();
+    // right: all rows of A, and all rows of C
+    for (int r = tid; r < n + l; r += NT) {
+      double* base;
+      int64_t ld;
+      if (r < n) { base = A + r; ld = n; }
+      else { base = C + (r - n); ld = l; }
+      double w = 0.0;
+      for (int c = 0; c < L; ++c) w += base[(j + 1 + c) * ld] * s.v[c];
+      w *= tau;
+      for (int c = 0; c < L; ++c) base[(j + 1 + c) * ld] -= w * s.v[c];
+    }
+    __syncthreads();
+  }
+
+  // ---------------- banded copy into shared memory
+  for (int i = 0; i < n; ++i)
+    for (int c = band_lo(i) + tid; c < n; c += NT) Hat(s, i, c) = A[i + int64_t(c) * n];
+  __syncthreads();
+
+  // ---------------- Francis double-shift QR (dlahqr structure, wantt = wantz = true)
+  int ihi = n - 1;
+  int its = 0, total_its = 0;
+  const int itmax = 30 * (n > 10 ? n : 10);
+  while (ihi >= 0) {
+    if (tid == 0) {
+      int ll = ihi;
+      for (; ll > 0; --ll) {
+        const double h = fabs(Hat(s, ll, ll - 1));
+        if (h <= kSafeMin) break;
+        double tst = fabs(Hat(s, ll - 1, ll - 1)) + fabs(Hat(s, ll, ll));
+        if (tst == 0.0) {
+          if (ll - 2 >= 0) tst += fabs(Hat(s, ll - 1, ll - 2));
+          if (ll + 1 <= ihi) tst += fabs(Hat(s, ll + 1, ll));
+        }
+        if (h <= kUlp * tst) break;
+      }
+      if (ll > 0) Hat(s, ll, ll - 1) = 0.0;
+      sh_l = ll;
+    }
+    __syncthreads();
+    const int lo = sh_l;
+    if (lo == ihi) { ihi -= 1; its = 0; __syncthreads(); continue; }
+    if (lo == ihi - 1) {
+      const int p = ihi - 1, q = ihi;
+      if (tid == 0) {
+        double a = Hat(s, p, p), b = Hat(s, p, q), c = Hat(s, q, p), d = Hat(s, q, q), cs, sn;
+        dlanv2(a, b, c, d, cs, sn);
+        Hat(s, p, p) = a; Hat(s, p, q) = b; Hat(s, q, p) = c; Hat(s, q, q) = d;
+        sh_cs = cs; sh_sn = sn;
+      }
+      __syncthreads();
+      const double cs = sh_cs, sn = sh_sn;
+      for (int c = q + 1 + tid; c < n; c += NT) {
+        const double x = Hat(s, p, c), y = Hat(s, q, c);
+        Hat(s, p, c) = cs * x + sn * y;
+        Hat(s, q, c) = cs * y - sn * x;
+      }
+      for (int r = tid; r < p + l; r += NT) {
+        if (r < p) {
+          const double x = Hat(s, r, p), y = Hat(s, r, q);
+          Hat(s, r, p) = cs * x + sn * y;
+          Hat(s, r, q) = cs * y - sn * x;
+        } else {
+          double* cr = C + (r - p);
+          const double x = cr[int64_t(p) * l], y = cr[int64_t(q) * l];
+          cr[int64_t(p) * l] = cs * x + sn * y;
+          cr[int64_t(q) * l] = cs * y - sn * x;
+        }
+      }
+      __syncthreads();
+      ihi -= 2; its = 0;
+      continue;
+    }
+    ++its; ++total_its;
+    if (its > 100 || total_its > itmax) {
+      if (tid == 0) sh_fail = 1;
+      __syncthreads();
+      break;
+    }
+    // shifts (exceptional at its == 10, 20) and first column of (H - s1)(H - s2) e_lo
+    if (tid == 0) {
+      double h11, h12, h21, h22;
+      if (its == 10) {
+        const double ex = fabs(Hat(s, lo + 1, lo)) + fabs(Hat(s, lo + 2, lo + 1));
+        h11 = 0.75 * ex + Hat(s, lo, lo); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
+      } else if (its == 20) {
+        const double ex = fabs(Hat(s, ihi, ihi - 1)) + fabs(Hat(s, ihi - 1, ihi - 2));
+        h11 = 0.75 * ex + Hat(s, ihi, ihi); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
+      } else {
+        h11 = Hat(s, ihi - 1, ihi - 1); h12 = Hat(s, ihi - 1, ihi);
+        h21 = Hat(s, ihi, ihi - 1); h22 = Hat(s, ihi, ihi);
+      }
+      const double tr = h11 + h22, det = h11 * h22 - h12 * h21;
+      const double a00 = Hat(s, lo, lo), a01 = Hat(s, lo, lo + 1);
+      const double a10 = Hat(s, lo + 1, lo), a11 = Hat(s, lo + 1, lo + 1);
+      const double a21 = Hat(s, lo + 2, lo + 1);
+      double x = a00 * a00 + a01 * a10 - tr * a00 + det;
+      double y = a10 * (a00 + a11 - tr);
+      double z = a10 * a21;
+      const double sc = fabs(x) + fabs(y) + fabs(z);
+      if (sc > 0.0) { x /= sc; y /= sc; z /= sc; }
+      s.refl[0] = x; s.refl[1] = y; s.refl[2] = z;   // seed for k = lo
+    }
+    __syncthreads();
+    for (int k = lo; k < ihi; ++k) {
+      if (tid == 0) {
+        const int nr = (ihi - k + 1) < 3 ? (ihi - k + 1) : 3;
+        double x, y, z;
+        if (k == lo) { x = s.refl[0]; y = s.refl[1]; z = s.refl[2]; if (nr < 3) z = 0.0; }
+        else { x = Hat(s, k, k - 1); y = Hat(s, k + 1, k - 1); z = nr == 3 ? Hat(s, k + 2, k - 1) : 0.0; }
+        const double xn = hypot(y, z);
+        double tau = 0.0, v1 = 0.0, v2 = 0.0;
+        if (xn != 0.0) {
+          const double beta = -copysign(hypot(x, xn), x);
+          tau = (beta - x) / beta;
+          const double sc = 1.0 / (x - beta);
+          v1 = y * sc; v2 = z * sc;
+          if (k > lo) {
+            Hat(s, k, k - 1) = beta; Hat(s, k + 1, k - 1) = 0.0;
+            if (nr == 3) Hat(s, k + 2, k - 1) = 0.0;
+          }
+        }
+        sh_tau = tau; sh_v1 = v1; sh_v2 = v2; sh_nr = nr;
+        s.refl[3 * (k - lo) + 0] = v1;   // overwrites the seed only after reading it
+        s.refl[3 * (k - lo) + 1] = v2;
+        s.refl[3 * (k - lo) + 2] = tau;
+      }
+      __syncthreads();
+      const double tau = sh_tau, v1 = sh_v1, v2 = sh_v2;
+      const int nr = sh_nr;
+      if (tau != 0.0) {
+        for (int c = k + tid; c < n; c += NT) {          // left: rows k..k+nr-1
+          double sum = Hat(s, k, c) + v1 * Hat(s, k + 1, c);
+          if (nr == 3) sum += v2 * Hat(s, k + 2, c);
+          sum *= tau;
+          Hat(s, k, c) -= sum;
+          Hat(s, k + 1, c) -= sum * v1;
+          if (nr == 3) Hat(s, k + 2, c) -= sum * v2;
+        }
+        __syncthreads();
+        const int rmax = (k + 3 < ihi ? k + 3 : ihi);
+        for (int r = tid; r <= rmax; r += NT) {          // right: cols k..k+nr-1
+          double sum = Hat(s, r, k) + v1 * Hat(s, r, k + 1);
+          if (nr == 3) sum += v2 * Hat(s, r, k + 2);
+          sum *= tau;
+          Hat(s, r, k) -= sum;
+          Hat(s, r, k + 1) -= sum * v1;
+          if (nr == 3) Hat(s, r, k + 2) -= sum * v2;
+        }
+      }
+      __syncthreads();
+    }
+    // deferred C <- C P_lo ... P_{ihi-1}: each row of C streams through the reflectors
+    for (int r = tid; r < l; r += NT) {
+      double* cr = C + r;
+      double c0 = cr[int64_t(lo) * l], c1 = cr[int64_t(lo + 1) * l];
+      for (int k = lo; k < ihi; ++k) {
+        const double v1 = s.refl[3 * (k - lo)], v2 = s.refl[3 * (k - lo) + 1];
+        const double tau = s.refl[3 * (k - lo) + 2];
+        const bool three = (k + 2 <= ihi);
+        double c2 = three ? cr[int64_t(k + 2) * l] : 0.0;
+        if (tau != 0.0) {
+          double sum = c0 + v1 * c1 + (three ? v2 * c2 : 0.0);
+          sum *= tau;
+          c0 -= sum; c1 -= sum * v1;
+          if (three) c2 -= sum * v2;
+        }
+        cr[int64_t(k) * l] = c0;
+        c0 = c1; c1 = c2;
+      }
+      cr[int64_t(ihi) * l] = c0;
+    }
+    __syncthreads();
+  }
+  if (sh_fail) {
+    if (tid == 0) T.count[o] = -1;
+    return;
+  }
+
+  // ---------------- poles: complex pairs of the standardized Schur form
+  if (tid == 0) {
+    int nc = 0;
+    for (int i = 0; i < n;) {
+      if (i + 1 < n && Hat(s, i + 1, i) != 0.0) {
+        const double wr = Hat(s, i, i);
+        const double wi = sqrt(fabs(Hat(s, i, i + 1))) * sqrt(fabs(Hat(s, i + 1, i)));
+        // lambda = ln(mu)/dt (principal branch); f = |lambda|/2pi; xi = -Re/|lambda|
+        const double lr = log(hypot(wr, wi)) / g.dt, li = atan2(wi, wr) / g.dt;
+        const double al = hypot(lr, li);
+        const double f = al / (2.0 * 3.141592653589793), xi = -lr / al;
+        if (wi > 0.0 && xi > 0.0 && xi < 1.0 && nc < cap) {
+          // insertion by (f, xi)
+          int pos = nc;
+          while (pos > 0 && (s.cf[pos - 1] > f || (s.cf[pos - 1] == f && s.cxi[pos - 1] > xi))) {
+            s.cf[pos] = s.cf[pos - 1]; s.cxi[pos] = s.cxi[pos - 1];
+            s.cre[pos] = s.cre[pos - 1]; s.cim[pos] = s.cim[pos - 1]; s.cj[pos] = s.cj[pos - 1];
+            --pos;
+          }
+          s.cf[pos] = f; s.cxi[pos] = xi; s.cre[pos] = wr; s.cim[pos] = wi; s.cj[pos] = i;
+          ++nc;
+        }
+        i += 2;
+      } else {
+        i += 1;
+      }
+    }
+    sh_ncand = nc;
+    T.count[o] = nc;
+  }
+  __syncthreads();
+  const int nc = sh_ncand;
+
+  // ---------------- eigenvectors (warp per pole): back substitution on T, Phi = C x
+  double* xr = s.x + warp * 2 * g.n_max;
+  double* xim = xr + g.n_max;
+  for (int c = warp; c < nc; c += NW) {
+    const int j = s.cj[c];
+    const double wr = s.cre[c], wi = s.cim[c];
+    const double smin = fmax(kUlp * hypot(wr, wi), kSafeMin);
+    if (lane == 0) {
+      xr[j] = 1.0; xim[j] = 0.0;
+      const double b = Hat(s, j, j + 1);
+      xr[j + 1] = (wr - Hat(s, j, j)) / b; xim[j + 1] = wi / b;
+    }
+    __syncwarp();
+    int i = j - 1;
+    while (i >= 0) {
+      const bool two = (i >= 1) && (Hat(s, i, i - 1) != 0.0);
+      double r1r = 0.0, r1i = 0.0, r2r = 0.0, r2i = 0.0;
+      for (int p = i + 1 + lane; p <= j + 1; p += 32) {
+        const double h = Hat(s, i, p);
+        r2r -= h * xr[p]; r2i -= h * xim[p];
+        if (two) { const double h1 = Hat(s, i - 1, p); r1r -= h1 * xr[p]; r1i -= h1 * xim[p]; }
+      }
+      r2r = warp_sum(r2r); r2i = warp_sum(r2i);
+      if (two) { r1r = warp_sum(r1r); r1i = warp_sum(r1i); }
+      if (lane == 0) {
+        if (!two) {
+          double dr = Hat(s, i, i) - wr, di = -wi;
+          if (hypot(dr, di) < smin) { dr = smin; di = 0.0; }
+          const double den = dr * dr + di * di;
+          xr[i] = (r2r * dr + r2i * di) / den;
+          xim[i] = (r2i * dr - r2r * di) / den;
+        } else {
+          // [[m00, m01], [m10, m11]] [x_{i-1}; x_i] = [r1; r2]
+          const double m00r = Hat(s, i - 1, i - 1) - wr, m00i = -wi, m01 = Hat(s, i - 1, i);
+          const double m10 = Hat(s, i, i - 1), m11r = Hat(s, i, i) - wr, m11i = -wi;
+          double detr = (m00r * m11r - m00i * m11i) - m01 * m10;
+          double deti = (m00r * m11i + m00i * m11r);
+          if (hypot(detr, deti) < smin) { detr = smin; deti = 0.0; }
+          const double den = detr * detr + deti * deti;
+          // x_{i-1} = (r1 m11 - m01 r2) / det ; x_i = (m00 r2 - m10 r1) / det
+          const double n1r = (r1r * m11r - r1i * m11i) - m01 * r2r;
+          const double n1i = (r1r * m11i + r1i * m11r) - m01 * r2i;
+          const double n2r = (m00r * r2r - m00i * r2i) - m10 * r1r;
+          const double n2i = (m00r * r2i + m00i * r2r) - m10 * r1i;
+          xr[i - 1] = (n1r * detr + n1i * deti) / den; xim[i - 1] = (n1i * detr - n1r * deti) / den;
+          xr[i] = (n2r * detr + n2i * deti) / den;     xim[i] = (n2i * detr - n2r * deti) / den;
+        }
+      }
+      __syncwarp();
+      i -= two ? 2 : 1;
+    }
+    // Phi = C x (C: l x n col-major), raw into the output slot
+    double* shp = T.shape + (int64_t(o) * cap + c) * int64_t(l) * 2;
+    double nrm2 = 0.0, best = -1.0;
+    int besti = 0;
+    for (int a = lane; a < l; a += 32) {
+      double pr = 0.0, pi = 0.0;
+      for (int p = 0; p <= j + 1; ++p) {
+        const double cv = C[a + int64_t(p) * l];
+        pr += cv * xr[p]; pi += cv * xim[p];
+      }
+      shp[2 * a] = pr; shp[2 * a + 1] = pi;
+      const double m2 = pr * pr + pi * pi;
+      nrm2 += m2;
+      if (m2 > best) { best = m2; besti = a; }
+    }
+    nrm2 = warp_sum(nrm2);
+#pragma unroll
+    for (int ofs = 16; ofs > 0; ofs >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, ofs);
+      const int oi = __shfl_xor_sync(0xffffffffu, besti, ofs);
+      if (ob > best || (ob == best && oi < besti)) { best = ob; besti = oi; }
+    }
+    __syncwarp();
+    const double pmr = shp[2 * besti], pmi = shp[2 * besti + 1];
+    const double am = hypot(pmr, pmi), inv = 1.0 / sqrt(nrm2);
+    const double rr = pmr / am * inv, ri = -pmi / am * inv;   // conj(phi_max)/|phi_max|/||phi||
+    double sxx = 0.0, syy = 0.0, sxy = 0.0;
+    __syncwarp();
+    for (int a = lane; a < l; a += 32) {
+      const double pr = shp[2 * a], pi = shp[2 * a + 1];
+      const double qr = pr * rr - pi * ri, qi = pr * ri + pi * rr;
+      shp[2 * a] = qr; shp[2 * a + 1] = qi;
+      sxx += qr * qr; syy += qi * qi; sxy += qr * qi;
+    }
+    sxx = warp_sum(sxx); syy = warp_sum(syy); sxy = warp_sum(sxy);
+    const double mpc = ((sxx - syy) * (sxx - syy) + 4.0 * sxy * sxy) / ((sxx + syy) * (sxx + syy));
+    const double th = 0.5 * atan2(2.0 * sxy, sxx - syy);
+    const double dx = cos(th), dy = sin(th);
+    double wsum = 0.0, dsum = 0.0;
+    for (int a = lane; a < l; a += 32) {
+      const double qr = shp[2 * a], qi = shp[2 * a + 1];
+      const double dot = qr * dx + qi * dy, crs = qr * dy - qi * dx;
+      const double mag = hypot(qr, qi);
+      wsum += mag; dsum += mag * atan2(fabs(crs), fabs(dot));
+    }
+    wsum = warp_sum(wsum); dsum = warp_sum(dsum);
+    if (lane == 0) {
+      const int64_t e = int64_t(o) * cap + c;
+      double mpd = dsum / wsum / (3.141592653589793 / 4.0);
+      mpd = fmin(fmax(mpd, 0.0), 1.0);
+      T.f[e] = s.cf[c]; T.xi[e] = s.cxi[c]; T.mu_re[e] = wr; T.mu_im[e] = wi;
+      T.mpc[e] = mpc; T.mpd[e] = mpd;
+    }
+  }
+}
+
+}  // namespace
+
+size_t modal_smem_bytes(int n_max, int cap) {
+  return sizeof(double) * (band_elems(n_max) + n_max + 3 * size_t(n_max) + size_t(NW) * 2 * n_max +
+                           4 * size_t(cap)) +
+         sizeof(int) * (size_t(n_max) + 1 + cap) + 64;
+}
+
+struct ModalWork {
+  double *Rinv, *W, *M, *C, *Qup;
+  CholQRWork cq;
+  double* partial;
+};
+
+static void modal_carve(Carver& c, int l, int i, int n_min, int n_max, int n_step, ModalWork& w) {
+  const int64_t m = int64_t(l) * i, mu = m - l;
+  const int no = (n_max - n_min) / n_step + 1;
+  int64_t sq = 0, lin = 0;
+  for (int b = 0; b < no; ++b) { const int64_t nb = n_min + int64_t(b) * n_step; sq += nb * nb; lin += nb; }
+  w.Rinv = c.take<double>(size_t(n_max) * n_max);
+  w.W = c.take<double>(size_t(n_max) * n_max);
+  w.M = c.take<double>(size_t(sq));
+  w.C = c.take<double>(size_t(lin) * l);
+  w.Qup = c.take<double>(size_t(mu) * n_max);
+  w.partial = c.take<double>(gemm_partial_elems(n_max, n_max, gemm_pick_splits(n_max, n_max, mu)) + 1);
+  cholqr_carve(c, mu, n_max, w.cq);
+}
+
+size_t modal_ws_bytes(int l, int i, int n_min, int n_max, int n_step) {
+  Carver c(nullptr);
+  ModalWork w;
+  modal_carve(c, l, i, n_min, n_max, n_step, w);
+  return c.bytes();
+}
+
+ssi_status modal_run(const double* U, int64_t ldU, const double* S, int l, int i, int n_min,
+                     int n_max, int n_step, double dt, const ssi_pole_table& tab, void* ws,
+                     int32_t* status, cudaStream_t st) {
+  Carver c(ws);
+  ModalWork w;
+  modal_carve(c, l, i, n_min, n_max, n_step, w);
+  const int64_t m = int64_t(l) * i, mu = m - l;
+  const int no = (n_max - n_min) / n_step + 1;
+  // U^up = Q R (CholeskyQR2); R^{-1} = Linv1^T Linv2^T (upper triangular)
+  SSI_TRY(cholqr2(U, ldU, mu, n_max, w.Qup, w.cq, status, st));
+  SSI_TRY(gemm_f64(n_max, n_max, n_max, 1.0, Operand{w.cq.Linv1, n_max, 1},
+                   Operand{w.cq.Linv2, n_max, 1}, w.Rinv, n_max, 1, nullptr, st));
+  // W = Q^T U^down, U^down = U[l:m, :n_max]
+  const int splits = gemm_pick_splits(n_max, n_max, mu);
+  SSI_TRY(gemm_f64(n_max, n_max, mu, 1.0, Operand{w.Qup, mu, 1}, Operand{U + l, 1, ldU}, w.W,
+                   n_max, splits, w.partial, st));
+  // M_n = Rinv[:n,:n] W[:n,:n] for every order
+  SSI_TRY(gemm_f64_orders(no, n_min, n_step, w.Rinv, n_max, w.W, n_max, w.M, st));
+  EigArgs g{w.M, w.C, U, ldU, S, l, n_min, n_step, no, n_max, tab.cap, dt, tab};
+  const size_t smem = modal_smem_bytes(n_max, tab.cap);
+  cudaFuncSetAttribute(eig_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  eig_order_kernel<<<no, NT, smem, st>>>(g);
+  return launch_check("eig_order_kernel");
+}
+
+}  // namespace ssi

@@ -1,0 +1,70 @@
+// A3-A8: randomized SVD of the block-Toeplitz T (Algorithm 1, with
+// the north star's q power iterations; reading A-12). Host-side orchestration of the
+// device kernels; every arithmetic step runs on the GPU.
+#include "covariance.cuh"
+#include "linalg.cuh"
+#include "rsvd.cuh"
+
+namespace ssi {
+
+struct RsvdWork {
+  double *Omega, *Y, *Q, *Q2, *G, *Ut, *Sk;
+  CholQRWork cq;
+};
+
+static void rsvd_carve(Carver& c, int64_t m, int k, RsvdWork& w) {
+  w.Omega = c.take<double>(size_t(m) * k);
+  w.Y = c.take<double>(size_t(m) * k);
+  w.Q = c.take<double>(size_t(m) * k);
+  w.Q2 = c.take<double>(size_t(m) * k);
+  w.G = c.take<double>(size_t(k) * k);
+  w.Ut = c.take<double>(size_t(k) * k);
+  w.Sk = c.take<double>(size_t(k));
+  cholqr_carve(c, m, k, w.cq);
+}
+
+size_t rsvd_ws_bytes(int64_t m, int k) {
+  Carver c(nullptr);
+  RsvdWork w;
+  rsvd_carve(c, m, k, w);
+  return c.bytes();
+}
+
+ssi_status rsvd_run(const double* T, int64_t ldT, int64_t m, int k, int q, uint64_t seed,
+                    uint64_t sid, int n_keep, double* U, int64_t ldU, double* S, void* ws,
+                    int32_t* status, cudaStream_t s) {
+  Carver c(ws);
+  RsvdWork w;
+  rsvd_carve(c, m, k, w);
+  const Operand Tn{T, ldT, 1};   // T(i,j) = T[i*ldT + j]  (row-major, k-contiguous)
+  const Operand Tt{T, 1, ldT};   // T^T(i,j) = T[j*ldT + i]
+  // line 1: Omega ~ N(0,1), Philox on device (Eq. 14 input; reading A-11)
+  SSI_TRY(sketch_launch(int(m), k, seed, sid, w.Omega, m, s));
+  // line 2: Y = T Omega (Eq. 14)
+  SSI_TRY(gemm_f64(m, k, m, 1.0, Tn, Operand{w.Omega, 1, m}, w.Y, m, 1, nullptr, s));
+  // line 3: Q = qr(Y)
+  SSI_TRY(cholqr2(w.Y, m, m, k, w.Q, w.cq, status, s));
+  // power iterations: Z = qr(T^T Q); Q = qr(T Z)
+  for (int it = 0; it < q; ++it) {
+    SSI_TRY(gemm_f64(m, k, m, 1.0, Tt, Operand{w.Q, 1, m}, w.Y, m, 1, nullptr, s));
+    SSI_TRY(cholqr2(w.Y, m, m, k, w.Q2, w.cq, status, s));
+    SSI_TRY(gemm_f64(m, k, m, 1.0, Tn, Operand{w.Q2, 1, m}, w.Y, m, 1, nullptr, s));
+    SSI_TRY(cholqr2(w.Y, m, m, k, w.Q, w.cq, status, s));
+  }
+  // line 4: B = Q^T T, formed as B^T = T^T Q (m x k) (Eq. 15)
+  SSI_TRY(gemm_f64(m, k, m, 1.0, Tt, Operand{w.Q, 1, m}, w.Y, m, 1, nullptr, s));
+  // line 5: B^T = Qb Rb (CholeskyQR2) -> B = Rb^T Qb^T; SVD(Rb^T) = U~ Sigma W^T
+  SSI_TRY(cholqr2(w.Y, m, m, k, w.Q2, w.cq, status, s));
+  // Rb^T = (L2^T L1^T)^T = L1 L2
+  SSI_TRY(gemm_f64(k, k, k, 1.0, Operand{w.cq.L1, 1, k}, Operand{w.cq.L2, 1, k}, w.G, k, 1,
+                   nullptr, s));
+  SSI_TRY(jacobi_svd(w.G, k, w.Ut, w.Sk, status, s));
+  // line 6: U = Q U~ (Eq. 18), leading n_keep columns
+  SSI_TRY(gemm_f64(m, n_keep, k, 1.0, Operand{w.Q, 1, m}, Operand{w.Ut, 1, k}, U, ldU, 1,
+                   nullptr, s));
+  if (cudaMemcpyAsync(S, w.Sk, sizeof(double) * k, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return launch_check("rsvd S copy");
+  return SSI_OK;
+}
+
+}  // namespace ssi

@@ -1,0 +1,83 @@
+"""CPU-side checks of the C-ABI boundary (-m "not gpu"): the library builds/loads, exports
+every symbol include/ssi.h declares, and its synchronous validation and workspace
+queries work without a GPU (no compute calls)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "ssi.h")
+
+
+def _declared():
+    txt = open(HDR).read()
+    return sorted(set(re.findall(r"SSI_API\s+[\w\s\*]+?\b(ssi_\w+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2411_05510_b200 import build, _lib
+    build.build()
+    return _lib.get()
+
+
+def test_header_declares_the_five_entry_points():
+    names = _declared()
+    for n in ("ssi_covariances", "ssi_toeplitz", "ssi_rsvd", "ssi_modal_sweep", "ssi_stab3d"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    for name in _declared():
+        assert hasattr(lib, name), name
+
+
+def test_python_binding_covers_every_symbol():
+    from paper_2411_05510_b200 import _lib
+    assert set(_declared()) == set(_lib.SIGNATURES)
+
+
+def test_status_strings_and_version(lib):
+    assert lib.ssi_status_string(0) == b"ok"
+    assert b"workspace" in lib.ssi_status_string(4)
+    assert b"sm_100a" in lib.ssi_version()
+
+
+def test_workspace_queries_are_host_only(lib):
+    b = C.c_size_t(0)
+    assert lib.ssi_covariances_ws(360000, 192, 1, 119, 0, C.byref(b)) == 0 and b.value > 0
+    assert lib.ssi_rsvd_ws(11520, 220, 200, C.byref(b)) == 0 and b.value > 11520 * 220 * 8 * 4
+    assert lib.ssi_modal_sweep_ws(192, 60, 2, 200, 2, C.byref(b)) == 0 and b.value > 0
+
+
+def test_synchronous_validation_without_gpu(lib):
+    """Argument errors are reported before any launch (no device needed)."""
+    b = C.c_size_t(0)
+    assert lib.ssi_rsvd_ws(100, 0, 1, C.byref(b)) == 1              # k < 1
+    assert lib.ssi_rsvd_ws(100, 20, 30, C.byref(b)) == 1            # n_keep > k
+    assert lib.ssi_modal_sweep_ws(6, 20, 3, 30, 2, C.byref(b)) == 1   # odd order
+    assert lib.ssi_covariances_ws(100, 6, 1, 9, 7, C.byref(b)) == 3   # unknown mode
+    dummy = C.c_void_p(16)
+    # record too short: lag_hi >= N
+    assert lib.ssi_covariances(dummy, 0, 10, 6, 6, 1, 10, 0, 0, 10, 1, dummy, dummy, 1 << 20, None) == 1
+    assert b"too short" in lib.ssi_last_error()
+    # ldY < l
+    assert lib.ssi_covariances(dummy, 0, 100, 6, 5, 1, 9, 0, 0, 100, 1, dummy, dummy, 1 << 20, None) == 2
+    # workspace too small
+    assert lib.ssi_covariances(dummy, 0, 100, 6, 6, 1, 9, 0, 0, 100, 1, dummy, dummy, 8, None) == 4
+    # toeplitz ld
+    assert lib.ssi_toeplitz(dummy, 6, 20, dummy, 100, None) == 2
+    # rsvd: n_keep > k
+    assert lib.ssi_rsvd(dummy, 120, 120, 40, 2, 1, 1, 41, dummy, 120, dummy, dummy, 1 << 30, None) == 1
+
+
+def test_oracle_is_not_imported_by_the_product():
+    """The product package never imports the oracle (independence)."""
+    pkg = os.path.join(ROOT, "paper_2411_05510_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower().replace("no oracle", ""), f
