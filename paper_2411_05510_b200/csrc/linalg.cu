@@ -6,140 +6,173 @@
 namespace ssi {
 namespace {
 
-constexpr int kCholThreads = 256;
+constexpr int kCholThreads = 512;
 constexpr int kJacThreads = 1024;
-
-__device__ __forceinline__ int64_t tri(int64_t i) { return i * (i + 1) / 2; }
 
 // W (k x k col-major, lower part read) -> L (lower) and Linv = L^{-1} (lower), both
 // col-major ld k with zeros above the diagonal. Packed row-major lower triangle P
 // (P[i(i+1)/2 + c], c <= i) in shared memory when it fits, else in gscratch.
+// Inverse: row i of X = L^{-1} overwrites row i of L; the dot products over p are split
+// into kGroups interleaved chunks (independent accumulators, unrolled) and reduced
+// through shared memory, so the per-row chain is short instead of k-long.
+constexpr int kGroups = 4;
+
 __global__ void __launch_bounds__(kCholThreads) chol_inv_kernel(const double* __restrict__ W, int k,
                                                                 double* __restrict__ L,
                                                                 double* __restrict__ Linv,
                                                                 double* gscratch, int use_smem,
                                                                 int32_t* status) {
   extern __shared__ __align__(16) double sm[];
-  double* vec = sm;                  // k: scaled column j / row i of L
-  double* P = use_smem ? sm + k : gscratch;
+  double* vec = sm;                          // k: scaled column j / row i of L
+  double* part = sm + k;                     // kGroups * k partial sums
+  double* P = use_smem ? sm + k + kGroups * k : gscratch;
   __shared__ int fail;
   const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
   if (tid == 0) fail = 0;
-  for (int64_t e = tid; e < tri(k); e += nt) {
-    // row i, col c of packed index e
-    int64_t i = int64_t((sqrt(8.0 * double(e) + 1.0) - 1.0) * 0.5);
-    while (tri(i + 1) <= e) ++i;
-    while (tri(i) > e) --i;
-    const int64_t c = e - tri(i);
-    P[e] = W[i + c * int64_t(k)];
+  for (int i = warp; i < k; i += nw) {
+    const int b = i * (i + 1) / 2;
+    for (int c = lane; c <= i; c += 32) P[b + c] = W[i + int64_t(c) * k];
   }
   __syncthreads();
   // Right-looking Cholesky, column by column.
   for (int j = 0; j < k; ++j) {
+    const int bj = j * (j + 1) / 2;
     if (tid == 0) {
-      const double d = P[tri(j) + j];
-      if (!(d > 0.0) || !isfinite(d)) { fail = 1; P[tri(j) + j] = 1.0; }
-      else P[tri(j) + j] = sqrt(d);
+      const double d = P[bj + j];
+      if (!(d > 0.0) || !isfinite(d)) { fail = 1; P[bj + j] = 1.0; }
+      else P[bj + j] = sqrt(d);
     }
     __syncthreads();
-    const double djj = P[tri(j) + j];
+    const double djj = P[bj + j];
     for (int i = j + 1 + tid; i < k; i += nt) {
-      const double v = P[tri(i) + j] / djj;
-      P[tri(i) + j] = v;
+      const double v = P[i * (i + 1) / 2 + j] / djj;
+      P[i * (i + 1) / 2 + j] = v;
       vec[i] = v;
     }
     __syncthreads();
-    // trailing update P[i][c] -= L[i][j] L[c][j], j < c <= i: warp per row i
-    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int i = j + 1 + warp; i < k; i += nw) {
+    for (int i = j + 1 + warp; i < k; i += nw) {   // trailing update, warp per row
       const double li = vec[i];
-      double* row = P + tri(i);
+      double* row = P + i * (i + 1) / 2;
       for (int c = j + 1 + lane; c <= i; c += 32) row[c] -= li * vec[c];
     }
     __syncthreads();
   }
   if (fail) set_status(status, SSI_ERR_NUMERIC);
-  // write L (col-major, zero upper)
   for (int64_t e = tid; e < int64_t(k) * k; e += nt) {
-    const int64_t r = e % k, c = e / k;
-    L[e] = (c <= r) ? P[tri(r) + c] : 0.0;
+    const int r = int(e % k), c = int(e / k);
+    L[e] = (c <= r) ? P[r * (r + 1) / 2 + c] : 0.0;
   }
   __syncthreads();
-  // In-place inverse: row i of X = L^{-1} overwrites row i of L.
   //   X[i][j] = (delta_ij - sum_{p=j}^{i-1} L[i][p] X[p][j]) / L[i][i]
+  const int g = tid / (nt / kGroups);           // p-chunk of this thread
+  const int jt = tid % (nt / kGroups);
+  const int jstride = nt / kGroups;
   for (int i = 0; i < k; ++i) {
-    for (int p = tid; p <= i; p += nt) vec[p] = P[tri(i) + p];
+    const int bi = i * (i + 1) / 2;
+    for (int p = tid; p <= i; p += nt) vec[p] = P[bi + p];
+    __syncthreads();
+    for (int j = jt; j < i; j += jstride) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int p = j + g;
+      int bp = p * (p + 1) / 2;                  // tri(p), advanced incrementally
+      for (; p + 3 * kGroups < i; p += 4 * kGroups) {
+        const int b1 = bp + (p + 1) + (p + 2) + (p + 3) + (p + 4);          // tri(p+4)
+        const int b2 = b1 + (p + 5) + (p + 6) + (p + 7) + (p + 8);          // tri(p+8)
+        const int b3 = b2 + (p + 9) + (p + 10) + (p + 11) + (p + 12);       // tri(p+12)
+        a0 += vec[p] * P[bp + j];
+        a1 += vec[p + 4] * P[b1 + j];
+        a2 += vec[p + 8] * P[b2 + j];
+        a3 += vec[p + 12] * P[b3 + j];
+        bp = b3 + (p + 13) + (p + 14) + (p + 15) + (p + 16);
+      }
+      for (; p < i; p += kGroups) {
+        a0 += vec[p] * P[bp + j];
+        bp += (p + 1) + (p + 2) + (p + 3) + (p + 4);
+      }
+      part[g * k + j] = (a0 + a1) + (a2 + a3);
+    }
     __syncthreads();
     const double lii = vec[i];
     for (int j = tid; j <= i; j += nt) {
-      double s0 = (j == i) ? 1.0 : 0.0, s1 = 0.0;
-      int p = j;
-      for (; p + 1 < i; p += 2) {
-        s0 -= vec[p] * P[tri(p) + j];
-        s1 -= vec[p + 1] * P[tri(p + 1) + j];
-      }
-      if (p < i) s0 -= vec[p] * P[tri(p) + j];
-      P[tri(i) + j] = (s0 + s1) / lii;
+      double s = (j == i) ? 1.0 : 0.0;
+      if (j < i) s -= (part[j] + part[k + j]) + (part[2 * k + j] + part[3 * k + j]);
+      P[bi + j] = s / lii;
     }
     __syncthreads();
   }
   for (int64_t e = tid; e < int64_t(k) * k; e += nt) {
-    const int64_t r = e % k, c = e / k;
-    Linv[e] = (c <= r) ? P[tri(r) + c] : 0.0;
+    const int r = int(e % k), c = int(e / k);
+    Linv[e] = (c <= r) ? P[r * (r + 1) / 2 + c] : 0.0;
   }
 }
 
-// One-sided Jacobi with the round-robin (circle) ordering; warp per column pair.
+// One-sided (Hestenes) Jacobi with the round-robin (circle) ordering; warp per column
+// pair. Round r pairs positions (i, n-1-i); position 0 holds column 0, position p >= 1
+// holds column 1 + (p - 1 + r) mod (n - 1). Column norms live in shared memory and are
+// updated with Rutishauser's formulas (|p'|^2 = a - t g, |q'|^2 = b + t g), so a pair
+// costs one dot product; norms are recomputed exactly at the start of every sweep.
+template <int KPL>   // column elements per lane (k <= 32 * KPL)
 __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict__ G, int k,
                                                              double* __restrict__ Ut,
                                                              double* __restrict__ S,
                                                              int32_t* status) {
   extern __shared__ __align__(16) double jsm[];
   double* nrm = jsm;                                    // k
-  int* arr = reinterpret_cast<int*>(jsm + k);           // n (even)
-  int* rank = arr + (k + 2);                            // k
+  int* rank = reinterpret_cast<int*>(jsm + k);          // k
   __shared__ int rot;
   const int n = (k + 1) & ~1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  for (int i = tid; i < n; i += blockDim.x) arr[i] = i;
   const double tol = sqrt(double(k)) * 1.1102230246251565e-16;
-  int sweep = 0;
   bool converged = false;
-  __syncthreads();
-  for (; sweep < 60 && !converged; ++sweep) {
+  for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
+    for (int j = warp; j < k; j += nw) {
+      double a = 0.0;
+      for (int r = lane; r < k; r += 32) { const double x = G[int64_t(j) * k + r]; a += x * x; }
+      a = warp_sum(a);
+      if (lane == 0) nrm[j] = a;
+    }
     if (tid == 0) rot = 0;
     __syncthreads();
     for (int round = 0; round < n - 1; ++round) {
       for (int pr = warp; pr < n / 2; pr += nw) {
-        int p = arr[pr], q = arr[n - 1 - pr];
+        const int pa = pr, pb = n - 1 - pr;
+        int p = pa == 0 ? 0 : 1 + (pa - 1 + round) % (n - 1);
+        int q = 1 + (pb - 1 + round) % (n - 1);
         if (p >= k || q >= k) continue;
         if (p > q) { const int t = p; p = q; q = t; }
         double* gp = G + int64_t(p) * k;
         double* gq = G + int64_t(q) * k;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        for (int r = lane; r < k; r += 32) {
-          const double x = gp[r], y = gq[r];
-          al += x * x; be += y * y; ga += x * y;
+        double x[KPL], y[KPL];
+#pragma unroll
+        for (int u = 0; u < KPL; ++u) {
+          const int r = lane + 32 * u;
+          x[u] = r < k ? gp[r] : 0.0;
+          y[u] = r < k ? gq[r] : 0.0;
         }
-        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-        if (fabs(ga) > tol * sqrt(al * be) && ga != 0.0) {
+        double ga = 0.0;
+#pragma unroll
+        for (int u = 0; u < KPL; ++u) ga += x[u] * y[u];
+        ga = warp_sum(ga);
+        const double al = nrm[p], be = nrm[q];
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
           const double zeta = (be - al) / (2.0 * ga);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int r = lane; r < k; r += 32) {
-            const double x = gp[r], y = gq[r];
-            gp[r] = c * x - s * y;
-            gq[r] = s * x + c * y;
+#pragma unroll
+          for (int u = 0; u < KPL; ++u) {
+            const int r = lane + 32 * u;
+            if (r < k) {
+              gp[r] = c * x[u] - s * y[u];
+              gq[r] = s * x[u] + c * y[u];
+            }
           }
-          if (lane == 0) atomicAdd(&rot, 1);
+          if (lane == 0) {
+            nrm[p] = al - t * ga;
+            nrm[q] = be + t * ga;
+            atomicAdd(&rot, 1);
+          }
         }
-      }
-      __syncthreads();
-      // rotate positions 1..n-1 by one (position 0 fixed)
-      if (tid == 0) {
-        const int last = arr[n - 1];
-        for (int i = n - 1; i > 1; --i) arr[i] = arr[i - 1];
-        arr[1] = last;
       }
       __syncthreads();
     }
@@ -149,10 +182,10 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
   if (!converged && tid == 0) set_status(status, SSI_ERR_NUMERIC);
   // singular values = column norms; sort descending (rank by counting, ties by index)
   for (int j = warp; j < k; j += nw) {
-    double s = 0.0;
-    for (int r = lane; r < k; r += 32) s += G[int64_t(j) * k + r] * G[int64_t(j) * k + r];
-    s = warp_sum(s);
-    if (lane == 0) nrm[j] = sqrt(s);
+    double a = 0.0;
+    for (int r = lane; r < k; r += 32) { const double x = G[int64_t(j) * k + r]; a += x * x; }
+    a = warp_sum(a);
+    if (lane == 0) nrm[j] = sqrt(a);
   }
   __syncthreads();
   for (int j = tid; j < k; j += blockDim.x) {
@@ -187,13 +220,15 @@ void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w) {
   w.partial = c.take<double>(cholqr_partial_elems(m, k) + 1);
 }
 
-static size_t chol_smem_bytes(int k) { return (size_t(k) + size_t(k) * (k + 1) / 2) * sizeof(double); }
+static size_t chol_smem_bytes(int k) {
+  return (size_t(k) * (1 + kGroups) + size_t(k) * (k + 1) / 2) * sizeof(double);
+}
 
 ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* gscratch,
                     int32_t* status, cudaStream_t s) {
   const size_t smem_full = chol_smem_bytes(k);
   const bool use_smem = smem_full <= 220 * 1024;
-  const size_t smem = use_smem ? smem_full : size_t(k) * sizeof(double);
+  const size_t smem = use_smem ? smem_full : size_t(k) * (1 + kGroups) * sizeof(double);
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   }
@@ -217,11 +252,23 @@ ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, Ch
   return gemm_f64(m, k, k, 1.0, Operand{w.Q1, 1, m}, Operand{w.Linv2, k, 1}, Q, m, 1, nullptr, s);
 }
 
-ssi_status jacobi_svd(double* G, int k, double* Ut, double* S, int32_t* status, cudaStream_t s) {
-  const size_t smem = size_t(k) * sizeof(double) + size_t(2 * k + 4) * sizeof(int);
+template <int KPL>
+static void jacobi_launch(double* G, int k, double* Ut, double* S, int32_t* status, cudaStream_t s) {
+  const size_t smem = size_t(k) * (sizeof(double) + sizeof(int));
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  jacobi_kernel<<<1, kJacThreads, smem, s>>>(G, k, Ut, S, status);
+    cudaFuncSetAttribute(jacobi_kernel<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  jacobi_kernel<KPL><<<1, kJacThreads, smem, s>>>(G, k, Ut, S, status);
+}
+
+ssi_status jacobi_svd(double* G, int k, double* Ut, double* S, int32_t* status, cudaStream_t s) {
+  if (k <= 64) jacobi_launch<2>(G, k, Ut, S, status, s);
+  else if (k <= 128) jacobi_launch<4>(G, k, Ut, S, status, s);
+  else if (k <= 256) jacobi_launch<8>(G, k, Ut, S, status, s);
+  else if (k <= 512) jacobi_launch<16>(G, k, Ut, S, status, s);
+  else {
+    set_last_error("jacobi_svd: k = %d > 512 unsupported", k);
+    return SSI_ERR_INVALID_ARG;
+  }
   return launch_check("jacobi_kernel");
 }
 
