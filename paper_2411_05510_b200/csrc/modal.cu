@@ -11,6 +11,9 @@
 //   complex back substitution on T for every pole (Im mu > 0, 0 < xi < 1),
 //   Phi = C x, normalization (reading A-15), MPC / MPD (A-16), f / xi (A-1),
 // and writes the poles sorted by (f, xi).
+#include <cstdio>
+#include <cstdlib>
+
 #include "linalg.cuh"
 #include "rsvd.cuh"
 
@@ -21,6 +24,24 @@ constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr double kUlp = 2.220446049250313e-16;
 constexpr double kSafeMin = 2.2250738585072014e-308;
+
+// FP64 reciprocal / rsqrt: hardware approximation refined by Newton steps to full precision
+// (a few ulp), off the IEEE division subroutine on the bulge-chase critical path.
+__device__ __forceinline__ double fast_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = fma(r, fma(-d, r, 1.0), r);
+  r = fma(r, fma(-d, r, 1.0), r);
+  return fma(r, fma(-d, r, 1.0), r);
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double hx = 0.5 * x;
+  r = r * fma(-hx * r, r, 1.5);
+  r = r * fma(-hx * r, r, 1.5);
+  return r * fma(-hx * r, r, 1.5);
+}
 
 __host__ __device__ inline int band_lo(int i) { return i > 3 ? i - 3 : 0; }
 __host__ __device__ inline size_t band_elems(int n) {
@@ -43,6 +64,7 @@ struct EigArgs {
   int l, n_min, n_step, n_orders, n_max, cap;
   double dt;
   ssi_pole_table tab;
+  int profile;          // development: print phase clocks of the largest order
 };
 
 struct Smem {
@@ -128,11 +150,144 @@ __device__ void dlanv2(double& a, double& b, double& c, double& d, double& cs, d
   }
 }
 
+__device__ __forceinline__ bool order_truncated(const EigArgs& g, int n) {
+  // orders above the numerical rank are reported (count = -1), not solved
+  return !(g.S[n - 1] >= 1e-12 * g.S[0]);
+}
+
+__device__ __forceinline__ double* order_A(const EigArgs& g, int o) {
+  return g.M + order_off_sq(g.n_min, g.n_step, o);
+}
+__device__ __forceinline__ double* order_C(const EigArgs& g, int o) {
+  return g.C + int64_t(g.l) * (int64_t(o) * g.n_min + int64_t(g.n_step) * (int64_t(o) * (o - 1) / 2));
+}
+
+// ---------------------------------------------------------------- Householder Hessenberg
+// One CTA (1024 threads) per order: A <- Q_H^T A Q_H in place (global, L2-resident) and
+// C <- U[0:l, :n] Q_H. Left update: warp per column (coalesced, lanes over rows); right update:
+// 4 warps per 32-row block split the columns (coalesced, many loads in flight).
+constexpr int HT = 1024;
+constexpr int HW = HT / 32;
+
+__global__ void __launch_bounds__(HT) hess_order_kernel(EigArgs g) {
+  __shared__ double v[256 + 8];
+  __shared__ double red[HW];
+  __shared__ double part[4][256];
+  __shared__ double sh_tau, sh_scal, sh_beta;
+  const int o = blockIdx.x;
+  const int n = g.n_min + o * g.n_step;
+  if (order_truncated(g, n)) return;
+  const int l = g.l;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* A = order_A(g, o);
+  double* C = order_C(g, o);
+  for (int64_t e = tid; e < int64_t(l) * n; e += HT) {
+    const int64_t a = e % l, c = e / l;
+    C[e] = g.U[a + c * g.ldU];
+  }
+  __syncthreads();
+  for (int j = 0; j + 2 < n; ++j) {
+    const int L = n - j - 1;   // rows j+1..n-1
+    double pt = 0.0;
+    for (int r = j + 2 + tid; r < n; r += HT) { const double t = A[r + int64_t(j) * n]; pt += t * t; }
+    pt = warp_sum(pt);
+    if (lane == 0) red[warp] = pt;
+    __syncthreads();
+    if (tid == 0) {
+      double xn2 = 0.0;
+      for (int w = 0; w < HW; ++w) xn2 += red[w];
+      const double alpha = A[j + 1 + int64_t(j) * n];
+      if (xn2 == 0.0) {
+        sh_tau = 0.0;
+      } else {
+        const double beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        sh_tau = (beta - alpha) / beta;
+        sh_scal = 1.0 / (alpha - beta);
+        sh_beta = beta;
+      }
+    }
+    __syncthreads();
+    const double tau = sh_tau;
+    if (tau == 0.0) continue;
+    {
+      double* col = A + int64_t(j) * n;
+      const double scal = sh_scal;
+      for (int r = tid; r < L; r += HT) {
+        if (r == 0) { v[0] = 1.0; col[j + 1] = sh_beta; }
+        else { v[r] = col[j + 1 + r] * scal; col[j + 1 + r] = 0.0; }
+      }
+    }
+    __syncthreads();
+    // left: columns j+1..n-1, two columns per warp iteration
+    for (int c = j + 1 + 2 * warp; c < n; c += 2 * HW) {
+      const bool two = c + 1 < n;
+      double* c0 = A + int64_t(c) * n + j + 1;
+      double* c1 = c0 + n;
+      double w0 = 0.0, w1 = 0.0;
+      for (int r = lane; r < L; r += 32) {
+        const double vr = v[r];
+        w0 += vr * c0[r];
+        if (two) w1 += vr * c1[r];
+      }
+      w0 = warp_sum(w0) * tau;
+      w1 = warp_sum(w1) * tau;
+      for (int r = lane; r < L; r += 32) {
+        const double vr = v[r];
+        c0[r] -= w0 * vr;
+        if (two) c1[r] -= w1 * vr;
+      }
+    }
+    __syncthreads();
+    // right: rows of A (0..n-1) then rows of C (n..n+l-1); 4 warps share a 32-row block
+    const int q = warp & 3;
+    for (int rb0 = 0; rb0 < n + l; rb0 += (HW / 4) * 32) {   // uniform trip count (barriers)
+      const int rb = rb0 + (warp >> 2) * 32;
+      const int r = rb + lane;
+      const bool valid = r < n + l;
+      double* base = nullptr;
+      int64_t ld = 0;
+      if (valid) {
+        if (r < n) { base = A + r; ld = n; }
+        else { base = C + (r - n); ld = l; }
+      }
+      double w = 0.0;
+      if (valid) {
+#pragma unroll 4
+        for (int c = q; c < L; c += 4) w += base[(j + 1 + c) * ld] * v[c];
+      }
+      part[q][(warp >> 2) * 32 + lane] = w;
+      __syncthreads();
+      if (valid) {
+        const int pi = (warp >> 2) * 32 + lane;
+        const double ws = ((part[0][pi] + part[1][pi]) + (part[2][pi] + part[3][pi])) * tau;
+#pragma unroll 4
+        for (int c = q; c < L; c += 4) base[(j + 1 + c) * ld] -= ws * v[c];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------- Francis QR + vectors
+// One CTA (256 threads) per order. The Hessenberg matrix lives in shared memory with up to
+// three sub-diagonals (room for the bulge); warp 0 chases the bulge alone (warp-synchronous),
+// all threads run the deflation test and apply each sweep's reflectors to C rows.
+__device__ __forceinline__ int band_off(int n, int i) {
+  // offset of row i: rows 0..3 have n entries, row r >= 4 has n - r + 3
+  return i <= 4 ? i * n : 4 * n + (i - 4) * (n + 3) - ((i - 1) * i / 2 - 6);
+}
+struct Band {
+  double* H;
+  int n;
+  __device__ __forceinline__ double& operator()(int i, int c) const {
+    return H[band_off(n, i) + c - band_lo(i)];
+  }
+};
+
 __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   extern __shared__ __align__(16) double dsm[];
-  __shared__ double red[NW];
-  __shared__ double sh_tau, sh_scal, sh_beta, sh_cs, sh_sn, sh_v1, sh_v2;
-  __shared__ int sh_l, sh_fail, sh_nr, sh_ncand;
+  __shared__ double sh_cs, sh_sn;
+  __shared__ int sh_l, sh_fail, sh_ncand;
 
   const int o = blockIdx.x;
   const int n = g.n_min + o * g.n_step;
@@ -140,19 +295,17 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   ssi_pole_table T = g.tab;
   const int cap = T.cap;
+  long long clk0 = clock64(), clk1 = 0, clk2 = 0, qr_its = 0;
 
-  // scalar outputs default to zero for every slot
   for (int sidx = tid; sidx < cap; sidx += NT) {
     const int64_t e = int64_t(o) * cap + sidx;
     T.f[e] = 0.0; T.xi[e] = 0.0; T.mu_re[e] = 0.0; T.mu_im[e] = 0.0; T.mpc[e] = 0.0; T.mpd[e] = 0.0;
   }
-  // orders above the numerical rank are reported, not solved
-  if (!(g.S[n - 1] >= 1e-12 * g.S[0])) {
+  if (order_truncated(g, n)) {
     if (tid == 0) T.count[o] = -1;
     return;
   }
 
-  // ---------------- shared memory carve (sized for n_max on the host)
   Smem s;
   {
     char* p = reinterpret_cast<char*>(dsm);
@@ -168,120 +321,63 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     s.rowoff = reinterpret_cast<int*>(p);    p += sizeof(int) * (nm + 1);
     s.cj = reinterpret_cast<int*>(p);
   }
-  if (tid == 0) {
-    int off = 0;
-    for (int i = 0; i < n; ++i) { s.rowoff[i] = off; off += n - band_lo(i); }
-    s.rowoff[n] = off;
-    sh_fail = 0;
-  }
-
-  double* A = g.M + order_off_sq(g.n_min, g.n_step, o);      // n x n col-major
-  double* C = g.C + int64_t(l) * (int64_t(o) * g.n_min + int64_t(g.n_step) * (int64_t(o) * (o - 1) / 2));
-  // C <- U[0:l, 0:n]
-  for (int64_t e = tid; e < int64_t(l) * n; e += NT) {
-    const int64_t a = e % l, c = e / l;
-    C[e] = g.U[a + c * g.ldU];
-  }
-  __syncthreads();
-
-  // ---------------- Householder Hessenberg reduction, A <- Q^T A Q, C <- C Q
-  for (int j = 0; j + 2 < n; ++j) {
-    const int L = n - j - 1;   // rows j+1..n-1
-    double part = 0.0;
-    for (int r = j + 2 + tid; r < n; r += NT) { const double t = A[r + int64_t(j) * n]; part += t * t; }
-    const double xn2 = block_sum(part, red);
-    if (tid == 0) {
-      const double alpha = A[j + 1 + int64_t(j) * n];
-      if (xn2 == 0.0) {
-        sh_tau = 0.0;
-      } else {
-        const double beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        sh_tau = (beta - alpha) / beta;
-        sh_scal = 1.0 / (alpha - beta);
-        sh_beta = beta;
-      }
-    }
-    __syncthreads();
-    const double tau = sh_tau;
-    if (tau == 0.0) continue;
-    const double scal = sh_scal;
-    for (int r = tid; r < L; r += NT) {
-      double* col = A + int64_t(j) * n;
-      if (r == 0) { s.v[0] = 1.0; col[j + 1] = sh_beta; }
-      else { s.v[r] = col[j + 1 + r] * scal; col[j + 1 + r] = 0.0; }
-    }
-    __syncthreads();
-    // left: columns j+1..n-1
-    for (int c = j + 1 + warp; c < n; c += NW) {
-      double* col = A + int64_t(c) * n + j + 1;
-      double w = 0.0;
-      for (int r = lane; r < L; r += 32) w += s.v[r] * col[r];
-      w = warp_sum(w) * tau;
-      for (int r = lane; r < L; r += 32) col[r] -= w * s.v[r];
-    }
-    __syncthreads();
-    // right: all rows of A, and all rows of C
-    for (int r = tid; r < n + l; r += NT) {
-      double* base;
-      int64_t ld;
-      if (r < n) { base = A + r; ld = n; }
-      else { base = C + (r - n); ld = l; }
-      double w = 0.0;
-      for (int c = 0; c < L; ++c) w += base[(j + 1 + c) * ld] * s.v[c];
-      w *= tau;
-      for (int c = 0; c < L; ++c) base[(j + 1 + c) * ld] -= w * s.v[c];
-    }
-    __syncthreads();
-  }
-
-  // ---------------- banded copy into shared memory
+  const Band H{s.H, n};
+  if (tid == 0) sh_fail = 0;
+  const double* A = order_A(g, o);
+  double* C = order_C(g, o);
   for (int i = 0; i < n; ++i)
-    for (int c = band_lo(i) + tid; c < n; c += NT) Hat(s, i, c) = A[i + int64_t(c) * n];
+    for (int c = band_lo(i) + tid; c < n; c += NT) H(i, c) = A[i + int64_t(c) * n];
   __syncthreads();
+  clk1 = clock64();
 
-  // ---------------- Francis double-shift QR (dlahqr structure, wantt = wantz = true)
   int ihi = n - 1;
   int its = 0, total_its = 0;
   const int itmax = 30 * (n > 10 ? n : 10);
+  long long t_scan = 0, t_chase = 0, t_cupd = 0, t_2x2 = 0, steps = 0;
   while (ihi >= 0) {
-    if (tid == 0) {
-      int ll = ihi;
-      for (; ll > 0; --ll) {
-        const double h = fabs(Hat(s, ll, ll - 1));
-        if (h <= kSafeMin) break;
-        double tst = fabs(Hat(s, ll - 1, ll - 1)) + fabs(Hat(s, ll, ll));
+    long long ta = clock64();
+    // deflation test, in parallel: largest ll in (0, ihi] with a negligible subdiagonal
+    if (tid == 0) sh_l = 0;
+    __syncthreads();
+    for (int ll = ihi - tid; ll > 0; ll -= NT) {
+      const double h = fabs(H(ll, ll - 1));
+      bool small = h <= kSafeMin;
+      if (!small) {
+        double tst = fabs(H(ll - 1, ll - 1)) + fabs(H(ll, ll));
         if (tst == 0.0) {
-          if (ll - 2 >= 0) tst += fabs(Hat(s, ll - 1, ll - 2));
-          if (ll + 1 <= ihi) tst += fabs(Hat(s, ll + 1, ll));
+          if (ll - 2 >= 0) tst += fabs(H(ll - 1, ll - 2));
+          if (ll + 1 <= ihi) tst += fabs(H(ll + 1, ll));
         }
-        if (h <= kUlp * tst) break;
+        small = h <= kUlp * tst;
       }
-      if (ll > 0) Hat(s, ll, ll - 1) = 0.0;
-      sh_l = ll;
+      if (small) { atomicMax(&sh_l, ll); break; }
     }
     __syncthreads();
     const int lo = sh_l;
+    long long tb = clock64();
+    t_scan += tb - ta;
+    if (lo > 0 && tid == 0) H(lo, lo - 1) = 0.0;
     if (lo == ihi) { ihi -= 1; its = 0; __syncthreads(); continue; }
     if (lo == ihi - 1) {
       const int p = ihi - 1, q = ihi;
       if (tid == 0) {
-        double a = Hat(s, p, p), b = Hat(s, p, q), c = Hat(s, q, p), d = Hat(s, q, q), cs, sn;
+        double a = H(p, p), b = H(p, q), c = H(q, p), d = H(q, q), cs, sn;
         dlanv2(a, b, c, d, cs, sn);
-        Hat(s, p, p) = a; Hat(s, p, q) = b; Hat(s, q, p) = c; Hat(s, q, q) = d;
+        H(p, p) = a; H(p, q) = b; H(q, p) = c; H(q, q) = d;
         sh_cs = cs; sh_sn = sn;
       }
       __syncthreads();
       const double cs = sh_cs, sn = sh_sn;
       for (int c = q + 1 + tid; c < n; c += NT) {
-        const double x = Hat(s, p, c), y = Hat(s, q, c);
-        Hat(s, p, c) = cs * x + sn * y;
-        Hat(s, q, c) = cs * y - sn * x;
+        const double x = H(p, c), y = H(q, c);
+        H(p, c) = cs * x + sn * y;
+        H(q, c) = cs * y - sn * x;
       }
       for (int r = tid; r < p + l; r += NT) {
         if (r < p) {
-          const double x = Hat(s, r, p), y = Hat(s, r, q);
-          Hat(s, r, p) = cs * x + sn * y;
-          Hat(s, r, q) = cs * y - sn * x;
+          const double x = H(r, p), y = H(r, q);
+          H(r, p) = cs * x + sn * y;
+          H(r, q) = cs * y - sn * x;
         } else {
           double* cr = C + (r - p);
           const double x = cr[int64_t(p) * l], y = cr[int64_t(q) * l];
@@ -291,6 +387,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       }
       __syncthreads();
       ihi -= 2; its = 0;
+      t_2x2 += clock64() - tb;
       continue;
     }
     ++its; ++total_its;
@@ -299,101 +396,152 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       __syncthreads();
       break;
     }
-    // shifts (exceptional at its == 10, 20) and first column of (H - s1)(H - s2) e_lo
-    if (tid == 0) {
-      double h11, h12, h21, h22;
-      if (its == 10) {
-        const double ex = fabs(Hat(s, lo + 1, lo)) + fabs(Hat(s, lo + 2, lo + 1));
-        h11 = 0.75 * ex + Hat(s, lo, lo); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
-      } else if (its == 20) {
-        const double ex = fabs(Hat(s, ihi, ihi - 1)) + fabs(Hat(s, ihi - 1, ihi - 2));
-        h11 = 0.75 * ex + Hat(s, ihi, ihi); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
-      } else {
-        h11 = Hat(s, ihi - 1, ihi - 1); h12 = Hat(s, ihi - 1, ihi);
-        h21 = Hat(s, ihi, ihi - 1); h22 = Hat(s, ihi, ihi);
+    if (warp == 0) {
+      // ---------------- one double-shift sweep over [lo, ihi], warp-synchronous
+      double x = 0.0, y = 0.0, z = 0.0;
+      {  // every lane computes the shifts: the reflector below is formed redundantly per lane
+        double h11, h12, h21, h22;
+        if (its == 10) {
+          const double ex = fabs(H(lo + 1, lo)) + fabs(H(lo + 2, lo + 1));
+          h11 = 0.75 * ex + H(lo, lo); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
+        } else if (its == 20) {
+          const double ex = fabs(H(ihi, ihi - 1)) + fabs(H(ihi - 1, ihi - 2));
+          h11 = 0.75 * ex + H(ihi, ihi); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
+        } else {
+          h11 = H(ihi - 1, ihi - 1); h12 = H(ihi - 1, ihi);
+          h21 = H(ihi, ihi - 1); h22 = H(ihi, ihi);
+        }
+        const double tr = h11 + h22, det = h11 * h22 - h12 * h21;
+        const double a00 = H(lo, lo), a01 = H(lo, lo + 1), a10 = H(lo + 1, lo), a11 = H(lo + 1, lo + 1);
+        const double a21 = H(lo + 2, lo + 1);
+        x = a00 * a00 + a01 * a10 - tr * a00 + det;
+        y = a10 * (a00 + a11 - tr);
+        z = a10 * a21;
+        const double sc = fabs(x) + fabs(y) + fabs(z);
+        if (sc > 0.0) { x /= sc; y /= sc; z /= sc; }
       }
-      const double tr = h11 + h22, det = h11 * h22 - h12 * h21;
-      const double a00 = Hat(s, lo, lo), a01 = Hat(s, lo, lo + 1);
-      const double a10 = Hat(s, lo + 1, lo), a11 = Hat(s, lo + 1, lo + 1);
-      const double a21 = Hat(s, lo + 2, lo + 1);
-      double x = a00 * a00 + a01 * a10 - tr * a00 + det;
-      double y = a10 * (a00 + a11 - tr);
-      double z = a10 * a21;
-      const double sc = fabs(x) + fabs(y) + fabs(z);
-      if (sc > 0.0) { x /= sc; y /= sc; z /= sc; }
-      s.refl[0] = x; s.refl[1] = y; s.refl[2] = z;   // seed for k = lo
-    }
-    __syncthreads();
-    for (int k = lo; k < ihi; ++k) {
-      if (tid == 0) {
+      for (int k = lo; k < ihi; ++k) {
         const int nr = (ihi - k + 1) < 3 ? (ihi - k + 1) : 3;
-        double x, y, z;
-        if (k == lo) { x = s.refl[0]; y = s.refl[1]; z = s.refl[2]; if (nr < 3) z = 0.0; }
-        else { x = Hat(s, k, k - 1); y = Hat(s, k + 1, k - 1); z = nr == 3 ? Hat(s, k + 2, k - 1) : 0.0; }
-        const double xn = hypot(y, z);
-        double tau = 0.0, v1 = 0.0, v2 = 0.0;
-        if (xn != 0.0) {
-          const double beta = -copysign(hypot(x, xn), x);
-          tau = (beta - x) / beta;
-          const double sc = 1.0 / (x - beta);
-          v1 = y * sc; v2 = z * sc;
-          if (k > lo) {
-            Hat(s, k, k - 1) = beta; Hat(s, k + 1, k - 1) = 0.0;
-            if (nr == 3) Hat(s, k + 2, k - 1) = 0.0;
+        // row pointers: rows k, k+1, k+2 indexed by absolute column
+        double* r0 = s.H + band_off(n, k) - band_lo(k);
+        double* r1 = s.H + band_off(n, k + 1) - band_lo(k + 1);
+        double* r2 = s.H + band_off(n, k + 2) - band_lo(k + 2);
+        // every lane forms the reflector (broadcast smem reads, no shuffles)
+        if (k > lo) { x = r0[k - 1]; y = r1[k - 1]; z = nr == 3 ? r2[k - 1] : 0.0; }
+        else if (nr < 3) { z = 0.0; }
+        double tau = 0.0, v1 = 0.0, v2 = 0.0, beta = 0.0;
+        const double yz = y * y + z * z;
+        if (yz != 0.0) {
+          // beta = -sign(x) sqrt(s); tau = (beta - x)/beta = 1 + |x|/sqrt(s);
+          // v = (y, z)/(x - beta) = sign(x) (y, z)/(|x| + sqrt(s))      (one rsqrt, one rcp)
+          const double ss = x * x + yz;
+          const double rs = fast_rsqrt(ss);
+          const double sq = ss * rs;
+          beta = -copysign(sq, x);
+          tau = fma(fabs(x), rs, 1.0);
+          const double inv = copysign(fast_rcp(fabs(x) + sq), x);
+          v1 = y * inv; v2 = z * inv;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          if (yz != 0.0 && k > lo) {
+            r0[k - 1] = beta; r1[k - 1] = 0.0;
+            if (nr == 3) r2[k - 1] = 0.0;
+          }
+          s.refl[3 * (k - lo) + 0] = v1;
+          s.refl[3 * (k - lo) + 1] = v2;
+          s.refl[3 * (k - lo) + 2] = tau;
+        }
+        if (tau != 0.0) {
+          // (a) left update of the corner columns k..k+nr-1 (shared with the right update)
+          if (lane < nr) {
+            const int c = k + lane;
+            const double b0 = r0[c], b1 = r1[c], b2 = nr == 3 ? r2[c] : 0.0;
+            const double sum = (b0 + v1 * b1 + v2 * b2) * tau;
+            r0[c] = b0 - sum; r1[c] = b1 - sum * v1;
+            if (nr == 3) r2[c] = b2 - sum * v2;
+          }
+          __syncwarp();
+          // (b) disjoint remainder in one pass: left columns k+nr..n-1 (rows k..k+nr-1) and
+          //     right rows 0..min(k+3, ihi) (columns k..k+nr-1)
+          const int rmax = (k + 3 < ihi ? k + 3 : ihi);
+          const int nl = n - (k + nr);
+          const int total = nl + rmax + 1;
+#pragma unroll 2
+          for (int it = lane; it < total; it += 32) {
+            double* p0;
+            int st;                                   // stride between the three elements
+            if (it < nl) {
+              const int c = k + nr + it;
+              p0 = r0 + c;
+              st = 0;
+            } else {
+              const int r = it - nl;
+              p0 = s.H + band_off(n, r) - band_lo(r) + k;
+              st = 1;
+            }
+            double* p1 = st ? p0 + 1 : r1 + (p0 - r0);
+            double* p2 = st ? p0 + 2 : r2 + (p0 - r0);
+            const double b0 = *p0, b1 = *p1, b2 = nr == 3 ? *p2 : 0.0;
+            const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
+            *p0 = b0 - sum; *p1 = fma(-sum, v1, b1);
+            if (nr == 3) *p2 = fma(-sum, v2, b2);
           }
         }
-        sh_tau = tau; sh_v1 = v1; sh_v2 = v2; sh_nr = nr;
-        s.refl[3 * (k - lo) + 0] = v1;   // overwrites the seed only after reading it
-        s.refl[3 * (k - lo) + 1] = v2;
-        s.refl[3 * (k - lo) + 2] = tau;
+        __syncwarp();
       }
-      __syncthreads();
-      const double tau = sh_tau, v1 = sh_v1, v2 = sh_v2;
-      const int nr = sh_nr;
-      if (tau != 0.0) {
-        for (int c = k + tid; c < n; c += NT) {          // left: rows k..k+nr-1
-          double sum = Hat(s, k, c) + v1 * Hat(s, k + 1, c);
-          if (nr == 3) sum += v2 * Hat(s, k + 2, c);
-          sum *= tau;
-          Hat(s, k, c) -= sum;
-          Hat(s, k + 1, c) -= sum * v1;
-          if (nr == 3) Hat(s, k + 2, c) -= sum * v2;
-        }
-        __syncthreads();
-        const int rmax = (k + 3 < ihi ? k + 3 : ihi);
-        for (int r = tid; r <= rmax; r += NT) {          // right: cols k..k+nr-1
-          double sum = Hat(s, r, k) + v1 * Hat(s, r, k + 1);
-          if (nr == 3) sum += v2 * Hat(s, r, k + 2);
-          sum *= tau;
-          Hat(s, r, k) -= sum;
-          Hat(s, r, k + 1) -= sum * v1;
-          if (nr == 3) Hat(s, r, k + 2) -= sum * v2;
-        }
-      }
-      __syncthreads();
     }
-    // deferred C <- C P_lo ... P_{ihi-1}: each row of C streams through the reflectors
+    __syncthreads();
+    long long tc = clock64();
+    t_chase += tc - tb;
+    steps += ihi - lo;
+    // C <- C P_lo ... P_{ihi-1}: each row streams through the sweep's reflectors; the
+    // column k+2 read at step k still holds its pre-sweep value, so it is prefetched.
     for (int r = tid; r < l; r += NT) {
       double* cr = C + r;
       double c0 = cr[int64_t(lo) * l], c1 = cr[int64_t(lo + 1) * l];
-      for (int k = lo; k < ihi; ++k) {
-        const double v1 = s.refl[3 * (k - lo)], v2 = s.refl[3 * (k - lo) + 1];
-        const double tau = s.refl[3 * (k - lo) + 2];
-        const bool three = (k + 2 <= ihi);
-        double c2 = three ? cr[int64_t(k + 2) * l] : 0.0;
-        if (tau != 0.0) {
-          double sum = c0 + v1 * c1 + (three ? v2 * c2 : 0.0);
-          sum *= tau;
-          c0 -= sum; c1 -= sum * v1;
-          if (three) c2 -= sum * v2;
+      constexpr int PF = 8;
+      double pf[PF];
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        const int col = lo + 2 + u;
+        pf[u] = col <= ihi ? cr[int64_t(col) * l] : 0.0;
+      }
+      for (int k0 = lo; k0 < ihi; k0 += PF) {
+        double nx[PF];
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+          const int col = k0 + 2 + PF + u;
+          nx[u] = col <= ihi ? cr[int64_t(col) * l] : 0.0;
         }
-        cr[int64_t(k) * l] = c0;
-        c0 = c1; c1 = c2;
+#pragma unroll
+        for (int u = 0; u < PF; ++u) {
+          const int k = k0 + u;
+          if (k < ihi) {
+            const double v1 = s.refl[3 * (k - lo)], v2 = s.refl[3 * (k - lo) + 1];
+            const double tau = s.refl[3 * (k - lo) + 2];
+            const bool three = (k + 2 <= ihi);
+            double c2 = pf[u];
+            if (tau != 0.0) {
+              double sum = c0 + v1 * c1 + (three ? v2 * c2 : 0.0);
+              sum *= tau;
+              c0 -= sum; c1 -= sum * v1;
+              if (three) c2 -= sum * v2;
+            }
+            cr[int64_t(k) * l] = c0;
+            c0 = c1; c1 = c2;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < PF; ++u) pf[u] = nx[u];
       }
       cr[int64_t(ihi) * l] = c0;
     }
     __syncthreads();
+    t_cupd += clock64() - tc;
   }
+  clk2 = clock64();
+  qr_its = total_its;
   if (sh_fail) {
     if (tid == 0) T.count[o] = -1;
     return;
@@ -403,15 +551,14 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   if (tid == 0) {
     int nc = 0;
     for (int i = 0; i < n;) {
-      if (i + 1 < n && Hat(s, i + 1, i) != 0.0) {
-        const double wr = Hat(s, i, i);
-        const double wi = sqrt(fabs(Hat(s, i, i + 1))) * sqrt(fabs(Hat(s, i + 1, i)));
+      if (i + 1 < n && H(i + 1, i) != 0.0) {
+        const double wr = H(i, i);
+        const double wi = sqrt(fabs(H(i, i + 1))) * sqrt(fabs(H(i + 1, i)));
         // lambda = ln(mu)/dt (principal branch); f = |lambda|/2pi; xi = -Re/|lambda|
         const double lr = log(hypot(wr, wi)) / g.dt, li = atan2(wi, wr) / g.dt;
         const double al = hypot(lr, li);
         const double f = al / (2.0 * 3.141592653589793), xi = -lr / al;
         if (wi > 0.0 && xi > 0.0 && xi < 1.0 && nc < cap) {
-          // insertion by (f, xi)
           int pos = nc;
           while (pos > 0 && (s.cf[pos - 1] > f || (s.cf[pos - 1] == f && s.cxi[pos - 1] > xi))) {
             s.cf[pos] = s.cf[pos - 1]; s.cxi[pos] = s.cxi[pos - 1];
@@ -441,37 +588,36 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     const double smin = fmax(kUlp * hypot(wr, wi), kSafeMin);
     if (lane == 0) {
       xr[j] = 1.0; xim[j] = 0.0;
-      const double b = Hat(s, j, j + 1);
-      xr[j + 1] = (wr - Hat(s, j, j)) / b; xim[j + 1] = wi / b;
+      const double b = H(j, j + 1);
+      xr[j + 1] = (wr - H(j, j)) / b; xim[j + 1] = wi / b;
     }
     __syncwarp();
     int i = j - 1;
     while (i >= 0) {
-      const bool two = (i >= 1) && (Hat(s, i, i - 1) != 0.0);
+      const bool two = (i >= 1) && (H(i, i - 1) != 0.0);
       double r1r = 0.0, r1i = 0.0, r2r = 0.0, r2i = 0.0;
       for (int p = i + 1 + lane; p <= j + 1; p += 32) {
-        const double h = Hat(s, i, p);
+        const double h = H(i, p);
         r2r -= h * xr[p]; r2i -= h * xim[p];
-        if (two) { const double h1 = Hat(s, i - 1, p); r1r -= h1 * xr[p]; r1i -= h1 * xim[p]; }
+        if (two) { const double h1 = H(i - 1, p); r1r -= h1 * xr[p]; r1i -= h1 * xim[p]; }
       }
       r2r = warp_sum(r2r); r2i = warp_sum(r2i);
       if (two) { r1r = warp_sum(r1r); r1i = warp_sum(r1i); }
       if (lane == 0) {
         if (!two) {
-          double dr = Hat(s, i, i) - wr, di = -wi;
+          double dr = H(i, i) - wr, di = -wi;
           if (hypot(dr, di) < smin) { dr = smin; di = 0.0; }
           const double den = dr * dr + di * di;
           xr[i] = (r2r * dr + r2i * di) / den;
           xim[i] = (r2i * dr - r2r * di) / den;
         } else {
           // [[m00, m01], [m10, m11]] [x_{i-1}; x_i] = [r1; r2]
-          const double m00r = Hat(s, i - 1, i - 1) - wr, m00i = -wi, m01 = Hat(s, i - 1, i);
-          const double m10 = Hat(s, i, i - 1), m11r = Hat(s, i, i) - wr, m11i = -wi;
+          const double m00r = H(i - 1, i - 1) - wr, m00i = -wi, m01 = H(i - 1, i);
+          const double m10 = H(i, i - 1), m11r = H(i, i) - wr, m11i = -wi;
           double detr = (m00r * m11r - m00i * m11i) - m01 * m10;
           double deti = (m00r * m11i + m00i * m11r);
           if (hypot(detr, deti) < smin) { detr = smin; deti = 0.0; }
           const double den = detr * detr + deti * deti;
-          // x_{i-1} = (r1 m11 - m01 r2) / det ; x_i = (m00 r2 - m10 r1) / det
           const double n1r = (r1r * m11r - r1i * m11i) - m01 * r2r;
           const double n1i = (r1r * m11i + r1i * m11r) - m01 * r2i;
           const double n2r = (m00r * r2r - m00i * r2i) - m10 * r1r;
@@ -488,11 +634,15 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     double nrm2 = 0.0, best = -1.0;
     int besti = 0;
     for (int a = lane; a < l; a += 32) {
-      double pr = 0.0, pi = 0.0;
-      for (int p = 0; p <= j + 1; ++p) {
-        const double cv = C[a + int64_t(p) * l];
-        pr += cv * xr[p]; pi += cv * xim[p];
+      double pr = 0.0, pi = 0.0, qr = 0.0, qi = 0.0;
+      int p = 0;
+      for (; p + 1 <= j + 1; p += 2) {
+        const double c0 = C[a + int64_t(p) * l], c1 = C[a + int64_t(p + 1) * l];
+        pr += c0 * xr[p]; pi += c0 * xim[p];
+        qr += c1 * xr[p + 1]; qi += c1 * xim[p + 1];
       }
+      if (p <= j + 1) { const double c0 = C[a + int64_t(p) * l]; pr += c0 * xr[p]; pi += c0 * xim[p]; }
+      pr += qr; pi += qi;
       shp[2 * a] = pr; shp[2 * a + 1] = pi;
       const double m2 = pr * pr + pi * pi;
       nrm2 += m2;
@@ -522,6 +672,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     const double th = 0.5 * atan2(2.0 * sxy, sxx - syy);
     const double dx = cos(th), dy = sin(th);
     double wsum = 0.0, dsum = 0.0;
+    __syncwarp();
     for (int a = lane; a < l; a += 32) {
       const double qr = shp[2 * a], qi = shp[2 * a + 1];
       const double dot = qr * dx + qi * dy, crs = qr * dy - qi * dx;
@@ -537,6 +688,9 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       T.mpc[e] = mpc; T.mpd[e] = mpd;
     }
   }
+  if (g.profile && tid == 0 && (o == g.n_orders - 1 || o == g.n_orders / 2))
+    printf("eig order n=%d: band load %lld qr %lld (its %lld) vectors %lld cycles | scan %lld chase %lld (steps %lld) cupd %lld 2x2 %lld\n", n, clk1 - clk0,
+           clk2 - clk1, qr_its, clock64() - clk2, t_scan, t_chase, steps, t_cupd, t_2x2);
 }
 
 }  // namespace
@@ -592,9 +746,11 @@ ssi_status modal_run(const double* U, int64_t ldU, const double* S, int l, int i
                    n_max, splits, w.partial, st));
   // M_n = Rinv[:n,:n] W[:n,:n] for every order
   SSI_TRY(gemm_f64_orders(no, n_min, n_step, w.Rinv, n_max, w.W, n_max, w.M, st));
-  EigArgs g{w.M, w.C, U, ldU, S, l, n_min, n_step, no, n_max, tab.cap, dt, tab};
+  EigArgs g{w.M, w.C, U, ldU, S, l, n_min, n_step, no, n_max, tab.cap, dt, tab, getenv("SSI_EIG_PROFILE") ? 1 : 0};
   const size_t smem = modal_smem_bytes(n_max, tab.cap);
   cudaFuncSetAttribute(eig_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  hess_order_kernel<<<no, HT, 0, st>>>(g);
+  SSI_TRY(launch_check("hess_order_kernel"));
   eig_order_kernel<<<no, NT, smem, st>>>(g);
   return launch_check("eig_order_kernel");
 }
