@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--cov", default=os.environ.get("SSI_COV_MODE", "int8x3"), choices=["fp64", "int8x3"])
     ap.add_argument("--config", default="c3")
     ap.add_argument("--records", type=int, default=2)
+    ap.add_argument("--streams", type=int, default=6, help="records in flight (one engine per stream)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -210,36 +211,34 @@ def main():
         Yh, _ = synth.make_record(synth.config(args.config, seed=cfg.seed + 100 * (rank * args.records + j) if j or rank else cfg.seed))
         host.append(Yh)
     Ys = [torch.from_numpy(h).to(dev) for h in host]
-    eng = drivers.Engine(P, cfg.N, dev)
+    pipe = drivers.RecordPipeline(P, cfg.N, dev, n_streams=args.streams)
+    eng = pipe.engines[0]
     stream = torch.cuda.current_stream()
 
     def step(j, ev=None):
-        Y = Ys[j % len(Ys)]
-        if ev is not None:
-            ev[0].record(stream)
-        R = eng.covariances(Y)
-        if ev is not None:
-            ev[1].record(stream)
-        tab, _ = eng.decompose(R, cfg.i, stream_id=(j << 32) | cfg.i)
+        tab, _ = pipe.submit(Ys[j % len(Ys)], (j << 32) | cfg.i, ev)
         return tab
 
     for j in range(args.warmup):
         step(j)
+    pipe.join()
     torch.cuda.synchronize()
-    for ws in (eng.ws_cov, eng.ws_rsvd, eng.ws_modal):
-        code = api.device_status(ws)
-        if code != 0:
-            raise RuntimeError(f"device status {code} after warm-up")
-    n_launch, _ = count_launches(lambda: step(0))
+    for e in pipe.engines:
+        for ws in (e.ws_cov, e.ws_rsvd, e.ws_modal):
+            code = api.device_status(ws)
+            if code != 0:
+                raise RuntimeError(f"device status {code} after warm-up")
+    n_launch, _ = count_launches(lambda: (step(0), pipe.join()))
 
-    # per-stage breakdown (one extra untimed step, events between stages)
+    # per-stage breakdown (one extra untimed record on one stream, events between stages)
     stage = {}
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     Y = Ys[0]
     evs[0].record(stream); R = eng.covariances(Y); evs[1].record(stream)
     T = api.toeplitz(R, cfg.i, out=eng.T); evs[2].record(stream)
-    U, S = api.rsvd(T, P.k, P.q, P.seed, cfg.i, P.n_max, ws=eng.ws_rsvd); evs[3].record(stream)
-    api.modal_sweep(U, S, P.l, cfg.i, P.n_min, P.n_max, P.n_step, P.dt, ws=eng.ws_modal); evs[4].record(stream)
+    U, S = api.rsvd_into(T, P.k, P.q, P.seed, cfg.i, P.n_max, eng.U, eng.S, ws=eng.ws_rsvd); evs[3].record(stream)
+    api.modal_sweep(U, S, P.l, cfg.i, P.n_min, P.n_max, P.n_step, P.dt, out=eng.table, ws=eng.ws_modal)
+    evs[4].record(stream)
     torch.cuda.synchronize()
     for nm, a, b in (("cov", 0, 1), ("toeplitz", 1, 2), ("rsvd", 2, 3), ("modal", 3, 4)):
         stage[nm] = evs[a].elapsed_time(evs[b])
@@ -256,8 +255,11 @@ def main():
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
+    for st in pipe.streams:
+        st.wait_stream(stream)
     for j in range(args.steps):
         step(j, cov_ev[j])
+    pipe.join(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
@@ -274,23 +276,30 @@ def main():
     # ---------------- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        ns = len(pipe.streams)
         pinned = [torch.from_numpy(h).pin_memory() for h in host[:2]]
-        Yd = torch.empty_like(Ys[0])
-        tab0 = step(0)
-        tab_host = [torch.empty_like(t, device="cpu").pin_memory() for t in tab0.tensors()]
-        d2h = sum(t.numel() * t.element_size() for t in tab_host)
+        Ydev = [torch.empty_like(Ys[0]) for _ in range(ns)]
+        tab_host = [[torch.empty_like(t, device="cpu").pin_memory() for t in e.table.tensors()]
+                    for e in pipe.engines]
+        d2h = sum(t.numel() * t.element_size() for t in tab_host[0])
         h2d = pinned[0].numel() * pinned[0].element_size()
         torch.cuda.synchronize()
         a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
         if world > 1:
             dist.barrier()
         a.record(stream)
+        for st in pipe.streams:
+            st.wait_stream(stream)
         for j in range(args.steps):
-            Yd.copy_(pinned[j % 2], non_blocking=True)
-            R = eng.covariances(Yd)
-            tab, _ = eng.decompose(R, cfg.i, stream_id=(j << 32) | cfg.i)
-            for hst, d in zip(tab_host, tab.tensors()):
-                hst.copy_(d, non_blocking=True)
+            slot = pipe.j % ns
+            st = pipe.streams[slot]
+            with torch.cuda.stream(st):
+                Ydev[slot].copy_(pinned[j % 2], non_blocking=True)       # H2D inside the step
+            tab, _ = pipe.submit(Ydev[slot], (j << 32) | cfg.i)
+            with torch.cuda.stream(st):
+                for hst, d in zip(tab_host[slot], tab.tensors()):      # D2H of the result
+                    hst.copy_(d, non_blocking=True)
+        pipe.join(stream)
         b.record(stream)
         torch.cuda.synchronize()
         ems = a.elapsed_time(b)
@@ -334,7 +343,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_desc(cfg), "cov_mode": args.cov,
-                           "records_rotated": len(Ys),
+                           "records_rotated": len(Ys), "streams": args.streams,
                            "l2": "inputs larger than L2 (276 MB FP32 record + 1.06 GB T per step)",
                            "parallelism": f"records sharded over {world} GPU(s)"},
                 "stage_ms": stage, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

@@ -118,6 +118,21 @@ def rsvd(T: torch.Tensor, k: int, q: int, seed: int, stream_id: int, n_keep: int
     return Ucm.t(), S
 
 
+def rsvd_into(T: torch.Tensor, k: int, q: int, seed: int, stream_id: int, n_keep: int,
+              U: torch.Tensor, S: torch.Tensor, ws: torch.Tensor | None = None, check: bool = False):
+    """rsvd() into caller buffers: U (m, n_keep) column-major view, S [k]."""
+    _require_cuda(T, U, S)
+    m = T.shape[0]
+    if U.stride(0) != 1 or U.shape != (m, n_keep) or S.numel() < k:
+        raise ValueError("U must be an (m, n_keep) column-major view and S hold k values")
+    if ws is None:
+        ws = _workspace(rsvd_ws_bytes(m, k, n_keep), T.device)
+    call("ssi_rsvd", _ptr(T), T.stride(0), m, k, q, C.c_uint64(seed), C.c_uint64(stream_id),
+         n_keep, _ptr(U), U.stride(1), _ptr(S), _ptr(ws), ws.numel(), _stream())
+    _check_device("ssi_rsvd", ws, check)
+    return U, S
+
+
 def philox_words(seed: int, stream_id: int, n_pairs: int, device="cuda") -> torch.Tensor:
     w = torch.empty((n_pairs, 4), dtype=torch.int32, device=device)
     call("ssi_philox_words", C.c_uint64(seed), C.c_uint64(stream_id), n_pairs, _ptr(w), _stream())

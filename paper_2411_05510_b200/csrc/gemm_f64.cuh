@@ -31,3 +31,13 @@ ssi_status gemm_f64_orders(int nb, int n0, int dn, const double* A, int64_t lda,
                            const double* B, int64_t ldb, double* Cbase, cudaStream_t s);
 
 }  // namespace ssi
+
+namespace ssi {
+// Tall-skinny FP64 DMMA GEMM for the RSVD passes (N <= 224): C (M x N, col-major, ldc) =
+// op(A) (M x K) * B (K x N); A row-major (a_rowmajor: A(i,k) = A[i*lda + k]) or col-major
+// (A[i + k*lda]); B col-major (B(k,j) = B[k + j*ldb]). One 64 x 224 tile per CTA, 3-stage
+// cp.async pipeline, split-K over whole waves with a fixed-order reduction.
+ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double* C, int64_t ldc, double* partial, cudaStream_t s);
+size_t gemm_tall_partial_elems(int64_t M, int64_t N, int64_t K);
+}  // namespace ssi

@@ -1,0 +1,195 @@
+// Tall-skinny FP64 DMMA GEMM for the RSVD passes T*Omega, T^T*Q, T*Z (Eqs. 14-15, PAPER.md:
+// 223-231): M = m (11520), N = k (220), K = m. A CTA owns a 64 x 224 tile, so T is streamed
+// from HBM exactly once per pass and X (m x k, 20 MB) is served from L2. 8 warps as 2 (M) x 4
+// (N), warp tile 32 x 56 = 4 x 7 m8n8k4 DMMA tiles; operands staged by cp.async (16 B) in a
+// 3-stage ring; split-K chosen so tiles x splits fill whole waves of the 148 SMs.
+#include <cmath>
+
+#include "gemm_f64.cuh"
+
+namespace ssi {
+namespace {
+
+constexpr int BM = 64, BN = 224, BK = 16, NT = 256, STAGES = 3;
+constexpr int LDK = BK + 4;            // k-contiguous rows (A row-major, B): 20 doubles
+constexpr int LDM = BM + 4;            // m-contiguous rows (A col-major): 68 doubles
+constexpr int A_ELEMS = BM * LDK > BK * LDM ? BM * LDK : BK * LDM;   // 1280
+constexpr int B_ELEMS = BN * LDK;                                     // 4480
+constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+
+__device__ __forceinline__ void cp16(double* dst, const double* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct TallArgs {
+  int64_t M, N, K;
+  const double* A;
+  int64_t lda;
+  const double* B;
+  int64_t ldb;
+  double* out;       // partial base (split z at z * M * N, col-major ld M) or C
+  int64_t ldo;
+  int64_t kchunk;
+};
+
+template <bool AROW>
+__device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_t m0, int64_t k0, int64_t ke) {
+  const int tid = threadIdx.x;
+  double* As = st;
+  double* Bs = st + A_ELEMS;
+  // A: 64 x 16 doubles = 512 16-byte pieces, 2 per thread
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int p = tid + q * NT;
+    if (AROW) {                      // row i: 16 k-contiguous doubles = 8 pieces
+      const int i = p >> 3, kk = (p & 7) * 2;
+      const int64_t gi = m0 + i, gk = k0 + kk;
+      const bool ok = gi < g.M && gk < ke;
+      cp16(As + i * LDK + kk, ok ? g.A + gi * g.lda + gk : g.A, ok);
+    } else {                         // k-row kk: 64 m-contiguous doubles = 32 pieces
+      const int kk = p >> 5, i = (p & 31) * 2;
+      const int64_t gi = m0 + i, gk = k0 + kk;
+      const bool ok = gi < g.M && gk < ke;
+      cp16(As + kk * LDM + i, ok ? g.A + gi + gk * g.lda : g.A, ok);
+    }
+  }
+  // B: 224 columns x 16 k-contiguous doubles = 1792 pieces, 7 per thread
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    const int p = tid + q * NT;
+    const int j = p >> 3, kk = (p & 7) * 2;
+    const int64_t gk = k0 + kk;
+    const bool ok = j < g.N && gk < ke;
+    cp16(Bs + j * LDK + kk, ok ? g.B + gk + int64_t(j) * g.ldb : g.B, ok);
+  }
+}
+
+template <bool AROW>
+__global__ void __launch_bounds__(NT, 1) gemm_tall_kernel(TallArgs g) {
+  extern __shared__ __align__(16) double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 56;
+  const int64_t m0 = int64_t(blockIdx.x) * BM;
+  const int64_t kb = int64_t(blockIdx.y) * g.kchunk;
+  const int64_t ke = kb + g.kchunk < g.K ? kb + g.kchunk : g.K;
+  const int nst = int((ke - kb + BK - 1) / BK);
+
+  double acc[4][7][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 7; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nst) load_stage<AROW>(g, sm + s * STAGE_ELEMS, m0, kb + s * BK, ke);
+    cp_commit();
+  }
+  for (int it = 0; it < nst; ++it) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nx = it + STAGES - 1;
+      if (nx < nst) load_stage<AROW>(g, sm + (nx % STAGES) * STAGE_ELEMS, m0, kb + int64_t(nx) * BK, ke);
+      cp_commit();
+    }
+    const double* As = sm + (it % STAGES) * STAGE_ELEMS;
+    const double* Bs = As + A_ELEMS;
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double af[4], bf[7];
+      const int kq = k4 + (lane & 3), r8 = lane >> 2;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        af[i] = AROW ? As[(wm + 8 * i + r8) * LDK + kq] : As[kq * LDM + wm + 8 * i + r8];
+#pragma unroll
+      for (int j = 0; j < 7; ++j) bf[j] = Bs[(wn + 8 * j + r8) * LDK + kq];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 7; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+  }
+  cp_wait<0>();
+  double* out = g.out + int64_t(blockIdx.y) * g.M * g.N;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 7; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t r = m0 + wm + 8 * i + (lane >> 2);
+        const int64_t c = wn + 8 * j + 2 * (lane & 3) + e;
+        if (r < g.M && c < g.N) out[r + c * g.ldo] = acc[i][j][e];
+      }
+}
+
+__global__ void tall_reduce(int64_t M, int64_t N, int splits, const double* __restrict__ part, double* __restrict__ C,
+                            int64_t ldc) {
+  const int64_t total = M * N;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += part[z * total + e];
+    C[(e % M) + (e / M) * ldc] = s;
+  }
+}
+
+int tall_splits(int64_t M, int64_t K) {
+  const int64_t tiles = (M + BM - 1) / BM;
+  // smallest split count whose tile count is within 3% of a whole number of waves
+  int best = 1;
+  double best_eff = 0.0;
+  for (int s = 1; s <= 16; ++s) {
+    if (K / s < 4 * BK) break;
+    const double units = double(tiles * s);
+    const double waves = units / 148.0;
+    const double eff = waves / std::ceil(waves);
+    if (eff > best_eff + 0.03) { best_eff = eff; best = s; }
+  }
+  return best;
+}
+
+}  // namespace
+
+size_t gemm_tall_partial_elems(int64_t M, int64_t N, int64_t K) {
+  const int s = tall_splits(M, K);
+  return s > 1 ? size_t(s) * size_t(M) * size_t(N) : 0;
+}
+
+ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double* C, int64_t ldc, double* partial, cudaStream_t s) {
+  if (N > BN) {
+    set_last_error("gemm_tall: N = %lld > %d", (long long)N, BN);
+    return SSI_ERR_INVALID_ARG;
+  }
+  const int splits = tall_splits(M, K);
+  int64_t kchunk = (K + splits - 1) / splits;
+  kchunk = (kchunk + BK - 1) / BK * BK;
+  const int z = int((K + kchunk - 1) / kchunk);
+  TallArgs g{M, N, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? M : ldc, kchunk};
+  const size_t smem = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
+  dim3 grid(unsigned((M + BM - 1) / BM), unsigned(z));
+  if (a_rowmajor) {
+    cudaFuncSetAttribute(gemm_tall_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    gemm_tall_kernel<true><<<grid, NT, smem, s>>>(g);
+  } else {
+    cudaFuncSetAttribute(gemm_tall_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    gemm_tall_kernel<false><<<grid, NT, smem, s>>>(g);
+  }
+  SSI_TRY(launch_check("gemm_tall_kernel"));
+  if (z > 1) {
+    const int64_t tot = M * N;
+    int blocks = int((tot + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    tall_reduce<<<blocks, 256, 0, s>>>(M, N, z, partial, C, ldc);
+    SSI_TRY(launch_check("tall_reduce"));
+  }
+  return SSI_OK;
+}
+
+}  // namespace ssi

@@ -8,7 +8,7 @@
 namespace ssi {
 
 struct RsvdWork {
-  double *Omega, *Y, *Q, *Q2, *G, *Ut, *Sk;
+  double *Omega, *Y, *Q, *Q2, *G, *Ut, *Sk, *tall;
   CholQRWork cq;
 };
 
@@ -20,6 +20,7 @@ static void rsvd_carve(Carver& c, int64_t m, int k, RsvdWork& w) {
   w.G = c.take<double>(size_t(k) * k);
   w.Ut = c.take<double>(size_t(k) * k);
   w.Sk = c.take<double>(size_t(k));
+  w.tall = c.take<double>(gemm_tall_partial_elems(m, k, m) + 1);
   cholqr_carve(c, m, k, w.cq);
 }
 
@@ -36,23 +37,30 @@ ssi_status rsvd_run(const double* T, int64_t ldT, int64_t m, int k, int q, uint6
   Carver c(ws);
   RsvdWork w;
   rsvd_carve(c, m, k, w);
+  // dedicated tall-skinny kernel (whole width in one tile; 16-byte cp.async alignment)
+  const bool tall = k <= 224 && m % 2 == 0 && ldT % 2 == 0 && (reinterpret_cast<uintptr_t>(T) & 15) == 0;
   const Operand Tn{T, ldT, 1};   // T(i,j) = T[i*ldT + j]  (row-major, k-contiguous)
   const Operand Tt{T, 1, ldT};   // T^T(i,j) = T[j*ldT + i]
+  // X -> T X (trans = false) or T^T X (trans = true), X and the result m x k col-major
+  auto pass = [&](bool trans, const double* X, double* out) -> ssi_status {
+    if (tall) return gemm_tall(m, k, m, !trans, T, ldT, X, m, out, m, w.tall, s);
+    return gemm_f64(m, k, m, 1.0, trans ? Tt : Tn, Operand{X, 1, m}, out, m, 1, nullptr, s);
+  };
   // line 1: Omega ~ N(0,1), Philox on device (Eq. 14 input; reading A-11)
   SSI_TRY(sketch_launch(int(m), k, seed, sid, w.Omega, m, s));
   // line 2: Y = T Omega (Eq. 14)
-  SSI_TRY(gemm_f64(m, k, m, 1.0, Tn, Operand{w.Omega, 1, m}, w.Y, m, 1, nullptr, s));
+  SSI_TRY(pass(false, w.Omega, w.Y));
   // line 3: Q = qr(Y)
   SSI_TRY(cholqr2(w.Y, m, m, k, w.Q, w.cq, status, s));
   // power iterations: Z = qr(T^T Q); Q = qr(T Z)
   for (int it = 0; it < q; ++it) {
-    SSI_TRY(gemm_f64(m, k, m, 1.0, Tt, Operand{w.Q, 1, m}, w.Y, m, 1, nullptr, s));
+    SSI_TRY(pass(true, w.Q, w.Y));
     SSI_TRY(cholqr2(w.Y, m, m, k, w.Q2, w.cq, status, s));
-    SSI_TRY(gemm_f64(m, k, m, 1.0, Tn, Operand{w.Q2, 1, m}, w.Y, m, 1, nullptr, s));
+    SSI_TRY(pass(false, w.Q2, w.Y));
     SSI_TRY(cholqr2(w.Y, m, m, k, w.Q, w.cq, status, s));
   }
   // line 4: B = Q^T T, formed as B^T = T^T Q (m x k) (Eq. 15)
-  SSI_TRY(gemm_f64(m, k, m, 1.0, Tt, Operand{w.Q, 1, m}, w.Y, m, 1, nullptr, s));
+  SSI_TRY(pass(true, w.Q, w.Y));
   // line 5: B^T = Qb Rb (CholeskyQR2) -> B = Rb^T Qb^T; SVD(Rb^T) = U~ Sigma W^T
   SSI_TRY(cholqr2(w.Y, m, m, k, w.Q2, w.cq, status, s));
   // Rb^T = (L2^T L1^T)^T = L1 L2

@@ -55,6 +55,9 @@ class Engine:
         d64 = dict(dtype=torch.float64, device=self.dev)
         self.R = torch.empty((self.lag_hi, P.l, P.l), **d64)
         self.T = torch.empty((P.m, P.m), **d64)
+        self.U = torch.empty((P.n_max, P.m), **d64).t()          # column-major m x n_max
+        self.S = torch.empty(P.k, **d64)
+        self.table = api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, self.dev)
         self.ws_cov = api._workspace(api.covariances_ws_bytes(N, P.l, self.lag_hi, 1, P.cov_mode), self.dev)
         self.ws_rsvd = api._workspace(api.rsvd_ws_bytes(P.m, P.k, P.n_max), self.dev)
         self.ws_modal = api._workspace(
@@ -68,7 +71,14 @@ class Engine:
         P = self.P
         i = i or P.i
         m = P.l * i
-        T = api.toeplitz(R, i, out=self.T[:m * m].view(m, m) if i != P.i else self.T)
+        if i == P.i:
+            T, U, S = self.T, self.U, self.S
+            api.toeplitz(R, i, out=T)
+            api.rsvd_into(T, P.k, P.q, P.seed, stream_id, P.n_max, U, S, ws=self.ws_rsvd)
+            tab = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, out=self.table,
+                                  ws=self.ws_modal)
+            return tab, (U, S)
+        T = api.toeplitz(R, i, out=self.T.view(-1)[:m * m].view(m, m))
         U, S = api.rsvd(T, P.k, P.q, P.seed, stream_id, P.n_max, ws=self.ws_rsvd)
         return api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=self.ws_modal), (U, S)
 
@@ -81,6 +91,38 @@ class Engine:
 
 def identify_record(Y: torch.Tensor, P: SweepParams, stream_id: int = 0) -> api.PoleTable:
     return Engine(P, Y.shape[0], Y.device).identify(Y, stream_id)
+
+
+class RecordPipeline:
+    """Continuous-monitoring batch: records go round-robin to n_streams
+    engines, each on its own CUDA stream, so one record's latency-bound kernels (Cholesky,
+    Jacobi, per-order eigen-solves) overlap the tensor-core work of the next ones.
+    submit() returns the engine's pole table, valid once that stream passes the record; an
+    engine's table is reused n_streams submissions later."""
+
+    def __init__(self, P: SweepParams, N: int, device="cuda", n_streams: int = 3):
+        self.engines = [Engine(P, N, device) for _ in range(n_streams)]
+        self.streams = [torch.cuda.Stream(device=device) for _ in range(n_streams)]
+        self.j = 0
+
+    def submit(self, Y: torch.Tensor, stream_id: int, events=None):
+        e = self.engines[self.j % len(self.engines)]
+        st = self.streams[self.j % len(self.streams)]
+        self.j += 1
+        with torch.cuda.stream(st):
+            if events is not None:
+                events[0].record(st)
+            R = e.covariances(Y)
+            if events is not None:
+                events[1].record(st)
+            tab, _ = e.decompose(R, e.P.i, stream_id)
+        return tab, st
+
+    def join(self, stream=None):
+        """Make `stream` (default: current) wait for all pipeline streams."""
+        cur = stream or torch.cuda.current_stream()
+        for st in self.streams:
+            cur.wait_stream(st)
 
 
 # ------------------------------------------------------------------ multi-GPU host logic
