@@ -169,52 +169,72 @@ def sharded_covariances(Y: torch.Tensor, lag_hi: int, rank: int, world: int, mod
 
 
 def record_assignment(n_records: int, world: int):
+    """Records are independent: round-robin over ranks."""
     return [list(range(r, n_records, world)) for r in range(world)]
 
 
-def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank=0, world=1,
+def gather_tables(local: dict, assignment, make_empty, rank: int, world: int, group=None) -> dict:
+    """All ranks receive every pole table: table key -> owner from `assignment` (a list of key
+    lists, one per rank); the owner broadcasts its fixed-size tensors (the sweep's/batch's
+    second and last collective). make_empty() allocates a receive table of the same shape."""
+    if world == 1:
+        return dict(local)
+    import torch.distributed as dist
+    out = {}
+    for r, keys in enumerate(assignment):
+        for key in keys:
+            t = local[key] if r == rank else make_empty()
+            for x in t.tensors():
+                dist.broadcast(x, src=r, group=group)
+            out[key] = t
+    return out
+
+
+def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank: int = 0, world: int = 1,
                  group=None):
-    """3D stabilization diagram: covariances once to lag 2 max(i) - 1
-    (time-sharded), RSVD + modal sweep per lag (LPT-sharded), all-gather, stab3d."""
-    lag_hi = 2 * max(lags) - 1
+    """3D stabilization diagram (steps i-ii) for the time-lag steps `lags`:
+    covariances once up to lag 2 max(i) - 1 (time-sharded over ranks + one all-reduce),
+    Toeplitz + RSVD + modal sweep per lag (lags assigned by LPT), all tables gathered,
+    ssi_stab3d over the lag axis. Returns ({i: PoleTable}, flags, stable_count)."""
+    lags = sorted(lags)
+    lag_hi = 2 * lags[-1] - 1
     R = sharded_covariances(Y, lag_hi, rank, world, P.cov_mode, group)
-    mine = lpt_assign(lags, world)[rank]
-    eng = Engine(P, Y.shape[0], Y.device, lag_hi=lag_hi)
-    eng.T = torch.empty((P.l * max(lags), P.l * max(lags)), dtype=torch.float64, device=Y.device)
-    tables = {}
-    for i in mine:
-        Pi = SweepParams(**{**P.__dict__, "i": i})
-        e2 = Engine.__new__(Engine)
-        e2.__dict__.update(eng.__dict__)
-        e2.P = Pi
-        e2.ws_rsvd = api._workspace(api.rsvd_ws_bytes(Pi.m, Pi.k, Pi.n_max), Y.device)
-        e2.ws_modal = api._workspace(api.modal_sweep_ws_bytes(Pi.l, i, Pi.n_min, Pi.n_max, Pi.n_step), Y.device)
-        m = Pi.m
-        T = api.toeplitz(R, i, out=eng.T.view(-1)[:m * m].view(m, m))
-        U, S = api.rsvd(T, Pi.k, Pi.q, Pi.seed, i, Pi.n_max, ws=e2.ws_rsvd)
-        tables[i] = api.modal_sweep(U, S, Pi.l, i, Pi.n_min, Pi.n_max, Pi.n_step, Pi.dt, ws=e2.ws_modal)
-    tables = gather_tables(tables, lags, rank, world, group)
-    flags, counts = api.stab3d([tables[i] for i in sorted(lags)], crit)
+    assign = lpt_assign(lags, world)
+    dev = Y.device
+    m_max = P.l * lags[-1]
+    Tbuf = torch.empty(m_max * m_max, dtype=torch.float64, device=dev)
+    ws_rsvd = api._workspace(api.rsvd_ws_bytes(m_max, P.k, P.n_max), dev)
+    ws_modal = api._workspace(max(api.modal_sweep_ws_bytes(P.l, i, P.n_min, P.n_max, P.n_step) for i in lags), dev)
+    local = {}
+    for i in assign[rank]:
+        m = P.l * i
+        T = api.toeplitz(R, i, out=Tbuf[:m * m].view(m, m))
+        U, S = api.rsvd(T, P.k, P.q, P.seed, i, P.n_max, ws=ws_rsvd)
+        local[i] = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=ws_modal)
+    tables = gather_tables(local, assign, lambda: api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, dev),
+                           rank, world, group)
+    flags, counts = api.stab3d([tables[i] for i in lags], crit)
     return tables, flags, counts
 
 
-def gather_tables(local: dict, keys, rank: int, world: int, group=None) -> dict:
-    """All-gather of fixed-size pole tables (the sweep's second collective)."""
-    if world == 1:
+def record_batch(records, P: SweepParams, rank: int = 0, world: int = 1, n_streams: int = 3, group=None,
+                 gather: bool = True):
+    """Continuous monitoring: records (a list of device tensors, or a
+    callable j -> device tensor) processed on this rank by a RecordPipeline; tables gathered
+    on every rank when `gather`. No data-path collective (records are independent)."""
+    n = len(records) if not callable(records) else records.n
+    assign = record_assignment(n, world)
+    fetch = records if callable(records) else (lambda j: records[j])
+    first = fetch(assign[rank][0]) if assign[rank] else fetch(0)
+    pipe = RecordPipeline(P, first.shape[0], first.device, n_streams)
+    local = {}
+    for j in assign[rank]:
+        tab, st = pipe.submit(fetch(j), (j << 32) | P.i)
+        with torch.cuda.stream(st):
+            local[j] = api.PoleTable(tab.n_min, tab.n_step, tab.l, tab.cap, *[t.clone() for t in tab.tensors()])
+    pipe.join()
+    torch.cuda.current_stream().synchronize()
+    if not gather:
         return local
-    import torch.distributed as dist
-    owner = {}
-    for r, ks in enumerate(lpt_assign(keys, world) if isinstance(keys, list) else keys):
-        for k in ks:
-            owner[k] = r
-    ref = next(iter(local.values())) if local else None
-    out = {}
-    for k in sorted(owner):
-        src = owner[k]
-        t = local.get(k) if src == rank else api.PoleTable.empty(
-            ref.n_min, ref.n_min + (ref.n_orders - 1) * ref.n_step, ref.n_step, ref.l,
-            ref.count.device, ref.cap)
-        for x in t.tensors():
-            dist.broadcast(x, src=src, group=group)
-        out[k] = t
-    return out
+    return gather_tables(local, assign, lambda: api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, first.device),
+                         rank, world, group)
