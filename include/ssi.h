@@ -120,6 +120,8 @@ SSI_API ssi_status ssi_rsvd(const double* T, int64_t ldT, int32_t m, int32_t k, 
                     uint64_t seed, uint64_t stream_id, int32_t n_keep,
                     double* U, int64_t ldU, double* S, void* ws, size_t ws_bytes,
                     void* stream);
+/* Workspace bytes of ssi_rsvd; pure host function. The size is non-decreasing in m, so a
+ * workspace sized for the largest m of a lag sweep serves every smaller lag. */
 SSI_API ssi_status ssi_rsvd_ws(int32_t m, int32_t k, int32_t n_keep, size_t* bytes);
 
 /* Raw Philox words and the Gaussian sketch, exposed for bit-exact verification

@@ -40,4 +40,6 @@ namespace ssi {
 ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
                      const double* B, int64_t ldb, double* C, int64_t ldc, double* partial, cudaStream_t s);
 size_t gemm_tall_partial_elems(int64_t M, int64_t N, int64_t K);
+// max of gemm_tall_partial_elems(m, N, m) over m <= M (workspace for every smaller square size)
+size_t gemm_tall_partial_elems_upto(int64_t M, int64_t N);
 }  // namespace ssi

@@ -161,6 +161,17 @@ size_t gemm_tall_partial_elems(int64_t M, int64_t N, int64_t K) {
   return s > 1 ? size_t(s) * size_t(M) * size_t(N) : 0;
 }
 
+size_t gemm_tall_partial_elems_upto(int64_t M, int64_t N) {
+  // the split count is not monotone in M: take the maximum over every square size <= M so a
+  // workspace sized for the largest lag of a sweep serves every smaller one
+  size_t best = 0;
+  for (int64_t m = 1; m <= M; ++m) {
+    const size_t e = gemm_tall_partial_elems(m, N, m);
+    if (e > best) best = e;
+  }
+  return best;
+}
+
 ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
                      const double* B, int64_t ldb, double* C, int64_t ldc, double* partial, cudaStream_t s) {
   if (N > BN) {

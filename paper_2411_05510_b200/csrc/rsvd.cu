@@ -20,7 +20,7 @@ static void rsvd_carve(Carver& c, int64_t m, int k, RsvdWork& w) {
   w.G = c.take<double>(size_t(k) * k);
   w.Ut = c.take<double>(size_t(k) * k);
   w.Sk = c.take<double>(size_t(k));
-  w.tall = c.take<double>(gemm_tall_partial_elems(m, k, m) + 1);
+  w.tall = c.take<double>(gemm_tall_partial_elems_upto(m, k) + 1);
   cholqr_carve(c, m, k, w.cq);
 }
 

@@ -81,3 +81,13 @@ def test_oracle_is_not_imported_by_the_product():
             if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower().replace("no oracle", ""), f
+
+
+def test_rsvd_workspace_is_monotone_in_m(lib):
+    """A workspace sized for the largest lag of a sweep (c4: i = 20..80) serves every lag."""
+    b = C.c_size_t(0)
+    prev = 0
+    for i in range(20, 81):
+        assert lib.ssi_rsvd_ws(192 * i, 220, 200, C.byref(b)) == 0
+        assert b.value >= prev, i
+        prev = b.value
