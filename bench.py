@@ -36,6 +36,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cov", default=os.environ.get("SSI_COV_MODE", "int8x3"), choices=["fp64", "int8x3"])
+    ap.add_argument("--explicit-t", action="store_true",
+                    help="materialize T (A2) and stream it through the RSVD GEMMs instead of "
+                         "applying it through its block structure")
     ap.add_argument("--config", default="c3")
     ap.add_argument("--records", type=int, default=2)
     ap.add_argument("--streams", type=int, default=6, help="records in flight (one engine per stream)")
@@ -204,7 +207,8 @@ def main():
 
     cfg = synth.config(args.config)
     P = drivers.SweepParams(l=cfg.l, i=cfg.i, n_max=cfg.n_max, p=cfg.p, q=cfg.q, fs=cfg.fs,
-                            n_min=cfg.n_min, n_step=cfg.n_step, seed=cfg.philox_key, cov_mode=args.cov)
+                            n_min=cfg.n_min, n_step=cfg.n_step, seed=cfg.philox_key, cov_mode=args.cov,
+                            structured=not args.explicit_t)
     # distinct records per rank (weak scaling): record index = rank * R + j
     host = []
     for j in range(args.records):
@@ -235,8 +239,13 @@ def main():
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     Y = Ys[0]
     evs[0].record(stream); R = eng.covariances(Y); evs[1].record(stream)
-    T = api.toeplitz(R, cfg.i, out=eng.T); evs[2].record(stream)
-    U, S = api.rsvd_into(T, P.k, P.q, P.seed, cfg.i, P.n_max, eng.U, eng.S, ws=eng.ws_rsvd); evs[3].record(stream)
+    if P.structured:
+        evs[2].record(stream)
+        U, S = api.rsvd_toeplitz(R, cfg.i, P.k, P.q, P.seed, cfg.i, P.n_max, U=eng.U, S=eng.S, ws=eng.ws_rsvd)
+    else:
+        T = api.toeplitz(R, cfg.i, out=eng.T); evs[2].record(stream)
+        U, S = api.rsvd_into(T, P.k, P.q, P.seed, cfg.i, P.n_max, eng.U, eng.S, ws=eng.ws_rsvd)
+    evs[3].record(stream)
     api.modal_sweep(U, S, P.l, cfg.i, P.n_min, P.n_max, P.n_step, P.dt, out=eng.table, ws=eng.ws_modal)
     evs[4].record(stream)
     torch.cuda.synchronize()
@@ -364,7 +373,9 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": {"workload": workload_desc(cfg), "cov_mode": args.cov,
                            "records_rotated": len(Ys), "streams": args.streams,
-                           "l2": "inputs larger than L2 (276 MB FP32 record + 1.06 GB T per step)",
+                           "toeplitz": ("explicit T (1.06 GB) streamed by the RSVD GEMMs" if args.explicit_t else
+                                        "T applied through its block structure (block DFT, T never formed)"),
+                           "l2": "inputs larger than L2 (276 MB FP32 record per step, 2 records rotated)",
                            "parallelism": f"records sharded over {world} GPU(s)"},
                 "stage_ms": stage, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": n_launch * args.steps, "clocks": clocks}

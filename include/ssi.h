@@ -124,6 +124,24 @@ SSI_API ssi_status ssi_rsvd(const double* T, int64_t ldT, int32_t m, int32_t k, 
  * workspace sized for the largest m of a lag sweep serves every smaller lag. */
 SSI_API ssi_status ssi_rsvd_ws(int32_t m, int32_t k, int32_t n_keep, size_t* bytes);
 
+/* ------------------------------------------------------------------------------
+ * A2-A8 without forming T: the same randomized SVD (same Omega, same steps and outputs as
+ * ssi_rsvd on T = ssi_toeplitz(R, l, i)), with every product T X / T^T X applied through
+ * the block structure of Eq. (6): (T X)_r = sum_c R_{i+r-c} X_c is a
+ * block convolution, evaluated exactly as a length-(2i-1) block DFT, i complex (l x l)(l x k)
+ * products per pass on the FP64 tensor cores, and the inverse DFT (north star (b): "exploit
+ * its block-Toeplitz structure"). Results equal ssi_rsvd's up to FP64 rounding order.
+ *  R : [>= 2i-1][l][l] row-major FP64, R_k at block k-1 (ssi_covariances, lag_lo = 1).
+ *  m = l*i; k, q, seed, stream_id, n_keep, U, ldU, S as in ssi_rsvd.
+ *  Errors: as ssi_rsvd; i < 1 or l < 1 -> INVALID_ARG.
+ * ---------------------------------------------------------------------------- */
+SSI_API ssi_status ssi_rsvd_toeplitz(const double* R, int32_t l, int32_t i, int32_t k, int32_t q,
+                             uint64_t seed, uint64_t stream_id, int32_t n_keep,
+                             double* U, int64_t ldU, double* S, void* ws, size_t ws_bytes,
+                             void* stream);
+/* Workspace bytes of ssi_rsvd_toeplitz; pure host function, non-decreasing in i. */
+SSI_API ssi_status ssi_rsvd_toeplitz_ws(int32_t l, int32_t i, int32_t k, int32_t n_keep, size_t* bytes);
+
 /* Raw Philox words and the Gaussian sketch, exposed for bit-exact verification
  * (P13). words: [n_pairs][4] uint32 for pairs 0..n_pairs-1; omega: m x k col-major. */
 SSI_API ssi_status ssi_philox_words(uint64_t seed, uint64_t stream_id, int64_t n_pairs,

@@ -35,6 +35,8 @@ SIGNATURES = {
     "ssi_toeplitz": (I32, [P, I32, I32, P, I64, P]),
     "ssi_rsvd": (I32, [P, I64, I32, I32, I32, U64, U64, I32, P, I64, P, P, SZ, P]),
     "ssi_rsvd_ws": (I32, [I32, I32, I32, C.POINTER(SZ)]),
+    "ssi_rsvd_toeplitz": (I32, [P, I32, I32, I32, I32, U64, U64, I32, P, I64, P, P, SZ, P]),
+    "ssi_rsvd_toeplitz_ws": (I32, [I32, I32, I32, I32, C.POINTER(SZ)]),
     "ssi_philox_words": (I32, [U64, U64, I64, P, P]),
     "ssi_gaussian_sketch": (I32, [I32, I32, U64, U64, P, I64, P]),
     "ssi_modal_sweep": (I32, [P, I64, P, I32, I32, I32, I32, I32, D, C.POINTER(PoleTableC), P, SZ, P]),

@@ -6,6 +6,7 @@ runs in the library's sm_100a kernels. Functions mirror the C entry points:
     covariances(Y, lag_hi, ...)      -> R [L][l][l] FP64            (A1, PAPER.md:126)
     toeplitz(R, i)                   -> T [m][m] FP64 row-major     (A2, Eq. 6)
     rsvd(T, k, q, seed, stream_id)   -> U [m][n_keep] (col-major), S [k]   (A3-A8, Alg. 1)
+    rsvd_toeplitz(R, l, i, k, ...)   -> same RSVD, T applied through its block structure (A2-A8)
     modal_sweep(U, S, l, i, ...)     -> PoleTable                   (A9-A11, Eqs. 9-12)
     stab3d(tables, criteria)         -> flags, stable_count         (A13)
 """
@@ -130,6 +131,38 @@ def rsvd_into(T: torch.Tensor, k: int, q: int, seed: int, stream_id: int, n_keep
     call("ssi_rsvd", _ptr(T), T.stride(0), m, k, q, C.c_uint64(seed), C.c_uint64(stream_id),
          n_keep, _ptr(U), U.stride(1), _ptr(S), _ptr(ws), ws.numel(), _stream())
     _check_device("ssi_rsvd", ws, check)
+    return U, S
+
+
+def rsvd_toeplitz_ws_bytes(l, i, k, n_keep) -> int:
+    b = C.c_size_t(0)
+    call("ssi_rsvd_toeplitz_ws", l, i, k, n_keep, C.byref(b))
+    return b.value
+
+
+def rsvd_toeplitz(R: torch.Tensor, i: int, k: int, q: int, seed: int, stream_id: int,
+                  n_keep: int | None = None, U: torch.Tensor | None = None, S: torch.Tensor | None = None,
+                  ws: torch.Tensor | None = None, check: bool = False):
+    """RSVD of the block-Toeplitz T of R (lags 1..2i-1) without forming T. Returns (U, S) as
+    rsvd(toeplitz(R, i), ...) does: U an (m, n_keep) column-major view, S [k]."""
+    _require_cuda(R)
+    if R.dtype != torch.float64 or not R.is_contiguous() or R.dim() != 3 or R.shape[0] < 2 * i - 1:
+        raise ValueError("R must be contiguous FP64 [>= 2i-1][l][l]")
+    l = R.shape[1]
+    m = l * i
+    n_keep = k if n_keep is None else n_keep
+    if U is None:
+        U = torch.empty((n_keep, m), dtype=torch.float64, device=R.device).t()
+    if S is None:
+        S = torch.empty(k, dtype=torch.float64, device=R.device)
+    _require_cuda(U, S)
+    if U.stride(0) != 1 or U.shape != (m, n_keep) or S.numel() < k:
+        raise ValueError("U must be an (m, n_keep) column-major view and S hold k values")
+    if ws is None:
+        ws = _workspace(rsvd_toeplitz_ws_bytes(l, i, k, n_keep), R.device)
+    call("ssi_rsvd_toeplitz", _ptr(R), l, i, k, q, C.c_uint64(seed), C.c_uint64(stream_id), n_keep,
+         _ptr(U), U.stride(1), _ptr(S), _ptr(ws), ws.numel(), _stream())
+    _check_device("ssi_rsvd_toeplitz", ws, check)
     return U, S
 
 

@@ -154,6 +154,33 @@ ssi_status ssi_rsvd(const double* T, int64_t ldT, int32_t m, int32_t k, int32_t 
                   static_cast<int32_t*>(ws), s);
 }
 
+ssi_status ssi_rsvd_toeplitz_ws(int32_t l, int32_t i, int32_t k, int32_t n_keep, size_t* bytes) {
+  SSI_REQUIRE(bytes, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz_ws: NULL bytes");
+  SSI_REQUIRE(l > 0 && i > 0 && k >= 1 && int64_t(k) <= int64_t(l) * i && n_keep >= 1 && n_keep <= k,
+              SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz_ws: bad sizes");
+  *bytes = rsvd_bt_ws_bytes(l, i, k);
+  return SSI_OK;
+}
+
+ssi_status ssi_rsvd_toeplitz(const double* R, int32_t l, int32_t i, int32_t k, int32_t q, uint64_t seed,
+                             uint64_t stream_id, int32_t n_keep, double* U, int64_t ldU, double* S_,
+                             void* ws, size_t ws_bytes, void* stream) {
+  SSI_REQUIRE(R && U && S_ && ws, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: NULL pointer");
+  SSI_REQUIRE(l > 0 && i > 0, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: l and i must be positive");
+  const int64_t m = int64_t(l) * i;
+  SSI_REQUIRE(m <= INT32_MAX, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: l*i too large");
+  SSI_REQUIRE(k >= 1 && k <= m, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: need 1 <= k <= l*i");
+  SSI_REQUIRE(n_keep >= 1 && n_keep <= k, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: need 1 <= n_keep <= k");
+  SSI_REQUIRE(q >= 0, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: q < 0");
+  SSI_REQUIRE(ldU >= m, SSI_ERR_SHAPE, "ssi_rsvd_toeplitz: ldU < l*i");
+  const size_t need = rsvd_bt_ws_bytes(l, i, k);
+  SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_rsvd_toeplitz: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = S(stream);
+  SSI_TRY(reset_status(ws, s));
+  return rsvd_bt_run(R, l, i, k, q, seed, stream_id, n_keep, U, ldU, S_, ws,
+                     static_cast<int32_t*>(ws), s);
+}
+
 ssi_status ssi_philox_words(uint64_t seed, uint64_t stream_id, int64_t n_pairs, uint32_t* words,
                             void* stream) {
   SSI_REQUIRE(words && n_pairs > 0, SSI_ERR_INVALID_ARG, "ssi_philox_words: bad arguments");

@@ -40,6 +40,12 @@ namespace ssi {
 ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
                      const double* B, int64_t ldb, double* C, int64_t ldc, double* partial, cudaStream_t s);
 size_t gemm_tall_partial_elems(int64_t M, int64_t N, int64_t K);
+constexpr int kTallMaxN = 224;
+// Batched form without split-K: for b in [0, batch), C_b = op(A_b) B_b with
+// A_b = A + b*sA, B_b = B + b*sB, C_b = C + b*sC (N <= kTallMaxN; lda, ldb even).
+ssi_status gemm_tall_batched(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
+                             int64_t sA, const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
+                             int64_t sC, int batch, cudaStream_t s);
 // max of gemm_tall_partial_elems(m, N, m) over m <= M (workspace for every smaller square size)
 size_t gemm_tall_partial_elems_upto(int64_t M, int64_t N);
 }  // namespace ssi

@@ -35,6 +35,7 @@ struct TallArgs {
   double* out;       // partial base (split z at z * M * N, col-major ld M) or C
   int64_t ldo;
   int64_t kchunk;
+  int64_t sA, sB, sO;   // batch strides (blockIdx.z); 0 when unbatched
 };
 
 template <bool AROW>
@@ -72,6 +73,11 @@ __device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_
 template <bool AROW>
 __global__ void __launch_bounds__(NT, 1) gemm_tall_kernel(TallArgs g) {
   extern __shared__ __align__(16) double sm[];
+  if (blockIdx.z) {
+    g.A += int64_t(blockIdx.z) * g.sA;
+    g.B += int64_t(blockIdx.z) * g.sB;
+    g.out += int64_t(blockIdx.z) * g.sO;
+  }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 56;
   const int64_t m0 = int64_t(blockIdx.x) * BM;
@@ -182,7 +188,7 @@ ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const dou
   int64_t kchunk = (K + splits - 1) / splits;
   kchunk = (kchunk + BK - 1) / BK * BK;
   const int z = int((K + kchunk - 1) / kchunk);
-  TallArgs g{M, N, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? M : ldc, kchunk};
+  TallArgs g{M, N, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? M : ldc, kchunk, 0, 0, 0};
   const size_t smem = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
   dim3 grid(unsigned((M + BM - 1) / BM), unsigned(z));
   if (a_rowmajor) {
@@ -201,6 +207,27 @@ ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const dou
     SSI_TRY(launch_check("tall_reduce"));
   }
   return SSI_OK;
+}
+
+ssi_status gemm_tall_batched(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
+                             int64_t sA, const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
+                             int64_t sC, int batch, cudaStream_t s) {
+  if (N > BN || batch < 1 || batch > 65535) {
+    set_last_error("gemm_tall_batched: N = %lld > %d or bad batch %d", (long long)N, BN, batch);
+    return SSI_ERR_INVALID_ARG;
+  }
+  const int64_t kchunk = (K + BK - 1) / BK * BK;
+  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, sA, sB, sC};
+  const size_t smem = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
+  dim3 grid(unsigned((M + BM - 1) / BM), 1u, unsigned(batch));
+  if (a_rowmajor) {
+    cudaFuncSetAttribute(gemm_tall_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    gemm_tall_kernel<true><<<grid, NT, smem, s>>>(g);
+  } else {
+    cudaFuncSetAttribute(gemm_tall_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    gemm_tall_kernel<false><<<grid, NT, smem, s>>>(g);
+  }
+  return launch_check("gemm_tall_kernel (batched)");
 }
 
 }  // namespace ssi

@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       T.mpc[e] = mpc; T.mpd[e] = mpd;
     }
   }
-  if (g.profile && tid == 0 && (o == g.n_orders - 1 || o == g.n_orders / 2))
+  if (g.profile && tid == 0 && (g.profile > 1 || o == g.n_orders - 1 || o == g.n_orders / 2))
     printf("eig order n=%d: band load %lld qr %lld (its %lld) vectors %lld cycles | scan %lld chase %lld (steps %lld) cupd %lld 2x2 %lld\n", n, clk1 - clk0,
            clk2 - clk1, qr_its, clock64() - clk2, t_scan, t_chase, steps, t_cupd, t_2x2);
 }
@@ -746,7 +746,7 @@ ssi_status modal_run(const double* U, int64_t ldU, const double* S, int l, int i
                    n_max, splits, w.partial, st));
   // M_n = Rinv[:n,:n] W[:n,:n] for every order
   SSI_TRY(gemm_f64_orders(no, n_min, n_step, w.Rinv, n_max, w.W, n_max, w.M, st));
-  EigArgs g{w.M, w.C, U, ldU, S, l, n_min, n_step, no, n_max, tab.cap, dt, tab, getenv("SSI_EIG_PROFILE") ? 1 : 0};
+  EigArgs g{w.M, w.C, U, ldU, S, l, n_min, n_step, no, n_max, tab.cap, dt, tab, getenv("SSI_EIG_PROFILE") ? atoi(getenv("SSI_EIG_PROFILE")) : 0};
   const size_t smem = modal_smem_bytes(n_max, tab.cap);
   cudaFuncSetAttribute(eig_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   hess_order_kernel<<<no, HT, 0, st>>>(g);

@@ -4,6 +4,7 @@
 #include "covariance.cuh"
 #include "linalg.cuh"
 #include "rsvd.cuh"
+#include "toeplitz_dft.cuh"
 
 namespace ssi {
 
@@ -31,21 +32,12 @@ size_t rsvd_ws_bytes(int64_t m, int k) {
   return c.bytes();
 }
 
-ssi_status rsvd_run(const double* T, int64_t ldT, int64_t m, int k, int q, uint64_t seed,
-                    uint64_t sid, int n_keep, double* U, int64_t ldU, double* S, void* ws,
-                    int32_t* status, cudaStream_t s) {
-  Carver c(ws);
-  RsvdWork w;
-  rsvd_carve(c, m, k, w);
-  // dedicated tall-skinny kernel (whole width in one tile; 16-byte cp.async alignment)
-  const bool tall = k <= 224 && m % 2 == 0 && ldT % 2 == 0 && (reinterpret_cast<uintptr_t>(T) & 15) == 0;
-  const Operand Tn{T, ldT, 1};   // T(i,j) = T[i*ldT + j]  (row-major, k-contiguous)
-  const Operand Tt{T, 1, ldT};   // T^T(i,j) = T[j*ldT + i]
-  // X -> T X (trans = false) or T^T X (trans = true), X and the result m x k col-major
-  auto pass = [&](bool trans, const double* X, double* out) -> ssi_status {
-    if (tall) return gemm_tall(m, k, m, !trans, T, ldT, X, m, out, m, w.tall, s);
-    return gemm_f64(m, k, m, 1.0, trans ? Tt : Tn, Operand{X, 1, m}, out, m, 1, nullptr, s);
-  };
+// Algorithm 1 with q power iterations, given the operator pass(trans, X, out): out = T X or
+// T^T X (X and out m x k col-major, ld m).
+template <typename Pass>
+static ssi_status rsvd_core(Pass&& pass, int64_t m, int k, int q, uint64_t seed, uint64_t sid,
+                            int n_keep, double* U, int64_t ldU, double* S, RsvdWork& w,
+                            int32_t* status, cudaStream_t s) {
   // line 1: Omega ~ N(0,1), Philox on device (Eq. 14 input; reading A-11)
   SSI_TRY(sketch_launch(int(m), k, seed, sid, w.Omega, m, s));
   // line 2: Y = T Omega (Eq. 14)
@@ -73,6 +65,68 @@ ssi_status rsvd_run(const double* T, int64_t ldT, int64_t m, int k, int q, uint6
   if (cudaMemcpyAsync(S, w.Sk, sizeof(double) * k, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
     return launch_check("rsvd S copy");
   return SSI_OK;
+}
+
+ssi_status rsvd_run(const double* T, int64_t ldT, int64_t m, int k, int q, uint64_t seed,
+                    uint64_t sid, int n_keep, double* U, int64_t ldU, double* S, void* ws,
+                    int32_t* status, cudaStream_t s) {
+  Carver c(ws);
+  RsvdWork w;
+  rsvd_carve(c, m, k, w);
+  // dedicated tall-skinny kernel (whole width in one tile; 16-byte cp.async alignment)
+  const bool tall = k <= 224 && m % 2 == 0 && ldT % 2 == 0 && (reinterpret_cast<uintptr_t>(T) & 15) == 0;
+  const Operand Tn{T, ldT, 1};   // T(i,j) = T[i*ldT + j]  (row-major, k-contiguous)
+  const Operand Tt{T, 1, ldT};   // T^T(i,j) = T[j*ldT + i]
+  // X -> T X (trans = false) or T^T X (trans = true), X and the result m x k col-major
+  auto pass = [&](bool trans, const double* X, double* out) -> ssi_status {
+    if (tall) return gemm_tall(m, k, m, !trans, T, ldT, X, m, out, m, w.tall, s);
+    return gemm_f64(m, k, m, 1.0, trans ? Tt : Tn, Operand{X, 1, m}, out, m, 1, nullptr, s);
+  };
+  return rsvd_core(pass, m, k, q, seed, sid, n_keep, U, ldU, S, w, status, s);
+}
+
+// ---------------------------------------------------------------- structured (T never formed)
+struct RsvdBtWork {
+  RsvdWork base;
+  double *Bb, *Xh, *Yh;
+};
+
+static void rsvd_bt_carve(Carver& c, int l, int i, int k, RsvdBtWork& w) {
+  const int64_t m = int64_t(l) * i;
+  w.base.Omega = c.take<double>(size_t(m) * k);
+  w.base.Y = c.take<double>(size_t(m) * k);
+  w.base.Q = c.take<double>(size_t(m) * k);
+  w.base.Q2 = c.take<double>(size_t(m) * k);
+  w.base.G = c.take<double>(size_t(k) * k);
+  w.base.Ut = c.take<double>(size_t(k) * k);
+  w.base.Sk = c.take<double>(size_t(k));
+  w.base.tall = nullptr;
+  cholqr_carve(c, m, k, w.base.cq);
+  w.Bb = c.take<double>(bt_spectrum_elems(l, i));
+  w.Xh = c.take<double>(bt_freq_elems(l, i, k));
+  w.Yh = c.take<double>(bt_freq_elems(l, i, k));
+}
+
+size_t rsvd_bt_ws_bytes(int l, int i, int k) {
+  Carver c(nullptr);
+  RsvdBtWork w;
+  rsvd_bt_carve(c, l, i, k, w);
+  return c.bytes();
+}
+
+ssi_status rsvd_bt_run(const double* R, int l, int i, int k, int q, uint64_t seed, uint64_t sid,
+                       int n_keep, double* U, int64_t ldU, double* S, void* ws, int32_t* status,
+                       cudaStream_t s) {
+  Carver c(ws);
+  RsvdBtWork w;
+  rsvd_bt_carve(c, l, i, k, w);
+  const int64_t m = int64_t(l) * i;
+  // spectrum of the block sequence B_d = R_{i+d}, once per call
+  SSI_TRY(bt_spectrum(R, l, i, w.Bb, s));
+  auto pass = [&](bool trans, const double* X, double* out) -> ssi_status {
+    return bt_apply(w.Bb, l, i, k, trans, X, m, out, m, w.Xh, w.Yh, s);
+  };
+  return rsvd_core(pass, m, k, q, seed, sid, n_keep, U, ldU, S, w.base, status, s);
 }
 
 }  // namespace ssi

@@ -8,6 +8,12 @@ ssi_status rsvd_run(const double* T, int64_t ldT, int64_t m, int k, int q, uint6
                     uint64_t sid, int n_keep, double* U, int64_t ldU, double* S, void* ws,
                     int32_t* status, cudaStream_t s);
 
+// RSVD of the block-Toeplitz T defined by R (lags 1..2i-1) without forming T.
+size_t rsvd_bt_ws_bytes(int l, int i, int k);
+ssi_status rsvd_bt_run(const double* R, int l, int i, int k, int q, uint64_t seed, uint64_t sid,
+                       int n_keep, double* U, int64_t ldU, double* S, void* ws, int32_t* status,
+                       cudaStream_t s);
+
 size_t modal_ws_bytes(int l, int i, int n_min, int n_max, int n_step);
 ssi_status modal_run(const double* U, int64_t ldU, const double* S, int l, int i, int n_min,
                      int n_max, int n_step, double dt, const ssi_pole_table& tab, void* ws,

@@ -1,0 +1,185 @@
+// Block-Toeplitz products without forming T (north star (b): "exploit its block-Toeplitz
+// structure"; Eq. 6). With B_d = R_{i+d} (d = r - c in [-(i-1), i-1]),
+//     (T X)_r   = sum_c B_{r-c}   X_c          (block convolution)
+//     (T^T X)_c = sum_r B_{r-c}^T X_r          (block correlation)
+// where X_c = X[c*l : (c+1)*l, :]. Both are exact circular convolutions of period P = 2i-1
+// (the 2i-1 block lags are distinct mod P), so with the length-P DFT along the block index
+//     hat(TX)_f = hatB_f hatX_f,   hat(T^T X)_f = hatB_f^H hatX_f,   hatB_f = sum_d B_d w^{fd},
+// w = exp(-2 pi i / P). All data are real, so only f = 0 .. (P-1)/2 = i-1 are formed (F = i).
+// The complex products are real GEMMs on the 2l x 2l real form [[Re, -Im], [Im, Re]] of hatB_f
+// (batched FP64 DMMA, gemm_tall_batched); T^T uses the transpose of the same storage.
+// Per pass: 2 F (2l)^2 k flop in the products (3.9e9 at c3 vs 2 m^2 k = 5.8e10 for explicit T)
+// plus two DFTs of 2 F i l k flop each; T (1.06 GB at c3) is never read.
+#include <cmath>
+
+#include "gemm_f64.cuh"
+#include "toeplitz_dft.cuh"
+
+namespace ssi {
+namespace {
+
+constexpr int DT = 256;          // threads per CTA (8 warps)
+constexpr int DW = DT / 32;
+
+// cos / sin of 2 pi t / P for t in [0, P): shared-memory table
+__device__ __forceinline__ void twiddles(int P, double* cs, double* sn) {
+  for (int t = threadIdx.x; t < P; t += blockDim.x) {
+    double s, c;
+    sincospi(2.0 * double(t) / double(P), &s, &c);
+    cs[t] = c;
+    sn[t] = s;
+  }
+}
+
+// hatB_f for f in [0, F), written as the real 2l x 2l block form, row-major:
+//   [a][b] = [l+a][l+b] = Re hatB_f[a][b],  [l+a][b] = Im,  [a][l+b] = -Im.
+// CTA: 32 consecutive (a, b) elements (lanes) x 8 warps over f. R: [>= 2i-1][l][l] row-major.
+__global__ void __launch_bounds__(DT) bt_spectrum_kernel(const double* __restrict__ R, int l, int i,
+                                                         double* __restrict__ Bb) {
+  extern __shared__ __align__(16) double sm[];
+  const int P = 2 * i - 1, F = i;
+  double* cs = sm;
+  double* sn = cs + P;
+  double* rs = sn + P;                    // [P][32]: rs[(d + i - 1)*32 + lane] = B_d[e]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ll = int64_t(l) * l;
+  const int64_t e = int64_t(blockIdx.x) * 32 + lane;
+  const bool ok = e < ll;
+  twiddles(P, cs, sn);
+  for (int d = warp; d < P; d += DW) rs[d * 32 + lane] = ok ? R[int64_t(d) * ll + e] : 0.0;
+  __syncthreads();
+  if (!ok) return;
+  const int a = int(e / l), b = int(e % l);
+  const int64_t L2 = 2 * int64_t(l);
+  for (int f = warp; f < F; f += DW) {
+    double re = 0.0, im = 0.0;
+    // d = -(i-1) .. i-1, phase t = f d mod P, starting at f (P - (i-1)) mod P
+    int t = int((int64_t(f) * (P - (i - 1))) % P);
+    for (int dd = 0; dd < P; ++dd) {
+      const double v = rs[dd * 32 + lane];
+      re = fma(v, cs[t], re);
+      im = fma(-v, sn[t], im);
+      t += f;
+      if (t >= P) t -= P;
+    }
+    double* blk = Bb + int64_t(f) * L2 * L2;
+    blk[int64_t(a) * L2 + b] = re;
+    blk[int64_t(l + a) * L2 + (l + b)] = re;
+    blk[int64_t(l + a) * L2 + b] = im;
+    blk[int64_t(a) * L2 + (l + b)] = -im;
+  }
+}
+
+// hatX_f = sum_{c<i} X_c w^{fc}: Xh[f][j][0:l] = Re, Xh[f][j][l:2l] = Im (per f a 2l x k
+// col-major matrix, ld 2l). CTA: 32 rows a of one column j; 8 warps over f.
+__global__ void __launch_bounds__(DT) bt_forward_kernel(const double* __restrict__ X, int64_t ldx, int l, int i,
+                                                        int k, double* __restrict__ Xh) {
+  extern __shared__ __align__(16) double sm[];
+  const int P = 2 * i - 1, F = i;
+  double* cs = sm;
+  double* sn = cs + P;
+  double* xs = sn + P;                    // [i][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int a = blockIdx.x * 32 + lane;
+  const int j = blockIdx.y;
+  const bool ok = a < l;
+  twiddles(P, cs, sn);
+  const double* xc = X + int64_t(j) * ldx;
+  for (int c = warp; c < i; c += DW) xs[c * 32 + lane] = ok ? xc[int64_t(c) * l + a] : 0.0;
+  __syncthreads();
+  if (!ok) return;
+  const int64_t L2 = 2 * int64_t(l);
+  for (int f = warp; f < F; f += DW) {
+    double re = 0.0, im = 0.0;
+    int t = 0;
+    for (int c = 0; c < i; ++c) {
+      const double v = xs[c * 32 + lane];
+      re = fma(v, cs[t], re);
+      im = fma(-v, sn[t], im);
+      t += f;
+      if (t >= P) t -= P;
+    }
+    double* o = Xh + (int64_t(f) * k + j) * L2;
+    o[a] = re;
+    o[l + a] = im;
+  }
+}
+
+// Y_r = (1/P) [Re hatY_0 + 2 sum_{f=1}^{F-1} (Re hatY_f cos(2 pi r f / P) - Im hatY_f sin(...))],
+// r in [0, i): Y[r*l + a + j*ldy]. CTA: 32 rows a of one column j; 8 warps over r.
+__global__ void __launch_bounds__(DT) bt_inverse_kernel(const double* __restrict__ Yh, int l, int i, int k,
+                                                        double* __restrict__ Y, int64_t ldy) {
+  extern __shared__ __align__(16) double sm[];
+  const int P = 2 * i - 1, F = i;
+  double* cs = sm;
+  double* sn = cs + P;
+  double* ys = sn + P;                    // [F][2][32]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int a = blockIdx.x * 32 + lane;
+  const int j = blockIdx.y;
+  const bool ok = a < l;
+  twiddles(P, cs, sn);
+  const int64_t L2 = 2 * int64_t(l);
+  for (int f = warp; f < F; f += DW) {
+    const double* src = Yh + (int64_t(f) * k + j) * L2;
+    ys[(2 * f) * 32 + lane] = ok ? src[a] : 0.0;
+    ys[(2 * f + 1) * 32 + lane] = ok ? src[l + a] : 0.0;
+  }
+  __syncthreads();
+  if (!ok) return;
+  const double invP = 1.0 / double(P);
+  for (int r = warp; r < i; r += DW) {
+    double acc = 0.0;
+    int t = r;
+    if (t >= P) t -= P;
+    for (int f = 1; f < F; ++f) {
+      acc = fma(ys[(2 * f) * 32 + lane], cs[t], acc);
+      acc = fma(-ys[(2 * f + 1) * 32 + lane], sn[t], acc);
+      t += r;
+      if (t >= P) t -= P;
+    }
+    Y[int64_t(r) * l + a + int64_t(j) * ldy] = fma(2.0, acc, ys[lane]) * invP;
+  }
+}
+
+size_t smem_twiddle(int i) { return sizeof(double) * 2 * size_t(2 * i - 1); }
+
+}  // namespace
+
+size_t bt_spectrum_elems(int l, int i) { return size_t(i) * 4 * size_t(l) * l; }
+size_t bt_freq_elems(int l, int i, int k) { return size_t(i) * 2 * size_t(l) * k; }
+
+ssi_status bt_spectrum(const double* R, int l, int i, double* Bb, cudaStream_t s) {
+  const int P = 2 * i - 1;
+  const size_t smem = smem_twiddle(i) + sizeof(double) * size_t(P) * 32;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(bt_spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  const int64_t ll = int64_t(l) * l;
+  bt_spectrum_kernel<<<unsigned((ll + 31) / 32), DT, smem, s>>>(R, l, i, Bb);
+  return launch_check("bt_spectrum_kernel");
+}
+
+ssi_status bt_apply(const double* Bb, int l, int i, int k, bool trans, const double* X, int64_t ldx,
+                    double* Y, int64_t ldy, double* Xh, double* Yh, cudaStream_t s) {
+  const int F = i;
+  const size_t smem_f = smem_twiddle(i) + sizeof(double) * size_t(i) * 32;
+  const size_t smem_i = smem_twiddle(i) + sizeof(double) * size_t(F) * 2 * 32;
+  if (smem_f > 48 * 1024)
+    cudaFuncSetAttribute(bt_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_f));
+  if (smem_i > 48 * 1024)
+    cudaFuncSetAttribute(bt_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_i));
+  const dim3 grid(unsigned((l + 31) / 32), unsigned(k));
+  bt_forward_kernel<<<grid, DT, smem_f, s>>>(X, ldx, l, i, k, Xh);
+  SSI_TRY(launch_check("bt_forward_kernel"));
+  const int64_t L2 = 2 * int64_t(l);
+  // hatY_f = Bblk_f hatX_f (T X) or Bblk_f^T hatX_f (T^T X), in column chunks of <= 224
+  for (int j0 = 0; j0 < k; j0 += kTallMaxN) {
+    const int nj = k - j0 < kTallMaxN ? k - j0 : kTallMaxN;
+    SSI_TRY(gemm_tall_batched(L2, nj, L2, !trans, Bb, L2, L2 * L2, Xh + j0 * L2, L2, L2 * k,
+                              Yh + j0 * L2, L2, L2 * k, F, s));
+  }
+  bt_inverse_kernel<<<grid, DT, smem_i, s>>>(Yh, l, i, k, Y, ldy);
+  return launch_check("bt_inverse_kernel");
+}
+
+}  // namespace ssi

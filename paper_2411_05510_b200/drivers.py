@@ -30,6 +30,7 @@ class SweepParams:
     n_step: int = 2
     seed: int = 0
     cov_mode: str = "fp64"
+    structured: bool = True     # RSVD through the block structure of T (T never formed)
 
     @property
     def k(self):
@@ -54,12 +55,14 @@ class Engine:
         self.lag_hi = lag_hi or 2 * P.i - 1
         d64 = dict(dtype=torch.float64, device=self.dev)
         self.R = torch.empty((self.lag_hi, P.l, P.l), **d64)
-        self.T = torch.empty((P.m, P.m), **d64)
+        self.T = None if P.structured else torch.empty((P.m, P.m), **d64)
         self.U = torch.empty((P.n_max, P.m), **d64).t()          # column-major m x n_max
         self.S = torch.empty(P.k, **d64)
         self.table = api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, self.dev)
         self.ws_cov = api._workspace(api.covariances_ws_bytes(N, P.l, self.lag_hi, 1, P.cov_mode), self.dev)
-        self.ws_rsvd = api._workspace(api.rsvd_ws_bytes(P.m, P.k, P.n_max), self.dev)
+        self.ws_rsvd = api._workspace(
+            api.rsvd_toeplitz_ws_bytes(P.l, P.i, P.k, P.n_max) if P.structured
+            else api.rsvd_ws_bytes(P.m, P.k, P.n_max), self.dev)
         self.ws_modal = api._workspace(
             api.modal_sweep_ws_bytes(P.l, P.i, P.n_min, P.n_max, P.n_step), self.dev)
 
@@ -71,6 +74,16 @@ class Engine:
         P = self.P
         i = i or P.i
         m = P.l * i
+        if P.structured:
+            if i == P.i:
+                U, S = api.rsvd_toeplitz(R, i, P.k, P.q, P.seed, stream_id, P.n_max, U=self.U, S=self.S,
+                                         ws=self.ws_rsvd)
+                tab = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, out=self.table,
+                                      ws=self.ws_modal)
+            else:
+                U, S = api.rsvd_toeplitz(R, i, P.k, P.q, P.seed, stream_id, P.n_max, ws=self.ws_rsvd)
+                tab = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=self.ws_modal)
+            return tab, (U, S)
         if i == P.i:
             T, U, S = self.T, self.U, self.S
             api.toeplitz(R, i, out=T)
@@ -202,14 +215,21 @@ def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank
     assign = lpt_assign(lags, world)
     dev = Y.device
     m_max = P.l * lags[-1]
-    Tbuf = torch.empty(m_max * m_max, dtype=torch.float64, device=dev)
-    ws_rsvd = api._workspace(api.rsvd_ws_bytes(m_max, P.k, P.n_max), dev)
+    if P.structured:
+        Tbuf = None
+        ws_rsvd = api._workspace(api.rsvd_toeplitz_ws_bytes(P.l, lags[-1], P.k, P.n_max), dev)
+    else:
+        Tbuf = torch.empty(m_max * m_max, dtype=torch.float64, device=dev)
+        ws_rsvd = api._workspace(api.rsvd_ws_bytes(m_max, P.k, P.n_max), dev)
     ws_modal = api._workspace(max(api.modal_sweep_ws_bytes(P.l, i, P.n_min, P.n_max, P.n_step) for i in lags), dev)
     local = {}
     for i in assign[rank]:
         m = P.l * i
-        T = api.toeplitz(R, i, out=Tbuf[:m * m].view(m, m))
-        U, S = api.rsvd(T, P.k, P.q, P.seed, i, P.n_max, ws=ws_rsvd)
+        if P.structured:
+            U, S = api.rsvd_toeplitz(R, i, P.k, P.q, P.seed, i, P.n_max, ws=ws_rsvd)
+        else:
+            T = api.toeplitz(R, i, out=Tbuf[:m * m].view(m, m))
+            U, S = api.rsvd(T, P.k, P.q, P.seed, i, P.n_max, ws=ws_rsvd)
         local[i] = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=ws_modal)
     tables = gather_tables(local, assign, lambda: api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, dev),
                            rank, world, group)

@@ -91,3 +91,19 @@ def test_rsvd_workspace_is_monotone_in_m(lib):
         assert lib.ssi_rsvd_ws(192 * i, 220, 200, C.byref(b)) == 0
         assert b.value >= prev, i
         prev = b.value
+
+
+def test_rsvd_toeplitz_workspace_and_validation(lib):
+    """Structured RSVD: workspace non-decreasing in i (one workspace serves a lag sweep);
+    argument errors before any launch."""
+    b = C.c_size_t(0)
+    prev = 0
+    for i in range(20, 81, 4):
+        assert lib.ssi_rsvd_toeplitz_ws(192, i, 220, 200, C.byref(b)) == 0
+        assert b.value >= prev, i
+        prev = b.value
+    assert lib.ssi_rsvd_toeplitz_ws(6, 2, 13, 1, C.byref(b)) == 1      # k > l*i
+    dummy = C.c_void_p(16)
+    assert lib.ssi_rsvd_toeplitz(dummy, 6, 20, 40, 2, 1, 1, 41, dummy, 120, dummy, dummy, 1 << 30, None) == 1
+    assert lib.ssi_rsvd_toeplitz(dummy, 6, 20, 40, 2, 1, 1, 30, dummy, 119, dummy, dummy, 1 << 30, None) == 2
+    assert lib.ssi_rsvd_toeplitz(dummy, 6, 20, 40, 2, 1, 1, 30, dummy, 120, dummy, dummy, 64, None) == 4

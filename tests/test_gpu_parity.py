@@ -175,6 +175,54 @@ def test_rsvd_edge_cases(ssi):
     assert abs(abs(U[:, 0] @ Uo[:, 0]) - 1) < 1e-10
 
 
+# ------------------------------------------------------------------ A2-A8 structured RSVD
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_rsvd_toeplitz_matches_oracle_same_sketch(ssi, name):
+    """ssi_rsvd_toeplitz (T applied through its block structure, never formed) vs the oracle's
+    RSVD of the explicit Toeplitz, same Philox sketch."""
+    api, _ = ssi
+    cfg = synth.config(name)
+    Y, _ = synth.make_record(cfg)
+    R = oracle.covariances(Y, 2 * cfg.i - 1)
+    U, S = api.rsvd_toeplitz(_dev(R), cfg.i, cfg.k, cfg.q, cfg.philox_key, cfg.i, cfg.n_max, check=True)
+    U, S = U.cpu().numpy(), S.cpu().numpy()
+    Uo, So, _ = oracle.rsvd(oracle.toeplitz(R, cfg.i), cfg.k, cfg.q, cfg.philox_key, cfg.i, cfg.n_max)
+    rel = np.abs(S[:cfg.n_max] - So[:cfg.n_max]) / So[:cfg.n_max]
+    assert rel.max() <= 1e-5                  # contract: leading singular values
+    assert rel.max() <= 1e-9                  # internal FP64 tripwire
+    np.testing.assert_allclose(U.T @ U, np.eye(cfg.n_max), atol=1e-10)
+    gap = np.minimum(np.abs(np.diff(So[:cfg.n_max + 1]))[:cfg.n_max],
+                     np.r_[np.inf, np.abs(np.diff(So[:cfg.n_max]))]) / So[0]
+    ok = gap > 1e-6
+    d = np.abs(np.sum(U * Uo, axis=0))
+    assert np.all(d[ok] > 1 - 1e-6)
+
+
+def test_rsvd_toeplitz_edge_cases(ssi):
+    """Ragged l (not a multiple of 32), i = 1 and 2 (DFT periods 1 and 3), l = 1, k > 224
+    (column chunks of the batched product), full width k = m (exact SVD of T), exact rank."""
+    api, _ = ssi
+    rng = np.random.default_rng(31)
+    for (l, i, k, q, n_keep) in ((5, 7, 12, 2, 10), (3, 1, 3, 1, 3), (4, 2, 8, 0, 8), (1, 9, 9, 2, 9),
+                                 (3, 4, 12, 1, 12), (20, 15, 250, 1, 240), (33, 3, 40, 2, 30)):
+        R = rng.standard_normal((2 * i - 1, l, l))
+        U, S = api.rsvd_toeplitz(_dev(R), i, k, q, 77, i, n_keep, check=True)
+        U, S = U.cpu().numpy(), S.cpu().numpy()
+        T = oracle.toeplitz(R, i)
+        Uo, So, _ = oracle.rsvd(T, k, q, 77, i, n_keep)
+        np.testing.assert_allclose(S, So, rtol=1e-9, atol=1e-12 * So[0])
+        if k == l * i:
+            np.testing.assert_allclose(S, np.linalg.svd(T, compute_uv=False), rtol=1e-10, atol=1e-12 * So[0])
+        np.testing.assert_allclose(U.T @ U, np.eye(n_keep), atol=1e-9)
+    cfg = synth.config("c1")
+    from tests.analytic import exact_covariances
+    R = exact_covariances(synth.make_modes(cfg), 2 * cfg.i - 1)
+    Sf = oracle.full_svd(oracle.toeplitz(R, cfg.i))[1]
+    for q in (0, 2):
+        _, S = api.rsvd_toeplitz(_dev(R), cfg.i, 6, q, 5, 1, 6, check=True)
+        np.testing.assert_allclose(S.cpu().numpy(), Sf[:6], rtol=1e-12)
+
+
 # ------------------------------------------------------------------ A9-A11 modal sweep
 @pytest.fixture(scope="module")
 def c2_chain():
