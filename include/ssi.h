@@ -61,7 +61,7 @@ enum { SSI_F32 = 0, SSI_F64 = 1 };
 /* Covariance arithmetic (ssi_covariances cov_mode).
  *  SSI_COV_FP64   : FP64 products and sums (DMMA tensor-core path).
  *  SSI_COV_INT8X3 : each sample is cut into three int8 slices against a per-channel
- *                   power-of-two scale; the six leading slice products are summed
+ *                   power-of-two scale; the eight leading slice products (all but d3*d3) are summed
  *                   EXACTLY in int32 on the 5th-gen tensor cores (tcgen05 kind::i8)
  *                   and promoted to FP64. Error is the slicing rounding only
  *                   (<= 2^-22 of the channel's max |y| per sample); see DESIGN.md. */

@@ -22,6 +22,8 @@ namespace {
 
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
+constexpr int WIN = 32;        // bulge-chase window (rows/cols) of the windowed Francis sweep
+constexpr int TLD = WIN + 1;    // tile row stride (doubles)
 constexpr double kUlp = 2.220446049250313e-16;
 constexpr double kSafeMin = 2.2250738585072014e-308;
 
@@ -43,6 +45,11 @@ __device__ __forceinline__ double fast_rsqrt(double x) {
   return r * fma(-hx * r, r, 1.5);
 }
 
+// eigenvector scratch (NW complex vectors), also the windowed sweep's tile
+__host__ __device__ inline size_t x_elems(int n_max) {
+  const size_t a = size_t(NW) * 2 * n_max, b = size_t(WIN) * TLD;
+  return a > b ? a : b;
+}
 __host__ __device__ inline int band_lo(int i) { return i > 3 ? i - 3 : 0; }
 __host__ __device__ inline size_t band_elems(int n) {
   size_t s = 0;
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     s.H = reinterpret_cast<double*>(p);      p += sizeof(double) * band_elems(nm);
     s.v = reinterpret_cast<double*>(p);      p += sizeof(double) * nm;
     s.refl = reinterpret_cast<double*>(p);   p += sizeof(double) * 3 * nm;
-    s.x = reinterpret_cast<double*>(p);      p += sizeof(double) * NW * 2 * nm;
+    s.x = reinterpret_cast<double*>(p);      p += sizeof(double) * x_elems(nm);
     s.cre = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
     s.cim = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
     s.cf = reinterpret_cast<double*>(p);     p += sizeof(double) * cap;
@@ -325,6 +332,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   if (tid == 0) sh_fail = 0;
   const double* A = order_A(g, o);
   double* C = order_C(g, o);
+  for (int i = tid; i < n; i += NT) s.rowoff[i] = band_off(n, i) - band_lo(i);   // H(i, c) = H[rowoff[i] + c]
   for (int i = 0; i < n; ++i)
     for (int c = band_lo(i) + tid; c < n; c += NT) H(i, c) = A[i + int64_t(c) * n];
   __syncthreads();
@@ -333,7 +341,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   int ihi = n - 1;
   int its = 0, total_its = 0;
   const int itmax = 30 * (n > 10 ? n : 10);
-  long long t_scan = 0, t_chase = 0, t_cupd = 0, t_2x2 = 0, steps = 0;
+  long long t_scan = 0, t_chase = 0, t_cupd = 0, t_2x2 = 0, steps = 0, t_wchase = 0, t_wdef = 0;
   while (ihi >= 0) {
     long long ta = clock64();
     // deflation test, in parallel: largest ll in (0, ihi] with a negligible subdiagonal
@@ -396,10 +404,17 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       __syncthreads();
       break;
     }
-    if (warp == 0) {
-      // ---------------- one double-shift sweep over [lo, ihi], warp-synchronous
-      double x = 0.0, y = 0.0, z = 0.0;
-      {  // every lane computes the shifts: the reflector below is formed redundantly per lane
+    // ---------------- one double-shift sweep over [lo, ihi], in windows of WIN rows/cols.
+    // Inside a window [w0, w1) (dense tile in shared memory) warp 0 chases the bulge alone
+    // (warp-synchronous); the parts of each reflector outside the window -- rows [w0, w1) x
+    // columns >= w1 (left), rows < w0 x columns [w0, w1) (right) and the Schur vectors C --
+    // are applied afterwards by all warps, each row / column segment held in registers while
+    // the window's reflectors stream through it. Same arithmetic per element as applying each
+    // reflector in turn (dlahqr), only the order of independent element updates changes.
+    {
+      // shift polynomial (first column of (H - s1)(H - s2)), Francis / exceptional shifts
+      double x0, y0, z0;
+      {
         double h11, h12, h21, h22;
         if (its == 10) {
           const double ex = fabs(H(lo + 1, lo)) + fabs(H(lo + 2, lo + 1));
@@ -414,131 +429,142 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
         const double tr = h11 + h22, det = h11 * h22 - h12 * h21;
         const double a00 = H(lo, lo), a01 = H(lo, lo + 1), a10 = H(lo + 1, lo), a11 = H(lo + 1, lo + 1);
         const double a21 = H(lo + 2, lo + 1);
-        x = a00 * a00 + a01 * a10 - tr * a00 + det;
-        y = a10 * (a00 + a11 - tr);
-        z = a10 * a21;
-        const double sc = fabs(x) + fabs(y) + fabs(z);
-        if (sc > 0.0) { x /= sc; y /= sc; z /= sc; }
+        x0 = a00 * a00 + a01 * a10 - tr * a00 + det;
+        y0 = a10 * (a00 + a11 - tr);
+        z0 = a10 * a21;
+        const double sc = fabs(x0) + fabs(y0) + fabs(z0);
+        if (sc > 0.0) { x0 /= sc; y0 /= sc; z0 /= sc; }
       }
-      for (int k = lo; k < ihi; ++k) {
-        const int nr = (ihi - k + 1) < 3 ? (ihi - k + 1) : 3;
-        // row pointers: rows k, k+1, k+2 indexed by absolute column
-        double* r0 = s.H + band_off(n, k) - band_lo(k);
-        double* r1 = s.H + band_off(n, k + 1) - band_lo(k + 1);
-        double* r2 = s.H + band_off(n, k + 2) - band_lo(k + 2);
-        // every lane forms the reflector (broadcast smem reads, no shuffles)
-        if (k > lo) { x = r0[k - 1]; y = r1[k - 1]; z = nr == 3 ? r2[k - 1] : 0.0; }
-        else if (nr < 3) { z = 0.0; }
-        double tau = 0.0, v1 = 0.0, v2 = 0.0, beta = 0.0;
-        const double yz = y * y + z * z;
-        if (yz != 0.0) {
-          // beta = -sign(x) sqrt(s); tau = (beta - x)/beta = 1 + |x|/sqrt(s);
-          // v = (y, z)/(x - beta) = sign(x) (y, z)/(|x| + sqrt(s))      (one rsqrt, one rcp)
-          const double ss = x * x + yz;
-          const double rs = fast_rsqrt(ss);
-          const double sq = ss * rs;
-          beta = -copysign(sq, x);
-          tau = fma(fabs(x), rs, 1.0);
-          const double inv = copysign(fast_rcp(fabs(x) + sq), x);
-          v1 = y * inv; v2 = z * inv;
+      double* D = s.x;                 // WIN x TLD tile (aliases the eigenvector scratch)
+      for (int w0 = lo; w0 < ihi; ) {
+        const int kend = (w0 + WIN - 3 < ihi) ? w0 + WIN - 3 : ihi;   // steps k in [w0, kend)
+        const int w1 = (w0 + WIN < ihi + 1) ? w0 + WIN : ihi + 1;    // window rows/cols [w0, w1)
+        const int nw = w1 - w0;
+        // tile D[lr][lc] = H(w0 + lr, w0 - 1 + lc), lr < nw, lc <= nw (structural zeros as 0)
+        for (int e = tid; e < WIN * TLD; e += NT) {
+          const int lr = e / TLD, lc = e - lr * TLD;
+          const int r = w0 + lr, c = w0 - 1 + lc;
+          D[e] = (lr < nw && lc <= nw && c >= 0 && c >= band_lo(r)) ? s.H[s.rowoff[r] + c] : 0.0;
         }
-        __syncwarp();
-        if (lane == 0) {
-          if (yz != 0.0 && k > lo) {
-            r0[k - 1] = beta; r1[k - 1] = 0.0;
-            if (nr == 3) r2[k - 1] = 0.0;
-          }
-          s.refl[3 * (k - lo) + 0] = v1;
-          s.refl[3 * (k - lo) + 1] = v2;
-          s.refl[3 * (k - lo) + 2] = tau;
-        }
-        if (tau != 0.0) {
-          // (a) left update of the corner columns k..k+nr-1 (shared with the right update)
-          if (lane < nr) {
-            const int c = k + lane;
-            const double b0 = r0[c], b1 = r1[c], b2 = nr == 3 ? r2[c] : 0.0;
-            const double sum = (b0 + v1 * b1 + v2 * b2) * tau;
-            r0[c] = b0 - sum; r1[c] = b1 - sum * v1;
-            if (nr == 3) r2[c] = b2 - sum * v2;
-          }
-          __syncwarp();
-          // (b) disjoint remainder in one pass: left columns k+nr..n-1 (rows k..k+nr-1) and
-          //     right rows 0..min(k+3, ihi) (columns k..k+nr-1)
-          const int rmax = (k + 3 < ihi ? k + 3 : ihi);
-          const int nl = n - (k + nr);
-          const int total = nl + rmax + 1;
-#pragma unroll 2
-          for (int it = lane; it < total; it += 32) {
-            double* p0;
-            int st;                                   // stride between the three elements
-            if (it < nl) {
-              const int c = k + nr + it;
-              p0 = r0 + c;
-              st = 0;
-            } else {
-              const int r = it - nl;
-              p0 = s.H + band_off(n, r) - band_lo(r) + k;
-              st = 1;
+        __syncthreads();
+        const long long tw0 = clock64();
+        if (warp == 0) {
+          for (int k = w0; k < kend; ++k) {
+            const int t = k - w0;
+            const int nr = (ihi - k + 1) < 3 ? (ihi - k + 1) : 3;
+            double x, y, z;
+            if (k == lo) { x = x0; y = y0; z = nr == 3 ? z0 : 0.0; }
+            else { x = D[t * TLD + t]; y = D[(t + 1) * TLD + t]; z = nr == 3 ? D[(t + 2) * TLD + t] : 0.0; }
+            double tau = 0.0, v1 = 0.0, v2 = 0.0, beta = 0.0;
+            const double yz = y * y + z * z;
+            if (yz != 0.0) {
+              // beta = -sign(x) sqrt(s); tau = 1 + |x|/sqrt(s); v = sign(x) (y, z)/(|x| + sqrt(s))
+              const double ss = x * x + yz;
+              const double rs = fast_rsqrt(ss);
+              const double sq = ss * rs;
+              beta = -copysign(sq, x);
+              tau = fma(fabs(x), rs, 1.0);
+              const double inv = copysign(fast_rcp(fabs(x) + sq), x);
+              v1 = y * inv; v2 = z * inv;
             }
-            double* p1 = st ? p0 + 1 : r1 + (p0 - r0);
-            double* p2 = st ? p0 + 2 : r2 + (p0 - r0);
-            const double b0 = *p0, b1 = *p1, b2 = nr == 3 ? *p2 : 0.0;
-            const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
-            *p0 = b0 - sum; *p1 = fma(-sum, v1, b1);
-            if (nr == 3) *p2 = fma(-sum, v2, b2);
+            __syncwarp();
+            if (lane == 0) {
+              if (yz != 0.0 && k > lo) {
+                D[t * TLD + t] = beta; D[(t + 1) * TLD + t] = 0.0;
+                if (nr == 3) D[(t + 2) * TLD + t] = 0.0;
+              }
+              s.refl[3 * t + 0] = v1;
+              s.refl[3 * t + 1] = v2;
+              s.refl[3 * t + 2] = tau;
+            }
+            if (tau != 0.0) {
+              // left: rows t..t+nr-1, columns k..w1-1 (local t+1 .. nw)
+              {
+                const int lc = t + 1 + lane;
+                if (lc <= nw) {
+                  double* p0 = D + t * TLD + lc;
+                  const double b0 = p0[0], b1 = p0[TLD], b2 = nr == 3 ? p0[2 * TLD] : 0.0;
+                  const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
+                  p0[0] = b0 - sum; p0[TLD] = fma(-sum, v1, b1);
+                  if (nr == 3) p0[2 * TLD] = fma(-sum, v2, b2);
+                }
+              }
+              __syncwarp();
+              // right: columns k..k+nr-1 (local t+1..), rows w0..min(k+3, ihi)
+              {
+                const int rmax = (k + 3 < ihi ? k + 3 : ihi) - w0;
+                if (lane <= rmax) {
+                  double* p0 = D + lane * TLD + t + 1;
+                  const double b0 = p0[0], b1 = p0[1], b2 = nr == 3 ? p0[2] : 0.0;
+                  const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
+                  p0[0] = b0 - sum; p0[1] = fma(-sum, v1, b1);
+                  if (nr == 3) p0[2] = fma(-sum, v2, b2);
+                }
+              }
+            }
+            __syncwarp();
           }
         }
-        __syncwarp();
+        __syncthreads();
+        const long long tw1 = clock64();
+        t_wchase += tw1 - tw0;
+        const int nsteps = kend - w0;
+        // write the tile back
+        for (int e = tid; e < WIN * TLD; e += NT) {
+          const int lr = e / TLD, lc = e - lr * TLD;
+          const int r = w0 + lr, c = w0 - 1 + lc;
+          if (lr < nw && lc <= nw && c >= 0 && c >= band_lo(r)) s.H[s.rowoff[r] + c] = D[e];
+        }
+        // deferred parts: (L) columns c in [w1, n), rows [w0, w1); (R) rows r in [0, w0),
+        // columns [w0, w1); (C) Schur vectors C[a][w0..w1), a in [0, l)
+        const int nL = n - w1, nR = w0;
+        for (int task = tid; task < nL + nR + l; task += NT) {
+          double seg[WIN];
+          if (task < nL) {
+            const int c = w1 + task;
+#pragma unroll
+            for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? s.H[s.rowoff[w0 + u] + c] : 0.0;
+          } else if (task < nL + nR) {
+            const double* row = s.H + s.rowoff[task - nL] + w0;
+#pragma unroll
+            for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? row[u] : 0.0;
+          } else {
+            const double* cr = C + (task - nL - nR) + int64_t(w0) * l;
+#pragma unroll
+            for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? cr[int64_t(u) * l] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < WIN - 3; ++u) {
+            if (u < nsteps) {
+              const double v1 = s.refl[3 * u], v2 = s.refl[3 * u + 1], tau = s.refl[3 * u + 2];
+              const double sum = fma(v2, seg[u + 2], fma(v1, seg[u + 1], seg[u])) * tau;
+              seg[u] -= sum;
+              seg[u + 1] = fma(-sum, v1, seg[u + 1]);
+              seg[u + 2] = fma(-sum, v2, seg[u + 2]);
+            }
+          }
+          if (task < nL) {
+            const int c = w1 + task;
+#pragma unroll
+            for (int u = 0; u < WIN; ++u) if (u < nw) s.H[s.rowoff[w0 + u] + c] = seg[u];
+          } else if (task < nL + nR) {
+            double* row = s.H + s.rowoff[task - nL] + w0;
+#pragma unroll
+            for (int u = 0; u < WIN; ++u) if (u < nw) row[u] = seg[u];
+          } else {
+            double* cr = C + (task - nL - nR) + int64_t(w0) * l;
+#pragma unroll
+            for (int u = 0; u < WIN; ++u) if (u < nw) cr[int64_t(u) * l] = seg[u];
+          }
+        }
+        __syncthreads();
+        t_wdef += clock64() - tw1;
+        w0 = kend;
       }
     }
-    __syncthreads();
     long long tc = clock64();
     t_chase += tc - tb;
     steps += ihi - lo;
-    // C <- C P_lo ... P_{ihi-1}: each row streams through the sweep's reflectors; the
-    // column k+2 read at step k still holds its pre-sweep value, so it is prefetched.
-    for (int r = tid; r < l; r += NT) {
-      double* cr = C + r;
-      double c0 = cr[int64_t(lo) * l], c1 = cr[int64_t(lo + 1) * l];
-      constexpr int PF = 8;
-      double pf[PF];
-#pragma unroll
-      for (int u = 0; u < PF; ++u) {
-        const int col = lo + 2 + u;
-        pf[u] = col <= ihi ? cr[int64_t(col) * l] : 0.0;
-      }
-      for (int k0 = lo; k0 < ihi; k0 += PF) {
-        double nx[PF];
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-          const int col = k0 + 2 + PF + u;
-          nx[u] = col <= ihi ? cr[int64_t(col) * l] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < PF; ++u) {
-          const int k = k0 + u;
-          if (k < ihi) {
-            const double v1 = s.refl[3 * (k - lo)], v2 = s.refl[3 * (k - lo) + 1];
-            const double tau = s.refl[3 * (k - lo) + 2];
-            const bool three = (k + 2 <= ihi);
-            double c2 = pf[u];
-            if (tau != 0.0) {
-              double sum = c0 + v1 * c1 + (three ? v2 * c2 : 0.0);
-              sum *= tau;
-              c0 -= sum; c1 -= sum * v1;
-              if (three) c2 -= sum * v2;
-            }
-            cr[int64_t(k) * l] = c0;
-            c0 = c1; c1 = c2;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < PF; ++u) pf[u] = nx[u];
-      }
-      cr[int64_t(ihi) * l] = c0;
-    }
-    __syncthreads();
-    t_cupd += clock64() - tc;
   }
   clk2 = clock64();
   qr_its = total_its;
@@ -689,14 +715,14 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     }
   }
   if (g.profile && tid == 0 && (g.profile > 1 || o == g.n_orders - 1 || o == g.n_orders / 2))
-    printf("eig order n=%d: band load %lld qr %lld (its %lld) vectors %lld cycles | scan %lld chase %lld (steps %lld) cupd %lld 2x2 %lld\n", n, clk1 - clk0,
-           clk2 - clk1, qr_its, clock64() - clk2, t_scan, t_chase, steps, t_cupd, t_2x2);
+    printf("eig order n=%d: band load %lld qr %lld (its %lld) vectors %lld cycles | scan %lld chase %lld (steps %lld) cupd %lld 2x2 %lld | wchase %lld wdef %lld\n", n, clk1 - clk0,
+           clk2 - clk1, qr_its, clock64() - clk2, t_scan, t_chase, steps, t_cupd, t_2x2, t_wchase, t_wdef);
 }
 
 }  // namespace
 
 size_t modal_smem_bytes(int n_max, int cap) {
-  return sizeof(double) * (band_elems(n_max) + n_max + 3 * size_t(n_max) + size_t(NW) * 2 * n_max +
+  return sizeof(double) * (band_elems(n_max) + n_max + 3 * size_t(n_max) + x_elems(n_max) +
                            4 * size_t(cap)) +
          sizeof(int) * (size_t(n_max) + 1 + cap) + 64;
 }
