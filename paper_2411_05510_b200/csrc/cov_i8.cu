@@ -16,9 +16,9 @@
 // KT + 16 samples starting at t0 + k0, any k0). An MN-major SWIZZLE_NONE descriptor with
 // LBO = 128 B (K groups of 8 samples) and SBO = 16 B (16-row MN groups) makes row group g
 // read the same column g samples later, so ONE M = 128 MMA covers 16 channels x 8 consecutive
-// lags; a second descriptor 8 samples further covers the next 8 lags (two "units" per CTA).
+// lags (one "unit"; UNITS > 1 would add descriptors 8 samples further for the next lags).
 // B (un-shifted record, N = 64 channels) is a K-major 128B-swizzled TMA tile whose time
-// start is always 16-aligned. TMEM: 2 units x 4 weights x 64 int32 columns = 512 columns.
+// start is always 16-aligned. TMEM: 1 unit x 4 weights x N (<= 128) int32 columns <= 512.
 // Warp 0 issues TMA, warp 1 issues tcgen05.mma, all four warps drain TMEM at the end.
 // (TMA on this driver faults for 1-byte boxes whose innermost start is not 16-B aligned and
 // for boxes entirely out of bounds; the layout above never issues either.)
@@ -31,12 +31,13 @@ namespace {
 
 constexpr int KT = 128;                 // time samples per K-block (= one 128 B row of B)
 constexpr int LPU = 8;                  // lags per unit (8 row groups of 16 channels)
-constexpr int UNITS = 2;                // units per CTA: lags k0 .. k0 + 15
-constexpr int AW = KT + UNITS * LPU;    // A window samples (144)
+constexpr int UNITS = 1;                // units per CTA: lags k0 .. k0 + 7
+constexpr int AW = KT + UNITS * LPU;    // A window samples (136)
 constexpr int A_SLICE_BYTES = AW * 16;                       // 2304
 constexpr int A_BYTES = 3 * A_SLICE_BYTES;                   // 6912
 constexpr int A_PAD = (A_BYTES + 1023) / 1024 * 1024;        // 7168 (B stays 1024-aligned)
-constexpr int STAGES = 6;
+constexpr int MAX_STAGES = 6;
+constexpr int SMEM_CAP = 232448;        // 227 KB dynamic shared memory per CTA
 constexpr int NT = 128;
 constexpr int BLK_PER_CHUNK_MAX = 340;                       // 43520 samples -> exact int32
 constexpr int NW = 4;                                        // weight classes 2..5
@@ -50,6 +51,7 @@ struct I8Geom {
   int64_t t_grid0;         // 16-aligned start of the time grid
   int64_t nblk;            // K-blocks over [t_grid0, t_end)
   int bpc;                 // K-blocks per chunk
+  int stages;              // smem ring depth
 };
 
 __host__ __device__ inline int b_bytes(int nb) { return 3 * nb * KT; }
@@ -218,6 +220,7 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int SB = stage_bytes(g.nb);
+  const int STAGES = g.stages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
@@ -228,7 +231,7 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
   int u = blockIdx.x;
   const int bt = u % nbt; u /= nbt;
   const int cg = u % ncg; u /= ncg;
-  const int lb = u;                                   // lag block: lags k0 .. k0 + 15
+  const int lb = u;                                   // lag block: lags k0 .. k0 + 8 UNITS - 1
   const int k0 = g.lag_lo + lb * (UNITS * LPU);
   const int b0 = bt * g.nb;
   const int chunk = blockIdx.y;
@@ -241,7 +244,7 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1) {   // TMEM: 2 units x 4 weights x nb <= 512 columns
+  if (warp == 1) {   // TMEM: UNITS x 4 weights x nb <= 512 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -265,7 +268,7 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
         tma_load_3d(B, &mapB, full + s, int(t0), b0, 0);
       }
     } else if (warp == 1 && lane == 0) {
-      // ---------------- MMA issuer: 4 K-steps x 2 units x 8 slice products per block
+      // ---------------- MMA issuer: 4 K-steps x UNITS x 8 slice products per block
       // idesc: S32 accum, signed int8 A/B, A MN-major (bit 15), B K-major, N>>3, M>>4
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
                              (uint32_t(g.nb >> 3) << 17) | (uint32_t(128 >> 4) << 24);
@@ -376,9 +379,13 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// B tile width (N): the widest of 128 / 96 / 64 channels dividing l, else l itself (l % 16 == 0,
+// l <= 128). One unit x 4 weight classes x N <= 512 TMEM columns; a wide N amortizes the A
+// (lag-shifted) operand read from shared memory over more output columns.
 int pick_nb(int l) {
-  if (l % 64 == 0) return 64;
-  if (l % 16 == 0 && l <= 64) return l;
+  for (int nb : {128, 96, 64})
+    if (l % nb == 0) return nb;
+  if (l % 16 == 0 && l <= 128) return l;
   return 0;
 }
 
@@ -493,8 +500,10 @@ ssi_status cov_i8(const void* Y, int dtype, int64_t N, int l, int64_t ldY, int l
     }
   }
   // 4. tcgen05 contraction + fixed-order chunk reduction
-  I8Geom g{l, p.nb, p.Tpad, lag_lo, lag_hi, p.lag_blocks, p.t_grid0, p.nblk, p.bpc};
-  const size_t smem = size_t(STAGES) * stage_bytes(p.nb) + 1024 + 256;
+  int stages = int((SMEM_CAP - 1024 - 256) / stage_bytes(p.nb));
+  if (stages > MAX_STAGES) stages = MAX_STAGES;
+  I8Geom g{l, p.nb, p.Tpad, lag_lo, lag_hi, p.lag_blocks, p.t_grid0, p.nblk, p.bpc, stages};
+  const size_t smem = size_t(stages) * stage_bytes(p.nb) + 1024 + 256;
   cudaFuncSetAttribute(cov_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   dim3 grid(unsigned(p.lag_blocks * (l / 16) * (l / p.nb)), unsigned(p.nchunks));
   cov_i8_kernel<<<grid, NT, smem, s>>>(mapA, mapB, g, e, part);

@@ -24,6 +24,15 @@ constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr int WIN = 32;        // bulge-chase window (rows/cols) of the windowed Francis sweep
 constexpr int TLD = WIN + 1;    // tile row stride (doubles)
+constexpr int HG_WARPS = 4;     // H group (band QR) warps; the rest form the C group
+constexpr int HG_T = HG_WARPS * 32;
+constexpr int CG_T = NT - HG_T;
+constexpr int NSLOT = 8;        // H -> C queue depth
+enum { QWIN = 0, QROT = 1, QEND = 2 };
+struct QEntry {
+  int type, w0, nw, nsteps;
+  double r[3 * (WIN - 3)];      // window reflectors (v1, v2, tau) or rotation (cs, sn)
+};
 constexpr double kUlp = 2.220446049250313e-16;
 constexpr double kSafeMin = 2.2250738585072014e-308;
 
@@ -51,6 +60,42 @@ __host__ __device__ inline size_t x_elems(int n_max) {
   return a > b ? a : b;
 }
 __host__ __device__ inline int band_lo(int i) { return i > 3 ? i - 3 : 0; }
+
+__device__ __forceinline__ void hsync() { asm volatile("bar.sync 1, %0;" ::"n"(HG_T) : "memory"); }
+__device__ __forceinline__ void csync() { asm volatile("bar.sync 2, %0;" ::"n"(CG_T) : "memory"); }
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a), "r"(parity)
+      : "memory");
+}
+
+// seg (a row segment for right updates, a column segment for left updates: element u is index
+// w0 + u) <- seg after the window's reflectors 0..nsteps-1, reflector t acting on u = t..t+2.
+__device__ __forceinline__ void apply_window(double (&seg)[WIN], const double* refl, int nsteps) {
+#pragma unroll
+  for (int u = 0; u < WIN - 3; ++u) {
+    if (u < nsteps) {
+      const double v1 = refl[3 * u], v2 = refl[3 * u + 1], tau = refl[3 * u + 2];
+      const double sum = fma(v2, seg[u + 2], fma(v1, seg[u + 1], seg[u])) * tau;
+      seg[u] -= sum;
+      seg[u + 1] = fma(-sum, v1, seg[u + 1]);
+      seg[u + 2] = fma(-sum, v2, seg[u + 2]);
+    }
+  }
+}
 __host__ __device__ inline size_t band_elems(int n) {
   size_t s = 0;
   for (int i = 0; i < n; ++i) s += size_t(n - band_lo(i));
@@ -81,23 +126,11 @@ struct Smem {
   double* refl;   // 3 n: (v1, v2, tau) per bulge step
   double* x;      // NW * 2 * n: per-warp complex eigenvector
   int* cj;        // cap: block start of candidate
+  QEntry* q;      // NSLOT queue entries (H group -> C group)
+  uint64_t* q_full;
+  uint64_t* q_empty;
   double* cre; double* cim; double* cf; double* cxi;  // cap each
 };
-
-__device__ __forceinline__ double& Hat(const Smem& s, int i, int c) {
-  return s.H[s.rowoff[i] + c - band_lo(i)];
-}
-
-__device__ double block_sum(double v, double* red) {
-  v = warp_sum(v);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int w = 0; w < NW; ++w) t += red[w];
-  return t;
-}
 
 // LAPACK dlanv2: Schur factorization of a real 2x2 nonsymmetric matrix in standardized
 // form. Returns rotation (cs, sn) with [a b; c d]_in = [cs -sn; sn cs][a b; c d]_out[cs sn; -sn cs].
@@ -325,8 +358,15 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     s.cim = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
     s.cf = reinterpret_cast<double*>(p);     p += sizeof(double) * cap;
     s.cxi = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
+    s.q = reinterpret_cast<QEntry*>(p);      p += sizeof(QEntry) * NSLOT;
+    s.q_full = reinterpret_cast<uint64_t*>(p); p += sizeof(uint64_t) * NSLOT;
+    s.q_empty = reinterpret_cast<uint64_t*>(p); p += sizeof(uint64_t) * NSLOT;
     s.rowoff = reinterpret_cast<int*>(p);    p += sizeof(int) * (nm + 1);
     s.cj = reinterpret_cast<int*>(p);
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NSLOT; ++i) { mbar_init1(&s.q_full[i]); mbar_init1(&s.q_empty[i]); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const Band H{s.H, n};
   if (tid == 0) sh_fail = 0;
@@ -338,234 +378,273 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   __syncthreads();
   clk1 = clock64();
 
-  int ihi = n - 1;
-  int its = 0, total_its = 0;
-  const int itmax = 30 * (n > 10 ? n : 10);
-  long long t_scan = 0, t_chase = 0, t_cupd = 0, t_2x2 = 0, steps = 0, t_wchase = 0, t_wdef = 0;
-  while (ihi >= 0) {
-    long long ta = clock64();
-    // deflation test, in parallel: largest ll in (0, ihi] with a negligible subdiagonal
-    if (tid == 0) sh_l = 0;
-    __syncthreads();
-    for (int ll = ihi - tid; ll > 0; ll -= NT) {
-      const double h = fabs(H(ll, ll - 1));
-      bool small = h <= kSafeMin;
-      if (!small) {
-        double tst = fabs(H(ll - 1, ll - 1)) + fabs(H(ll, ll));
-        if (tst == 0.0) {
-          if (ll - 2 >= 0) tst += fabs(H(ll - 1, ll - 2));
-          if (ll + 1 <= ihi) tst += fabs(H(ll + 1, ll));
+  // ---------------- Francis double-shift QR: warps 0-3 (H group) iterate on the band in shared
+  // memory; warps 4-7 (C group) apply the same transformations, in the same order, to the Schur
+  // vectors C (l x n, global/L2), fed through a queue of window-reflector / rotation entries.
+  long long t_scan = 0, t_chase = 0, t_2x2 = 0, steps = 0, t_wchase = 0, t_wdef = 0, t_cwait = 0;
+  int total_its = 0;
+  if (warp < HG_WARPS) {
+    const int htid = tid;
+    int ihi = n - 1;
+    int its = 0;
+    int qslot = 0, quse = 0;          // next queue slot to fill and its use count
+    const int itmax = 30 * (n > 10 ? n : 10);
+    // acquire the next queue slot (all H threads call; thread 0 waits for the C group)
+    auto acquire = [&]() -> QEntry* {
+      if (htid == 0) { const long long tq = clock64(); mbar_wait_parity(&s.q_empty[qslot], (quse & 1) ^ 1); t_cwait += clock64() - tq; }
+      hsync();
+      return s.q + qslot;
+    };
+    auto publish = [&]() {
+      hsync();
+      if (htid == 0) mbar_arrive(&s.q_full[qslot]);
+      if (++qslot == NSLOT) { qslot = 0; ++quse; }
+    };
+    while (ihi >= 0) {
+      long long ta = clock64();
+      // deflation test, in parallel: largest ll in (0, ihi] with a negligible subdiagonal
+      if (htid == 0) sh_l = 0;
+      hsync();
+      for (int ll = ihi - htid; ll > 0; ll -= HG_T) {
+        const double h = fabs(H(ll, ll - 1));
+        bool small = h <= kSafeMin;
+        if (!small) {
+          double tst = fabs(H(ll - 1, ll - 1)) + fabs(H(ll, ll));
+          if (tst == 0.0) {
+            if (ll - 2 >= 0) tst += fabs(H(ll - 1, ll - 2));
+            if (ll + 1 <= ihi) tst += fabs(H(ll + 1, ll));
+          }
+          small = h <= kUlp * tst;
         }
-        small = h <= kUlp * tst;
+        if (small) { atomicMax(&sh_l, ll); break; }
       }
-      if (small) { atomicMax(&sh_l, ll); break; }
-    }
-    __syncthreads();
-    const int lo = sh_l;
-    long long tb = clock64();
-    t_scan += tb - ta;
-    if (lo > 0 && tid == 0) H(lo, lo - 1) = 0.0;
-    if (lo == ihi) { ihi -= 1; its = 0; __syncthreads(); continue; }
-    if (lo == ihi - 1) {
-      const int p = ihi - 1, q = ihi;
-      if (tid == 0) {
-        double a = H(p, p), b = H(p, q), c = H(q, p), d = H(q, q), cs, sn;
-        dlanv2(a, b, c, d, cs, sn);
-        H(p, p) = a; H(p, q) = b; H(q, p) = c; H(q, q) = d;
-        sh_cs = cs; sh_sn = sn;
-      }
-      __syncthreads();
-      const double cs = sh_cs, sn = sh_sn;
-      for (int c = q + 1 + tid; c < n; c += NT) {
-        const double x = H(p, c), y = H(q, c);
-        H(p, c) = cs * x + sn * y;
-        H(q, c) = cs * y - sn * x;
-      }
-      for (int r = tid; r < p + l; r += NT) {
-        if (r < p) {
+      hsync();
+      const int lo = sh_l;
+      long long tb = clock64();
+      t_scan += tb - ta;
+      if (lo > 0 && htid == 0) H(lo, lo - 1) = 0.0;
+      if (lo == ihi) { ihi -= 1; its = 0; hsync(); continue; }
+      if (lo == ihi - 1) {
+        const int p = ihi - 1, q = ihi;
+        QEntry* e = acquire();
+        if (htid == 0) {
+          double a = H(p, p), b = H(p, q), c = H(q, p), d = H(q, q), cs, sn;
+          dlanv2(a, b, c, d, cs, sn);
+          H(p, p) = a; H(p, q) = b; H(q, p) = c; H(q, q) = d;
+          sh_cs = cs; sh_sn = sn;
+          e->type = QROT; e->w0 = p; e->nw = 2; e->nsteps = 0; e->r[0] = cs; e->r[1] = sn;
+        }
+        hsync();
+        const double cs = sh_cs, sn = sh_sn;
+        for (int c = q + 1 + htid; c < n; c += HG_T) {
+          const double x = H(p, c), y = H(q, c);
+          H(p, c) = cs * x + sn * y;
+          H(q, c) = cs * y - sn * x;
+        }
+        for (int r = htid; r < p; r += HG_T) {
           const double x = H(r, p), y = H(r, q);
           H(r, p) = cs * x + sn * y;
           H(r, q) = cs * y - sn * x;
-        } else {
-          double* cr = C + (r - p);
-          const double x = cr[int64_t(p) * l], y = cr[int64_t(q) * l];
-          cr[int64_t(p) * l] = cs * x + sn * y;
-          cr[int64_t(q) * l] = cs * y - sn * x;
         }
+        publish();
+        ihi -= 2; its = 0;
+        t_2x2 += clock64() - tb;
+        continue;
       }
-      __syncthreads();
-      ihi -= 2; its = 0;
-      t_2x2 += clock64() - tb;
-      continue;
-    }
-    ++its; ++total_its;
-    if (its > 100 || total_its > itmax) {
-      if (tid == 0) sh_fail = 1;
-      __syncthreads();
-      break;
-    }
-    // ---------------- one double-shift sweep over [lo, ihi], in windows of WIN rows/cols.
-    // Inside a window [w0, w1) (dense tile in shared memory) warp 0 chases the bulge alone
-    // (warp-synchronous); the parts of each reflector outside the window -- rows [w0, w1) x
-    // columns >= w1 (left), rows < w0 x columns [w0, w1) (right) and the Schur vectors C --
-    // are applied afterwards by all warps, each row / column segment held in registers while
-    // the window's reflectors stream through it. Same arithmetic per element as applying each
-    // reflector in turn (dlahqr), only the order of independent element updates changes.
-    {
-      // shift polynomial (first column of (H - s1)(H - s2)), Francis / exceptional shifts
-      double x0, y0, z0;
+      ++its; ++total_its;
+      if (its > 100 || total_its > itmax) {
+        if (htid == 0) sh_fail = 1;
+        hsync();
+        break;
+      }
+      // ---------------- one double-shift sweep over [lo, ihi], in windows of WIN rows/cols.
+      // Inside a window [w0, w1) (dense tile in shared memory) warp 0 chases the bulge alone
+      // (warp-synchronous); the parts of each reflector outside the window -- rows [w0, w1) x
+      // columns >= w1 (left) and rows < w0 x columns [w0, w1) (right) -- are applied afterwards by
+      // the H group, each row / column segment held in registers while the window's reflectors
+      // stream through it; the C group applies them to the Schur vectors. Same arithmetic per
+      // element as applying each reflector in turn (dlahqr); only independent updates reorder.
       {
-        double h11, h12, h21, h22;
-        if (its == 10) {
-          const double ex = fabs(H(lo + 1, lo)) + fabs(H(lo + 2, lo + 1));
-          h11 = 0.75 * ex + H(lo, lo); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
-        } else if (its == 20) {
-          const double ex = fabs(H(ihi, ihi - 1)) + fabs(H(ihi - 1, ihi - 2));
-          h11 = 0.75 * ex + H(ihi, ihi); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
-        } else {
-          h11 = H(ihi - 1, ihi - 1); h12 = H(ihi - 1, ihi);
-          h21 = H(ihi, ihi - 1); h22 = H(ihi, ihi);
+        // shift polynomial (first column of (H - s1)(H - s2)), Francis / exceptional shifts
+        double x0, y0, z0;
+        {
+          double h11, h12, h21, h22;
+          if (its == 10) {
+            const double ex = fabs(H(lo + 1, lo)) + fabs(H(lo + 2, lo + 1));
+            h11 = 0.75 * ex + H(lo, lo); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
+          } else if (its == 20) {
+            const double ex = fabs(H(ihi, ihi - 1)) + fabs(H(ihi - 1, ihi - 2));
+            h11 = 0.75 * ex + H(ihi, ihi); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
+          } else {
+            h11 = H(ihi - 1, ihi - 1); h12 = H(ihi - 1, ihi);
+            h21 = H(ihi, ihi - 1); h22 = H(ihi, ihi);
+          }
+          const double tr = h11 + h22, det = h11 * h22 - h12 * h21;
+          const double a00 = H(lo, lo), a01 = H(lo, lo + 1), a10 = H(lo + 1, lo), a11 = H(lo + 1, lo + 1);
+          const double a21 = H(lo + 2, lo + 1);
+          x0 = a00 * a00 + a01 * a10 - tr * a00 + det;
+          y0 = a10 * (a00 + a11 - tr);
+          z0 = a10 * a21;
+          const double sc = fabs(x0) + fabs(y0) + fabs(z0);
+          if (sc > 0.0) { x0 /= sc; y0 /= sc; z0 /= sc; }
         }
-        const double tr = h11 + h22, det = h11 * h22 - h12 * h21;
-        const double a00 = H(lo, lo), a01 = H(lo, lo + 1), a10 = H(lo + 1, lo), a11 = H(lo + 1, lo + 1);
-        const double a21 = H(lo + 2, lo + 1);
-        x0 = a00 * a00 + a01 * a10 - tr * a00 + det;
-        y0 = a10 * (a00 + a11 - tr);
-        z0 = a10 * a21;
-        const double sc = fabs(x0) + fabs(y0) + fabs(z0);
-        if (sc > 0.0) { x0 /= sc; y0 /= sc; z0 /= sc; }
-      }
-      double* D = s.x;                 // WIN x TLD tile (aliases the eigenvector scratch)
-      for (int w0 = lo; w0 < ihi; ) {
-        const int kend = (w0 + WIN - 3 < ihi) ? w0 + WIN - 3 : ihi;   // steps k in [w0, kend)
-        const int w1 = (w0 + WIN < ihi + 1) ? w0 + WIN : ihi + 1;    // window rows/cols [w0, w1)
-        const int nw = w1 - w0;
-        // tile D[lr][lc] = H(w0 + lr, w0 - 1 + lc), lr < nw, lc <= nw (structural zeros as 0)
-        for (int e = tid; e < WIN * TLD; e += NT) {
-          const int lr = e / TLD, lc = e - lr * TLD;
-          const int r = w0 + lr, c = w0 - 1 + lc;
-          D[e] = (lr < nw && lc <= nw && c >= 0 && c >= band_lo(r)) ? s.H[s.rowoff[r] + c] : 0.0;
-        }
-        __syncthreads();
-        const long long tw0 = clock64();
-        if (warp == 0) {
-          for (int k = w0; k < kend; ++k) {
-            const int t = k - w0;
-            const int nr = (ihi - k + 1) < 3 ? (ihi - k + 1) : 3;
-            double x, y, z;
-            if (k == lo) { x = x0; y = y0; z = nr == 3 ? z0 : 0.0; }
-            else { x = D[t * TLD + t]; y = D[(t + 1) * TLD + t]; z = nr == 3 ? D[(t + 2) * TLD + t] : 0.0; }
-            double tau = 0.0, v1 = 0.0, v2 = 0.0, beta = 0.0;
-            const double yz = y * y + z * z;
-            if (yz != 0.0) {
-              // beta = -sign(x) sqrt(s); tau = 1 + |x|/sqrt(s); v = sign(x) (y, z)/(|x| + sqrt(s))
-              const double ss = x * x + yz;
-              const double rs = fast_rsqrt(ss);
-              const double sq = ss * rs;
-              beta = -copysign(sq, x);
-              tau = fma(fabs(x), rs, 1.0);
-              const double inv = copysign(fast_rcp(fabs(x) + sq), x);
-              v1 = y * inv; v2 = z * inv;
-            }
-            __syncwarp();
-            if (lane == 0) {
-              if (yz != 0.0 && k > lo) {
-                D[t * TLD + t] = beta; D[(t + 1) * TLD + t] = 0.0;
-                if (nr == 3) D[(t + 2) * TLD + t] = 0.0;
+        double* D = s.x;                 // WIN x TLD tile (aliases the eigenvector scratch)
+        for (int w0 = lo; w0 < ihi; ) {
+          const int kend = (w0 + WIN - 3 < ihi) ? w0 + WIN - 3 : ihi;   // steps k in [w0, kend)
+          const int w1 = (w0 + WIN < ihi + 1) ? w0 + WIN : ihi + 1;    // window rows/cols [w0, w1)
+          const int nw = w1 - w0;
+          const int nsteps = kend - w0;
+          QEntry* qe = acquire();
+          // tile D[lr][lc] = H(w0 + lr, w0 - 1 + lc), lr < nw, lc <= nw (structural zeros as 0)
+          for (int e = htid; e < WIN * TLD; e += HG_T) {
+            const int lr = e / TLD, lc = e - lr * TLD;
+            const int r = w0 + lr, c = w0 - 1 + lc;
+            D[e] = (lr < nw && lc <= nw && c >= 0 && c >= band_lo(r)) ? s.H[s.rowoff[r] + c] : 0.0;
+          }
+          hsync();
+          const long long tw0 = clock64();
+          if (warp == 0) {
+            double* refl = qe->r;
+            for (int k = w0; k < kend; ++k) {
+              const int t = k - w0;
+              const int nr = (ihi - k + 1) < 3 ? (ihi - k + 1) : 3;
+              double x, y, z;
+              if (k == lo) { x = x0; y = y0; z = nr == 3 ? z0 : 0.0; }
+              else { x = D[t * TLD + t]; y = D[(t + 1) * TLD + t]; z = nr == 3 ? D[(t + 2) * TLD + t] : 0.0; }
+              double tau = 0.0, v1 = 0.0, v2 = 0.0, beta = 0.0;
+              const double yz = y * y + z * z;
+              if (yz != 0.0) {
+                // beta = -sign(x) sqrt(s); tau = 1 + |x|/sqrt(s); v = sign(x) (y, z)/(|x| + sqrt(s))
+                const double ss = x * x + yz;
+                const double rs = fast_rsqrt(ss);
+                const double sq = ss * rs;
+                beta = -copysign(sq, x);
+                tau = fma(fabs(x), rs, 1.0);
+                const double inv = copysign(fast_rcp(fabs(x) + sq), x);
+                v1 = y * inv; v2 = z * inv;
               }
-              s.refl[3 * t + 0] = v1;
-              s.refl[3 * t + 1] = v2;
-              s.refl[3 * t + 2] = tau;
-            }
-            if (tau != 0.0) {
-              // left: rows t..t+nr-1, columns k..w1-1 (local t+1 .. nw)
-              {
-                const int lc = t + 1 + lane;
-                if (lc <= nw) {
-                  double* p0 = D + t * TLD + lc;
-                  const double b0 = p0[0], b1 = p0[TLD], b2 = nr == 3 ? p0[2 * TLD] : 0.0;
-                  const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
-                  p0[0] = b0 - sum; p0[TLD] = fma(-sum, v1, b1);
-                  if (nr == 3) p0[2 * TLD] = fma(-sum, v2, b2);
+              __syncwarp();
+              if (lane == 0) {
+                if (yz != 0.0 && k > lo) {
+                  D[t * TLD + t] = beta; D[(t + 1) * TLD + t] = 0.0;
+                  if (nr == 3) D[(t + 2) * TLD + t] = 0.0;
+                }
+                refl[3 * t + 0] = v1;
+                refl[3 * t + 1] = v2;
+                refl[3 * t + 2] = tau;
+              }
+              if (tau != 0.0) {
+                // left: rows t..t+nr-1, columns k..w1-1 (local t+1 .. nw)
+                {
+                  const int lc = t + 1 + lane;
+                  if (lc <= nw) {
+                    double* p0 = D + t * TLD + lc;
+                    const double b0 = p0[0], b1 = p0[TLD], b2 = nr == 3 ? p0[2 * TLD] : 0.0;
+                    const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
+                    p0[0] = b0 - sum; p0[TLD] = fma(-sum, v1, b1);
+                    if (nr == 3) p0[2 * TLD] = fma(-sum, v2, b2);
+                  }
+                }
+                __syncwarp();
+                // right: columns k..k+nr-1 (local t+1..), rows w0..min(k+3, ihi)
+                {
+                  const int rmax = (k + 3 < ihi ? k + 3 : ihi) - w0;
+                  if (lane <= rmax) {
+                    double* p0 = D + lane * TLD + t + 1;
+                    const double b0 = p0[0], b1 = p0[1], b2 = nr == 3 ? p0[2] : 0.0;
+                    const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
+                    p0[0] = b0 - sum; p0[1] = fma(-sum, v1, b1);
+                    if (nr == 3) p0[2] = fma(-sum, v2, b2);
+                  }
                 }
               }
               __syncwarp();
-              // right: columns k..k+nr-1 (local t+1..), rows w0..min(k+3, ihi)
-              {
-                const int rmax = (k + 3 < ihi ? k + 3 : ihi) - w0;
-                if (lane <= rmax) {
-                  double* p0 = D + lane * TLD + t + 1;
-                  const double b0 = p0[0], b1 = p0[1], b2 = nr == 3 ? p0[2] : 0.0;
-                  const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
-                  p0[0] = b0 - sum; p0[1] = fma(-sum, v1, b1);
-                  if (nr == 3) p0[2] = fma(-sum, v2, b2);
-                }
-              }
             }
-            __syncwarp();
+            if (lane == 0) { qe->type = QWIN; qe->w0 = w0; qe->nw = nw; qe->nsteps = nsteps; }
           }
-        }
-        __syncthreads();
-        const long long tw1 = clock64();
-        t_wchase += tw1 - tw0;
-        const int nsteps = kend - w0;
-        // write the tile back
-        for (int e = tid; e < WIN * TLD; e += NT) {
-          const int lr = e / TLD, lc = e - lr * TLD;
-          const int r = w0 + lr, c = w0 - 1 + lc;
-          if (lr < nw && lc <= nw && c >= 0 && c >= band_lo(r)) s.H[s.rowoff[r] + c] = D[e];
-        }
-        // deferred parts: (L) columns c in [w1, n), rows [w0, w1); (R) rows r in [0, w0),
-        // columns [w0, w1); (C) Schur vectors C[a][w0..w1), a in [0, l)
-        const int nL = n - w1, nR = w0;
-        for (int task = tid; task < nL + nR + l; task += NT) {
-          double seg[WIN];
-          if (task < nL) {
+          publish();                     // the C group may start on this window
+          const long long tw1 = clock64();
+          t_wchase += tw1 - tw0;
+          const double* refl = qe->r;
+          // write the tile back
+          for (int e = htid; e < WIN * TLD; e += HG_T) {
+            const int lr = e / TLD, lc = e - lr * TLD;
+            const int r = w0 + lr, c = w0 - 1 + lc;
+            if (lr < nw && lc <= nw && c >= 0 && c >= band_lo(r)) s.H[s.rowoff[r] + c] = D[e];
+          }
+          // deferred parts: (L) columns c in [w1, n), rows [w0, w1); (R) rows r in [0, w0),
+          // columns [w0, w1)
+          const int nL = n - w1, nR = w0;
+          for (int task = htid; task < nL + nR; task += HG_T) {
+            double seg[WIN];
+            const bool isL = task < nL;
             const int c = w1 + task;
+            double* row = s.H + (isL ? 0 : s.rowoff[task - nL] + w0);
+            if (isL) {
 #pragma unroll
-            for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? s.H[s.rowoff[w0 + u] + c] : 0.0;
-          } else if (task < nL + nR) {
-            const double* row = s.H + s.rowoff[task - nL] + w0;
+              for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? s.H[s.rowoff[w0 + u] + c] : 0.0;
+            } else {
 #pragma unroll
-            for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? row[u] : 0.0;
-          } else {
-            const double* cr = C + (task - nL - nR) + int64_t(w0) * l;
+              for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? row[u] : 0.0;
+            }
+            apply_window(seg, refl, nsteps);
+            if (isL) {
 #pragma unroll
-            for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? cr[int64_t(u) * l] : 0.0;
-          }
+              for (int u = 0; u < WIN; ++u) if (u < nw) s.H[s.rowoff[w0 + u] + c] = seg[u];
+            } else {
 #pragma unroll
-          for (int u = 0; u < WIN - 3; ++u) {
-            if (u < nsteps) {
-              const double v1 = s.refl[3 * u], v2 = s.refl[3 * u + 1], tau = s.refl[3 * u + 2];
-              const double sum = fma(v2, seg[u + 2], fma(v1, seg[u + 1], seg[u])) * tau;
-              seg[u] -= sum;
-              seg[u + 1] = fma(-sum, v1, seg[u + 1]);
-              seg[u + 2] = fma(-sum, v2, seg[u + 2]);
+              for (int u = 0; u < WIN; ++u) if (u < nw) row[u] = seg[u];
             }
           }
-          if (task < nL) {
-            const int c = w1 + task;
-#pragma unroll
-            for (int u = 0; u < WIN; ++u) if (u < nw) s.H[s.rowoff[w0 + u] + c] = seg[u];
-          } else if (task < nL + nR) {
-            double* row = s.H + s.rowoff[task - nL] + w0;
-#pragma unroll
-            for (int u = 0; u < WIN; ++u) if (u < nw) row[u] = seg[u];
-          } else {
-            double* cr = C + (task - nL - nR) + int64_t(w0) * l;
-#pragma unroll
-            for (int u = 0; u < WIN; ++u) if (u < nw) cr[int64_t(u) * l] = seg[u];
-          }
+          hsync();
+          t_wdef += clock64() - tw1;
+          w0 = kend;
         }
-        __syncthreads();
-        t_wdef += clock64() - tw1;
-        w0 = kend;
       }
+      long long tc = clock64();
+      t_chase += tc - tb;
+      steps += ihi - lo;
     }
-    long long tc = clock64();
-    t_chase += tc - tb;
-    steps += ihi - lo;
+    // end of the queue
+    acquire();
+    if (htid == 0) s.q[qslot].type = QEND;
+    publish();
+  } else {
+    // ---------------- C group: C[:, w0:w0+nw) <- C[:, w0:w0+nw) P_w0 ... P_{kend-1}, rotations
+    const int ctid = tid - HG_T;
+    int slot = 0, use = 0;
+    while (true) {
+      mbar_wait_parity(&s.q_full[slot], use & 1);
+      const QEntry* e = s.q + slot;
+      const int type = e->type;
+      if (type == QEND) break;
+      const int w0 = e->w0, nw = e->nw;
+      if (type == QWIN) {
+        const int nsteps = e->nsteps;
+        for (int a = ctid; a < l; a += CG_T) {
+          double* cr = C + a + int64_t(w0) * l;
+          double seg[WIN];
+#pragma unroll
+          for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? cr[int64_t(u) * l] : 0.0;
+          apply_window(seg, e->r, nsteps);
+#pragma unroll
+          for (int u = 0; u < WIN; ++u) if (u < nw) cr[int64_t(u) * l] = seg[u];
+        }
+      } else {   // QROT: columns p = w0, q = w0 + 1
+        const double cs = e->r[0], sn = e->r[1];
+        for (int a = ctid; a < l; a += CG_T) {
+          double* cr = C + a;
+          const double x = cr[int64_t(w0) * l], y = cr[int64_t(w0 + 1) * l];
+          cr[int64_t(w0) * l] = cs * x + sn * y;
+          cr[int64_t(w0 + 1) * l] = cs * y - sn * x;
+        }
+      }
+      csync();
+      if (ctid == 0) mbar_arrive(&s.q_empty[slot]);
+      if (++slot == NSLOT) { slot = 0; ++use; }
+    }
   }
+  __syncthreads();
   clk2 = clock64();
   qr_its = total_its;
   if (sh_fail) {
@@ -715,14 +794,15 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     }
   }
   if (g.profile && tid == 0 && (g.profile > 1 || o == g.n_orders - 1 || o == g.n_orders / 2))
-    printf("eig order n=%d: band load %lld qr %lld (its %lld) vectors %lld cycles | scan %lld chase %lld (steps %lld) cupd %lld 2x2 %lld | wchase %lld wdef %lld\n", n, clk1 - clk0,
-           clk2 - clk1, qr_its, clock64() - clk2, t_scan, t_chase, steps, t_cupd, t_2x2, t_wchase, t_wdef);
+    printf("eig order n=%d: band load %lld qr %lld (its %lld) vectors %lld cycles | scan %lld chase %lld (steps %lld) cwait %lld 2x2 %lld | wchase %lld wdef %lld\n", n, clk1 - clk0,
+           clk2 - clk1, qr_its, clock64() - clk2, t_scan, t_chase, steps, t_cwait, t_2x2, t_wchase, t_wdef);
 }
 
 }  // namespace
 
 size_t modal_smem_bytes(int n_max, int cap) {
-  return sizeof(double) * (band_elems(n_max) + n_max + 3 * size_t(n_max) + x_elems(n_max) +
+  return sizeof(QEntry) * NSLOT + 2 * sizeof(uint64_t) * NSLOT +
+         sizeof(double) * (band_elems(n_max) + n_max + 3 * size_t(n_max) + x_elems(n_max) +
                            4 * size_t(cap)) +
          sizeof(int) * (size_t(n_max) + 1 + cap) + 64;
 }
