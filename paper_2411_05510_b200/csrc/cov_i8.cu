@@ -255,10 +255,10 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
 
   if (nblk > 0) {
     if (warp == 0 && lane == 0) {
-      // ---------------- TMA producer
+      // ---------------- TMA producer (stage index and phase kept incrementally)
+      int s = 0;
+      uint32_t ph = 0;
       for (int64_t it = 0; it < nblk; ++it) {
-        const int s = int(it % STAGES);
-        const uint32_t ph = uint32_t((it / STAGES) & 1);
         mbar_wait(empty + s, ph ^ 1);
         uint8_t* A = smem + s * SB;
         uint8_t* B = A + A_PAD;
@@ -266,6 +266,7 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
         mbar_expect_tx(full + s, A_BYTES + b_bytes(g.nb));
         tma_load_4d(A, &mapA, full + s, 0, int(t0 + k0), cg, 0);
         tma_load_3d(B, &mapB, full + s, int(t0), b0, 0);
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     } else if (warp == 1 && lane == 0) {
       // ---------------- MMA issuer: 4 K-steps x UNITS x 8 slice products per block
@@ -275,13 +276,20 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
       const int pa[8] = {0, 0, 1, 1, 0, 2, 1, 2};
       const int pb[8] = {0, 1, 0, 1, 2, 0, 2, 1};
       const int pw[8] = {0, 1, 1, 2, 2, 2, 3, 3};
+      // descriptors of stage 0; a stage / slice / K offset adds (bytes >> 4) to the start-address
+      // field (addresses < 256 KB: the 14-bit field never carries)
+      const uint32_t abase0 = smem_u32(smem);
+      const uint64_t ad0 = umma_desc(abase0, 128, 16, 0);
+      const uint64_t bd0 = umma_desc(abase0 + A_PAD, 16, 1024, 2);
+      const uint32_t b_slice16 = uint32_t(g.nb * KT) >> 4;
+      const uint32_t sb16 = uint32_t(SB) >> 4;
+      int s = 0;
+      uint32_t ph = 0;
       for (int64_t it = 0; it < nblk; ++it) {
-        const int s = int(it % STAGES);
-        const uint32_t ph = uint32_t((it / STAGES) & 1);
         mbar_wait(full + s, ph);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t abase = smem_u32(smem + s * SB);
-        const uint32_t bbase = abase + A_PAD;
+        const uint64_t ads = ad0 + uint64_t(uint32_t(s) * sb16);
+        const uint64_t bds = bd0 + uint64_t(uint32_t(s) * sb16);
 #pragma unroll
         for (int j = 0; j < KT / 32; ++j) {
 #pragma unroll
@@ -289,14 +297,15 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               // A: slice column, K offset 32 j samples, unit offset 8 un samples (16 B each)
-              const uint64_t ad = umma_desc(abase + pa[q] * A_SLICE_BYTES + (32 * j + LPU * un) * 16, 128, 16, 0);
-              const uint64_t bd = umma_desc(bbase + pb[q] * (g.nb * KT) + 32 * j, 16, 1024, 2);
+              const uint64_t ad = ads + uint64_t((pa[q] * A_SLICE_BYTES + (32 * j + LPU * un) * 16) >> 4);
+              const uint64_t bd = bds + uint64_t(uint32_t(pb[q]) * b_slice16 + uint32_t((32 * j) >> 4));
               const bool first = (it == 0 && j == 0) && (q == 0 || q == 1 || q == 3 || q == 6);
               umma_i8(tmem + uint32_t((un * NW + pw[q]) * g.nb), ad, bd, idesc, first ? 0u : 1u);
             }
           }
         }
         umma_commit(empty + s);      // frees the smem stage when these MMAs complete
+        if (++s == STAGES) { s = 0; ph ^= 1; }
       }
       umma_commit(done);
     }
@@ -320,6 +329,9 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
         tmem_ld16(lane_base + col + uint32_t(2 * g.nb), v4);
         tmem_ld16(lane_base + col + uint32_t(3 * g.nb), v5);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        double sb[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) sb[c] = ldexp(1.0, __ldg(e + b0 + c0 + c));
         if (valid) {
 #pragma unroll
           for (int c = 0; c < 16; c += 2) {
@@ -329,7 +341,7 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
               constexpr double i2 = 1.0 / (kBase * kBase), i3 = i2 / kBase, i4 = i3 / kBase, i5 = i4 / kBase;
               const double acc = ((double(v5[c + h]) * i5 + double(v4[c + h]) * i4) + double(v3[c + h]) * i3) +
                                  double(v2[c + h]) * i2;
-              r[h] = acc * sa * ldexp(1.0, __ldg(e + b0 + c0 + c + h));
+              r[h] = acc * sa * sb[c + h];
             }
             *reinterpret_cast<double2*>(out + c0 + c) = make_double2(r[0], r[1]);
           }
