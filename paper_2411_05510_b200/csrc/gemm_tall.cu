@@ -150,7 +150,7 @@ int tall_splits(int64_t M, int64_t K) {
   // smallest split count whose tile count is within 3% of a whole number of waves
   int best = 1;
   double best_eff = 0.0;
-  for (int s = 1; s <= 16; ++s) {
+  for (int s = 1; s <= 64; ++s) {
     if (K / s < 4 * BK) break;
     const double units = double(tiles * s);
     const double waves = units / 148.0;

@@ -20,6 +20,7 @@ constexpr int kGroups = 4;
 __global__ void __launch_bounds__(kCholThreads) chol_inv_kernel(const double* __restrict__ W, int k,
                                                                 double* __restrict__ L,
                                                                 double* __restrict__ Linv,
+                                                                double* __restrict__ LinvT,
                                                                 double* gscratch, int use_smem,
                                                                 int32_t* status) {
   extern __shared__ __align__(16) double sm[];
@@ -104,6 +105,7 @@ __global__ void __launch_bounds__(kCholThreads) chol_inv_kernel(const double* __
   for (int64_t e = tid; e < int64_t(k) * k; e += nt) {
     const int r = int(e % k), c = int(e / k);
     Linv[e] = (c <= r) ? P[r * (r + 1) / 2 + c] : 0.0;
+    if (LinvT) LinvT[e] = (r <= c) ? P[c * (c + 1) / 2 + r] : 0.0;
   }
 }
 
@@ -215,16 +217,22 @@ void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w) {
   w.Linv1 = c.take<double>(size_t(k) * k);
   w.L2 = c.take<double>(size_t(k) * k);
   w.Linv2 = c.take<double>(size_t(k) * k);
+  w.LinvT1 = c.take<double>(size_t(k) * k);
+  w.LinvT2 = c.take<double>(size_t(k) * k);
   w.Q1 = c.take<double>(size_t(m) * k);
   w.chol_g = c.take<double>(size_t(k) * (k + 1) / 2);
   w.partial = c.take<double>(cholqr_partial_elems(m, k) + 1);
+  // gemm_tall uses s <= min(64, K/64) splits: upper bounds, non-decreasing in m
+  const size_t s2 = size_t(k / 64 > 1 ? (k / 64 < 64 ? k / 64 : 64) : 1);
+  const size_t t1 = size_t(64) * k * k, t2 = s2 > 1 ? s2 * size_t(m) * k : 0;
+  w.tallp = c.take<double>((t1 > t2 ? t1 : t2) + 1);
 }
 
 static size_t chol_smem_bytes(int k) {
   return (size_t(k) * (1 + kGroups) + size_t(k) * (k + 1) / 2) * sizeof(double);
 }
 
-ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* gscratch,
+ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* LinvT, double* gscratch,
                     int32_t* status, cudaStream_t s) {
   const size_t smem_full = chol_smem_bytes(k);
   const bool use_smem = smem_full <= 220 * 1024;
@@ -232,24 +240,31 @@ ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* gsc
   if (smem > 48 * 1024) {
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   }
-  chol_inv_kernel<<<1, kCholThreads, smem, s>>>(W, k, L, Linv, gscratch, use_smem ? 1 : 0, status);
+  chol_inv_kernel<<<1, kCholThreads, smem, s>>>(W, k, L, Linv, LinvT, gscratch, use_smem ? 1 : 0, status);
   return launch_check("chol_inv_kernel");
 }
 
 ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, CholQRWork& w,
                    int32_t* status, cudaStream_t s) {
+  // tall-skinny DMMA kernels (cp.async 16-byte pieces) when the shapes and alignment allow
+  const bool tall = k <= kTallMaxN && ldy % 2 == 0 && m % 2 == 0 && k % 2 == 0 &&
+                    (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0;
   const int splits = gemm_pick_splits(k, k, m);
-  // W = Y^T Y : A(i,kk) = Y[kk + i*ldy] (k-contiguous), B(kk,j) = Y[kk + j*ldy]
-  SSI_TRY(gemm_f64(k, k, m, 1.0, Operand{Y, ldy, 1}, Operand{Y, 1, ldy}, w.W, k, splits,
-                   w.partial, s));
-  SSI_TRY(chol_inv(w.W, k, w.L1, w.Linv1, w.chol_g, status, s));
-  // Q1 = Y Linv1^T : B(kk,j) = Linv1[j + kk*k]
-  SSI_TRY(gemm_f64(m, k, k, 1.0, Operand{Y, 1, ldy}, Operand{w.Linv1, k, 1}, w.Q1, m, 1,
-                   nullptr, s));
-  SSI_TRY(gemm_f64(k, k, m, 1.0, Operand{w.Q1, m, 1}, Operand{w.Q1, 1, m}, w.W, k, splits,
-                   w.partial, s));
-  SSI_TRY(chol_inv(w.W, k, w.L2, w.Linv2, w.chol_g, status, s));
-  return gemm_f64(m, k, k, 1.0, Operand{w.Q1, 1, m}, Operand{w.Linv2, k, 1}, Q, m, 1, nullptr, s);
+  auto gram = [&](const double* X, int64_t ldx) -> ssi_status {   // W = X^T X
+    if (tall) return gemm_tall(k, k, m, true, X, ldx, X, ldx, w.W, k, w.tallp, s);
+    return gemm_f64(k, k, m, 1.0, Operand{X, ldx, 1}, Operand{X, 1, ldx}, w.W, k, splits, w.partial, s);
+  };
+  auto trmul = [&](const double* X, int64_t ldx, const double* Linv, const double* LinvT, double* out) {
+    // out = X Linv^T  (B(kk, j) = Linv(j, kk) = LinvT[kk + j k])
+    if (tall) return gemm_tall(m, k, k, false, X, ldx, LinvT, k, out, m, w.tallp, s);
+    return gemm_f64(m, k, k, 1.0, Operand{X, 1, ldx}, Operand{Linv, k, 1}, out, m, 1, nullptr, s);
+  };
+  SSI_TRY(gram(Y, ldy));
+  SSI_TRY(chol_inv(w.W, k, w.L1, w.Linv1, w.LinvT1, w.chol_g, status, s));
+  SSI_TRY(trmul(Y, ldy, w.Linv1, w.LinvT1, w.Q1));
+  SSI_TRY(gram(w.Q1, m));
+  SSI_TRY(chol_inv(w.W, k, w.L2, w.Linv2, w.LinvT2, w.chol_g, status, s));
+  return trmul(w.Q1, m, w.Linv2, w.LinvT2, Q);
 }
 
 template <int KPL>

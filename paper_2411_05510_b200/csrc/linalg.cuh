@@ -11,9 +11,12 @@ struct CholQRWork {
   double* Linv1;    // k x k lower, its inverse
   double* L2;
   double* Linv2;
+  double* LinvT1;   // Linv1^T and Linv2^T (col-major k x k): B operands of the tall products
+  double* LinvT2;
   double* Q1;       // m x k intermediate
   double* chol_g;   // packed triangle when k is too large for shared memory
   double* partial;  // split-K partials
+  double* tallp;    // split-K partials of the tall-skinny kernels
 };
 size_t cholqr_partial_elems(int64_t m, int k);
 void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w);
@@ -24,7 +27,7 @@ ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, Ch
                    int32_t* status, cudaStream_t s);
 
 // Single-CTA Cholesky W = L L^T and L^{-1} (lower, col-major ld k).
-ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* gscratch,
+ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* LinvT, double* gscratch,
                     int32_t* status, cudaStream_t s);
 
 // One-sided (Hestenes) Jacobi SVD of a k x k matrix G (col-major, overwritten):

@@ -88,7 +88,7 @@ ssi_status rsvd_run(const double* T, int64_t ldT, int64_t m, int k, int q, uint6
 // ---------------------------------------------------------------- structured (T never formed)
 struct RsvdBtWork {
   RsvdWork base;
-  double *Bb, *Xh, *Yh;
+  double *Bb, *Xh, *Yh, *tables;
 };
 
 static void rsvd_bt_carve(Carver& c, int l, int i, int k, RsvdBtWork& w) {
@@ -105,6 +105,7 @@ static void rsvd_bt_carve(Carver& c, int l, int i, int k, RsvdBtWork& w) {
   w.Bb = c.take<double>(bt_spectrum_elems(l, i));
   w.Xh = c.take<double>(bt_freq_elems(l, i, k));
   w.Yh = c.take<double>(bt_freq_elems(l, i, k));
+  w.tables = c.take<double>(bt_table_elems(i));
 }
 
 size_t rsvd_bt_ws_bytes(int l, int i, int k) {
@@ -122,9 +123,9 @@ ssi_status rsvd_bt_run(const double* R, int l, int i, int k, int q, uint64_t see
   rsvd_bt_carve(c, l, i, k, w);
   const int64_t m = int64_t(l) * i;
   // spectrum of the block sequence B_d = R_{i+d}, once per call
-  SSI_TRY(bt_spectrum(R, l, i, w.Bb, s));
+  SSI_TRY(bt_spectrum(R, l, i, w.Bb, w.tables, s));
   auto pass = [&](bool trans, const double* X, double* out) -> ssi_status {
-    return bt_apply(w.Bb, l, i, k, trans, X, m, out, m, w.Xh, w.Yh, s);
+    return bt_apply(w.Bb, w.tables, l, i, k, trans, X, m, out, m, w.Xh, w.Yh, s);
   };
   return rsvd_core(pass, m, k, q, seed, sid, n_keep, U, ldU, S, w.base, status, s);
 }

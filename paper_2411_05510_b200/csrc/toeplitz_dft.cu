@@ -70,8 +70,9 @@ __global__ void __launch_bounds__(DT) bt_spectrum_kernel(const double* __restric
   }
 }
 
-// hatX_f = sum_{c<i} X_c w^{fc}: Xh[f][j][0:l] = Re, Xh[f][j][l:2l] = Im (per f a 2l x k
-// col-major matrix, ld 2l). CTA: 32 rows a of one column j; 8 warps over f.
+// hatX_f = sum_{c<i} X_c w^{fc}: Xh[j][f][0:l] = Re, Xh[j][f][l:2l] = Im (per f a 2l x k
+// col-major matrix, ld 2l F). CTA: 32 rows a of one column j; 8 warps over f. (Odd l; for even l
+// the forward and inverse DFTs run as batched DMMA GEMMs against the tables of bt_tables_kernel.)
 __global__ void __launch_bounds__(DT) bt_forward_kernel(const double* __restrict__ X, int64_t ldx, int l, int i,
                                                         int k, double* __restrict__ Xh) {
   extern __shared__ __align__(16) double sm[];
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(DT) bt_forward_kernel(const double* __restrict
       t += f;
       if (t >= P) t -= P;
     }
-    double* o = Xh + (int64_t(f) * k + j) * L2;
+    double* o = Xh + (int64_t(j) * F + f) * L2;
     o[a] = re;
     o[l + a] = im;
   }
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(DT) bt_inverse_kernel(const double* __restrict
   twiddles(P, cs, sn);
   const int64_t L2 = 2 * int64_t(l);
   for (int f = warp; f < F; f += DW) {
-    const double* src = Yh + (int64_t(f) * k + j) * L2;
+    const double* src = Yh + (int64_t(j) * F + f) * L2;
     ys[(2 * f) * 32 + lane] = ok ? src[a] : 0.0;
     ys[(2 * f + 1) * 32 + lane] = ok ? src[l + a] : 0.0;
   }
@@ -144,12 +145,38 @@ __global__ void __launch_bounds__(DT) bt_inverse_kernel(const double* __restrict
 
 size_t smem_twiddle(int i) { return sizeof(double) * 2 * size_t(2 * i - 1); }
 
+// DFT matrices of the GEMM form (l even): Ft (i x 2F col-major, ld ldF): Ft[c][2f] = cos(2 pi f c/P),
+// Ft[c][2f+1] = -sin(...); Gt (2F x i col-major): Gt[2f][r] = w_f cos(2 pi r f/P)/P,
+// Gt[2f+1][r] = -w_f sin(2 pi r f/P)/P, w_0 = 1, w_f = 2 (f >= 1).
+__global__ void bt_tables_kernel(int i, int ldF, double* __restrict__ Ft, double* __restrict__ Gt) {
+  const int P = 2 * i - 1, F = i;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < F * i; e += gridDim.x * blockDim.x) {
+    const int f = e / i, c = e % i;            // (f, c) for Ft; (f, r = c) for Gt
+    const int t = int((int64_t(f) * c) % P);
+    double sn, cs;
+    sincospi(2.0 * double(t) / double(P), &sn, &cs);
+    Ft[c + int64_t(2 * f) * ldF] = cs;
+    Ft[c + int64_t(2 * f + 1) * ldF] = -sn;
+    const double w = (f == 0 ? 1.0 : 2.0) / double(P);
+    Gt[2 * f + int64_t(c) * 2 * F] = w * cs;
+    Gt[2 * f + 1 + int64_t(c) * 2 * F] = -w * sn;
+    if (c == 0 && ldF > i) {               // zero pad row (read in 16-byte pairs by the GEMM)
+      for (int cc = i; cc < ldF; ++cc) { Ft[cc + int64_t(2 * f) * ldF] = 0.0; Ft[cc + int64_t(2 * f + 1) * ldF] = 0.0; }
+    }
+  }
+}
+
 }  // namespace
 
 size_t bt_spectrum_elems(int l, int i) { return size_t(i) * 4 * size_t(l) * l; }
+int bt_ldF(int i) { return (i + 1) & ~1; }
+size_t bt_table_elems(int i) { return size_t(bt_ldF(i)) * 2 * i + size_t(2 * i) * i; }
 size_t bt_freq_elems(int l, int i, int k) { return size_t(i) * 2 * size_t(l) * k; }
 
-ssi_status bt_spectrum(const double* R, int l, int i, double* Bb, cudaStream_t s) {
+ssi_status bt_spectrum(const double* R, int l, int i, double* Bb, double* tables, cudaStream_t s) {
+  bt_tables_kernel<<<unsigned((i * i + 255) / 256), 256, 0, s>>>(i, bt_ldF(i), tables,
+                                                              tables + size_t(bt_ldF(i)) * 2 * i);
+  SSI_TRY(launch_check("bt_tables_kernel"));
   const int P = 2 * i - 1;
   const size_t smem = smem_twiddle(i) + sizeof(double) * size_t(P) * 32;
   if (smem > 48 * 1024)
@@ -159,25 +186,43 @@ ssi_status bt_spectrum(const double* R, int l, int i, double* Bb, cudaStream_t s
   return launch_check("bt_spectrum_kernel");
 }
 
-ssi_status bt_apply(const double* Bb, int l, int i, int k, bool trans, const double* X, int64_t ldx,
-                    double* Y, int64_t ldy, double* Xh, double* Yh, cudaStream_t s) {
+bool bt_gemm_form(int l, int i) { return l % 2 == 0 && 2 * i <= kTallMaxN; }
+
+ssi_status bt_apply(const double* Bb, const double* tables, int l, int i, int k, bool trans, const double* X,
+                    int64_t ldx, double* Y, int64_t ldy, double* Xh, double* Yh, cudaStream_t s) {
   const int F = i;
-  const size_t smem_f = smem_twiddle(i) + sizeof(double) * size_t(i) * 32;
-  const size_t smem_i = smem_twiddle(i) + sizeof(double) * size_t(F) * 2 * 32;
-  if (smem_f > 48 * 1024)
-    cudaFuncSetAttribute(bt_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_f));
-  if (smem_i > 48 * 1024)
-    cudaFuncSetAttribute(bt_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_i));
-  const dim3 grid(unsigned((l + 31) / 32), unsigned(k));
-  bt_forward_kernel<<<grid, DT, smem_f, s>>>(X, ldx, l, i, k, Xh);
-  SSI_TRY(launch_check("bt_forward_kernel"));
   const int64_t L2 = 2 * int64_t(l);
+  const bool gemm_form = bt_gemm_form(l, i) && ldx % 2 == 0 && ldy % 2 == 0 &&
+                         (reinterpret_cast<uintptr_t>(X) & 15) == 0 && (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  // frequency-domain layout: per column j, F blocks of (Re[l], Im[l]): hatX[j][f][part][a]
+  const int64_t ldh = L2 * F;                 // column stride of one frequency's 2l x k matrix
+  if (gemm_form) {
+    // hatX(:, (f, part)) of column j = X_j (l x i, col-major ld l) * Ft (i x 2F)
+    const double* Ft = tables;
+    SSI_TRY(gemm_tall_batched(l, 2 * F, i, false, X, l, ldx, Ft, bt_ldF(i), 0, Xh, l, ldh, k, s));
+  } else {
+    const size_t smem_f = smem_twiddle(i) + sizeof(double) * size_t(i) * 32;
+    if (smem_f > 48 * 1024)
+      cudaFuncSetAttribute(bt_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_f));
+    const dim3 grid(unsigned((l + 31) / 32), unsigned(k));
+    bt_forward_kernel<<<grid, DT, smem_f, s>>>(X, ldx, l, i, k, Xh);
+    SSI_TRY(launch_check("bt_forward_kernel"));
+  }
   // hatY_f = Bblk_f hatX_f (T X) or Bblk_f^T hatX_f (T^T X), in column chunks of <= 224
   for (int j0 = 0; j0 < k; j0 += kTallMaxN) {
     const int nj = k - j0 < kTallMaxN ? k - j0 : kTallMaxN;
-    SSI_TRY(gemm_tall_batched(L2, nj, L2, !trans, Bb, L2, L2 * L2, Xh + j0 * L2, L2, L2 * k,
-                              Yh + j0 * L2, L2, L2 * k, F, s));
+    SSI_TRY(gemm_tall_batched(L2, nj, L2, !trans, Bb, L2, L2 * L2, Xh + j0 * ldh, ldh, L2,
+                              Yh + j0 * ldh, ldh, L2, F, s));
   }
+  if (gemm_form) {
+    // Y_j (l x i, col-major ld l) = hatY_j (l x 2F) * Gt (2F x i)
+    const double* Gt = tables + size_t(bt_ldF(i)) * 2 * i;
+    return gemm_tall_batched(l, i, 2 * F, false, Yh, l, ldh, Gt, 2 * F, 0, Y, l, ldy, k, s);
+  }
+  const size_t smem_i = smem_twiddle(i) + sizeof(double) * size_t(F) * 2 * 32;
+  if (smem_i > 48 * 1024)
+    cudaFuncSetAttribute(bt_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_i));
+  const dim3 grid(unsigned((l + 31) / 32), unsigned(k));
   bt_inverse_kernel<<<grid, DT, smem_i, s>>>(Yh, l, i, k, Y, ldy);
   return launch_check("bt_inverse_kernel");
 }

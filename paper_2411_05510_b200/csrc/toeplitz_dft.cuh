@@ -7,9 +7,11 @@ namespace ssi {
 // Spectrum: i blocks of (2l)^2 doubles; per-pass frequency buffers: i * 2l * k doubles each.
 size_t bt_spectrum_elems(int l, int i);
 size_t bt_freq_elems(int l, int i, int k);
-ssi_status bt_spectrum(const double* R, int l, int i, double* Bb, cudaStream_t s);
+size_t bt_table_elems(int i);
+// spectrum of the block sequence + the forward / inverse DFT tables
+ssi_status bt_spectrum(const double* R, int l, int i, double* Bb, double* tables, cudaStream_t s);
 // Y (m x k col-major, ldy) = T X or T^T X (trans), X m x k col-major (ldx), m = l i.
-ssi_status bt_apply(const double* Bb, int l, int i, int k, bool trans, const double* X, int64_t ldx,
-                    double* Y, int64_t ldy, double* Xh, double* Yh, cudaStream_t s);
+ssi_status bt_apply(const double* Bb, const double* tables, int l, int i, int k, bool trans, const double* X,
+                    int64_t ldx, double* Y, int64_t ldy, double* Xh, double* Yh, cudaStream_t s);
 
 }  // namespace ssi
