@@ -1,13 +1,19 @@
 // Small dense FP64 kernels of the RSVD (A5, A8): Cholesky + triangular inverse for
 // CholeskyQR2, and a one-sided Jacobi SVD for the k x k factor of B = Q^T T
 // (Eq. 16). One CTA per problem; latency-bound by construction.
+#include <cstdio>
+#include <cstdlib>
+
 #include "linalg.cuh"
 
 namespace ssi {
 namespace {
 
 constexpr int kCholThreads = 512;
-constexpr int kJacThreads = 1024;
+constexpr int kJacThreads = 512;
+constexpr int JC = 8;                // Jacobi cluster size (CTAs)
+constexpr int kJacMaxSweeps = 60;
+
 
 // W (k x k col-major, lower part read) -> L (lower) and Linv = L^{-1} (lower), both
 // col-major ld k with zeros above the diagonal. Packed row-major lower triangle P
@@ -111,33 +117,55 @@ __global__ void __launch_bounds__(kCholThreads) chol_inv_kernel(const double* __
 
 // One-sided (Hestenes) Jacobi with the round-robin (circle) ordering; warp per column
 // pair. Round r pairs positions (i, n-1-i); position 0 holds column 0, position p >= 1
-// holds column 1 + (p - 1 + r) mod (n - 1). Column norms live in shared memory and are
-// updated with Rutishauser's formulas (|p'|^2 = a - t g, |q'|^2 = b + t g), so a pair
-// costs one dot product; norms are recomputed exactly at the start of every sweep.
+// holds column 1 + (p - 1 + r) mod (n - 1). Column norms are updated with Rutishauser's
+// formulas (|p'|^2 = a - t g, |q'|^2 = b + t g), so a pair costs one dot product; norms are
+// recomputed exactly at the start of every sweep.
+// The k x k matrix (387 KB at k = 220) does not fit one SM, and one SM's L2 bandwidth bounds a
+// round (every column is read and written once per round), so the pairs of a round are spread
+// over a cluster of JC CTAs that meet at a cluster barrier after every round; G and the norms
+// live in L2 (ld/st.global.cg, coherent across the cluster's SMs).
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 template <int KPL>   // column elements per lane (k <= 32 * KPL)
-__global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict__ G, int k,
+__global__ void __launch_bounds__(kJacThreads, 1) jacobi_kernel(double* __restrict__ G, int k,
                                                              double* __restrict__ Ut,
                                                              double* __restrict__ S,
-                                                             int32_t* status) {
+                                                             double* __restrict__ gnrm,   // k
+                                                             int* __restrict__ gflag,     // kJacMaxSweeps
+                                                             int32_t* status, int profile) {
   extern __shared__ __align__(16) double jsm[];
-  double* nrm = jsm;                                    // k
+  double* nrm = jsm;                                    // k (final phase, CTA 0)
   int* rank = reinterpret_cast<int*>(jsm + k);          // k
   __shared__ int rot;
   const int n = (k + 1) & ~1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int cr = int(cluster_rank());
+  const int gw = cr * nw + warp, gnw = JC * nw;         // warp index / count over the cluster
   const double tol = sqrt(double(k)) * 1.1102230246251565e-16;
+  if (cr == 0)
+    for (int i = tid; i < kJacMaxSweeps; i += blockDim.x) gflag[i] = 0;
   bool converged = false;
-  for (int sweep = 0; sweep < 60 && !converged; ++sweep) {
-    for (int j = warp; j < k; j += nw) {
+  int sweeps = 0;
+  const long long c0 = clock64();
+  for (int sweep = 0; sweep < kJacMaxSweeps && !converged; ++sweep) {
+    ++sweeps;
+    for (int j = gw; j < k; j += gnw) {
       double a = 0.0;
-      for (int r = lane; r < k; r += 32) { const double x = G[int64_t(j) * k + r]; a += x * x; }
+      for (int r = lane; r < k; r += 32) { const double x = __ldcg(G + int64_t(j) * k + r); a += x * x; }
       a = warp_sum(a);
-      if (lane == 0) nrm[j] = a;
+      if (lane == 0) __stcg(gnrm + j, a);
     }
     if (tid == 0) rot = 0;
-    __syncthreads();
+    cluster_sync_all();
     for (int round = 0; round < n - 1; ++round) {
-      for (int pr = warp; pr < n / 2; pr += nw) {
+      for (int pr = gw; pr < n / 2; pr += gnw) {
         const int pa = pr, pb = n - 1 - pr;
         int p = pa == 0 ? 0 : 1 + (pa - 1 + round) % (n - 1);
         int q = 1 + (pb - 1 + round) % (n - 1);
@@ -149,43 +177,47 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
 #pragma unroll
         for (int u = 0; u < KPL; ++u) {
           const int r = lane + 32 * u;
-          x[u] = r < k ? gp[r] : 0.0;
-          y[u] = r < k ? gq[r] : 0.0;
+          x[u] = r < k ? __ldcg(gp + r) : 0.0;
+          y[u] = r < k ? __ldcg(gq + r) : 0.0;
         }
+        const double al = __ldcg(gnrm + p), be = __ldcg(gnrm + q);
         double ga = 0.0;
 #pragma unroll
         for (int u = 0; u < KPL; ++u) ga += x[u] * y[u];
         ga = warp_sum(ga);
-        const double al = nrm[p], be = nrm[q];
         if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
           const double zeta = (be - al) / (2.0 * ga);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          const double c = 1.0 / sqrt(1.0 + t * t), sn = c * t;
 #pragma unroll
           for (int u = 0; u < KPL; ++u) {
             const int r = lane + 32 * u;
             if (r < k) {
-              gp[r] = c * x[u] - s * y[u];
-              gq[r] = s * x[u] + c * y[u];
+              __stcg(gp + r, c * x[u] - sn * y[u]);
+              __stcg(gq + r, sn * x[u] + c * y[u]);
             }
           }
           if (lane == 0) {
-            nrm[p] = al - t * ga;
-            nrm[q] = be + t * ga;
-            atomicAdd(&rot, 1);
+            __stcg(gnrm + p, al - t * ga);
+            __stcg(gnrm + q, be + t * ga);
+            rot = 1;
           }
         }
       }
-      __syncthreads();
+      cluster_sync_all();
     }
-    converged = (rot == 0);
     __syncthreads();
+    if (tid == 0 && rot) atomicAdd(gflag + sweep, 1);
+    cluster_sync_all();
+    converged = (__ldcg(gflag + sweep) == 0);
   }
+  if (cr != 0) return;
   if (!converged && tid == 0) set_status(status, SSI_ERR_NUMERIC);
+  if (profile && tid == 0) printf("jacobi k=%d: %d sweeps, %lld cycles\n", k, sweeps, clock64() - c0);
   // singular values = column norms; sort descending (rank by counting, ties by index)
   for (int j = warp; j < k; j += nw) {
     double a = 0.0;
-    for (int r = lane; r < k; r += 32) { const double x = G[int64_t(j) * k + r]; a += x * x; }
+    for (int r = lane; r < k; r += 32) { const double x = __ldcg(G + int64_t(j) * k + r); a += x * x; }
     a = warp_sum(a);
     if (lane == 0) nrm[j] = sqrt(a);
   }
@@ -201,7 +233,7 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_kernel(double* __restrict_
   for (int j = warp; j < k; j += nw) {
     const double inv = nrm[j] > 0.0 ? 1.0 / nrm[j] : 0.0;
     const int dst = rank[j];
-    for (int r = lane; r < k; r += 32) Ut[int64_t(dst) * k + r] = G[int64_t(j) * k + r] * inv;
+    for (int r = lane; r < k; r += 32) Ut[int64_t(dst) * k + r] = __ldcg(G + int64_t(j) * k + r) * inv;
   }
 }
 
@@ -268,22 +300,44 @@ ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, Ch
 }
 
 template <int KPL>
-static void jacobi_launch(double* G, int k, double* Ut, double* S, int32_t* status, cudaStream_t s) {
+static ssi_status jacobi_launch(double* G, int k, double* Ut, double* S, double* scratch, int32_t* status,
+                                cudaStream_t s) {
   const size_t smem = size_t(k) * (sizeof(double) + sizeof(int));
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(jacobi_kernel<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  jacobi_kernel<KPL><<<1, kJacThreads, smem, s>>>(G, k, Ut, S, status);
+  static const int profile = getenv("SSI_JAC_PROFILE") ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(JC);
+  cfg.blockDim = dim3(kJacThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = JC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  double* gnrm = scratch;
+  int* gflag = reinterpret_cast<int*>(scratch + k);
+  if (cudaLaunchKernelEx(&cfg, jacobi_kernel<KPL>, G, k, Ut, S, gnrm, gflag, status, profile) != cudaSuccess)
+    return launch_check("jacobi_kernel (cluster launch)");
+  return SSI_OK;
 }
 
-ssi_status jacobi_svd(double* G, int k, double* Ut, double* S, int32_t* status, cudaStream_t s) {
-  if (k <= 64) jacobi_launch<2>(G, k, Ut, S, status, s);
-  else if (k <= 128) jacobi_launch<4>(G, k, Ut, S, status, s);
-  else if (k <= 256) jacobi_launch<8>(G, k, Ut, S, status, s);
-  else if (k <= 512) jacobi_launch<16>(G, k, Ut, S, status, s);
+size_t jacobi_scratch_elems(int k) { return size_t(k) + kJacMaxSweeps / 2 + 1; }
+
+ssi_status jacobi_svd(double* G, int k, double* Ut, double* S, double* scratch, int32_t* status, cudaStream_t s) {
+  ssi_status st;
+  if (k <= 64) st = jacobi_launch<2>(G, k, Ut, S, scratch, status, s);
+  else if (k <= 128) st = jacobi_launch<4>(G, k, Ut, S, scratch, status, s);
+  else if (k <= 256) st = jacobi_launch<8>(G, k, Ut, S, scratch, status, s);
+  else if (k <= 512) st = jacobi_launch<16>(G, k, Ut, S, scratch, status, s);
   else {
     set_last_error("jacobi_svd: k = %d > 512 unsupported", k);
     return SSI_ERR_INVALID_ARG;
   }
+  if (st != SSI_OK) return st;
   return launch_check("jacobi_kernel");
 }
 

@@ -32,6 +32,8 @@ ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* Lin
 
 // One-sided (Hestenes) Jacobi SVD of a k x k matrix G (col-major, overwritten):
 // G V = U Sigma; Ut = U sorted by descending sigma (col-major k x k), S = sigma.
-ssi_status jacobi_svd(double* G, int k, double* Ut, double* S, int32_t* status, cudaStream_t s);
+// scratch: jacobi_scratch_elems(k) doubles of device memory (norms and sweep flags).
+size_t jacobi_scratch_elems(int k);
+ssi_status jacobi_svd(double* G, int k, double* Ut, double* S, double* scratch, int32_t* status, cudaStream_t s);
 
 }  // namespace ssi

@@ -9,7 +9,7 @@
 namespace ssi {
 
 struct RsvdWork {
-  double *Omega, *Y, *Q, *Q2, *G, *Ut, *Sk, *tall;
+  double *Omega, *Y, *Q, *Q2, *G, *Ut, *Sk, *tall, *jac;
   CholQRWork cq;
 };
 
@@ -21,6 +21,7 @@ static void rsvd_carve(Carver& c, int64_t m, int k, RsvdWork& w) {
   w.G = c.take<double>(size_t(k) * k);
   w.Ut = c.take<double>(size_t(k) * k);
   w.Sk = c.take<double>(size_t(k));
+  w.jac = c.take<double>(jacobi_scratch_elems(k));
   w.tall = c.take<double>(gemm_tall_partial_elems_upto(m, k) + 1);
   cholqr_carve(c, m, k, w.cq);
 }
@@ -58,7 +59,7 @@ static ssi_status rsvd_core(Pass&& pass, int64_t m, int k, int q, uint64_t seed,
   // Rb^T = (L2^T L1^T)^T = L1 L2
   SSI_TRY(gemm_f64(k, k, k, 1.0, Operand{w.cq.L1, 1, k}, Operand{w.cq.L2, 1, k}, w.G, k, 1,
                    nullptr, s));
-  SSI_TRY(jacobi_svd(w.G, k, w.Ut, w.Sk, status, s));
+  SSI_TRY(jacobi_svd(w.G, k, w.Ut, w.Sk, w.jac, status, s));
   // line 6: U = Q U~ (Eq. 18), leading n_keep columns
   SSI_TRY(gemm_f64(m, n_keep, k, 1.0, Operand{w.Q, 1, m}, Operand{w.Ut, 1, k}, U, ldU, 1,
                    nullptr, s));
@@ -100,6 +101,7 @@ static void rsvd_bt_carve(Carver& c, int l, int i, int k, RsvdBtWork& w) {
   w.base.G = c.take<double>(size_t(k) * k);
   w.base.Ut = c.take<double>(size_t(k) * k);
   w.base.Sk = c.take<double>(size_t(k));
+  w.base.jac = c.take<double>(jacobi_scratch_elems(k));
   w.base.tall = nullptr;
   cholqr_carve(c, m, k, w.base.cq);
   w.Bb = c.take<double>(bt_spectrum_elems(l, i));
