@@ -368,7 +368,7 @@ __global__ void cov_i8_finalize(const double* __restrict__ part, int nchunks, in
                                 int64_t N, int normalize, double* __restrict__ R) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < per; e += int64_t(gridDim.x) * blockDim.x) {
     double s = 0.0;
-    for (int z = 0; z < nchunks; ++z) s += part[z * per + e];
+    s = ordered_sum(part + e, per, nchunks);
     if (normalize) s /= double(N - (lag_lo + int(e / (int64_t(l) * l))));
     R[e] = s;
   }

@@ -123,7 +123,7 @@ __global__ void cov_finalize(const double* __restrict__ part, int splits, int ro
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += part[z * total + e];
+    s = ordered_sum(part + e, total, splits);
     if (normalize) {
       const int k = lag_lo + int(e / (int64_t(l) * l));
       s /= double(N - k);

@@ -137,7 +137,7 @@ __global__ void splitk_reduce(int64_t M, int64_t N, int splits, const double* __
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
     double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += part[z * total + e];
+    s = ordered_sum(part + e, total, splits);
     const int64_t r = e % M, c = e / M;
     C[r + c * ldc] = alpha * s;
   }

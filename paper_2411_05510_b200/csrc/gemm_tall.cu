@@ -140,7 +140,7 @@ __global__ void tall_reduce(int64_t M, int64_t N, int splits, const double* __re
   const int64_t total = M * N;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
     double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += part[z * total + e];
+    s = ordered_sum(part + e, total, splits);
     C[(e % M) + (e / M) * ldc] = s;
   }
 }

@@ -26,7 +26,8 @@ constexpr int WIN = 32;        // bulge-chase window (rows/cols) of the windowed
 constexpr int TLD = WIN + 1;    // tile row stride (doubles)
 constexpr int HG_WARPS = 4;     // H group (band QR) warps; the rest form the C group
 constexpr int HG_T = HG_WARPS * 32;
-constexpr int CG_T = NT - HG_T;
+constexpr int CG_W0 = HG_WARPS + 1;   // C group: warps 5..7 (warp 4 would share warp 0's SMSP)
+constexpr int CG_T = NT - CG_W0 * 32;
 constexpr int NSLOT = 8;        // H -> C queue depth
 enum { QWIN = 0, QROT = 1, QEND = 2 };
 struct QEntry {
@@ -609,9 +610,11 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     acquire();
     if (htid == 0) s.q[qslot].type = QEND;
     publish();
-  } else {
-    // ---------------- C group: C[:, w0:w0+nw) <- C[:, w0:w0+nw) P_w0 ... P_{kend-1}, rotations
-    const int ctid = tid - HG_T;
+  } else if (warp >= CG_W0) {
+    // ---------------- C group: C[:, w0:w0+nw) <- C[:, w0:w0+nw) P_w0 ... P_{kend-1}, rotations.
+    // Warp 4 stays idle: warps w and w+4 share a sub-partition, and warp 0 runs the
+    // latency-bound bulge chase.
+    const int ctid = tid - CG_W0 * 32;
     int slot = 0, use = 0;
     while (true) {
       mbar_wait_parity(&s.q_full[slot], use & 1);
