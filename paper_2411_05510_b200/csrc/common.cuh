@@ -56,6 +56,24 @@ __device__ __forceinline__ double ordered_sum(const double* __restrict__ p, int6
   return s;
 }
 
+// FP64 reciprocal / rsqrt: hardware approximation refined by Newton steps to full precision
+// (a few ulp), inline (no call to the IEEE division / sqrt slow-path subroutines).
+__device__ __forceinline__ double fast_rcp(double d) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = fma(r, fma(-d, r, 1.0), r);
+  r = fma(r, fma(-d, r, 1.0), r);
+  return fma(r, fma(-d, r, 1.0), r);
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double hx = 0.5 * x;
+  r = r * fma(-hx * r, r, 1.5);
+  r = r * fma(-hx * r, r, 1.5);
+  return r * fma(-hx * r, r, 1.5);
+}
+
 // ---------------------------------------------------------------- FP64 tensor core
 // mma.sync m8n8k4 f64 (SASS DMMA.8x8x4). Fragments (PTX ISA, m8n8k4 .f64):
 //   A 8x4 row : lane holds A[lane>>2][lane&3]

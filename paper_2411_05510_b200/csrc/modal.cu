@@ -37,24 +37,6 @@ struct QEntry {
 constexpr double kUlp = 2.220446049250313e-16;
 constexpr double kSafeMin = 2.2250738585072014e-308;
 
-// FP64 reciprocal / rsqrt: hardware approximation refined by Newton steps to full precision
-// (a few ulp), off the IEEE division subroutine on the bulge-chase critical path.
-__device__ __forceinline__ double fast_rcp(double d) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  r = fma(r, fma(-d, r, 1.0), r);
-  r = fma(r, fma(-d, r, 1.0), r);
-  return fma(r, fma(-d, r, 1.0), r);
-}
-__device__ __forceinline__ double fast_rsqrt(double x) {
-  double r;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  const double hx = 0.5 * x;
-  r = r * fma(-hx * r, r, 1.5);
-  r = r * fma(-hx * r, r, 1.5);
-  return r * fma(-hx * r, r, 1.5);
-}
-
 // eigenvector scratch (NW complex vectors), also the windowed sweep's tile
 __host__ __device__ inline size_t x_elems(int n_max) {
   const size_t a = size_t(NW) * 2 * n_max, b = size_t(WIN) * TLD;
