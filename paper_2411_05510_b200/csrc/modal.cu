@@ -23,7 +23,8 @@ namespace {
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr int WIN = 32;        // bulge-chase window (rows/cols) of the windowed Francis sweep
-constexpr int TLD = WIN + 1;    // tile row stride (doubles)
+constexpr int TLD = WIN + 3;    // tile row stride (doubles): columns w0-1 .. w0+WIN+1 (zero padded)
+constexpr int TROWS = WIN + 1;  // tile rows (one zero-padded row below the window)
 constexpr int HG_WARPS = 4;     // H group (band QR) warps; the rest form the C group
 constexpr int HG_T = HG_WARPS * 32;
 constexpr int CG_W0 = HG_WARPS + 1;   // C group: warps 5..7 (warp 4 would share warp 0's SMSP)
@@ -39,7 +40,7 @@ constexpr double kSafeMin = 2.2250738585072014e-308;
 
 // eigenvector scratch (NW complex vectors), also the windowed sweep's tile
 __host__ __device__ inline size_t x_elems(int n_max) {
-  const size_t a = size_t(NW) * 2 * n_max, b = size_t(WIN) * TLD;
+  const size_t a = size_t(NW) * 2 * n_max, b = size_t(TROWS) * TLD;
   return a > b ? a : b;
 }
 __host__ __device__ inline int band_lo(int i) { return i > 3 ? i - 3 : 0; }
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
           const int nsteps = kend - w0;
           QEntry* qe = acquire();
           // tile D[lr][lc] = H(w0 + lr, w0 - 1 + lc), lr < nw, lc <= nw (structural zeros as 0)
-          for (int e = htid; e < WIN * TLD; e += HG_T) {
+          for (int e = htid; e < TROWS * TLD; e += HG_T) {
             const int lr = e / TLD, lc = e - lr * TLD;
             const int r = w0 + lr, c = w0 - 1 + lc;
             D[e] = (lr < nw && lc <= nw && c >= 0 && c >= band_lo(r)) ? s.H[s.rowoff[r] + c] : 0.0;
@@ -488,57 +489,51 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
           const long long tw0 = clock64();
           if (warp == 0) {
             double* refl = qe->r;
+            // Branch-free step (predicated code, the warp stays converged): when nr == 2 the
+            // third reflector component is 0 and the third row / column update is an exact
+            // no-op on the zero-padded tile; when y = z = 0 (tau = 0) every update is a no-op.
             for (int k = w0; k < kend; ++k) {
               const int t = k - w0;
-              const int nr = (ihi - k + 1) < 3 ? (ihi - k + 1) : 3;
-              double x, y, z;
-              if (k == lo) { x = x0; y = y0; z = nr == 3 ? z0 : 0.0; }
-              else { x = D[t * TLD + t]; y = D[(t + 1) * TLD + t]; z = nr == 3 ? D[(t + 2) * TLD + t] : 0.0; }
-              double tau = 0.0, v1 = 0.0, v2 = 0.0, beta = 0.0;
-              const double yz = y * y + z * z;
-              if (yz != 0.0) {
-                // beta = -sign(x) sqrt(s); tau = 1 + |x|/sqrt(s); v = sign(x) (y, z)/(|x| + sqrt(s))
-                const double ss = x * x + yz;
-                const double rs = fast_rsqrt(ss);
-                const double sq = ss * rs;
-                beta = -copysign(sq, x);
-                tau = fma(fabs(x), rs, 1.0);
-                const double inv = copysign(fast_rcp(fabs(x) + sq), x);
-                v1 = y * inv; v2 = z * inv;
+              const bool three = (ihi - k + 1) >= 3;
+              const bool first = (k == lo);
+              const double x = first ? x0 : D[t * TLD + t];
+              const double y = first ? y0 : D[(t + 1) * TLD + t];
+              const double zr = first ? z0 : D[(t + 2) * TLD + t];
+              const double z = three ? zr : 0.0;
+              const double yz = fma(z, z, y * y);
+              const bool refl_on = (yz != 0.0);
+              // beta = -sign(x) sqrt(s); tau = 1 + |x|/sqrt(s); v = sign(x) (y, z)/(|x| + sqrt(s))
+              const double ss = fma(x, x, yz);
+              const double rs = fast_rsqrt(refl_on ? ss : 1.0);
+              const double sq = ss * rs;
+              const double beta = -copysign(sq, x);
+              const double tau = refl_on ? fma(fabs(x), rs, 1.0) : 0.0;
+              const double inv = refl_on ? copysign(fast_rcp(fabs(x) + sq), x) : 0.0;
+              const double v1 = y * inv, v2 = z * inv;
+              __syncwarp();
+              if (lane == 0 && refl_on && !first) {
+                D[t * TLD + t] = beta; D[(t + 1) * TLD + t] = 0.0; D[(t + 2) * TLD + t] = three ? 0.0 : zr;
+              }
+              if (lane == 0) { refl[3 * t + 0] = v1; refl[3 * t + 1] = v2; refl[3 * t + 2] = tau; }
+              // left: rows t..t+2, columns k..w1-1 (local t+1 .. nw)
+              {
+                const int lc = t + 1 + lane;
+                if (lc <= nw) {
+                  double* p0 = D + t * TLD + lc;
+                  const double b0 = p0[0], b1 = p0[TLD], b2 = p0[2 * TLD];
+                  const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
+                  p0[0] = b0 - sum; p0[TLD] = fma(-sum, v1, b1); p0[2 * TLD] = fma(-sum, v2, b2);
+                }
               }
               __syncwarp();
-              if (lane == 0) {
-                if (yz != 0.0 && k > lo) {
-                  D[t * TLD + t] = beta; D[(t + 1) * TLD + t] = 0.0;
-                  if (nr == 3) D[(t + 2) * TLD + t] = 0.0;
-                }
-                refl[3 * t + 0] = v1;
-                refl[3 * t + 1] = v2;
-                refl[3 * t + 2] = tau;
-              }
-              if (tau != 0.0) {
-                // left: rows t..t+nr-1, columns k..w1-1 (local t+1 .. nw)
-                {
-                  const int lc = t + 1 + lane;
-                  if (lc <= nw) {
-                    double* p0 = D + t * TLD + lc;
-                    const double b0 = p0[0], b1 = p0[TLD], b2 = nr == 3 ? p0[2 * TLD] : 0.0;
-                    const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
-                    p0[0] = b0 - sum; p0[TLD] = fma(-sum, v1, b1);
-                    if (nr == 3) p0[2 * TLD] = fma(-sum, v2, b2);
-                  }
-                }
-                __syncwarp();
-                // right: columns k..k+nr-1 (local t+1..), rows w0..min(k+3, ihi)
-                {
-                  const int rmax = (k + 3 < ihi ? k + 3 : ihi) - w0;
-                  if (lane <= rmax) {
-                    double* p0 = D + lane * TLD + t + 1;
-                    const double b0 = p0[0], b1 = p0[1], b2 = nr == 3 ? p0[2] : 0.0;
-                    const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
-                    p0[0] = b0 - sum; p0[1] = fma(-sum, v1, b1);
-                    if (nr == 3) p0[2] = fma(-sum, v2, b2);
-                  }
+              // right: columns k..k+2 (local t+1..t+3), rows w0..min(k+3, ihi)
+              {
+                const int rmax = (k + 3 < ihi ? k + 3 : ihi) - w0;
+                if (lane <= rmax) {
+                  double* p0 = D + lane * TLD + t + 1;
+                  const double b0 = p0[0], b1 = p0[1], b2 = p0[2];
+                  const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
+                  p0[0] = b0 - sum; p0[1] = fma(-sum, v1, b1); p0[2] = fma(-sum, v2, b2);
                 }
               }
               __syncwarp();
@@ -550,7 +545,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
           t_wchase += tw1 - tw0;
           const double* refl = qe->r;
           // write the tile back
-          for (int e = htid; e < WIN * TLD; e += HG_T) {
+          for (int e = htid; e < TROWS * TLD; e += HG_T) {
             const int lr = e / TLD, lc = e - lr * TLD;
             const int r = w0 + lr, c = w0 - 1 + lc;
             if (lr < nw && lc <= nw && c >= 0 && c >= band_lo(r)) s.H[s.rowoff[r] + c] = D[e];
