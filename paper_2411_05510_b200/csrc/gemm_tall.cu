@@ -10,12 +10,14 @@
 namespace ssi {
 namespace {
 
+// N-tile widths: 224 (the RSVD panels, k <= 224), 128 and 64 (the narrow DFT products; a
+// smaller tile also fits 2-3 CTAs per SM).
 constexpr int BM = 64, BN = 224, BK = 16, NT = 256, STAGES = 3;
 constexpr int LDK = BK + 4;            // k-contiguous rows (A row-major, B): 20 doubles
 constexpr int LDM = BM + 4;            // m-contiguous rows (A col-major): 68 doubles
 constexpr int A_ELEMS = BM * LDK > BK * LDM ? BM * LDK : BK * LDM;   // 1280
-constexpr int B_ELEMS = BN * LDK;                                     // 4480
-constexpr int STAGE_ELEMS = A_ELEMS + B_ELEMS;
+template <int TBN> constexpr int stage_elems() { return A_ELEMS + TBN * LDK; }
+template <int TBN> constexpr size_t tall_smem() { return size_t(STAGES) * stage_elems<TBN>() * sizeof(double); }
 
 __device__ __forceinline__ void cp16(double* dst, const double* src, bool valid) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -38,7 +40,7 @@ struct TallArgs {
   int64_t sA, sB, sO;   // batch strides (blockIdx.z); 0 when unbatched
 };
 
-template <bool AROW>
+template <bool AROW, int TBN>
 __device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_t m0, int64_t k0, int64_t ke) {
   const int tid = threadIdx.x;
   double* As = st;
@@ -59,9 +61,9 @@ __device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_
       cp16(As + kk * LDM + i, ok ? g.A + gi + gk * g.lda : g.A, ok);
     }
   }
-  // B: 224 columns x 16 k-contiguous doubles = 1792 pieces, 7 per thread
+  // B: TBN columns x 16 k-contiguous doubles = 8 TBN pieces, TBN / 32 per thread
 #pragma unroll
-  for (int q = 0; q < 7; ++q) {
+  for (int q = 0; q < TBN / 32; ++q) {
     const int p = tid + q * NT;
     const int j = p >> 3, kk = (p & 7) * 2;
     const int64_t gk = k0 + kk;
@@ -70,8 +72,11 @@ __device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_
   }
 }
 
-template <bool AROW>
-__global__ void __launch_bounds__(NT, 1) gemm_tall_kernel(TallArgs g) {
+template <bool AROW, int TBN>
+__global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
+  constexpr int WN = TBN / 4;          // warp tile N (56 / 32 / 16)
+  constexpr int NJ = WN / 8;           // m8n8k4 tiles per warp along N
+  constexpr int STAGE_ELEMS = stage_elems<TBN>();
   extern __shared__ __align__(16) double sm[];
   if (blockIdx.z) {
     g.A += int64_t(blockIdx.z) * g.sA;
@@ -79,21 +84,21 @@ __global__ void __launch_bounds__(NT, 1) gemm_tall_kernel(TallArgs g) {
     g.out += int64_t(blockIdx.z) * g.sO;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 56;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * WN;
   const int64_t m0 = int64_t(blockIdx.x) * BM;
   const int64_t kb = int64_t(blockIdx.y) * g.kchunk;
   const int64_t ke = kb + g.kchunk < g.K ? kb + g.kchunk : g.K;
   const int nst = int((ke - kb + BK - 1) / BK);
 
-  double acc[4][7][2];
+  double acc[4][NJ][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 7; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nst) load_stage<AROW>(g, sm + s * STAGE_ELEMS, m0, kb + s * BK, ke);
+    if (s < nst) load_stage<AROW, TBN>(g, sm + s * STAGE_ELEMS, m0, kb + s * BK, ke);
     cp_commit();
   }
   for (int it = 0; it < nst; ++it) {
@@ -101,24 +106,24 @@ __global__ void __launch_bounds__(NT, 1) gemm_tall_kernel(TallArgs g) {
     __syncthreads();
     {
       const int nx = it + STAGES - 1;
-      if (nx < nst) load_stage<AROW>(g, sm + (nx % STAGES) * STAGE_ELEMS, m0, kb + int64_t(nx) * BK, ke);
+      if (nx < nst) load_stage<AROW, TBN>(g, sm + (nx % STAGES) * STAGE_ELEMS, m0, kb + int64_t(nx) * BK, ke);
       cp_commit();
     }
     const double* As = sm + (it % STAGES) * STAGE_ELEMS;
     const double* Bs = As + A_ELEMS;
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
-      double af[4], bf[7];
+      double af[4], bf[NJ];
       const int kq = k4 + (lane & 3), r8 = lane >> 2;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
         af[i] = AROW ? As[(wm + 8 * i + r8) * LDK + kq] : As[kq * LDM + wm + 8 * i + r8];
 #pragma unroll
-      for (int j = 0; j < 7; ++j) bf[j] = Bs[(wn + 8 * j + r8) * LDK + kq];
+      for (int j = 0; j < NJ; ++j) bf[j] = Bs[(wn + 8 * j + r8) * LDK + kq];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 7; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
   }
   cp_wait<0>();
@@ -126,7 +131,7 @@ __global__ void __launch_bounds__(NT, 1) gemm_tall_kernel(TallArgs g) {
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 7; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int64_t r = m0 + wm + 8 * i + (lane >> 2);
@@ -143,6 +148,21 @@ __global__ void tall_reduce(int64_t M, int64_t N, int splits, const double* __re
     s = ordered_sum(part + e, total, splits);
     C[(e % M) + (e / M) * ldc] = s;
   }
+}
+
+template <bool AROW, int TBN>
+ssi_status launch_one(dim3 grid, const TallArgs& g, cudaStream_t s) {
+  constexpr size_t smem = tall_smem<TBN>();
+  cudaFuncSetAttribute(gemm_tall_kernel<AROW, TBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  gemm_tall_kernel<AROW, TBN><<<grid, NT, smem, s>>>(g);
+  return launch_check("gemm_tall_kernel");
+}
+
+// narrowest N tile that covers N
+ssi_status launch_tall(bool arow, int64_t N, dim3 grid, const TallArgs& g, cudaStream_t s) {
+  if (N <= 64) return arow ? launch_one<true, 64>(grid, g, s) : launch_one<false, 64>(grid, g, s);
+  if (N <= 128) return arow ? launch_one<true, 128>(grid, g, s) : launch_one<false, 128>(grid, g, s);
+  return arow ? launch_one<true, 224>(grid, g, s) : launch_one<false, 224>(grid, g, s);
 }
 
 int tall_splits(int64_t M, int64_t K) {
@@ -189,16 +209,8 @@ ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const dou
   kchunk = (kchunk + BK - 1) / BK * BK;
   const int z = int((K + kchunk - 1) / kchunk);
   TallArgs g{M, N, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? M : ldc, kchunk, 0, 0, 0};
-  const size_t smem = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
   dim3 grid(unsigned((M + BM - 1) / BM), unsigned(z));
-  if (a_rowmajor) {
-    cudaFuncSetAttribute(gemm_tall_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    gemm_tall_kernel<true><<<grid, NT, smem, s>>>(g);
-  } else {
-    cudaFuncSetAttribute(gemm_tall_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    gemm_tall_kernel<false><<<grid, NT, smem, s>>>(g);
-  }
-  SSI_TRY(launch_check("gemm_tall_kernel"));
+  SSI_TRY(launch_tall(a_rowmajor, N, grid, g, s));
   if (z > 1) {
     const int64_t tot = M * N;
     int blocks = int((tot + 255) / 256);
@@ -218,16 +230,8 @@ ssi_status gemm_tall_batched(int64_t M, int64_t N, int64_t K, bool a_rowmajor, c
   }
   const int64_t kchunk = (K + BK - 1) / BK * BK;
   TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, sA, sB, sC};
-  const size_t smem = size_t(STAGES) * STAGE_ELEMS * sizeof(double);
   dim3 grid(unsigned((M + BM - 1) / BM), 1u, unsigned(batch));
-  if (a_rowmajor) {
-    cudaFuncSetAttribute(gemm_tall_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    gemm_tall_kernel<true><<<grid, NT, smem, s>>>(g);
-  } else {
-    cudaFuncSetAttribute(gemm_tall_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    gemm_tall_kernel<false><<<grid, NT, smem, s>>>(g);
-  }
-  return launch_check("gemm_tall_kernel (batched)");
+  return launch_tall(a_rowmajor, N, grid, g, s);
 }
 
 }  // namespace ssi
