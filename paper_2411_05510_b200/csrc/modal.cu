@@ -23,8 +23,11 @@ namespace {
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr int WIN = 32;        // bulge-chase window (rows/cols) of the windowed Francis sweep
-constexpr int TLD = WIN + 3;    // tile row stride (doubles): columns w0-1 .. w0+WIN+1 (zero padded)
-constexpr int TROWS = WIN + 1;  // tile rows (one zero-padded row below the window)
+constexpr int BS = 5;          // reflector length: a bulge of 4 shifts (two double shifts)
+constexpr int SUB = BS;        // sub-diagonals the band holds (Hessenberg + bulge)
+constexpr int SPW = WIN - BS;  // bulge steps per window
+constexpr int TLD = WIN + BS + 2;   // tile row stride (doubles): columns w0-1 .. (zero padded)
+constexpr int TROWS = WIN + BS;     // tile rows (zero-padded rows below the window)
 constexpr int HG_WARPS = 4;     // H group (band QR) warps; the rest form the C group
 constexpr int HG_T = HG_WARPS * 32;
 constexpr int CG_W0 = HG_WARPS + 1;   // C group: warps 5..7 (warp 4 would share warp 0's SMSP)
@@ -33,7 +36,7 @@ constexpr int NSLOT = 8;        // H -> C queue depth
 enum { QWIN = 0, QROT = 1, QEND = 2 };
 struct QEntry {
   int type, w0, nw, nsteps;
-  double r[3 * (WIN - 3)];      // window reflectors (v1, v2, tau) or rotation (cs, sn)
+  double r[BS * SPW];           // window reflectors (v1..v4, tau) or rotation (cs, sn)
 };
 constexpr double kUlp = 2.220446049250313e-16;
 constexpr double kSafeMin = 2.2250738585072014e-308;
@@ -43,7 +46,7 @@ __host__ __device__ inline size_t x_elems(int n_max) {
   const size_t a = size_t(NW) * 2 * n_max, b = size_t(TROWS) * TLD;
   return a > b ? a : b;
 }
-__host__ __device__ inline int band_lo(int i) { return i > 3 ? i - 3 : 0; }
+__host__ __device__ inline int band_lo(int i) { return i > SUB ? i - SUB : 0; }
 
 __device__ __forceinline__ void hsync() { asm volatile("bar.sync 1, %0;" ::"n"(HG_T) : "memory"); }
 __device__ __forceinline__ void csync() { asm volatile("bar.sync 2, %0;" ::"n"(CG_T) : "memory"); }
@@ -67,19 +70,25 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 }
 
 // seg (a row segment for right updates, a column segment for left updates: element u is index
-// w0 + u) <- seg after the window's reflectors 0..nsteps-1, reflector t acting on u = t..t+2.
+// w0 + u) <- seg after the window's reflectors 0..nsteps-1, reflector t acting on u = t..t+BS-1
+// (refl: v1..v4, tau per reflector; v_j = 0 past the reflector's length).
 __device__ __forceinline__ void apply_window(double (&seg)[WIN], const double* refl, int nsteps) {
 #pragma unroll
-  for (int u = 0; u < WIN - 3; ++u) {
+  for (int u = 0; u < SPW; ++u) {
     if (u < nsteps) {
-      const double v1 = refl[3 * u], v2 = refl[3 * u + 1], tau = refl[3 * u + 2];
-      const double sum = fma(v2, seg[u + 2], fma(v1, seg[u + 1], seg[u])) * tau;
+      const double* rf = refl + BS * u;
+      const double v1 = rf[0], v2 = rf[1], v3 = rf[2], v4 = rf[3], tau = rf[4];
+      double sum = fma(v4, seg[u + 4], fma(v3, seg[u + 3], fma(v2, seg[u + 2], fma(v1, seg[u + 1], seg[u]))));
+      sum *= tau;
       seg[u] -= sum;
       seg[u + 1] = fma(-sum, v1, seg[u + 1]);
       seg[u + 2] = fma(-sum, v2, seg[u + 2]);
+      seg[u + 3] = fma(-sum, v3, seg[u + 3]);
+      seg[u + 4] = fma(-sum, v4, seg[u + 4]);
     }
   }
 }
+
 __host__ __device__ inline size_t band_elems(int n) {
   size_t s = 0;
   for (int i = 0; i < n; ++i) s += size_t(n - band_lo(i));
@@ -172,6 +181,60 @@ __device__ void dlanv2(double& a, double& b, double& c, double& d, double& cs, d
       }
     }
   }
+}
+
+// Eigenvalues of a 4 x 4 upper Hessenberg block (the shifts of a 4-shift sweep), one thread:
+// double-shift Francis iterations with deflation (dlahqr structure, no Schur vectors), 2 x 2
+// blocks by dlanv2. Returns false when it does not converge (the caller falls back to one
+// double shift).
+__device__ bool eig4(double (&G)[4][4], double (&wr)[4], double (&wi)[4]) {
+  int i = 3, its = 0;
+  while (i >= 0) {
+    int l = i;
+    for (; l > 0; --l) {
+      const double h = fabs(G[l][l - 1]);
+      double tst = fabs(G[l - 1][l - 1]) + fabs(G[l][l]);
+      if (tst == 0.0) tst = 1.0;
+      if (h <= kUlp * tst) break;
+    }
+    if (l > 0) G[l][l - 1] = 0.0;
+    if (l == i) { wr[i] = G[i][i]; wi[i] = 0.0; --i; its = 0; continue; }
+    if (l == i - 1) {
+      double a = G[i - 1][i - 1], b = G[i - 1][i], c = G[i][i - 1], d = G[i][i], cs, sn;
+      dlanv2(a, b, c, d, cs, sn);
+      if (c == 0.0) { wr[i - 1] = a; wi[i - 1] = 0.0; wr[i] = d; wi[i] = 0.0; }
+      else { const double im = sqrt(fabs(b)) * sqrt(fabs(c)); wr[i - 1] = a; wi[i - 1] = im; wr[i] = d; wi[i] = -im; }
+      i -= 2; its = 0; continue;
+    }
+    if (++its > 40) return false;
+    // one Francis double step on rows/cols l..i (shifts: trailing 2 x 2)
+    const double tr = G[i - 1][i - 1] + G[i][i];
+    const double det = G[i - 1][i - 1] * G[i][i] - G[i - 1][i] * G[i][i - 1];
+    double x = G[l][l] * G[l][l] + G[l][l + 1] * G[l + 1][l] - tr * G[l][l] + det;
+    double y = G[l + 1][l] * (G[l][l] + G[l + 1][l + 1] - tr);
+    double z = (l + 2 <= i) ? G[l + 1][l] * G[l + 2][l + 1] : 0.0;
+    for (int k = l; k < i; ++k) {
+      const int nr = (i - k + 1) < 3 ? (i - k + 1) : 3;
+      if (k > l) { x = G[k][k - 1]; y = G[k + 1][k - 1]; z = nr == 3 ? G[k + 2][k - 1] : 0.0; }
+      const double yz = y * y + z * z;
+      if (yz == 0.0) continue;
+      const double sq = sqrt(x * x + yz);
+      const double beta = -copysign(sq, x);
+      const double tau = (beta - x) / beta;
+      const double v1 = y / (x - beta), v2 = z / (x - beta);
+      if (k > l) { G[k][k - 1] = beta; G[k + 1][k - 1] = 0.0; if (nr == 3) G[k + 2][k - 1] = 0.0; }
+      for (int c = k; c <= i; ++c) {
+        const double sum = (G[k][c] + v1 * G[k + 1][c] + (nr == 3 ? v2 * G[k + 2][c] : 0.0)) * tau;
+        G[k][c] -= sum; G[k + 1][c] -= sum * v1; if (nr == 3) G[k + 2][c] -= sum * v2;
+      }
+      const int rmax = (k + 3 < i) ? k + 3 : i;
+      for (int r = l; r <= rmax; ++r) {
+        const double sum = (G[r][k] + v1 * G[r][k + 1] + (nr == 3 ? v2 * G[r][k + 2] : 0.0)) * tau;
+        G[r][k] -= sum; G[r][k + 1] -= sum * v1; if (nr == 3) G[r][k + 2] -= sum * v2;
+      }
+    }
+  }
+  return true;
 }
 
 __device__ __forceinline__ bool order_truncated(const EigArgs& g, int n) {
@@ -297,8 +360,9 @@ __global__ void __launch_bounds__(HT) hess_order_kernel(EigArgs g) {
 // three sub-diagonals (room for the bulge); warp 0 chases the bulge alone (warp-synchronous),
 // all threads run the deflation test and apply each sweep's reflectors to C rows.
 __device__ __forceinline__ int band_off(int n, int i) {
-  // offset of row i: rows 0..3 have n entries, row r >= 4 has n - r + 3
-  return i <= 4 ? i * n : 4 * n + (i - 4) * (n + 3) - ((i - 1) * i / 2 - 6);
+  // offset of row i: rows 0..SUB have n entries, row r > SUB has n - r + SUB
+  return i <= SUB + 1 ? i * n
+                      : (SUB + 1) * n + (i - SUB - 1) * (n + SUB) - ((i - 1) * i / 2 - SUB * (SUB + 1) / 2);
 }
 struct Band {
   double* H;
@@ -310,7 +374,8 @@ struct Band {
 
 __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   extern __shared__ __align__(16) double dsm[];
-  __shared__ double sh_cs, sh_sn;
+  __shared__ double sh_cs, sh_sn, sh_pt[2], sh_pd[2];
+  __shared__ int sh_ok4;
   __shared__ int sh_l, sh_fail, sh_ncand;
 
   const int o = blockIdx.x;
@@ -449,10 +514,15 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       // stream through it; the C group applies them to the Schur vectors. Same arithmetic per
       // element as applying each reflector in turn (dlahqr); only independent updates reorder.
       {
-        // shift polynomial (first column of (H - s1)(H - s2)), Francis / exceptional shifts
-        double x0, y0, z0;
+        // First column of the shift polynomial. Normally two double shifts (4 shifts per sweep,
+        // one bulge of length 5): the eigenvalue pairs of the trailing 2 x 2 block (t1, d1) and of
+        // the 2 x 2 block above it (t2, d2), w = (H^2 - t1 H + d1)(H^2 - t2 H + d2) e_lo formed in
+        // factored form. Exceptional sweeps (its = 10, 20) and active blocks of < 6 rows use one
+        // double shift (w has 3 nonzeros; the same chase code runs with v3 = v4 = 0).
+        double w0v[BS];
         {
           double h11, h12, h21, h22;
+          const bool exc = (its == 10 || its == 20);
           if (its == 10) {
             const double ex = fabs(H(lo + 1, lo)) + fabs(H(lo + 2, lo + 1));
             h11 = 0.75 * ex + H(lo, lo); h12 = -0.4375 * ex; h21 = ex; h22 = h11;
@@ -463,18 +533,88 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
             h11 = H(ihi - 1, ihi - 1); h12 = H(ihi - 1, ihi);
             h21 = H(ihi, ihi - 1); h22 = H(ihi, ihi);
           }
-          const double tr = h11 + h22, det = h11 * h22 - h12 * h21;
-          const double a00 = H(lo, lo), a01 = H(lo, lo + 1), a10 = H(lo + 1, lo), a11 = H(lo + 1, lo + 1);
-          const double a21 = H(lo + 2, lo + 1);
-          x0 = a00 * a00 + a01 * a10 - tr * a00 + det;
-          y0 = a10 * (a00 + a11 - tr);
-          z0 = a10 * a21;
-          const double sc = fabs(x0) + fabs(y0) + fabs(z0);
-          if (sc > 0.0) { x0 /= sc; y0 /= sc; z0 /= sc; }
+          const double t1 = h11 + h22, d1 = h11 * h22 - h12 * h21;
+          const bool four = !exc && (ihi - lo + 1 >= 6);
+          // leading 5 x 4 block of the active part
+          double hh[BS][4];
+#pragma unroll
+          for (int r = 0; r < BS; ++r)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              hh[r][c] = (lo + r <= ihi && lo + c <= ihi && r <= c + 1) ? H(lo + r, lo + c) : 0.0;
+          // u = (H^2 - t H + d) e_lo (rows 0..2), then optionally w = (H^2 - t' H + d') u
+          auto quad = [&](const double* x, double t, double d, double* y) {
+            double hx[BS], h2x[BS];
+#pragma unroll
+            for (int r = 0; r < BS; ++r) {
+              double acc = 0.0;
+#pragma unroll
+              for (int c = 0; c < 4; ++c) acc = fma(hh[r][c], x[c], acc);
+              hx[r] = acc;
+            }
+#pragma unroll
+            for (int r = 0; r < BS; ++r) {
+              double acc = 0.0;
+#pragma unroll
+              for (int c = 0; c < 4; ++c) acc = fma(hh[r][c], hx[c], acc);
+              h2x[r] = acc;
+            }
+#pragma unroll
+            for (int r = 0; r < BS; ++r) y[r] = fma(d, x[r], fma(-t, hx[r], h2x[r]));
+          };
+          double e1[BS] = {1.0, 0.0, 0.0, 0.0, 0.0}, u[BS];
+          // four shifts = eigenvalues of the trailing 4 x 4 block, paired into real quadratics
+          // (conjugate pairs together, real shifts two by two)
+          double pt[2], pd[2];
+          bool ok4 = false;
+          if (four) {
+            if (htid == 0) {
+              double G[4][4], wr[4], wi[4];
+              for (int r = 0; r < 4; ++r)
+                for (int c = 0; c < 4; ++c) G[r][c] = (r <= c + 1) ? H(ihi - 3 + r, ihi - 3 + c) : 0.0;
+              int okk = eig4(G, wr, wi) ? 1 : 0;
+              if (okk) {
+                int np = 0;
+                double rr[4];
+                int nrl = 0;
+                for (int q = 0; q < 4; ++q) {
+                  if (wi[q] > 0.0) { sh_pt[np] = 2.0 * wr[q]; sh_pd[np] = wr[q] * wr[q] + wi[q] * wi[q]; ++np; }
+                  else if (wi[q] == 0.0) rr[nrl++] = wr[q];
+                }
+                for (int q = 0; q + 1 < nrl; q += 2) { sh_pt[np] = rr[q] + rr[q + 1]; sh_pd[np] = rr[q] * rr[q + 1]; ++np; }
+                okk = (np == 2);
+              }
+              sh_ok4 = okk;
+            }
+            hsync();
+            ok4 = sh_ok4 != 0;
+            pt[0] = sh_pt[0]; pd[0] = sh_pd[0]; pt[1] = sh_pt[1]; pd[1] = sh_pd[1];
+            hsync();
+          }
+          if (ok4) {
+            quad(e1, pt[1], pd[1], u);
+            double sc = 0.0;
+#pragma unroll
+            for (int r = 0; r < BS; ++r) sc += fabs(u[r]);
+            if (sc > 0.0) {
+#pragma unroll
+              for (int r = 0; r < BS; ++r) u[r] /= sc;
+            }
+            quad(u, pt[0], pd[0], w0v);
+          } else {
+            quad(e1, t1, d1, w0v);
+          }
+          double sc = 0.0;
+#pragma unroll
+          for (int r = 0; r < BS; ++r) sc += fabs(w0v[r]);
+          if (sc > 0.0) {
+#pragma unroll
+            for (int r = 0; r < BS; ++r) w0v[r] /= sc;
+          }
         }
         double* D = s.x;                 // WIN x TLD tile (aliases the eigenvector scratch)
         for (int w0 = lo; w0 < ihi; ) {
-          const int kend = (w0 + WIN - 3 < ihi) ? w0 + WIN - 3 : ihi;   // steps k in [w0, kend)
+          const int kend = (w0 + SPW < ihi) ? w0 + SPW : ihi;           // steps k in [w0, kend)
           const int w1 = (w0 + WIN < ihi + 1) ? w0 + WIN : ihi + 1;    // window rows/cols [w0, w1)
           const int nw = w1 - w0;
           const int nsteps = kend - w0;
@@ -489,51 +629,79 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
           const long long tw0 = clock64();
           if (warp == 0) {
             double* refl = qe->r;
-            // Branch-free step (predicated code, the warp stays converged): when nr == 2 the
-            // third reflector component is 0 and the third row / column update is an exact
-            // no-op on the zero-padded tile; when y = z = 0 (tau = 0) every update is a no-op.
+            // Branch-free step (predicated code, the warp stays converged): components past the
+            // reflector's length nr = min(BS, ihi - k + 1) are 0 and their row / column updates
+            // are exact no-ops on the zero-padded tile; when y = 0 (tau = 0) every update is a no-op.
             for (int k = w0; k < kend; ++k) {
               const int t = k - w0;
-              const bool three = (ihi - k + 1) >= 3;
+              const int nr = (ihi - k + 1) < BS ? (ihi - k + 1) : BS;
               const bool first = (k == lo);
-              const double x = first ? x0 : D[t * TLD + t];
-              const double y = first ? y0 : D[(t + 1) * TLD + t];
-              const double zr = first ? z0 : D[(t + 2) * TLD + t];
-              const double z = three ? zr : 0.0;
-              const double yz = fma(z, z, y * y);
+              double xv[BS];
+#pragma unroll
+              for (int j = 0; j < BS; ++j) {
+                const double dv = first ? w0v[j] : D[(t + j) * TLD + t];
+                xv[j] = j < nr ? dv : 0.0;
+              }
+              const double x = xv[0];
+              double yz = 0.0;
+#pragma unroll
+              for (int j = 1; j < BS; ++j) yz = fma(xv[j], xv[j], yz);
               const bool refl_on = (yz != 0.0);
-              // beta = -sign(x) sqrt(s); tau = 1 + |x|/sqrt(s); v = sign(x) (y, z)/(|x| + sqrt(s))
+              // beta = -sign(x) sqrt(s); tau = 1 + |x|/sqrt(s); v = sign(x) y/(|x| + sqrt(s))
               const double ss = fma(x, x, yz);
               const double rs = fast_rsqrt(refl_on ? ss : 1.0);
               const double sq = ss * rs;
               const double beta = -copysign(sq, x);
               const double tau = refl_on ? fma(fabs(x), rs, 1.0) : 0.0;
               const double inv = refl_on ? copysign(fast_rcp(fabs(x) + sq), x) : 0.0;
-              const double v1 = y * inv, v2 = z * inv;
+              double v[BS];
+              v[0] = 1.0;
+#pragma unroll
+              for (int j = 1; j < BS; ++j) v[j] = xv[j] * inv;
               __syncwarp();
               if (lane == 0 && refl_on && !first) {
-                D[t * TLD + t] = beta; D[(t + 1) * TLD + t] = 0.0; D[(t + 2) * TLD + t] = three ? 0.0 : zr;
+                D[t * TLD + t] = beta;
+#pragma unroll
+                for (int j = 1; j < BS; ++j) if (j < nr) D[(t + j) * TLD + t] = 0.0;
               }
-              if (lane == 0) { refl[3 * t + 0] = v1; refl[3 * t + 1] = v2; refl[3 * t + 2] = tau; }
-              // left: rows t..t+2, columns k..w1-1 (local t+1 .. nw)
+              if (lane == 0) {
+#pragma unroll
+                for (int j = 1; j < BS; ++j) refl[BS * t + j - 1] = v[j];
+                refl[BS * t + BS - 1] = tau;
+              }
+              // left: rows t..t+BS-1, columns k..w1-1 (local t+1 .. nw)
               {
                 const int lc = t + 1 + lane;
                 if (lc <= nw) {
                   double* p0 = D + t * TLD + lc;
-                  const double b0 = p0[0], b1 = p0[TLD], b2 = p0[2 * TLD];
-                  const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
-                  p0[0] = b0 - sum; p0[TLD] = fma(-sum, v1, b1); p0[2 * TLD] = fma(-sum, v2, b2);
+                  double b[BS];
+#pragma unroll
+                  for (int j = 0; j < BS; ++j) b[j] = p0[j * TLD];
+                  double sum = b[0];
+#pragma unroll
+                  for (int j = 1; j < BS; ++j) sum = fma(v[j], b[j], sum);
+                  sum *= tau;
+                  p0[0] = b[0] - sum;
+#pragma unroll
+                  for (int j = 1; j < BS; ++j) p0[j * TLD] = fma(-sum, v[j], b[j]);
                 }
               }
               __syncwarp();
-              // right: columns k..k+2 (local t+1..t+3), rows w0..min(k+3, ihi)
+              // right: columns k..k+BS-1 (local t+1..t+BS), rows w0..min(k+BS, ihi)
               {
-                const int rmax = (k + 3 < ihi ? k + 3 : ihi) - w0;
+                const int rmax = (k + BS < ihi ? k + BS : ihi) - w0;
                 if (lane <= rmax) {
                   double* p0 = D + lane * TLD + t + 1;
-                  const double b0 = p0[0], b1 = p0[1], b2 = p0[2];
-                  const double sum = fma(v2, b2, fma(v1, b1, b0)) * tau;
-                  p0[0] = b0 - sum; p0[1] = fma(-sum, v1, b1); p0[2] = fma(-sum, v2, b2);
+                  double b[BS];
+#pragma unroll
+                  for (int j = 0; j < BS; ++j) b[j] = p0[j];
+                  double sum = b[0];
+#pragma unroll
+                  for (int j = 1; j < BS; ++j) sum = fma(v[j], b[j], sum);
+                  sum *= tau;
+                  p0[0] = b[0] - sum;
+#pragma unroll
+                  for (int j = 1; j < BS; ++j) p0[j] = fma(-sum, v[j], b[j]);
                 }
               }
               __syncwarp();
