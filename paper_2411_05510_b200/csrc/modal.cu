@@ -23,7 +23,8 @@ namespace {
 constexpr int NT = 256;
 constexpr int NW = NT / 32;
 constexpr int WIN = 32;        // bulge-chase window (rows/cols) of the windowed Francis sweep
-constexpr int BS = 5;          // reflector length: a bulge of 4 shifts (two double shifts)
+constexpr int BS = 5;          // reflector length: a bulge of BS - 1 shifts (6 shifts measured slower: per-sweep overhead)
+constexpr int NSH = BS - 1;    // shifts per sweep (even)
 constexpr int SUB = BS;        // sub-diagonals the band holds (Hessenberg + bulge)
 constexpr int SPW = WIN - BS;  // bulge steps per window
 constexpr int TLD = WIN + BS + 2;   // tile row stride (doubles): columns w0-1 .. (zero padded)
@@ -36,7 +37,7 @@ constexpr int NSLOT = 8;        // H -> C queue depth
 enum { QWIN = 0, QROT = 1, QEND = 2 };
 struct QEntry {
   int type, w0, nw, nsteps;
-  double r[BS * SPW];           // window reflectors (v1..v4, tau) or rotation (cs, sn)
+  double r[BS * SPW];           // window reflectors (v_1..v_{BS-1}, tau) or rotation (cs, sn)
 };
 constexpr double kUlp = 2.220446049250313e-16;
 constexpr double kSafeMin = 2.2250738585072014e-308;
@@ -71,20 +72,19 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 
 // seg (a row segment for right updates, a column segment for left updates: element u is index
 // w0 + u) <- seg after the window's reflectors 0..nsteps-1, reflector t acting on u = t..t+BS-1
-// (refl: v1..v4, tau per reflector; v_j = 0 past the reflector's length).
+// (refl: v_1..v_{BS-1}, tau per reflector; v_j = 0 past the reflector's length).
 __device__ __forceinline__ void apply_window(double (&seg)[WIN], const double* refl, int nsteps) {
 #pragma unroll
   for (int u = 0; u < SPW; ++u) {
     if (u < nsteps) {
       const double* rf = refl + BS * u;
-      const double v1 = rf[0], v2 = rf[1], v3 = rf[2], v4 = rf[3], tau = rf[4];
-      double sum = fma(v4, seg[u + 4], fma(v3, seg[u + 3], fma(v2, seg[u + 2], fma(v1, seg[u + 1], seg[u]))));
-      sum *= tau;
+      double sum = seg[u];
+#pragma unroll
+      for (int j = 1; j < BS; ++j) sum = fma(rf[j - 1], seg[u + j], sum);
+      sum *= rf[BS - 1];
       seg[u] -= sum;
-      seg[u + 1] = fma(-sum, v1, seg[u + 1]);
-      seg[u + 2] = fma(-sum, v2, seg[u + 2]);
-      seg[u + 3] = fma(-sum, v3, seg[u + 3]);
-      seg[u + 4] = fma(-sum, v4, seg[u + 4]);
+#pragma unroll
+      for (int j = 1; j < BS; ++j) seg[u + j] = fma(-sum, rf[j - 1], seg[u + j]);
     }
   }
 }
@@ -183,54 +183,89 @@ __device__ void dlanv2(double& a, double& b, double& c, double& d, double& cs, d
   }
 }
 
-// Eigenvalues of a 4 x 4 upper Hessenberg block (the shifts of a 4-shift sweep), one thread:
-// double-shift Francis iterations with deflation (dlahqr structure, no Schur vectors), 2 x 2
-// blocks by dlanv2. Returns false when it does not converge (the caller falls back to one
+// Eigenvalues of a small N x N upper Hessenberg block (the shifts of an N-shift sweep), one
+// thread: double-shift Francis iterations with deflation (dlahqr structure, no Schur vectors),
+// 2 x 2 blocks by dlanv2. Returns false when it does not converge (the caller falls back to one
 // double shift).
-__device__ bool eig4(double (&G)[4][4], double (&wr)[4], double (&wi)[4]) {
-  int i = 3, its = 0;
+template <int N>
+__device__ bool eig_small(double (&G)[N][N], double (&wr)[N], double (&wi)[N]) {
+  // every array index is a compile-time constant (loops over fixed ranges with predicates), so
+  // G stays in registers
+  int i = N - 1, its = 0;
   while (i >= 0) {
-    int l = i;
-    for (; l > 0; --l) {
-      const double h = fabs(G[l][l - 1]);
-      double tst = fabs(G[l - 1][l - 1]) + fabs(G[l][l]);
-      if (tst == 0.0) tst = 1.0;
-      if (h <= kUlp * tst) break;
+    int l = 0;
+#pragma unroll
+    for (int ll = N - 1; ll > 0; --ll) {
+      if (ll <= i && l == 0) {
+        const double h = fabs(G[ll][ll - 1]);
+        double tst = fabs(G[ll - 1][ll - 1]) + fabs(G[ll][ll]);
+        if (tst == 0.0) tst = 1.0;
+        if (h <= kUlp * tst) { l = ll; G[ll][ll - 1] = 0.0; }
+      }
     }
-    if (l > 0) G[l][l - 1] = 0.0;
-    if (l == i) { wr[i] = G[i][i]; wi[i] = 0.0; --i; its = 0; continue; }
+    if (l == i) {
+#pragma unroll
+      for (int q = 0; q < N; ++q) if (q == i) { wr[q] = G[q][q]; wi[q] = 0.0; }
+      --i; its = 0; continue;
+    }
     if (l == i - 1) {
-      double a = G[i - 1][i - 1], b = G[i - 1][i], c = G[i][i - 1], d = G[i][i], cs, sn;
-      dlanv2(a, b, c, d, cs, sn);
-      if (c == 0.0) { wr[i - 1] = a; wi[i - 1] = 0.0; wr[i] = d; wi[i] = 0.0; }
-      else { const double im = sqrt(fabs(b)) * sqrt(fabs(c)); wr[i - 1] = a; wi[i - 1] = im; wr[i] = d; wi[i] = -im; }
+#pragma unroll
+      for (int q = 1; q < N; ++q) {
+        if (q == i) {
+          double a = G[q - 1][q - 1], b = G[q - 1][q], c = G[q][q - 1], d = G[q][q], cs, sn;
+          dlanv2(a, b, c, d, cs, sn);
+          if (c == 0.0) { wr[q - 1] = a; wi[q - 1] = 0.0; wr[q] = d; wi[q] = 0.0; }
+          else { const double im = sqrt(fabs(b)) * sqrt(fabs(c)); wr[q - 1] = a; wi[q - 1] = im; wr[q] = d; wi[q] = -im; }
+        }
+      }
       i -= 2; its = 0; continue;
     }
     if (++its > 40) return false;
-    // one Francis double step on rows/cols l..i (shifts: trailing 2 x 2)
-    const double tr = G[i - 1][i - 1] + G[i][i];
-    const double det = G[i - 1][i - 1] * G[i][i] - G[i - 1][i] * G[i][i - 1];
-    double x = G[l][l] * G[l][l] + G[l][l + 1] * G[l + 1][l] - tr * G[l][l] + det;
-    double y = G[l + 1][l] * (G[l][l] + G[l + 1][l + 1] - tr);
-    double z = (l + 2 <= i) ? G[l + 1][l] * G[l + 2][l + 1] : 0.0;
-    for (int k = l; k < i; ++k) {
-      const int nr = (i - k + 1) < 3 ? (i - k + 1) : 3;
-      if (k > l) { x = G[k][k - 1]; y = G[k + 1][k - 1]; z = nr == 3 ? G[k + 2][k - 1] : 0.0; }
+    // one Francis double step on rows/cols l..i (shifts: trailing 2 x 2 of the active block)
+    double t11 = 0, t12 = 0, t21 = 0, t22 = 0, a00 = 0, a01 = 0, a10 = 0, a11 = 0, a21 = 0;
+#pragma unroll
+    for (int q = 1; q < N; ++q)
+      if (q == i) { t11 = G[q - 1][q - 1]; t12 = G[q - 1][q]; t21 = G[q][q - 1]; t22 = G[q][q]; }
+#pragma unroll
+    for (int q = 0; q < N - 1; ++q)
+      if (q == l) {
+        a00 = G[q][q]; a01 = G[q][q + 1]; a10 = G[q + 1][q]; a11 = G[q + 1][q + 1];
+        if (q + 2 < N) a21 = G[q + 2][q + 1];
+      }
+    const double tr = t11 + t22, det = t11 * t22 - t12 * t21;
+    double x = a00 * a00 + a01 * a10 - tr * a00 + det;
+    double y = a10 * (a00 + a11 - tr);
+    double z = (l + 2 <= i) ? a10 * a21 : 0.0;
+#pragma unroll
+    for (int k = 0; k < N - 1; ++k) {
+      if (k < l || k >= i) continue;
+      const bool three = (k + 2 <= i);
+      if (k > l) { x = G[k][k - 1]; y = G[k + 1][k - 1]; z = (three && k + 2 < N) ? G[k + 2 < N ? k + 2 : k][k - 1] : 0.0; }
       const double yz = y * y + z * z;
       if (yz == 0.0) continue;
       const double sq = sqrt(x * x + yz);
       const double beta = -copysign(sq, x);
       const double tau = (beta - x) / beta;
       const double v1 = y / (x - beta), v2 = z / (x - beta);
-      if (k > l) { G[k][k - 1] = beta; G[k + 1][k - 1] = 0.0; if (nr == 3) G[k + 2][k - 1] = 0.0; }
-      for (int c = k; c <= i; ++c) {
-        const double sum = (G[k][c] + v1 * G[k + 1][c] + (nr == 3 ? v2 * G[k + 2][c] : 0.0)) * tau;
-        G[k][c] -= sum; G[k + 1][c] -= sum * v1; if (nr == 3) G[k + 2][c] -= sum * v2;
+      if (k > l) {
+        G[k][k - 1] = beta; G[k + 1][k - 1] = 0.0;
+        if (three && k + 2 < N) G[k + 2 < N ? k + 2 : k][k - 1] = 0.0;
       }
-      const int rmax = (k + 3 < i) ? k + 3 : i;
-      for (int r = l; r <= rmax; ++r) {
-        const double sum = (G[r][k] + v1 * G[r][k + 1] + (nr == 3 ? v2 * G[r][k + 2] : 0.0)) * tau;
-        G[r][k] -= sum; G[r][k + 1] -= sum * v1; if (nr == 3) G[r][k + 2] -= sum * v2;
+#pragma unroll
+      for (int c = 0; c < N; ++c) {
+        if (c < k || c > i) continue;
+        const double g2 = (three && k + 2 < N) ? G[k + 2 < N ? k + 2 : k][c] : 0.0;
+        const double sum = (G[k][c] + v1 * G[k + 1][c] + v2 * g2) * tau;
+        G[k][c] -= sum; G[k + 1][c] -= sum * v1;
+        if (three && k + 2 < N) G[k + 2 < N ? k + 2 : k][c] = g2 - sum * v2;
+      }
+#pragma unroll
+      for (int r = 0; r < N; ++r) {
+        if (r < l || r > (k + 3 < i ? k + 3 : i)) continue;
+        const double g2 = (three && k + 2 < N) ? G[r][k + 2 < N ? k + 2 : k] : 0.0;
+        const double sum = (G[r][k] + v1 * G[r][k + 1] + v2 * g2) * tau;
+        G[r][k] -= sum; G[r][k + 1] -= sum * v1;
+        if (three && k + 2 < N) G[r][k + 2 < N ? k + 2 : k] = g2 - sum * v2;
       }
     }
   }
@@ -374,7 +409,7 @@ struct Band {
 
 __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   extern __shared__ __align__(16) double dsm[];
-  __shared__ double sh_cs, sh_sn, sh_pt[2], sh_pd[2];
+  __shared__ double sh_cs, sh_sn, sh_pt[NSH / 2], sh_pd[NSH / 2];
   __shared__ int sh_ok4;
   __shared__ int sh_l, sh_fail, sh_ncand;
 
@@ -430,7 +465,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   // ---------------- Francis double-shift QR: warps 0-3 (H group) iterate on the band in shared
   // memory; warps 4-7 (C group) apply the same transformations, in the same order, to the Schur
   // vectors C (l x n, global/L2), fed through a queue of window-reflector / rotation entries.
-  long long t_scan = 0, t_chase = 0, t_2x2 = 0, steps = 0, t_wchase = 0, t_wdef = 0, t_cwait = 0;
+  long long t_scan = 0, t_chase = 0, t_2x2 = 0, steps = 0, t_wchase = 0, t_wdef = 0, t_cwait = 0, t_shift = 0;
   int total_its = 0;
   if (warp < HG_WARPS) {
     const int htid = tid;
@@ -444,10 +479,17 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       hsync();
       return s.q + qslot;
     };
+    int last_slot = -1, last_use = 0;   // most recently published entry
     auto publish = [&]() {
       hsync();
       if (htid == 0) mbar_arrive(&s.q_full[qslot]);
+      last_slot = qslot; last_use = quse;
       if (++qslot == NSLOT) { qslot = 0; ++quse; }
+    };
+    // wait until the C group has finished entry (slot, use)
+    auto wait_done = [&](int slot, int use) {
+      if (htid == 0) { const long long tq = clock64(); mbar_wait_parity(&s.q_empty[slot], use & 1); t_cwait += clock64() - tq; }
+      hsync();
     };
     while (ihi >= 0) {
       long long ta = clock64();
@@ -514,12 +556,13 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       // stream through it; the C group applies them to the Schur vectors. Same arithmetic per
       // element as applying each reflector in turn (dlahqr); only independent updates reorder.
       {
-        // First column of the shift polynomial. Normally two double shifts (4 shifts per sweep,
-        // one bulge of length 5): the eigenvalue pairs of the trailing 2 x 2 block (t1, d1) and of
-        // the 2 x 2 block above it (t2, d2), w = (H^2 - t1 H + d1)(H^2 - t2 H + d2) e_lo formed in
-        // factored form. Exceptional sweeps (its = 10, 20) and active blocks of < 6 rows use one
-        // double shift (w has 3 nonzeros; the same chase code runs with v3 = v4 = 0).
+        // First column of the shift polynomial. Normally NSH shifts per sweep (one bulge of
+        // length BS = NSH + 1): the eigenvalues of the trailing NSH x NSH block, paired into real
+        // quadratics (H^2 - t H + d), w = prod_q (H^2 - t_q H + d_q) e_lo formed in factored form.
+        // Exceptional sweeps (its = 10, 20) and small active blocks use one double shift from the
+        // trailing 2 x 2 (w has 3 nonzeros; the same chase code runs with the other v_j = 0).
         double w0v[BS];
+        const long long tsh0 = clock64();
         {
           double h11, h12, h21, h22;
           const bool exc = (its == 10 || its == 20);
@@ -534,76 +577,79 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
             h21 = H(ihi, ihi - 1); h22 = H(ihi, ihi);
           }
           const double t1 = h11 + h22, d1 = h11 * h22 - h12 * h21;
-          const bool four = !exc && (ihi - lo + 1 >= 6);
-          // leading 5 x 4 block of the active part
-          double hh[BS][4];
+          const bool four = !exc && (ihi - lo + 1 >= NSH + 2);
+          // leading BS x NSH block of the active part
+          double hh[BS][NSH];
 #pragma unroll
           for (int r = 0; r < BS; ++r)
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < NSH; ++c)
               hh[r][c] = (lo + r <= ihi && lo + c <= ihi && r <= c + 1) ? H(lo + r, lo + c) : 0.0;
-          // u = (H^2 - t H + d) e_lo (rows 0..2), then optionally w = (H^2 - t' H + d') u
+          // y = (H^2 - t H + d) x for x supported on rows 0..BS-3
           auto quad = [&](const double* x, double t, double d, double* y) {
             double hx[BS], h2x[BS];
 #pragma unroll
             for (int r = 0; r < BS; ++r) {
               double acc = 0.0;
 #pragma unroll
-              for (int c = 0; c < 4; ++c) acc = fma(hh[r][c], x[c], acc);
+              for (int c = 0; c < NSH; ++c) acc = fma(hh[r][c], x[c], acc);
               hx[r] = acc;
             }
 #pragma unroll
             for (int r = 0; r < BS; ++r) {
               double acc = 0.0;
 #pragma unroll
-              for (int c = 0; c < 4; ++c) acc = fma(hh[r][c], hx[c], acc);
+              for (int c = 0; c < NSH; ++c) acc = fma(hh[r][c], hx[c], acc);
               h2x[r] = acc;
             }
 #pragma unroll
             for (int r = 0; r < BS; ++r) y[r] = fma(d, x[r], fma(-t, hx[r], h2x[r]));
           };
-          double e1[BS] = {1.0, 0.0, 0.0, 0.0, 0.0}, u[BS];
-          // four shifts = eigenvalues of the trailing 4 x 4 block, paired into real quadratics
+          double u[BS];
+#pragma unroll
+          for (int r = 0; r < BS; ++r) u[r] = r == 0 ? 1.0 : 0.0;
+          // NSH shifts = eigenvalues of the trailing NSH x NSH block, paired into real quadratics
           // (conjugate pairs together, real shifts two by two)
-          double pt[2], pd[2];
-          bool ok4 = false;
+          bool okn = false;
           if (four) {
             if (htid == 0) {
-              double G[4][4], wr[4], wi[4];
-              for (int r = 0; r < 4; ++r)
-                for (int c = 0; c < 4; ++c) G[r][c] = (r <= c + 1) ? H(ihi - 3 + r, ihi - 3 + c) : 0.0;
-              int okk = eig4(G, wr, wi) ? 1 : 0;
+              double G[NSH][NSH], wr[NSH], wi[NSH];
+              for (int r = 0; r < NSH; ++r)
+                for (int c = 0; c < NSH; ++c)
+                  G[r][c] = (r <= c + 1) ? H(ihi - NSH + 1 + r, ihi - NSH + 1 + c) : 0.0;
+              int okk = eig_small<NSH>(G, wr, wi) ? 1 : 0;
               if (okk) {
-                int np = 0;
-                double rr[4];
-                int nrl = 0;
-                for (int q = 0; q < 4; ++q) {
+                int np = 0, nrl = 0;
+                double rr[NSH];
+                for (int q = 0; q < NSH; ++q) {
                   if (wi[q] > 0.0) { sh_pt[np] = 2.0 * wr[q]; sh_pd[np] = wr[q] * wr[q] + wi[q] * wi[q]; ++np; }
                   else if (wi[q] == 0.0) rr[nrl++] = wr[q];
                 }
                 for (int q = 0; q + 1 < nrl; q += 2) { sh_pt[np] = rr[q] + rr[q + 1]; sh_pd[np] = rr[q] * rr[q + 1]; ++np; }
-                okk = (np == 2);
+                okk = (np == NSH / 2);
               }
               sh_ok4 = okk;
             }
             hsync();
-            ok4 = sh_ok4 != 0;
-            pt[0] = sh_pt[0]; pd[0] = sh_pd[0]; pt[1] = sh_pt[1]; pd[1] = sh_pd[1];
-            hsync();
+            okn = sh_ok4 != 0;
           }
-          if (ok4) {
-            quad(e1, pt[1], pd[1], u);
-            double sc = 0.0;
+          if (okn) {
+            for (int q = 0; q < NSH / 2; ++q) {
+              double y[BS];
+              quad(u, sh_pt[q], sh_pd[q], y);
+              double sc = 0.0;
 #pragma unroll
-            for (int r = 0; r < BS; ++r) sc += fabs(u[r]);
-            if (sc > 0.0) {
+              for (int r = 0; r < BS; ++r) sc += fabs(y[r]);
+              const double isc = sc > 0.0 ? 1.0 / sc : 1.0;
 #pragma unroll
-              for (int r = 0; r < BS; ++r) u[r] /= sc;
+              for (int r = 0; r < BS; ++r) u[r] = y[r] * isc;
             }
-            quad(u, pt[0], pd[0], w0v);
+#pragma unroll
+            for (int r = 0; r < BS; ++r) w0v[r] = u[r];
           } else {
-            quad(e1, t1, d1, w0v);
+            quad(u, t1, d1, w0v);
           }
+          if (four) hsync();            // sh_pt / sh_pd read before the next sweep rewrites them
           double sc = 0.0;
 #pragma unroll
           for (int r = 0; r < BS; ++r) sc += fabs(w0v[r]);
@@ -612,10 +658,11 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
             for (int r = 0; r < BS; ++r) w0v[r] /= sc;
           }
         }
-        double* D = s.x;                 // WIN x TLD tile (aliases the eigenvector scratch)
+        t_shift += clock64() - tsh0;
+        double* D = s.x;                 // TROWS x TLD tile (aliases the eigenvector scratch)
         for (int w0 = lo; w0 < ihi; ) {
           const int kend = (w0 + SPW < ihi) ? w0 + SPW : ihi;           // steps k in [w0, kend)
-          const int w1 = (w0 + WIN < ihi + 1) ? w0 + WIN : ihi + 1;    // window rows/cols [w0, w1)
+          const int w1 = (w0 + WIN < ihi + 1) ? w0 + WIN : ihi + 1;    // window rows [w0, w1)
           const int nw = w1 - w0;
           const int nsteps = kend - w0;
           QEntry* qe = acquire();
@@ -761,8 +808,12 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     // latency-bound bulge chase.
     const int ctid = tid - CG_W0 * 32;
     int slot = 0, use = 0;
+    long long c_busy = 0, c_wait = 0, c_n = 0;
     while (true) {
+      const long long cq0 = clock64();
       mbar_wait_parity(&s.q_full[slot], use & 1);
+      const long long cq1 = clock64();
+      c_wait += cq1 - cq0;
       const QEntry* e = s.q + slot;
       const int type = e->type;
       if (type == QEND) break;
@@ -790,7 +841,10 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       csync();
       if (ctid == 0) mbar_arrive(&s.q_empty[slot]);
       if (++slot == NSLOT) { slot = 0; ++use; }
+      c_busy += clock64() - cq1; ++c_n;
     }
+    if (g.profile && ctid == 0 && (g.profile > 1 || o == g.n_orders - 1 || o == g.n_orders / 2))
+      printf("eig order n=%d C group: %lld entries, busy %lld wait %lld cycles\n", n, c_n, c_busy, c_wait);
   }
   __syncthreads();
   clk2 = clock64();
@@ -942,8 +996,8 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     }
   }
   if (g.profile && tid == 0 && (g.profile > 1 || o == g.n_orders - 1 || o == g.n_orders / 2))
-    printf("eig order n=%d: band load %lld qr %lld (its %lld) vectors %lld cycles | scan %lld chase %lld (steps %lld) cwait %lld 2x2 %lld | wchase %lld wdef %lld\n", n, clk1 - clk0,
-           clk2 - clk1, qr_its, clock64() - clk2, t_scan, t_chase, steps, t_cwait, t_2x2, t_wchase, t_wdef);
+    printf("eig order n=%d: band load %lld qr %lld (its %lld) vectors %lld cycles | scan %lld chase %lld (steps %lld) cwait %lld 2x2 %lld | wchase %lld wdef %lld shift %lld\n", n, clk1 - clk0,
+           clk2 - clk1, qr_its, clock64() - clk2, t_scan, t_chase, steps, t_cwait, t_2x2, t_wchase, t_wdef, t_shift);
 }
 
 }  // namespace
