@@ -354,7 +354,15 @@ def main():
         peak_src = "of measured: 2 x bf16 dense burst (MEASURED_PEAKS.json) = nominal int8:bf16 ratio"
         work, unit = 8.0 * flops, "TOP/s"   # each multiply-add runs as eight int8 slice products
     achieved = work / (iso_ms / 1e3) / 1e12
-    roof = {"bound": "tensor", "kernel": f"covariance A1 ({args.cov}: chan_max + slice + tcgen05 contraction + reduce)"
+    share = None
+    try:
+        sm = json.load(open(os.path.join(ROOT, "profiles", "smtime_r01.json")))["kernels"]
+        share = {"kernel_sm_time_share_of_record": sm["ssi::<unnamed>::cov_i8_kernel"]["share_sm_time"],
+                 "kernel_serial_share_of_record": sm["ssi::<unnamed>::cov_i8_kernel"]["share_serial"],
+                 "source": "profiles/smtime_r01.json (ncu sm__cycles_active.sum over one c3 record)"}
+    except Exception:
+        share = None
+    roof = {"bound": "tensor", "step_share": share, "kernel": f"covariance A1 ({args.cov}: chan_max + slice + tcgen05 contraction + reduce)"
             if args.cov == "int8x3" else "covariance A1 (fp64 DMMA)",
             "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": traffic,
             "peak_source": peak_src, "kernel_ms": iso_ms, "kernel_ms_in_pipeline": cov_ms,
