@@ -16,9 +16,11 @@
 // KT + 16 samples starting at t0 + k0, any k0). An MN-major SWIZZLE_NONE descriptor with
 // LBO = 128 B (K groups of 8 samples) and SBO = 16 B (16-row MN groups) makes row group g
 // read the same column g samples later, so ONE M = 128 MMA covers 16 channels x 8 consecutive
-// lags (one "unit"; UNITS > 1 would add descriptors 8 samples further for the next lags).
+// lags; a second descriptor 8 samples further covers the next 8 lags (two "units" per CTA).
 // B (un-shifted record, N = 64 channels) is a K-major 128B-swizzled TMA tile whose time
-// start is always 16-aligned. TMEM: 1 unit x 4 weights x N (<= 128) int32 columns <= 512.
+// start is always 16-aligned. TMEM: 2 units x 4 weights x 64 int32 columns = 512. The three slice
+// products of one A slice run as ONE MMA over the concatenated B slices (N = 192), so each A slice
+// is read from shared memory once per K-step (3 MMAs per unit instead of 8).
 // Warp 0 issues TMA, warp 1 issues tcgen05.mma, all four warps drain TMEM at the end.
 // (TMA on this driver faults for 1-byte boxes whose innermost start is not 16-B aligned and
 // for boxes entirely out of bounds; the layout above never issues either.)
@@ -31,8 +33,8 @@ namespace {
 
 constexpr int KT = 128;                 // time samples per K-block (= one 128 B row of B)
 constexpr int LPU = 8;                  // lags per unit (8 row groups of 16 channels)
-constexpr int UNITS = 1;                // units per CTA: lags k0 .. k0 + 7
-constexpr int AW = KT + UNITS * LPU;    // A window samples (136)
+constexpr int UNITS = 2;                // units per CTA: lags k0 .. k0 + 15
+constexpr int AW = KT + UNITS * LPU;    // A window samples (144)
 constexpr int A_SLICE_BYTES = AW * 16;                       // 2304
 constexpr int A_BYTES = 3 * A_SLICE_BYTES;                   // 6912
 constexpr int A_PAD = (A_BYTES + 1023) / 1024 * 1024;        // 7168 (B stays 1024-aligned)
@@ -117,6 +119,14 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_st16_zero(uint32_t taddr) {
+  const uint32_t z = 0;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(z)
+      : "memory");
 }
 
 // ---------------------------------------------------------------- pre-pass
@@ -252,6 +262,18 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // weight class 3 (first written by an accumulating MMA) starts at zero: each warp clears its
+  // 32 TMEM lanes of the class-3 columns of every unit
+  {
+    const uint32_t lane_base = tmem + (uint32_t(warp * 32) << 16);
+    for (int un = 0; un < UNITS; ++un)
+      for (int c0 = 0; c0 < g.nb; c0 += 16)
+        tmem_st16_zero(lane_base + uint32_t((un * NW + 3) * g.nb + c0));
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
   if (nblk > 0) {
     if (warp == 0 && lane == 0) {
@@ -269,19 +291,19 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
         if (++s == STAGES) { s = 0; ph ^= 1; }
       }
     } else if (warp == 1 && lane == 0) {
-      // ---------------- MMA issuer: 4 K-steps x UNITS x 8 slice products per block
+      // ---------------- MMA issuer: per K-step and unit, three MMAs, one per A slice, each over
+      // the B slices concatenated along N (they are adjacent in shared memory): A_i x [B_0 B_1 B_2]
+      // lands in weight classes i, i+1, i+2 (adjacent TMEM column blocks of nb); A_2 takes
+      // [B_0 B_1] only (d3 d3 dropped). 8 slice products, 3 MMAs, each A slice read once.
       // idesc: S32 accum, signed int8 A/B, A MN-major (bit 15), B K-major, N>>3, M>>4
-      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
-                             (uint32_t(g.nb >> 3) << 17) | (uint32_t(128 >> 4) << 24);
-      const int pa[8] = {0, 0, 1, 1, 0, 2, 1, 2};
-      const int pb[8] = {0, 1, 0, 1, 2, 0, 2, 1};
-      const int pw[8] = {0, 1, 1, 2, 2, 2, 3, 3};
+      const uint32_t idesc_base = (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (uint32_t(128 >> 4) << 24);
+      const uint32_t idesc3 = idesc_base | (uint32_t((3 * g.nb) >> 3) << 17);
+      const uint32_t idesc2 = idesc_base | (uint32_t((2 * g.nb) >> 3) << 17);
       // descriptors of stage 0; a stage / slice / K offset adds (bytes >> 4) to the start-address
       // field (addresses < 256 KB: the 14-bit field never carries)
       const uint32_t abase0 = smem_u32(smem);
       const uint64_t ad0 = umma_desc(abase0, 128, 16, 0);
       const uint64_t bd0 = umma_desc(abase0 + A_PAD, 16, 1024, 2);
-      const uint32_t b_slice16 = uint32_t(g.nb * KT) >> 4;
       const uint32_t sb16 = uint32_t(SB) >> 4;
       int s = 0;
       uint32_t ph = 0;
@@ -292,15 +314,16 @@ cov_i8_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ 
         const uint64_t bds = bd0 + uint64_t(uint32_t(s) * sb16);
 #pragma unroll
         for (int j = 0; j < KT / 32; ++j) {
+          const uint64_t bd = bds + uint64_t(uint32_t((32 * j) >> 4));
 #pragma unroll
           for (int un = 0; un < UNITS; ++un) {
+            const uint32_t tcol = tmem + uint32_t(un * NW * g.nb);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              // A: slice column, K offset 32 j samples, unit offset 8 un samples (16 B each)
-              const uint64_t ad = ads + uint64_t((pa[q] * A_SLICE_BYTES + (32 * j + LPU * un) * 16) >> 4);
-              const uint64_t bd = bds + uint64_t(uint32_t(pb[q]) * b_slice16 + uint32_t((32 * j) >> 4));
-              const bool first = (it == 0 && j == 0) && (q == 0 || q == 1 || q == 3 || q == 6);
-              umma_i8(tmem + uint32_t((un * NW + pw[q]) * g.nb), ad, bd, idesc, first ? 0u : 1u);
+            for (int q = 0; q < 3; ++q) {
+              // A slice q, K offset 32 j samples, unit offset 8 un samples (16 B each)
+              const uint64_t ad = ads + uint64_t((q * A_SLICE_BYTES + (32 * j + LPU * un) * 16) >> 4);
+              const bool init = (it == 0 && j == 0 && q == 0);   // classes 0..2 (class 3 pre-zeroed)
+              umma_i8(tcol + uint32_t(q * g.nb), ad, bd, q < 2 ? idesc3 : idesc2, init ? 0u : 1u);
             }
           }
         }
@@ -391,13 +414,12 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// B tile width (N): the widest of 128 / 96 / 64 channels dividing l, else l itself (l % 16 == 0,
-// l <= 128). One unit x 4 weight classes x N <= 512 TMEM columns; a wide N amortizes the A
-// (lag-shifted) operand read from shared memory over more output columns.
+// B tile width nb: 64 channels if l % 64 == 0, else l itself (l % 16 == 0, l <= 64). The slice
+// products of one A slice are merged into one MMA over the concatenated B slices (N = 3 nb <= 256),
+// and TMEM holds UNITS x 4 weight classes x nb <= 512 columns.
 int pick_nb(int l) {
-  for (int nb : {128, 96, 64})
-    if (l % nb == 0) return nb;
-  if (l % 16 == 0 && l <= 128) return l;
+  if (l % 64 == 0) return 64;
+  if (l % 16 == 0 && l <= 64) return l;
   return 0;
 }
 
