@@ -41,7 +41,7 @@ def parse():
                          "applying it through its block structure")
     ap.add_argument("--config", default="c3")
     ap.add_argument("--records", type=int, default=2)
-    ap.add_argument("--streams", type=int, default=6, help="records in flight (one engine per stream)")
+    ap.add_argument("--streams", type=int, default=8, help="records in flight (one engine per stream)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()

@@ -374,8 +374,17 @@ __global__ void __launch_bounds__(HT) hess_order_kernel(EigArgs g) {
       }
       double w = 0.0;
       if (valid) {
-#pragma unroll 4
-        for (int c = q; c < L; c += 4) w += base[(j + 1 + c) * ld] * v[c];
+        // four independent partial sums, 16 loads in flight (L2 latency, not FMA, bounds this)
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+        int c = q;
+        for (; c + 12 < L; c += 16) {
+          const double x0 = base[(j + 1 + c) * ld], x1 = base[(j + 5 + c) * ld];
+          const double x2 = base[(j + 9 + c) * ld], x3 = base[(j + 13 + c) * ld];
+          w0 = fma(x0, v[c], w0); w1 = fma(x1, v[c + 4], w1);
+          w2 = fma(x2, v[c + 8], w2); w3 = fma(x3, v[c + 12], w3);
+        }
+        for (; c < L; c += 4) w0 = fma(base[(j + 1 + c) * ld], v[c], w0);
+        w = (w0 + w1) + (w2 + w3);
       }
       part[q][(warp >> 2) * 32 + lane] = w;
       __syncthreads();
