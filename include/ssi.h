@@ -163,7 +163,8 @@ SSI_API ssi_status ssi_gaussian_sketch(int32_t m, int32_t k, uint64_t seed, uint
  *  out : caller-allocated pole table (device arrays) with n_orders = number of orders,
  *        cap >= n_max/2, l = channels. count[o] = number of poles, or -1 when
  *        S[n-1] < 1e-12 S[0] (order above the numerical rank) or when the
- *        order's eigen-solve did not converge.
+ *        order's eigen-solve did not converge. Slots past count[o] hold zeros (every array),
+ *        so tables are bit-reproducible whatever the buffers held before.
  * ---------------------------------------------------------------------------- */
 typedef struct {
   int32_t n_orders;  /* number of model orders (rows) */

@@ -434,8 +434,14 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     const int64_t e = int64_t(o) * cap + sidx;
     T.f[e] = 0.0; T.xi[e] = 0.0; T.mu_re[e] = 0.0; T.mu_im[e] = 0.0; T.mpc[e] = 0.0; T.mpd[e] = 0.0;
   }
+  // unused pole slots hold zeros (deterministic tables, independent of earlier contents)
+  auto zero_shapes = [&](int from) {
+    double* sh = T.shape + int64_t(o) * cap * l * 2;
+    for (int64_t e = int64_t(from) * l * 2 + tid; e < int64_t(cap) * l * 2; e += NT) sh[e] = 0.0;
+  };
   if (order_truncated(g, n)) {
     if (tid == 0) T.count[o] = -1;
+    zero_shapes(0);
     return;
   }
 
@@ -860,6 +866,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   qr_its = total_its;
   if (sh_fail) {
     if (tid == 0) T.count[o] = -1;
+    zero_shapes(0);
     return;
   }
 
@@ -894,6 +901,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   }
   __syncthreads();
   const int nc = sh_ncand;
+  zero_shapes(nc);
 
   // ---------------- eigenvectors (warp per pole): back substitution on T, Phi = C x
   double* xr = s.x + warp * 2 * g.n_max;

@@ -111,3 +111,55 @@ def test_c5_record_batch_subset(mods):
         _check_contract(compare_tables(gpu_cells(tabs[j]), cells, flags_o[0]), f"c5 record {j}")
         _, counts = api.stab3d([tabs[j]], api.Criteria(**crit.__dict__))
         assert np.array_equal(counts.cpu().numpy(), counts_o)
+
+
+def test_c4_full_lag_sweep(mods):
+    """The whole c4 sweep (i = 20..80 step 4, 16 lags up to m = 15360) through drivers.lag_sweep_3d:
+    poles at the smallest and largest lag against the oracle, and ssi_stab3d over all 16 GPU
+    tables against the oracle's stab3d applied to the same tables."""
+    api, drivers = mods
+    cfg = synth.config("c4")
+    lags = list(cfg.lags)
+    Y, _ = synth.make_record(cfg)
+    P = _params(drivers, cfg, i=max(lags))
+    crit = oracle.SC_BRIDGE_3D
+    tables, flags, counts = drivers.lag_sweep_3d(torch.from_numpy(Y).cuda(), P, lags,
+                                                 api.Criteria(**crit.__dict__))
+    torch.cuda.synchronize()
+    Ro = oracle.covariances(Y, 2 * max(lags) - 1)
+    for i in (lags[0], lags[-1]):
+        To = oracle.toeplitz(Ro, i)
+        Uo, So, _ = oracle.rsvd(To, cfg.k, cfg.q, cfg.philox_key, i, cfg.n_max)
+        cells = oracle.modal_sweep(Uo, So, cfg.l, i, cfg.orders, cfg.dt)
+        flags_o, _ = oracle.stab3d([cells], crit, cfg.n_max // 2)
+        _check_contract(compare_tables(gpu_cells(tables[i]), cells, flags_o[0]), f"c4 full sweep, lag {i}")
+    gcells = [gpu_cells(tables[i]) for i in lags]
+    flags_ref, counts_ref = oracle.stab3d(gcells, crit, cfg.n_max // 2)
+    assert np.array_equal(counts.cpu().numpy(), counts_ref)
+    assert np.array_equal(flags.cpu().numpy(), flags_ref)
+
+
+def test_c5_batch_eight_records(mods):
+    """Continuous monitoring in bench.py's launch configuration (RecordPipeline, 8 streams,
+    records in flight): 8 drifting c5 records; two sampled records against the oracle, and every
+    record's table equal to the same record identified alone (stream pipelining changes nothing)."""
+    api, drivers = mods
+    cfg = synth.config("c5")
+    recs = [synth.make_record(cfg, r)[0] for r in range(8)]
+    P = _params(drivers, cfg)
+    dev = [torch.from_numpy(y).cuda() for y in recs]
+    tabs = drivers.record_batch(dev, P, n_streams=8)
+    crit = oracle.SC_BRIDGE_3D
+    for j in (0, 7):
+        Ro = oracle.covariances(recs[j], 2 * cfg.i - 1)
+        Uo, So, _ = oracle.rsvd(oracle.toeplitz(Ro, cfg.i), cfg.k, cfg.q, cfg.philox_key, (j << 32) | cfg.i,
+                                cfg.n_max)
+        cells = oracle.modal_sweep(Uo, So, cfg.l, cfg.i, cfg.orders, cfg.dt)
+        flags_o, _ = oracle.stab3d([cells], crit, cfg.n_max // 2)
+        _check_contract(compare_tables(gpu_cells(tabs[j]), cells, flags_o[0]), f"c5 batch record {j}")
+    eng = drivers.Engine(P, cfg.N)
+    for j in range(8):
+        alone = eng.identify(dev[j], stream_id=(j << 32) | cfg.i)
+        torch.cuda.synchronize()
+        for a, b in zip(alone.tensors(), tabs[j].tensors()):
+            assert torch.equal(a, b), j          # bit-identical: fixed reduction orders
