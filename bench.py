@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--records", type=int, default=2)
     ap.add_argument("--streams", type=int, default=8, help="records in flight (one engine per stream)")
+    ap.add_argument("--no-priority", action="store_true",
+                    help="one stream per record (no low-priority covariance streams)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -230,7 +232,7 @@ def main():
         Yh, _ = synth.make_record(synth.config(args.config, seed=cfg.seed + 100 * (rank * args.records + j) if j or rank else cfg.seed))
         host.append(Yh)
     Ys = [torch.from_numpy(h).to(dev) for h in host]
-    pipe = drivers.RecordPipeline(P, cfg.N, dev, n_streams=args.streams)
+    pipe = drivers.RecordPipeline(P, cfg.N, dev, n_streams=args.streams, split_priority=not args.no_priority)
     eng = pipe.engines[0]
     stream = torch.cuda.current_stream()
 

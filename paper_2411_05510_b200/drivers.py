@@ -113,21 +113,34 @@ class RecordPipeline:
     submit() returns the engine's pole table, valid once that stream passes the record; an
     engine's table is reused n_streams submissions later."""
 
-    def __init__(self, P: SweepParams, N: int, device="cuda", n_streams: int = 3):
+    def __init__(self, P: SweepParams, N: int, device="cuda", n_streams: int = 3, split_priority: bool = True):
         self.engines = [Engine(P, N, device) for _ in range(n_streams)]
-        self.streams = [torch.cuda.Stream(device=device) for _ in range(n_streams)]
+        # the latency-bound chain (RSVD: Cholesky, Jacobi; modal sweep: per-order eigen-solves)
+        # runs on high-priority streams so its small launches are scheduled ahead of the wide
+        # covariance grids of other records, which run on low-priority streams
+        lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+        self.split = split_priority
+        self.streams = [torch.cuda.Stream(device=device, priority=hi if split_priority else 0)
+                        for _ in range(n_streams)]
+        self.cov_streams = ([torch.cuda.Stream(device=device, priority=lo) for _ in range(n_streams)]
+                            if split_priority else self.streams)
         self.j = 0
 
     def submit(self, Y: torch.Tensor, stream_id: int, events=None):
-        e = self.engines[self.j % len(self.engines)]
-        st = self.streams[self.j % len(self.streams)]
+        k = self.j % len(self.engines)
+        e, st, cst = self.engines[k], self.streams[k], self.cov_streams[k]
         self.j += 1
-        with torch.cuda.stream(st):
+        if self.split:
+            cst.wait_stream(st)            # the engine's buffers are free; Y is ready on st
+        with torch.cuda.stream(cst):
             if events is not None:
-                events[0].record(st)
+                events[0].record(cst)
             R = e.covariances(Y)
             if events is not None:
-                events[1].record(st)
+                events[1].record(cst)
+        if self.split:
+            st.wait_stream(cst)
+        with torch.cuda.stream(st):
             tab, _ = e.decompose(R, e.P.i, stream_id)
         return tab, st
 
@@ -136,6 +149,9 @@ class RecordPipeline:
         cur = stream or torch.cuda.current_stream()
         for st in self.streams:
             cur.wait_stream(st)
+        if self.split:
+            for st in self.cov_streams:
+                cur.wait_stream(st)
 
 
 # ------------------------------------------------------------------ multi-GPU host logic
