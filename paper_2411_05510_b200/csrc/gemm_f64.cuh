@@ -43,6 +43,15 @@ size_t gemm_tall_partial_elems(int64_t M, int64_t N, int64_t K);
 constexpr int kTallMaxN = 224;
 // Batched form without split-K: for b in [0, batch), C_b = op(A_b) B_b with
 // A_b = A + b*sA, B_b = B + b*sB, C_b = C + b*sC (N <= kTallMaxN; lda, ldb even).
+// Lower-triangular 64 x 64 tiles of C (n x n) = op(A) (n x K) B (K x n) (A row-major: op(A)(i,k) =
+// A[i*lda + k]); the strictly-upper off-diagonal tiles of C are not written. partial: at least
+// 64 n^2 doubles (split-K slabs).
+ssi_status gemm_tall_syrk_lower(int64_t n, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
+                                double* C, int64_t ldc, double* partial, cudaStream_t s);
+// C (M x N) = A (M x K, col-major) B (K x N, col-major upper triangular, K == N): the N tile at
+// j0 reads only K rows [0, j0 + 64).
+ssi_status gemm_tall_triu(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                          int64_t ldb, double* C, int64_t ldc, cudaStream_t s);
 ssi_status gemm_tall_batched(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
                              int64_t sA, const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
                              int64_t sC, int batch, cudaStream_t s);

@@ -38,6 +38,9 @@ struct TallArgs {
   int64_t ldo;
   int64_t kchunk;
   int64_t sA, sB, sO;   // batch strides (blockIdx.z); 0 when unbatched
+  int mode;             // 0 plain / batched; 1 lower-triangular tiles of a square C (blockIdx.x
+                        // = triangular tile index, TBN = BM); 2 upper-triangular B (N tile
+                        // blockIdx.z only needs K rows [0, n0 + TBN))
 };
 
 template <bool AROW, int TBN>
@@ -78,14 +81,33 @@ __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
   constexpr int NJ = WN / 8;           // m8n8k4 tiles per warp along N
   constexpr int STAGE_ELEMS = stage_elems<TBN>();
   extern __shared__ __align__(16) double sm[];
-  if (blockIdx.z) {
-    g.A += int64_t(blockIdx.z) * g.sA;
-    g.B += int64_t(blockIdx.z) * g.sB;
-    g.out += int64_t(blockIdx.z) * g.sO;
+  int64_t m0 = int64_t(blockIdx.x) * BM, n0 = 0;
+  double* out = g.out + int64_t(blockIdx.y) * g.M * g.N;   // split-K slab (or C)
+  if (g.mode == 0) {
+    if (blockIdx.z) {
+      g.A += int64_t(blockIdx.z) * g.sA;
+      g.B += int64_t(blockIdx.z) * g.sB;
+      out += int64_t(blockIdx.z) * g.sO;
+    }
+  } else {
+    if (g.mode == 1) {
+      const int t = int(blockIdx.x);
+      int ti = int((sqrtf(8.0f * float(t) + 1.0f) - 1.0f) * 0.5f);
+      while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+      while (ti * (ti + 1) / 2 > t) --ti;
+      const int tj = t - ti * (ti + 1) / 2;
+      m0 = int64_t(ti) * BM;
+      n0 = int64_t(tj) * TBN;
+    } else {
+      n0 = int64_t(blockIdx.z) * TBN;
+      if (n0 + TBN < g.K) g.K = n0 + TBN;
+    }
+    g.B += n0 * g.ldb;
+    out += n0 * g.ldo;
+    g.N = (g.N - n0 < TBN) ? g.N - n0 : TBN;
   }
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * WN;
-  const int64_t m0 = int64_t(blockIdx.x) * BM;
   const int64_t kb = int64_t(blockIdx.y) * g.kchunk;
   const int64_t ke = kb + g.kchunk < g.K ? kb + g.kchunk : g.K;
   const int nst = int((ke - kb + BK - 1) / BK);
@@ -127,7 +149,6 @@ __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
     }
   }
   cp_wait<0>();
-  double* out = g.out + int64_t(blockIdx.y) * g.M * g.N;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -208,7 +229,7 @@ ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const dou
   int64_t kchunk = (K + splits - 1) / splits;
   kchunk = (kchunk + BK - 1) / BK * BK;
   const int z = int((K + kchunk - 1) / kchunk);
-  TallArgs g{M, N, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? M : ldc, kchunk, 0, 0, 0};
+  TallArgs g{M, N, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? M : ldc, kchunk, 0, 0, 0, 0};
   dim3 grid(unsigned((M + BM - 1) / BM), unsigned(z));
   SSI_TRY(launch_tall(a_rowmajor, N, grid, g, s));
   if (z > 1) {
@@ -221,6 +242,45 @@ ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const dou
   return SSI_OK;
 }
 
+// C (n x n, col-major, ldc) lower triangle (64 x 64 tiles on and below the diagonal) of
+// op(A) (n x K) * B (K x n); split-K over whole waves with a fixed-order reduction.
+ssi_status gemm_tall_syrk_lower(int64_t n, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
+                                double* C, int64_t ldc, double* partial, cudaStream_t s) {
+  const int nt = int((n + BM - 1) / BM);
+  const int tiles = nt * (nt + 1) / 2;
+  int splits = 1;
+  for (int sp = 1; sp <= 64; ++sp) {                       // ~3 CTAs per SM (61 KB smem each)
+    if (K / sp < 4 * BK) break;
+    splits = sp;
+    if (tiles * sp >= 3 * 148) break;
+  }
+  int64_t kchunk = (K + splits - 1) / splits;
+  kchunk = (kchunk + BK - 1) / BK * BK;
+  const int z = int((K + kchunk - 1) / kchunk);
+  TallArgs g{n, n, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? n : ldc, kchunk, 0, 0, 0, 1};
+  {
+    const ssi_status st = launch_one<true, 64>(dim3(unsigned(tiles), unsigned(z)), g, s);
+    if (st != SSI_OK) return st;
+  }
+  if (z > 1) {
+    const int64_t tot = n * n;
+    int blocks = int((tot + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    tall_reduce<<<blocks, 256, 0, s>>>(n, n, z, partial, C, ldc);
+    SSI_TRY(launch_check("tall_reduce"));
+  }
+  return SSI_OK;
+}
+
+// C (M x N, col-major) = A (M x K, col-major) * B (K x N, col-major, upper triangular: B(k, j) = 0
+// for k > j): N tiles of 64, tile j0 reads only K rows [0, j0 + 64); no split-K.
+ssi_status gemm_tall_triu(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                          int64_t ldb, double* C, int64_t ldc, cudaStream_t s) {
+  const int64_t kchunk = (K + BK - 1) / BK * BK;
+  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, 0, 0, 0, 2};
+  return launch_one<false, 64>(dim3(unsigned((M + BM - 1) / BM), 1u, unsigned((N + 63) / 64)), g, s);
+}
+
 ssi_status gemm_tall_batched(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
                              int64_t sA, const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
                              int64_t sC, int batch, cudaStream_t s) {
@@ -229,7 +289,7 @@ ssi_status gemm_tall_batched(int64_t M, int64_t N, int64_t K, bool a_rowmajor, c
     return SSI_ERR_INVALID_ARG;
   }
   const int64_t kchunk = (K + BK - 1) / BK * BK;
-  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, sA, sB, sC};
+  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, sA, sB, sC, 0};
   dim3 grid(unsigned((M + BM - 1) / BM), 1u, unsigned(batch));
   return launch_tall(a_rowmajor, N, grid, g, s);
 }

@@ -482,13 +482,13 @@ ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, Ch
   const bool tall = k <= kTallMaxN && ldy % 2 == 0 && m % 2 == 0 && k % 2 == 0 &&
                     (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0;
   const int splits = gemm_pick_splits(k, k, m);
-  auto gram = [&](const double* X, int64_t ldx) -> ssi_status {   // W = X^T X
-    if (tall) return gemm_tall(k, k, m, true, X, ldx, X, ldx, w.W, k, w.tallp, s);
+  auto gram = [&](const double* X, int64_t ldx) -> ssi_status {   // W = X^T X (lower triangle read)
+    if (tall) return gemm_tall_syrk_lower(k, m, X, ldx, X, ldx, w.W, k, w.tallp, s);
     return gemm_f64(k, k, m, 1.0, Operand{X, ldx, 1}, Operand{X, 1, ldx}, w.W, k, splits, w.partial, s);
   };
   auto trmul = [&](const double* X, int64_t ldx, const double* Linv, const double* LinvT, double* out) {
     // out = X Linv^T  (B(kk, j) = Linv(j, kk) = LinvT[kk + j k])
-    if (tall) return gemm_tall(m, k, k, false, X, ldx, LinvT, k, out, m, w.tallp, s);
+    if (tall) return gemm_tall_triu(m, k, k, X, ldx, LinvT, k, out, m, s);
     return gemm_f64(m, k, k, 1.0, Operand{X, 1, ldx}, Operand{Linv, k, 1}, out, m, 1, nullptr, s);
   };
   SSI_TRY(gram(Y, ldy));
