@@ -212,10 +212,19 @@ __device__ bool eig_small(double (&G)[N][N], double (&wr)[N], double (&wi)[N]) {
 #pragma unroll
       for (int q = 1; q < N; ++q) {
         if (q == i) {
-          double a = G[q - 1][q - 1], b = G[q - 1][q], c = G[q][q - 1], d = G[q][q], cs, sn;
-          dlanv2(a, b, c, d, cs, sn);
-          if (c == 0.0) { wr[q - 1] = a; wi[q - 1] = 0.0; wr[q] = d; wi[q] = 0.0; }
-          else { const double im = sqrt(fabs(b)) * sqrt(fabs(c)); wr[q - 1] = a; wi[q - 1] = im; wr[q] = d; wi[q] = -im; }
+          // eigenvalues of the 2 x 2 block (shift values only; no standardised Schur form needed)
+          const double a = G[q - 1][q - 1], b = G[q - 1][q], c = G[q][q - 1], d = G[q][q];
+          const double hm = 0.5 * (a - d), disc = fma(hm, hm, b * c), mid = 0.5 * (a + d);
+          if (disc >= 0.0) {
+            const double r = disc > 0.0 ? disc * fast_rsqrt(disc) : 0.0;
+            const double big = mid + copysign(r, mid);             // larger magnitude root
+            const double det = a * d - b * c;
+            const double small = big != 0.0 ? det * fast_rcp(big) : mid - copysign(r, mid);
+            wr[q - 1] = big; wi[q - 1] = 0.0; wr[q] = small; wi[q] = 0.0;
+          } else {
+            const double im = -disc * fast_rsqrt(-disc);
+            wr[q - 1] = mid; wi[q - 1] = im; wr[q] = mid; wi[q] = -im;
+          }
         }
       }
       i -= 2; its = 0; continue;
@@ -243,10 +252,12 @@ __device__ bool eig_small(double (&G)[N][N], double (&wr)[N], double (&wi)[N]) {
       if (k > l) { x = G[k][k - 1]; y = G[k + 1][k - 1]; z = (three && k + 2 < N) ? G[k + 2 < N ? k + 2 : k][k - 1] : 0.0; }
       const double yz = y * y + z * z;
       if (yz == 0.0) continue;
-      const double sq = sqrt(x * x + yz);
+      const double ss = fma(x, x, yz);
+      const double rs = fast_rsqrt(ss), sq = ss * rs;
       const double beta = -copysign(sq, x);
-      const double tau = (beta - x) / beta;
-      const double v1 = y / (x - beta), v2 = z / (x - beta);
+      const double tau = fma(fabs(x), rs, 1.0);
+      const double inv = copysign(fast_rcp(fabs(x) + sq), x);
+      const double v1 = y * inv, v2 = z * inv;
       if (k > l) {
         G[k][k - 1] = beta; G[k + 1][k - 1] = 0.0;
         if (three && k + 2 < N) G[k + 2 < N ? k + 2 : k][k - 1] = 0.0;
