@@ -158,67 +158,67 @@ __global__ void chan_exp_kernel(const unsigned long long* __restrict__ mx, int l
 // Tile of 128 samples x 32 channels: reads Y (time-major), writes
 //   DA[s][cg][t][16]   (channel-group time columns, whole record, zero past N)
 //   DB[s][a][t]        (channel rows, zero outside [t_begin, t_end))
+// The slices are staged twice in shared memory, time-major ([s][t][a], rows of 48 B) and
+// channel-major ([s][a][t], rows of 144 B), so both outputs are packed with 16-byte loads.
+constexpr int TT_LD = 48, TA_LD = KT + 16;
 template <typename T>
 __global__ void __launch_bounds__(256) slice_kernel(const T* __restrict__ Y, int64_t N, int l, int64_t ldY,
                                                    int64_t Tpad, int64_t t_begin, int64_t t_end,
                                                    const int* __restrict__ e, int8_t* __restrict__ DA,
                                                    int8_t* __restrict__ DB) {
-  __shared__ int8_t tile[3][KT][32 + 4];     // [s][t][a]
+  __shared__ __align__(16) int8_t tt_tile[3][KT][TT_LD];    // [s][t][a]
+  __shared__ __align__(16) int8_t ta_tile[3][32][TA_LD];    // [s][a][t]
   const int64_t t0 = int64_t(blockIdx.x) * KT;
   const int a0 = blockIdx.y * 32;
   const int tid = threadIdx.x;
   const int ncg = l / 16;
-  for (int q = tid; q < 32 * KT; q += 256) {
-    const int a = q % 32, tt = q / 32;
-    const int64_t t = t0 + tt;
-    int8_t d[3] = {0, 0, 0};
-    if (a0 + a < l && t < N) {
-      const double x = ldexp(double(Y[t * ldY + a0 + a]), -e[a0 + a]);
-      const double s1 = kBase * x;
-      const double r1 = rint(s1);
-      const double s2 = kBase * (s1 - r1);
-      const double r2 = rint(s2);
-      const double r3 = rint(kBase * (s2 - r2));
-      d[0] = int8_t(r1); d[1] = int8_t(r2); d[2] = int8_t(r3);
+  const int lane = tid & 31;
+  const bool ch_ok = a0 + lane < l;
+  const double scale = ldexp(1.0, ch_ok ? -e[a0 + lane] : 0);
+  for (int tg = tid >> 5; tg < KT / 4; tg += 8) {            // lane = channel, 4 samples per thread
+    uint32_t packed[3] = {0u, 0u, 0u};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int tt = 4 * tg + u;
+      const int64_t t = t0 + tt;
+      int8_t d[3] = {0, 0, 0};
+      if (ch_ok && t < N) {
+        // rint by the 1.5 * 2^52 trick (round to nearest even, |v| < 2^51): the rounded value as
+        // a double and, in the low word, as an integer -- full-rate DADDs instead of FRND / F2I
+        constexpr double kMagic = 6755399441055744.0;
+        const double x = double(Y[t * ldY + a0 + lane]) * scale;     // exact: power of two
+        const double s1 = kBase * x;
+        const double m1 = s1 + kMagic, r1 = m1 - kMagic;
+        const double s2 = kBase * (s1 - r1);
+        const double m2 = s2 + kMagic, r2 = m2 - kMagic;
+        const double m3 = kBase * (s2 - r2) + kMagic;
+        d[0] = int8_t(__double2loint(m1)); d[1] = int8_t(__double2loint(m2)); d[2] = int8_t(__double2loint(m3));
+      }
+      const bool in_shard = t >= t_begin && t < t_end;
+#pragma unroll
+      for (int sl = 0; sl < 3; ++sl) {
+        tt_tile[sl][tt][lane] = d[sl];
+        if (in_shard) packed[sl] |= uint32_t(uint8_t(d[sl])) << (8 * u);
+      }
     }
 #pragma unroll
-    for (int s = 0; s < 3; ++s) tile[s][tt][a] = d[s];
+    for (int sl = 0; sl < 3; ++sl) *reinterpret_cast<uint32_t*>(&ta_tile[sl][lane][4 * tg]) = packed[sl];
   }
   __syncthreads();
   // DA: (s, channel group of 2, t of 128) -> 16 bytes
   for (int q = tid; q < 3 * 2 * KT; q += 256) {
-    const int s = q / (2 * KT), rem = q % (2 * KT), g = rem / KT, tt = rem % KT;
+    const int sl = q / (2 * KT), rem = q % (2 * KT), g = rem / KT, tt = rem % KT;
     const int cg = a0 / 16 + g;
     if (cg >= ncg) continue;
-    uint32_t w[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int8_t* src = &tile[s][tt][16 * g + 4 * u];
-      w[u] = uint32_t(uint8_t(src[0])) | (uint32_t(uint8_t(src[1])) << 8) | (uint32_t(uint8_t(src[2])) << 16) |
-             (uint32_t(uint8_t(src[3])) << 24);
-    }
-    int8_t* dst = DA + ((int64_t(s) * ncg + cg) * Tpad + t0 + tt) * 16;
-    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    const uint4 v = *reinterpret_cast<const uint4*>(&tt_tile[sl][tt][16 * g]);
+    *reinterpret_cast<uint4*>(DA + ((int64_t(sl) * ncg + cg) * Tpad + t0 + tt) * 16) = v;
   }
-  // DB: (s, a, 16-byte piece of 8): zero outside the shard
+  // DB: (s, a, 16-byte piece of 8)
   for (int q = tid; q < 3 * 32 * 8; q += 256) {
-    const int s = q / 256, rem = q % 256, a = rem / 8, c = rem % 8;
+    const int sl = q / 256, rem = q % 256, a = rem / 8, c = rem % 8;
     if (a0 + a >= l) continue;
-    uint32_t w[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      uint32_t v = 0;
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const int tt = 16 * c + 4 * u + b;
-        const int64_t t = t0 + tt;
-        const uint8_t x = (t >= t_begin && t < t_end) ? uint8_t(tile[s][tt][a]) : 0;
-        v |= uint32_t(x) << (8 * b);
-      }
-      w[u] = v;
-    }
-    int8_t* dst = DB + (int64_t(s) * l + a0 + a) * Tpad + t0 + 16 * c;
-    *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    const uint4 v = *reinterpret_cast<const uint4*>(&ta_tile[sl][a][16 * c]);
+    *reinterpret_cast<uint4*>(DB + (int64_t(sl) * l + a0 + a) * Tpad + t0 + 16 * c) = v;
   }
 }
 
@@ -492,8 +492,11 @@ ssi_status cov_i8(const void* Y, int dtype, int64_t N, int l, int64_t ldY, int l
   if (cudaMemsetAsync(mx, 0, sizeof(unsigned long long) * l, s) != cudaSuccess) return launch_check("cov_i8 memset");
   {
     dim3 grid(592, (l + 31) / 32);
-    if (dtype == SSI_F32) chan_max_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(Y), N, l, ldY, mx, status);
-    else chan_max_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(Y), N, l, ldY, mx, status);
+    if (dtype == SSI_F32) {
+      chan_max_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(Y), N, l, ldY, mx, status);
+    } else {
+      chan_max_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double*>(Y), N, l, ldY, mx, status);
+    }
     SSI_TRY(launch_check("chan_max_kernel"));
     chan_exp_kernel<<<(l + 127) / 128, 128, 0, s>>>(mx, l, e);
     SSI_TRY(launch_check("chan_exp_kernel"));
