@@ -402,8 +402,16 @@ __global__ void __launch_bounds__(HT) hess_order_kernel(EigArgs g) {
       if (valid) {
         const int pi = (warp >> 2) * 32 + lane;
         const double ws = ((part[0][pi] + part[1][pi]) + (part[2][pi] + part[3][pi])) * tau;
-#pragma unroll 4
-        for (int c = q; c < L; c += 4) base[(j + 1 + c) * ld] -= ws * v[c];
+        // 16 read-modify-writes in flight (the row does not fit the registers at 1024 threads)
+        int c = q;
+        for (; c + 12 < L; c += 16) {
+          double* p0 = base + (j + 1 + c) * ld;
+          const int64_t d4 = 4 * ld;
+          const double x0 = p0[0], x1 = p0[d4], x2 = p0[2 * d4], x3 = p0[3 * d4];
+          p0[0] = fma(-ws, v[c], x0); p0[d4] = fma(-ws, v[c + 4], x1);
+          p0[2 * d4] = fma(-ws, v[c + 8], x2); p0[3 * d4] = fma(-ws, v[c + 12], x3);
+        }
+        for (; c < L; c += 4) base[(j + 1 + c) * ld] -= ws * v[c];
       }
       __syncthreads();
     }
