@@ -115,8 +115,6 @@ struct EigArgs {
 struct Smem {
   double* H;      // banded Hessenberg / Schur
   int* rowoff;    // n+1
-  double* v;      // n: Householder vector (Hessenberg phase)
-  double* refl;   // 3 n: (v1, v2, tau) per bulge step
   double* x;      // NW * 2 * n: per-warp complex eigenvector
   int* cj;        // cap: block start of candidate
   QEntry* q;      // NSLOT queue entries (H group -> C group)
@@ -419,9 +417,9 @@ __global__ void __launch_bounds__(HT) hess_order_kernel(EigArgs g) {
 }
 
 // ---------------------------------------------------------------- Francis QR + vectors
-// One CTA (256 threads) per order. The Hessenberg matrix lives in shared memory with up to
-// three sub-diagonals (room for the bulge); warp 0 chases the bulge alone (warp-synchronous),
-// all threads run the deflation test and apply each sweep's reflectors to C rows.
+// One CTA (256 threads) per order. The Hessenberg matrix lives in shared memory with SUB
+// sub-diagonals (room for the bulge); warps 0-3 iterate on it (warp 0 chases the bulge), warps
+// 5-7 apply the same transformations to the Schur vectors C.
 __device__ __forceinline__ int band_off(int n, int i) {
   // offset of row i: rows 0..SUB have n entries, row r > SUB has n - r + SUB
   return i <= SUB + 1 ? i * n
@@ -469,8 +467,6 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     char* p = reinterpret_cast<char*>(dsm);
     const int nm = g.n_max;
     s.H = reinterpret_cast<double*>(p);      p += sizeof(double) * band_elems(nm);
-    s.v = reinterpret_cast<double*>(p);      p += sizeof(double) * nm;
-    s.refl = reinterpret_cast<double*>(p);   p += sizeof(double) * 3 * nm;
     s.x = reinterpret_cast<double*>(p);      p += sizeof(double) * x_elems(nm);
     s.cre = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
     s.cim = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
@@ -513,17 +509,10 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       hsync();
       return s.q + qslot;
     };
-    int last_slot = -1, last_use = 0;   // most recently published entry
     auto publish = [&]() {
       hsync();
       if (htid == 0) mbar_arrive(&s.q_full[qslot]);
-      last_slot = qslot; last_use = quse;
       if (++qslot == NSLOT) { qslot = 0; ++quse; }
-    };
-    // wait until the C group has finished entry (slot, use)
-    auto wait_done = [&](int slot, int use) {
-      if (htid == 0) { const long long tq = clock64(); mbar_wait_parity(&s.q_empty[slot], use & 1); t_cwait += clock64() - tq; }
-      hsync();
     };
     while (ihi >= 0) {
       long long ta = clock64();
@@ -1040,7 +1029,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
 
 size_t modal_smem_bytes(int n_max, int cap) {
   return sizeof(QEntry) * NSLOT + 2 * sizeof(uint64_t) * NSLOT +
-         sizeof(double) * (band_elems(n_max) + n_max + 3 * size_t(n_max) + x_elems(n_max) +
+         sizeof(double) * (band_elems(n_max) + x_elems(n_max) +
                            4 * size_t(cap)) +
          sizeof(int) * (size_t(n_max) + 1 + cap) + 64;
 }
