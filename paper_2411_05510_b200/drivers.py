@@ -220,33 +220,52 @@ def gather_tables(local: dict, assignment, make_empty, rank: int, world: int, gr
 
 
 def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank: int = 0, world: int = 1,
-                 group=None):
+                 group=None, n_streams: int = 8):
     """3D stabilization diagram (steps i-ii) for the time-lag steps `lags`:
     covariances once up to lag 2 max(i) - 1 (time-sharded over ranks + one all-reduce),
-    Toeplitz + RSVD + modal sweep per lag (lags assigned by LPT), all tables gathered,
-    ssi_stab3d over the lag axis. Returns ({i: PoleTable}, flags, stable_count)."""
+    Toeplitz + RSVD + modal sweep per lag (lags assigned by LPT; on a rank the lags are
+    independent and run on `n_streams` CUDA streams, largest first, each stream with its own
+    workspaces), all tables gathered, ssi_stab3d over the lag axis.
+    Returns ({i: PoleTable}, flags, stable_count)."""
     lags = sorted(lags)
     lag_hi = 2 * lags[-1] - 1
     R = sharded_covariances(Y, lag_hi, rank, world, P.cov_mode, group)
     assign = lpt_assign(lags, world)
     dev = Y.device
-    m_max = P.l * lags[-1]
-    if P.structured:
-        Tbuf = None
-        ws_rsvd = api._workspace(api.rsvd_toeplitz_ws_bytes(P.l, lags[-1], P.k, P.n_max), dev)
-    else:
-        Tbuf = torch.empty(m_max * m_max, dtype=torch.float64, device=dev)
-        ws_rsvd = api._workspace(api.rsvd_ws_bytes(m_max, P.k, P.n_max), dev)
-    ws_modal = api._workspace(max(api.modal_sweep_ws_bytes(P.l, i, P.n_min, P.n_max, P.n_step) for i in lags), dev)
-    local = {}
-    for i in assign[rank]:
-        m = P.l * i
+    mine = sorted(assign[rank], reverse=True)            # largest lags first (longest chains)
+    ns = max(1, min(n_streams, len(mine)))
+    cur = torch.cuda.current_stream(dev)
+    lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
+    streams = [torch.cuda.Stream(device=dev, priority=hi) for _ in range(ns)]
+    slots = []
+    for j in range(ns):
+        lag_max = max(mine[j::ns])                       # workspaces sized for the slot's largest lag
+        m_max = P.l * lag_max
         if P.structured:
-            U, S = api.rsvd_toeplitz(R, i, P.k, P.q, P.seed, i, P.n_max, ws=ws_rsvd)
+            ws_r = api._workspace(api.rsvd_toeplitz_ws_bytes(P.l, lag_max, P.k, P.n_max), dev)
+            tb = None
         else:
-            T = api.toeplitz(R, i, out=Tbuf[:m * m].view(m, m))
-            U, S = api.rsvd(T, P.k, P.q, P.seed, i, P.n_max, ws=ws_rsvd)
-        local[i] = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=ws_modal)
+            ws_r = api._workspace(api.rsvd_ws_bytes(m_max, P.k, P.n_max), dev)
+            tb = torch.empty(m_max * m_max, dtype=torch.float64, device=dev)
+        ws_m = api._workspace(max(api.modal_sweep_ws_bytes(P.l, i, P.n_min, P.n_max, P.n_step)
+                                  for i in mine[j::ns]), dev)
+        slots.append((ws_r, tb, ws_m))
+    local = {}
+    for n_, i in enumerate(mine):
+        j = n_ % ns
+        st = streams[j]
+        st.wait_stream(cur)                              # R (and the workspaces) are ready
+        ws_r, tb, ws_m = slots[j]
+        with torch.cuda.stream(st):
+            m = P.l * i
+            if P.structured:
+                U, S = api.rsvd_toeplitz(R, i, P.k, P.q, P.seed, i, P.n_max, ws=ws_r)
+            else:
+                T = api.toeplitz(R, i, out=tb[:m * m].view(m, m))
+                U, S = api.rsvd(T, P.k, P.q, P.seed, i, P.n_max, ws=ws_r)
+            local[i] = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=ws_m)
+    for st in streams:
+        cur.wait_stream(st)
     tables = gather_tables(local, assign, lambda: api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, dev),
                            rank, world, group)
     flags, counts = api.stab3d([tables[i] for i in lags], crit)

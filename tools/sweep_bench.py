@@ -1,0 +1,56 @@
+"""Single-GPU timings of the two repetition workloads (not bench.py's metric):
+  c4: the full 3D lag sweep (i = 20..80 step 4, covariances once to lag 159, 16 structured RSVDs +
+      modal sweeps, stab3d) -- wall time on the device (CUDA events), after one warm-up sweep;
+  c5: continuous monitoring, records/s of the RecordPipeline (8 in flight) over 32 records
+      (8 distinct drifting c5 records rotated, device-resident).
+Prints one JSON line."""
+import json, os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import oracle
+import synth
+from paper_2411_05510_b200 import api, drivers
+
+out = {}
+# ---- c4
+cfg = synth.config("c4")
+lags = list(cfg.lags)
+Y = torch.from_numpy(synth.make_record(cfg)[0]).cuda()
+P = drivers.SweepParams(l=cfg.l, i=max(lags), n_max=cfg.n_max, p=cfg.p, q=cfg.q, fs=cfg.fs, n_min=cfg.n_min,
+                        n_step=cfg.n_step, seed=cfg.philox_key, cov_mode="int8x3")
+crit = api.Criteria(**oracle.SC_BRIDGE_3D.__dict__)
+drivers.lag_sweep_3d(Y, P, lags, crit)
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+tables, flags, counts = drivers.lag_sweep_3d(Y, P, lags, crit)
+b.record()
+torch.cuda.synchronize()
+out["c4_sweep_ms"] = a.elapsed_time(b)
+out["c4_lags"] = len(lags)
+out["c4_stable_poles"] = int(counts.sum().item())
+del Y
+# ---- c5
+cfg = synth.config("c5")
+recs = [torch.from_numpy(synth.make_record(cfg, r)[0]).cuda() for r in range(8)]
+P = drivers.SweepParams(l=cfg.l, i=cfg.i, n_max=cfg.n_max, p=cfg.p, q=cfg.q, fs=cfg.fs, n_min=cfg.n_min,
+                        n_step=cfg.n_step, seed=cfg.philox_key, cov_mode="int8x3")
+pipe = drivers.RecordPipeline(P, cfg.N, "cuda", n_streams=8)
+for j in range(8):
+    pipe.submit(recs[j], (j << 32) | cfg.i)
+pipe.join()
+torch.cuda.synchronize()
+n = 32
+a.record()
+for st in pipe.streams:
+    st.wait_stream(torch.cuda.current_stream())
+for j in range(n):
+    pipe.submit(recs[j % 8], (j << 32) | cfg.i)
+pipe.join()
+b.record()
+torch.cuda.synchronize()
+ms = a.elapsed_time(b)
+out["c5_records_per_s"] = n / (ms / 1e3)
+out["c5_ms_per_record"] = ms / n
+out["gpu"] = torch.cuda.get_device_name()
+print(json.dumps(out))
