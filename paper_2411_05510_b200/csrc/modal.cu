@@ -938,24 +938,24 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       if (lane == 0) {
         if (!two) {
           double dr = H(i, i) - wr, di = -wi;
-          if (hypot(dr, di) < smin) { dr = smin; di = 0.0; }
-          const double den = dr * dr + di * di;
-          xr[i] = (r2r * dr + r2i * di) / den;
-          xim[i] = (r2i * dr - r2r * di) / den;
+          if (fma(dr, dr, di * di) < smin * smin) { dr = smin; di = 0.0; }
+          const double iden = fast_rcp(fma(dr, dr, di * di));     // inline reciprocal: no slow-path call
+          xr[i] = (r2r * dr + r2i * di) * iden;
+          xim[i] = (r2i * dr - r2r * di) * iden;
         } else {
           // [[m00, m01], [m10, m11]] [x_{i-1}; x_i] = [r1; r2]
           const double m00r = H(i - 1, i - 1) - wr, m00i = -wi, m01 = H(i - 1, i);
           const double m10 = H(i, i - 1), m11r = H(i, i) - wr, m11i = -wi;
           double detr = (m00r * m11r - m00i * m11i) - m01 * m10;
           double deti = (m00r * m11i + m00i * m11r);
-          if (hypot(detr, deti) < smin) { detr = smin; deti = 0.0; }
-          const double den = detr * detr + deti * deti;
+          if (fma(detr, detr, deti * deti) < smin * smin) { detr = smin; deti = 0.0; }
+          const double iden = fast_rcp(fma(detr, detr, deti * deti));
           const double n1r = (r1r * m11r - r1i * m11i) - m01 * r2r;
           const double n1i = (r1r * m11i + r1i * m11r) - m01 * r2i;
           const double n2r = (m00r * r2r - m00i * r2i) - m10 * r1r;
           const double n2i = (m00r * r2i + m00i * r2r) - m10 * r1i;
-          xr[i - 1] = (n1r * detr + n1i * deti) / den; xim[i - 1] = (n1i * detr - n1r * deti) / den;
-          xr[i] = (n2r * detr + n2i * deti) / den;     xim[i] = (n2i * detr - n2r * deti) / den;
+          xr[i - 1] = (n1r * detr + n1i * deti) * iden; xim[i - 1] = (n1i * detr - n1r * deti) * iden;
+          xr[i] = (n2r * detr + n2i * deti) * iden;     xim[i] = (n2i * detr - n2r * deti) * iden;
         }
       }
       __syncwarp();
