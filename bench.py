@@ -10,7 +10,7 @@ A9-A11 (modal sweep). Records are device-resident (4 distinct records rotated, e
 276 MB > the 126 MB L2). Multi-GPU (torchrun): each rank processes its own records
 (weak scaling, no data-path collective); time = max over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--cov fp64|int8x3] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--cov fp64|int8x3|spectral] [--impl reference]
 """
 import argparse
 import json
@@ -35,7 +35,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cov", default=os.environ.get("SSI_COV_MODE", "int8x3"), choices=["fp64", "int8x3"])
+    ap.add_argument("--cov", default=os.environ.get("SSI_COV_MODE", "int8x3"), choices=["fp64", "int8x3", "spectral"])
     ap.add_argument("--explicit-t", action="store_true",
                     help="materialize T (A2) and stream it through the RSVD GEMMs instead of "
                          "applying it through its block structure")
@@ -362,7 +362,14 @@ def main():
             traffic = mb(nsum[key]["dram__bytes_read.sum"]) + mb(nsum[key]["dram__bytes_write.sum"])
     except Exception:
         traffic = None
-    if args.cov == "fp64":
+    if args.cov == "spectral":
+        # the stage's tensor work is the cross-spectral product + the inverse transform (FP64
+        # DMMA GEMMs); their algorithmic flops over the whole stage's time (FFT included)
+        f_main, f_inv = api.cov_spectral_flops(cfg.N, cfg.l, 2 * cfg.i - 1)
+        peak = extra["fp64_dgemm_tflops_burst"]
+        peak_src = "measured cuBLAS DGEMM 8192^3 on this pool's B200 (profiles/peaks_extra_r01.json)"
+        work, unit = f_main + f_inv, "TFLOP/s"
+    elif args.cov == "fp64":
         peak = extra["fp64_dgemm_tflops_burst"]
         peak_src = "measured cuBLAS DGEMM 8192^3 on this pool's B200 (profiles/peaks_extra_r01.json)"
         work, unit = flops, "TFLOP/s"
@@ -372,15 +379,19 @@ def main():
         work, unit = 8.0 * flops, "TOP/s"   # each multiply-add runs as eight int8 slice products
     achieved = work / (iso_ms / 1e3) / 1e12
     share = None
-    try:
-        sm = json.load(open(os.path.join(ROOT, "profiles", "smtime_r01.json")))["kernels"]
-        share = {"kernel_sm_time_share_of_record": sm["ssi::<unnamed>::cov_i8_kernel"]["share_sm_time"],
-                 "kernel_serial_share_of_record": sm["ssi::<unnamed>::cov_i8_kernel"]["share_serial"],
-                 "source": "profiles/smtime_r01.json (ncu sm__cycles_active.sum over one c3 record)"}
+    try:   # the covariance stage's share of one record's SM-time, from the committed ncu pass
+        src = {"int8x3": "smtime_r01.json", "spectral": "smtime_spectral_r01.json"}[args.cov]
+        sm = json.load(open(os.path.join(ROOT, "profiles", src)))
+        a1 = sm["stages"]["A1"]
+        share = {"stage_sm_time_share_of_record": a1["share_sm_time"],
+                 "stage_serial_share_of_record": a1["share_serial"],
+                 "source": f"profiles/{src} (ncu sm__cycles_active.sum over one c3 record)"}
     except Exception:
         share = None
-    roof = {"bound": "tensor", "step_share": share, "kernel": f"covariance A1 ({args.cov}: chan_max + slice + tcgen05 contraction + reduce)"
-            if args.cov == "int8x3" else "covariance A1 (fp64 DMMA)",
+    kname = {"int8x3": "covariance A1 (int8x3: chan_max + slice + tcgen05 contraction + reduce)",
+             "fp64": "covariance A1 (fp64 DMMA)",
+             "spectral": "covariance A1 (spectral: segment FFT + cross-spectral DMMA product + inverse-DFT DMMA GEMM)"}
+    roof = {"bound": "tensor", "step_share": share, "kernel": kname[args.cov],
             "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": traffic,
             "peak_source": peak_src, "kernel_ms": iso_ms, "kernel_ms_in_pipeline": cov_ms,
             "algorithmic_flop_per_launch": flops, "algorithmic_tflops": flops / (iso_ms / 1e3) / 1e12,

@@ -64,8 +64,15 @@ enum { SSI_F32 = 0, SSI_F64 = 1 };
  *                   power-of-two scale; the eight leading slice products (all but d3*d3) are summed
  *                   EXACTLY in int32 on the 5th-gen tensor cores (tcgen05 kind::i8)
  *                   and promoted to FP64. Error is the slicing rounding only
- *                   (<= 2^-22 of the channel's max |y| per sample); see DESIGN.md. */
-enum { SSI_COV_FP64 = 0, SSI_COV_INT8X3 = 1 };
+ *                   (<= 2^-22 of the channel's max |y| per sample); see DESIGN.md.
+ *  SSI_COV_SPECTRAL : the same sums through segment cross-spectra, FP64 throughout: the record
+ *                   is cut into segments of B = F - lag_hi samples (F a power of two <= 2048
+ *                   chosen by a flop model), one FFT per segment and channel gives the spectra
+ *                   of the segment and of the segment plus its lag_hi halo, their cross-spectra
+ *                   are summed over segments on the FP64 tensor cores (DMMA) and an inverse DFT
+ *                   at the requested lags yields R_k exactly up to FP64 rounding (relative error
+ *                   ~1e-15 of the lag-0 scale). Needs lag_hi < 2048. See DESIGN.md. */
+enum { SSI_COV_FP64 = 0, SSI_COV_INT8X3 = 1, SSI_COV_SPECTRAL = 2 };
 
 /* ------------------------------------------------------------------------------
  * A1. Lagged output covariances (§2.1; normalization 1/(N-k), reading
@@ -89,6 +96,12 @@ SSI_API ssi_status ssi_covariances(const void* Y, int32_t dtype, int64_t N, int3
                            double* R, void* ws, size_t ws_bytes, void* stream);
 SSI_API ssi_status ssi_covariances_ws(int64_t N, int32_t l, int32_t lag_lo, int32_t lag_hi,
                               int32_t cov_mode, size_t* bytes);
+/* SSI_COV_SPECTRAL plan for a record of N samples (pure host function): FFT length F (the
+ * segment length is F - lag_hi) and the number of segments S covering the full record. The
+ * cross-spectral product then costs 8 lp^2 S (F/2 + 1) flops and the inverse transform
+ * 2 lp^2 (lag_hi - lag_lo + 1) (F + 2), lp = l rounded up to even. */
+SSI_API ssi_status ssi_cov_spectral_plan(int64_t N, int32_t l, int32_t lag_lo, int32_t lag_hi,
+                                 int32_t* F, int64_t* S);
 
 /* ------------------------------------------------------------------------------
  * A2. Block-Toeplitz matrix T_{1|i}, Eq. (6) (§2.1):

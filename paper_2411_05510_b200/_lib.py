@@ -11,7 +11,7 @@ LIB_PATH = os.path.join(HERE, "libssi.so")
 
 SSI_OK = 0
 SSI_F32, SSI_F64 = 0, 1
-SSI_COV_FP64, SSI_COV_INT8X3 = 0, 1
+SSI_COV_FP64, SSI_COV_INT8X3, SSI_COV_SPECTRAL = 0, 1, 2
 
 
 class PoleTableC(C.Structure):
@@ -32,6 +32,7 @@ P, I32, I64, U64, SZ, D = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size
 SIGNATURES = {
     "ssi_covariances": (I32, [P, I32, I64, I32, I64, I32, I32, I32, I64, I64, I32, P, P, SZ, P]),
     "ssi_covariances_ws": (I32, [I64, I32, I32, I32, I32, C.POINTER(SZ)]),
+    "ssi_cov_spectral_plan": (I32, [I64, I32, I32, I32, C.POINTER(I32), C.POINTER(I64)]),
     "ssi_toeplitz": (I32, [P, I32, I32, P, I64, P]),
     "ssi_rsvd": (I32, [P, I64, I32, I32, I32, U64, U64, I32, P, I64, P, P, SZ, P]),
     "ssi_rsvd_ws": (I32, [I32, I32, I32, C.POINTER(SZ)]),

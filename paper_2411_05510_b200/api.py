@@ -18,9 +18,9 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import PoleTableC, CriteriaC, call, SSI_F32, SSI_F64, SSI_COV_FP64, SSI_COV_INT8X3
+from ._lib import PoleTableC, CriteriaC, call, SSI_F32, SSI_F64, SSI_COV_FP64, SSI_COV_INT8X3, SSI_COV_SPECTRAL
 
-COV_MODES = {"fp64": SSI_COV_FP64, "int8x3": SSI_COV_INT8X3}
+COV_MODES = {"fp64": SSI_COV_FP64, "int8x3": SSI_COV_INT8X3, "spectral": SSI_COV_SPECTRAL}
 
 
 def _ptr(t: torch.Tensor):
@@ -60,6 +60,20 @@ def covariances_ws_bytes(N, l, lag_hi, lag_lo=1, mode="fp64") -> int:
     b = C.c_size_t(0)
     call("ssi_covariances_ws", N, l, lag_lo, lag_hi, COV_MODES[mode], C.byref(b))
     return b.value
+
+
+def cov_spectral_plan(N, l, lag_hi, lag_lo=1):
+    """(F, S): FFT length and segment count SSI_COV_SPECTRAL uses for an N-sample record."""
+    F, S = C.c_int32(0), C.c_int64(0)
+    call("ssi_cov_spectral_plan", N, l, lag_lo, lag_hi, C.byref(F), C.byref(S))
+    return F.value, S.value
+
+
+def cov_spectral_flops(N, l, lag_hi, lag_lo=1):
+    """Algorithmic flops of SSI_COV_SPECTRAL: (cross-spectral product, inverse transform)."""
+    F, S = cov_spectral_plan(N, l, lag_hi, lag_lo)
+    lp = l + (l & 1)
+    return 8.0 * lp * lp * S * (F // 2 + 1), 2.0 * lp * lp * (lag_hi - lag_lo + 1) * (F + 2)
 
 
 def covariances(Y: torch.Tensor, lag_hi: int, lag_lo: int = 1, mode: str = "fp64",

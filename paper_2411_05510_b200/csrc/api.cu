@@ -6,6 +6,7 @@
 
 #include "covariance.cuh"
 #include "cov_i8.cuh"
+#include "cov_spectral.cuh"
 #include "linalg.cuh"
 #include "rsvd.cuh"
 
@@ -39,8 +40,14 @@ static ssi_status reset_status(void* ws, cudaStream_t s) {
 static size_t cov_ws(int64_t N, int l, int lag_lo, int lag_hi, int mode, int64_t span) {
   Carver c(nullptr);
   const int rows = (lag_hi - lag_lo + 1) * l;
-  if (mode == SSI_COV_FP64) c.take<double>(cov_fp64_partial_elems(span, rows, l));
-  else cov_i8_carve(c, N, l, lag_lo, lag_hi);
+  if (mode == SSI_COV_FP64) {
+    c.take<double>(cov_fp64_partial_elems(span, rows, l));
+  } else if (mode == SSI_COV_SPECTRAL) {
+    SpecBufs sb;
+    cov_spec_carve(c, N, span, l, lag_lo, lag_hi, sb);
+  } else {
+    cov_i8_carve(c, N, l, lag_lo, lag_hi);
+  }
   return c.bytes();
 }
 
@@ -82,9 +89,23 @@ ssi_status ssi_covariances_ws(int64_t N, int32_t l, int32_t lag_lo, int32_t lag_
   SSI_REQUIRE(bytes, SSI_ERR_INVALID_ARG, "ssi_covariances_ws: NULL bytes");
   SSI_REQUIRE(N > 0 && l > 0 && lag_lo >= 1 && lag_hi >= lag_lo, SSI_ERR_INVALID_ARG,
               "ssi_covariances_ws: bad sizes");
-  SSI_REQUIRE(cov_mode == SSI_COV_FP64 || cov_mode == SSI_COV_INT8X3, SSI_ERR_DTYPE,
+  SSI_REQUIRE(cov_mode == SSI_COV_FP64 || cov_mode == SSI_COV_INT8X3 || cov_mode == SSI_COV_SPECTRAL, SSI_ERR_DTYPE,
               "ssi_covariances_ws: unknown cov_mode %d", cov_mode);
+  SSI_REQUIRE(cov_mode != SSI_COV_SPECTRAL || cov_spec_supported(lag_hi), SSI_ERR_DTYPE,
+              "ssi_covariances_ws: SSI_COV_SPECTRAL needs lag_hi < %d", kSpecMaxF);
   *bytes = cov_ws(N, l, lag_lo, lag_hi, cov_mode, N);
+  return SSI_OK;
+}
+
+ssi_status ssi_cov_spectral_plan(int64_t N, int32_t l, int32_t lag_lo, int32_t lag_hi, int32_t* F,
+                                 int64_t* S) {
+  SSI_REQUIRE(F && S, SSI_ERR_INVALID_ARG, "ssi_cov_spectral_plan: NULL pointer");
+  SSI_REQUIRE(N > 0 && l > 0 && lag_lo >= 1 && lag_hi >= lag_lo, SSI_ERR_INVALID_ARG,
+              "ssi_cov_spectral_plan: bad sizes");
+  SSI_REQUIRE(cov_spec_supported(lag_hi), SSI_ERR_DTYPE, "ssi_cov_spectral_plan: lag_hi >= %d", kSpecMaxF);
+  const SpecPlan p = spec_plan(N, N, l, lag_lo, lag_hi);
+  *F = p.F;
+  *S = p.S;
   return SSI_OK;
 }
 
@@ -104,10 +125,12 @@ ssi_status ssi_covariances(const void* Y, int32_t dtype, int64_t N, int32_t l, i
               "ssi_covariances: normalize=1 requires the full record");
   SSI_REQUIRE(ldY >= l, SSI_ERR_SHAPE, "ssi_covariances: ldY < l");
   SSI_REQUIRE(dtype == SSI_F32 || dtype == SSI_F64, SSI_ERR_DTYPE, "ssi_covariances: bad dtype");
-  SSI_REQUIRE(cov_mode == SSI_COV_FP64 || cov_mode == SSI_COV_INT8X3, SSI_ERR_DTYPE,
+  SSI_REQUIRE(cov_mode == SSI_COV_FP64 || cov_mode == SSI_COV_INT8X3 || cov_mode == SSI_COV_SPECTRAL, SSI_ERR_DTYPE,
               "ssi_covariances: unknown cov_mode %d", cov_mode);
   SSI_REQUIRE(cov_mode != SSI_COV_INT8X3 || cov_i8_supported(l, lag_hi - lag_lo + 1, ldY, dtype),
               SSI_ERR_DTYPE, "ssi_covariances: SSI_COV_INT8X3 needs l %% 32 == 0 and l <= 256");
+  SSI_REQUIRE(cov_mode != SSI_COV_SPECTRAL || cov_spec_supported(lag_hi), SSI_ERR_DTYPE,
+              "ssi_covariances: SSI_COV_SPECTRAL needs lag_hi < %d", kSpecMaxF);
   const size_t need = cov_ws(N, l, lag_lo, lag_hi, cov_mode, t_end - t_begin);
   SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_covariances: workspace %zu < %zu",
               ws_bytes, need);
@@ -120,6 +143,8 @@ ssi_status ssi_covariances(const void* Y, int32_t dtype, int64_t N, int32_t l, i
     double* part = c.take<double>(cov_fp64_partial_elems(t_end - t_begin, rows, l));
     return cov_fp64(Y, dtype, N, l, ldY, lag_lo, lag_hi, t_begin, t_end, normalize, R, part, st, s);
   }
+  if (cov_mode == SSI_COV_SPECTRAL)
+    return cov_spectral(Y, dtype, N, l, ldY, lag_lo, lag_hi, t_begin, t_end, normalize, R, ws, st, s);
   return cov_i8(Y, dtype, N, l, ldY, lag_lo, lag_hi, t_begin, t_end, normalize, R, ws, st, s);
 }
 

@@ -1,0 +1,481 @@
+// SSI_COV_SPECTRAL: the lagged covariances of A1 (§2.1; R_k with 1/(N-k),
+// DESIGN.md reading A-6) through cross-spectra of time segments, FP64 throughout — the
+// structure-exploiting product SURVEY.md §8(f) NEXT-3 names.
+//
+// The record is cut into segments of B = F - K samples (K = lag_hi). For segment s, channel c:
+//   x_s[r]  = y[sB + r][c] for r < B (zero for r >= B and past the shard end),
+//   ye_s[r] = y[sB + r][c] for r < F (the segment plus a K-sample halo, zero past N).
+// For 0 <= k <= K no circular wrap occurs (r + k < B + K = F), so
+//   sum_t y[t+k][a] y[t][b] = (1/F) sum_f G_ab(f) e^{+2 pi i f k / F},
+//   G_ab(f) = sum_s Ye_{s,a}(f) conj(X_{s,b}(f))
+// exactly (up to rounding). Per segment and channel ONE complex FFT of z = x + i*ye gives
+// both spectra (X = (Z(f) + conj Z(F-f))/2, Ye = (Z(f) - conj Z(F-f))/2i). The sum over
+// segments is, per frequency, a real GEMM of K-dimension 2S on the FP64 tensor cores:
+//   A_f (2l x 2S) = [Xr Xi ..; -Xi Xr ..] (complex-stacked: only the top half is stored, the
+//   GEMM forms the bottom half while loading), B_f (2S x l) = [Yr; Yi],
+//   C_f = A_f B_f  ->  C_f(b, a) = Re G_ab(f), C_f(l + b, a) = Im G_ab(f).
+// The inverse DFT at the K needed lags (hermitian half spectrum, weights 1 / 2 / 1, 1/(N-k)
+// folded in) is a second GEMM R (l^2 x n_lags) = G (l^2 x (F+2)) W ((F+2) x n_lags).
+// Work: 4 l^2 N F/B (cross-spectra) + 2 l^2 n_lags (F+2) (inverse) flops against
+// 2 l^2 sum_k (N-k) for direct summation — about 1/3.4 of the FP64 product count at c3,
+// and the products run at FP64 accuracy (no slicing).
+#include <cmath>
+
+#include "cov_spectral.cuh"
+#include "gemm_f64.cuh"
+
+namespace ssi {
+namespace {
+
+constexpr int kFftThreads = 256;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+// twiddles tw[j] = e^{-2 pi i j / F}; inverse weights W[kk + col*(F+2)], kk = 2f + part.
+__global__ void spec_tables_kernel(int F, int n_lags, int lag_lo, int64_t N, int normalize, double2* tw,
+                                   double* W) {
+  const int64_t ld = F + 2;
+  const int64_t total = F + ld * n_lags;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    if (e < F) {
+      double sn, cs;
+      sincospi(2.0 * double(e) / double(F), &sn, &cs);   // exact argument: e / F is a dyadic
+      tw[e] = make_double2(cs, -sn);
+    } else {
+      const int64_t q = e - F;
+      const int col = int(q / ld), kk = int(q % ld);
+      const int f = kk >> 1, part = kk & 1;
+      const int64_t k = lag_lo + col;
+      const double wf = (f == 0 || 2 * f == F) ? 1.0 : 2.0;
+      double sn, cs;
+      sincospi(2.0 * double((int64_t(f) * k) % F) / double(F), &sn, &cs);
+      const double v = part ? -wf * sn : wf * cs;
+      const double den = double(F) * (normalize ? double(N - k) : 1.0);   // exact product
+      W[q] = v / den;
+    }
+  }
+}
+
+// position of frequency k in the in-place decimation-in-frequency output (mixed radix 2 / 4
+// digit reversal: one radix-2 stage first when log2 F is odd).
+__device__ __forceinline__ int dif_pos(int k, int F, bool r2) {
+  int p = 0, L = F;
+  if (r2) { p += (k & 1) * (L >> 1); k >>= 1; L >>= 1; }
+  while (L > 1) { p += (k & 3) * (L >> 2); k >>= 2; L >>= 2; }
+  return p;
+}
+
+struct FftArgs {
+  const void* Y;
+  int dtype;
+  int64_t N, ldY, t_begin, t_end;
+  int l, lp, F, B;
+  int64_t S;
+  const double2* tw;
+  double* A;   // [F/2+1][2S][lp]: column 2s = Re X_s, 2s+1 = Im X_s (channel contiguous)
+  double* Bs;  // [F/2+1][2S][lp]: row 2s = Re Ye_s, 2s+1 = Im Ye_s
+  int32_t* status;
+};
+
+// One CTA: CH channels of one segment. Load z = x + i ye, radix-2/4 DIF FFT in shared memory,
+// split the two real spectra and write them in the cross-spectral GEMM's operand layouts.
+// F is a compile-time constant so every loop unrolls: the record rows are loaded as CH-wide
+// vectors, all of a thread's loads issued before the first use.
+template <int F>
+__global__ void __launch_bounds__(kFftThreads, 3) spec_fft_kernel(FftArgs g) {
+  constexpr int CH = F <= 1024 ? 4 : 2;
+  constexpr int FP = F + 2;                        // padded channel row (distinct banks)
+  constexpr bool R2 = (__builtin_ctz(F) & 1) != 0;
+  extern __shared__ __align__(16) double2 z[];     // [CH][FP]
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * CH;
+  const int64_t s = blockIdx.y;
+  const int64_t t0 = g.t_begin + s * g.B;
+  bool bad = false;
+  // ---- load: row r of the segment, CH channels per row
+  constexpr int RPT = (F + kFftThreads - 1) / kFftThreads;   // rows per thread
+  const bool vec = g.dtype == SSI_F32 && CH == 4 && c0 + 4 <= g.l &&
+                   ((reinterpret_cast<uintptr_t>(g.Y) | uintptr_t(g.ldY * 4)) & 15) == 0;
+  double v[RPT][CH];
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + u * kFftThreads;
+    const int64_t t = t0 + r;
+    const bool in = r < F && t < g.N;
+    if (vec) {
+      float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (in) q = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(g.Y) + t * g.ldY + c0));
+      v[u][0] = q.x; v[u][1 % CH] = q.y; v[u][2 % CH] = q.z; v[u][3 % CH] = q.w;
+    } else {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int ch = c0 + c;
+        double x = 0.0;
+        if (in && ch < g.l)
+          x = g.dtype == SSI_F32 ? double(static_cast<const float*>(g.Y)[t * g.ldY + ch])
+                                 : static_cast<const double*>(g.Y)[t * g.ldY + ch];
+        v[u][c] = x;
+      }
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < RPT; ++u) {
+    const int r = tid + u * kFftThreads;
+    if (r < F) {
+      const int64_t t = t0 + r;
+      const bool xin = r < g.B && t < g.t_end;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        bad |= !isfinite(v[u][c]);
+        z[c * FP + r] = make_double2(xin ? v[u][c] : 0.0, v[u][c]);
+      }
+    }
+  }
+  if (bad) set_status(g.status, SSI_ERR_NONFINITE);
+  __syncthreads();
+  // ---- decimation-in-frequency stages
+  if (R2) {
+    constexpr int q = F >> 1;
+#pragma unroll
+    for (int e0 = 0; e0 < q * CH; e0 += kFftThreads) {
+      const int e = e0 + tid;
+      if (q * CH % kFftThreads == 0 || e < q * CH) {
+        const int c = e / q, n = e % q;
+        double2* zc = z + c * FP;
+        const double2 x0 = zc[n], x1 = zc[n + q];
+        zc[n] = cadd(x0, x1);
+        zc[n + q] = cmul(csub(x0, x1), __ldg(&g.tw[n]));
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int L = R2 ? (F >> 1) : F; L >= 4; L >>= 2) {
+    const int q = L >> 2, m = F / L;
+#pragma unroll
+    for (int e0 = 0; e0 < (F >> 2) * CH; e0 += kFftThreads) {
+      const int e = e0 + tid;
+      if ((F >> 2) * CH % kFftThreads == 0 || e < (F >> 2) * CH) {
+        const int c = e / (F >> 2), b = e % (F >> 2);
+        const int n = b % q, base = (b / q) * L + n;
+        double2* zc = z + c * FP;
+        const double2 w1 = __ldg(&g.tw[n * m]), w2 = __ldg(&g.tw[2 * n * m]), w3 = __ldg(&g.tw[3 * n * m]);
+        const double2 x0 = zc[base], x1 = zc[base + q], x2 = zc[base + 2 * q], x3 = zc[base + 3 * q];
+        const double2 a0 = cadd(x0, x2), a1 = csub(x0, x2), a2 = cadd(x1, x3);
+        const double2 d = csub(x1, x3);
+        const double2 a3 = make_double2(d.y, -d.x);   // -i (x1 - x3)
+        zc[base] = cadd(a0, a2);
+        zc[base + q] = cmul(cadd(a1, a3), w1);
+        zc[base + 2 * q] = cmul(csub(a0, a2), w2);
+        zc[base + 3 * q] = cmul(csub(a1, a3), w3);
+      }
+    }
+    __syncthreads();
+  }
+  // ---- spectra of x (real part of z) and ye (imaginary part), frequencies 0..F/2
+  constexpr int NF = (F >> 1) + 1;
+  const int64_t sS = 2 * g.S * g.lp;   // per-frequency stride of both spectra
+#pragma unroll 4
+  for (int e = tid; e < NF * CH; e += kFftThreads) {
+    const int f = e / CH, c = e % CH, ch = c0 + c;
+    if (ch >= g.lp) continue;   // ch = l < lp (odd l): the zero padding channel
+    const double2 zf = z[c * FP + dif_pos(f, F, R2)];
+    const double2 zm = z[c * FP + dif_pos((F - f) & (F - 1), F, R2)];
+    double* Af = g.A + f * sS + (2 * s) * g.lp + ch;
+    double* Bf = g.Bs + f * sS + (2 * s) * g.lp + ch;
+    __stcs(Af, 0.5 * (zf.x + zm.x));            // Re X
+    __stcs(Af + g.lp, 0.5 * (zf.y - zm.y));     // Im X
+    __stcs(Bf, 0.5 * (zf.y + zm.y));            // Re Ye
+    __stcs(Bf + g.lp, -0.5 * (zf.x - zm.x));    // Im Ye
+  }
+}
+
+// ---------------------------------------------------------------- F = 1024 fast path
+// Three in-register DIF passes (radix 16, 16, 4) instead of five shared-memory radix-4 stages;
+// shared rows padded by one element per 16 and the last pass's butterflies permuted so each
+// quarter-warp hits distinct banks; a butterfly's 15 twiddles w^{rn} are formed from two table
+// entries (w^n, w^{4n}) by at most two complex products; spectra written as 32-byte vectors.
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+constexpr int kF = 1024, kFP = kF + kF / 16;
+
+// in-register radix-2 DIF DFT of length R (R = 16 or 4): x[bitrev(r)] = sum_m x[m] w_R^{rm}
+template <int R>
+__device__ __forceinline__ void dft_dif(double2 (&x)[R]) {
+  // w_16^j, j < 8
+  constexpr double C16[8] = {1.0, 0.92387953251128674, 0.70710678118654752, 0.38268343236508974,
+                             0.0, -0.38268343236508974, -0.70710678118654752, -0.92387953251128674};
+  constexpr double S16[8] = {0.0, 0.38268343236508974, 0.70710678118654752, 0.92387953251128674,
+                             1.0, 0.92387953251128674, 0.70710678118654752, 0.38268343236508974};
+#pragma unroll
+  for (int h = R / 2; h >= 1; h >>= 1) {
+#pragma unroll
+    for (int b0 = 0; b0 < R; b0 += 2 * h) {
+#pragma unroll
+      for (int j = 0; j < h; ++j) {
+        const double2 a = x[b0 + j], b = x[b0 + j + h];
+        x[b0 + j] = cadd(a, b);
+        const double2 d = csub(a, b);
+        const int t = j * (16 / (2 * h));          // w_{2h}^j = w_16^t = cos - i sin
+        if (t == 0) x[b0 + j + h] = d;
+        else if (t == 4) x[b0 + j + h] = make_double2(d.y, -d.x);
+        else x[b0 + j + h] = cmul(d, make_double2(C16[t], -S16[t]));
+      }
+    }
+  }
+}
+template <int R>
+__device__ __forceinline__ constexpr int bitrev(int r) {
+  int v = 0;
+  for (int b = 1; b < R; b <<= 1) v = (v << 1) | ((r & b) ? 1 : 0);
+  return v;
+}
+
+// y_r = x[bitrev(r)] * w^{r n} stored at base + r q; w^{rn} = (w^{4n})^{r/4} (w^n)^{r%4}
+__device__ __forceinline__ void store_twiddled(double2* zc, int base, int q, const double2 (&x)[16], double2 w1,
+                                               double2 w4) {
+  const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+  const double2 w8 = cmul(w4, w4), w12 = cmul(w8, w4);
+  zc[pad16(base)] = x[0];
+#pragma unroll
+  for (int r = 1; r < 16; ++r) {
+    const int e = r & 3, hq = r >> 2;
+    const double2 we = e == 1 ? w1 : (e == 2 ? w2 : w3);
+    const double2 wq = hq == 1 ? w4 : (hq == 2 ? w8 : w12);
+    const double2 w = e == 0 ? wq : (hq == 0 ? we : cmul(wq, we));
+    zc[pad16(base + q * r)] = cmul(x[bitrev<16>(r)], w);
+  }
+}
+
+__global__ void __launch_bounds__(kFftThreads, 3) spec_fft1024_kernel(FftArgs g) {
+  constexpr int CH = 4;
+  extern __shared__ __align__(16) double2 z[];     // [CH][kFP]
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * CH;
+  const int64_t s = blockIdx.y;
+  const int64_t t0 = g.t_begin + s * g.B;
+  // ---- load (rows tid + 256u), CH channels per row
+  {
+    const bool vec = g.dtype == SSI_F32 && c0 + 4 <= g.l &&
+                     ((reinterpret_cast<uintptr_t>(g.Y) | uintptr_t(g.ldY * 4)) & 15) == 0;
+    double v[4][CH];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t t = t0 + tid + u * kFftThreads;
+      if (vec) {
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (t < g.N) q = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(g.Y) + t * g.ldY + c0));
+        v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
+      } else {
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const int ch = c0 + c;
+          double x = 0.0;
+          if (t < g.N && ch < g.l)
+            x = g.dtype == SSI_F32 ? double(static_cast<const float*>(g.Y)[t * g.ldY + ch])
+                                   : static_cast<const double*>(g.Y)[t * g.ldY + ch];
+          v[u][c] = x;
+        }
+      }
+    }
+    bool bad = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int r = tid + u * kFftThreads;
+      const bool xin = r < g.B && t0 + r < g.t_end;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        bad |= !isfinite(v[u][c]);
+        z[c * kFP + pad16(r)] = make_double2(xin ? v[u][c] : 0.0, v[u][c]);
+      }
+    }
+    if (bad) set_status(g.status, SSI_ERR_NONFINITE);
+  }
+  __syncthreads();
+  const int c = tid >> 6, b = tid & 63;
+  double2* zc = z + c * kFP;
+  // ---- pass 1: radix 16 over L = 1024 (q = 64), butterfly n = b
+  {
+    const double2 w1 = __ldg(&g.tw[b]), w4 = __ldg(&g.tw[4 * b]);   // w_1024^n, w_1024^{4n}
+    double2 x[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) x[m] = zc[pad16(b + 64 * m)];
+    dft_dif<16>(x);
+    store_twiddled(zc, b, 64, x, w1, w4);
+  }
+  __syncthreads();
+  // ---- pass 2: radix 16 over L = 64 (q = 4): block b >> 2, n = b & 3
+  {
+    const int n = b & 3, base = (b >> 2) * 64 + n;
+    const double2 w1 = __ldg(&g.tw[16 * n]), w4 = __ldg(&g.tw[64 * n]);   // w_64^n, w_64^{4n}
+    double2 x[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) x[m] = zc[pad16(base + 4 * m)];
+    dft_dif<16>(x);
+    store_twiddled(zc, base, 4, x, w1, w4);
+  }
+  __syncthreads();
+  // ---- pass 3: radix 4 over L = 4 (no twiddles), 4 butterflies per thread
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    // butterfly index permuted (bit 3 of b to bit 1) so 8 consecutive lanes cover 8 banks
+    const int bp = (b & 1) | ((b >> 3) & 1) << 1 | ((b >> 1) & 3) << 2 | (b & 48);
+    const int base = 4 * (bp + 64 * u);
+    double2 x[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) x[m] = zc[pad16(base + m)];
+    dft_dif<4>(x);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) zc[pad16(base + r)] = x[bitrev<4>(r)];
+  }
+  __syncthreads();
+  // ---- extraction: frequency f = d0 + 16 d1 + 256 d2 sits at d0*64 + d1*4 + d2. Positions with
+  // d2 < 2 are exactly f < 512 (f = 512 at position 2): thread p' -> position (p'>>1)*4 + (p'&1).
+  const int64_t sS = 2 * g.S * g.lp;
+#pragma unroll
+  for (int u = 0; u < 3; ++u) {
+    int pf;
+    if (u < 2) {
+      const int pp = tid + u * kFftThreads;
+      pf = (pp >> 1) * 4 + (pp & 1);
+    } else {
+      if (tid != 0) break;
+      pf = 2;                                         // f = 512
+    }
+    const int f = (pf >> 6) + 16 * ((pf >> 2) & 15) + 256 * (pf & 3);
+    const int fm = (kF - f) & (kF - 1);
+    const int pm = (fm & 15) * 64 + ((fm >> 4) & 15) * 4 + (fm >> 8);
+    double xr[CH], xi[CH], yr[CH], yi[CH];
+#pragma unroll
+    for (int cc = 0; cc < CH; ++cc) {
+      const double2 zf = z[cc * kFP + pad16(pf)], zm = z[cc * kFP + pad16(pm)];
+      xr[cc] = 0.5 * (zf.x + zm.x);
+      xi[cc] = 0.5 * (zf.y - zm.y);
+      yr[cc] = 0.5 * (zf.y + zm.y);
+      yi[cc] = -0.5 * (zf.x - zm.x);
+    }
+    double* Af = g.A + f * sS + (2 * s) * g.lp + c0;
+    double* Bf = g.Bs + f * sS + (2 * s) * g.lp + c0;
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(Af), "d"(xr[0]), "d"(xr[1]), "d"(xr[2]), "d"(xr[3]) : "memory");
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(Af + g.lp), "d"(xi[0]), "d"(xi[1]), "d"(xi[2]), "d"(xi[3]) : "memory");
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(Bf), "d"(yr[0]), "d"(yr[1]), "d"(yr[2]), "d"(yr[3]) : "memory");
+    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(Bf + g.lp), "d"(yi[0]), "d"(yi[1]), "d"(yi[2]), "d"(yi[3]) : "memory");
+  }
+}
+
+// R[lag][a][b] (l x l blocks) <- Rp[lag][a][b] (lp x lp blocks) for odd l
+__global__ void spec_compact_kernel(const double* __restrict__ Rp, int l, int lp, int n_lags, double* __restrict__ R) {
+  const int64_t total = int64_t(n_lags) * l * l;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = e / (int64_t(l) * l), r = e % (int64_t(l) * l);
+    const int a = int(r / l), b = int(r % l);
+    R[e] = Rp[k * lp * lp + int64_t(a) * lp + b];
+  }
+}
+
+template <int F>
+ssi_status launch_fft(const FftArgs& g, int l, cudaStream_t s) {
+  constexpr int CH = F <= 1024 ? 4 : 2;
+  const size_t smem = size_t(CH) * (F + 2) * sizeof(double2);
+  cudaFuncSetAttribute(spec_fft_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  spec_fft_kernel<F><<<dim3(unsigned((l + CH - 1) / CH), unsigned(g.S)), kFftThreads, smem, s>>>(g);
+  return launch_check("spec_fft_kernel");
+}
+
+}  // namespace
+
+// F minimises the flop model on the full record length N (so a time shard of the same record
+// uses the same F and never needs more workspace than the full record); S covers the shard.
+SpecPlan spec_plan(int64_t N, int64_t span, int l, int lag_lo, int lag_hi) {
+  SpecPlan p{};
+  p.lp = l + (l & 1);
+  p.n_lags = lag_hi - lag_lo + 1;
+  double best = -1.0;
+  for (int F = 64; F <= kSpecMaxF; F *= 2) {
+    if (F <= lag_hi) continue;
+    const int B = F - lag_hi;
+    const int64_t S = (N + B - 1) / B;
+    const double main = 2.0 * (2.0 * p.lp) * p.lp * (2.0 * S) * (F / 2 + 1);
+    const double inv = 2.0 * double(p.lp) * p.lp * p.n_lags * (F + 2);
+    if (best < 0 || main + inv < best) {
+      best = main + inv;
+      p.F = F;
+      p.B = B;
+    }
+  }
+  p.S = span > 0 ? (span + p.B - 1) / p.B : 1;
+  return p;
+}
+
+void cov_spec_carve(Carver& c, int64_t N, int64_t span, int l, int lag_lo, int lag_hi, SpecBufs& b) {
+  const SpecPlan p = spec_plan(N, span, l, lag_lo, lag_hi);
+  const int64_t nf = p.F / 2 + 1;
+  b.tw = c.take<double2>(size_t(p.F));
+  b.W = c.take<double>(size_t(p.F + 2) * p.n_lags);
+  b.A = c.take<double>(size_t(nf) * 2 * p.S * p.lp);
+  b.Bs = c.take<double>(size_t(nf) * 2 * p.S * p.lp);
+  b.G = c.take<double>(size_t(nf) * 2 * p.lp * p.lp);
+  const int chunk = p.n_lags < kTallMaxN ? p.n_lags : kTallMaxN;
+  b.partial = c.take<double>(gemm_tall_partial_elems(int64_t(p.lp) * p.lp, chunk, p.F + 2) + 1);
+  b.Rp = (p.lp != l) ? c.take<double>(size_t(p.n_lags) * p.lp * p.lp) : nullptr;
+}
+
+bool cov_spec_supported(int lag_hi) { return lag_hi < kSpecMaxF; }
+
+ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY, int lag_lo, int lag_hi,
+                        int64_t t_begin, int64_t t_end, int normalize, double* R, void* ws, int32_t* status,
+                        cudaStream_t s) {
+  Carver c(ws);
+  SpecBufs b;
+  cov_spec_carve(c, N, t_end - t_begin, l, lag_lo, lag_hi, b);
+  const SpecPlan p = spec_plan(N, t_end - t_begin, l, lag_lo, lag_hi);
+  const int64_t nf = p.F / 2 + 1, lp2 = int64_t(p.lp) * p.lp;
+  {
+    const int64_t total = p.F + int64_t(p.F + 2) * p.n_lags;
+    int blocks = int((total + 255) / 256);
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    spec_tables_kernel<<<blocks, 256, 0, s>>>(p.F, p.n_lags, lag_lo, N, normalize, b.tw, b.W);
+    SSI_TRY(launch_check("spec_tables_kernel"));
+  }
+  if (t_end > t_begin) {
+    FftArgs g{Y, dtype, N, ldY, t_begin, t_end, l, p.lp, p.F, p.B, p.S, b.tw, b.A, b.Bs, status};
+    if (p.F == kF && p.lp % 4 == 0) {
+      const size_t smem = size_t(4) * kFP * sizeof(double2);
+      cudaFuncSetAttribute(spec_fft1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      spec_fft1024_kernel<<<dim3(unsigned((l + 3) / 4), unsigned(p.S)), kFftThreads, smem, s>>>(g);
+      SSI_TRY(launch_check("spec_fft1024_kernel"));
+    } else switch (p.F) {
+      case 64: SSI_TRY(launch_fft<64>(g, l, s)); break;
+      case 128: SSI_TRY(launch_fft<128>(g, l, s)); break;
+      case 256: SSI_TRY(launch_fft<256>(g, l, s)); break;
+      case 512: SSI_TRY(launch_fft<512>(g, l, s)); break;
+      case 1024: SSI_TRY(launch_fft<1024>(g, l, s)); break;
+      default: SSI_TRY(launch_fft<2048>(g, l, s)); break;
+    }
+    // C_f (2lp x lp) = A_f (2lp x 2S) * B_f (2S x lp); imaginary half to G + lp^2
+    SSI_TRY(gemm_tall_batched_brow(2 * p.lp, p.lp, 2 * p.S, b.A, p.lp, 2 * p.S * p.lp, b.Bs, p.lp,
+                                   2 * p.S * p.lp, b.G, p.lp, 2 * lp2, int(nf), p.lp, lp2, s));
+  } else {
+    if (cudaMemsetAsync(b.G, 0, sizeof(double) * nf * 2 * lp2, s) != cudaSuccess) return launch_check("memset G");
+  }
+  // R (lp^2 x n_lags) = G (lp^2 x (F+2), col-major, ld lp^2) * W ((F+2) x n_lags)
+  double* Rout = b.Rp ? b.Rp : R;
+  for (int c0 = 0; c0 < p.n_lags; c0 += kTallMaxN) {
+    const int nc = p.n_lags - c0 < kTallMaxN ? p.n_lags - c0 : kTallMaxN;
+    SSI_TRY(gemm_tall(lp2, nc, p.F + 2, false, b.G, lp2, b.W + int64_t(c0) * (p.F + 2), p.F + 2,
+                      Rout + int64_t(c0) * lp2, lp2, b.partial, s));
+  }
+  if (b.Rp) {
+    const int64_t total = int64_t(p.n_lags) * l * l;
+    int blocks = int((total + 255) / 256);
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    spec_compact_kernel<<<blocks, 256, 0, s>>>(b.Rp, l, p.lp, p.n_lags, R);
+    SSI_TRY(launch_check("spec_compact_kernel"));
+  }
+  return SSI_OK;
+}
+
+}  // namespace ssi

@@ -19,11 +19,11 @@ constexpr int A_ELEMS = BM * LDK > BK * LDM ? BM * LDK : BK * LDM;   // 1280
 template <int TBN> constexpr int stage_elems() { return A_ELEMS + TBN * LDK; }
 template <int TBN> constexpr size_t tall_smem() { return size_t(STAGES) * stage_elems<TBN>() * sizeof(double); }
 
-__device__ __forceinline__ void cp16(double* dst, const double* src, bool valid) {
+__device__ __forceinline__ void cp16n(double* dst, const double* src, int nbytes) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
-  const int n = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n) : "memory");
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(nbytes) : "memory");
 }
+__device__ __forceinline__ void cp16(double* dst, const double* src, bool valid) { cp16n(dst, src, valid ? 16 : 0); }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
@@ -41,9 +41,10 @@ struct TallArgs {
   int mode;             // 0 plain / batched; 1 lower-triangular tiles of a square C (blockIdx.x
                         // = triangular tile index, TBN = BM); 2 upper-triangular B (N tile
                         // blockIdx.z only needs K rows [0, n0 + TBN))
+  int64_t rsplit, roff; // rsplit > 0: output rows r >= rsplit go to (r - rsplit) + c*ldo + roff
 };
 
-template <bool AROW, int TBN>
+template <bool AROW, bool BROW, int TBN, bool CST = false>
 __device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_t m0, int64_t k0, int64_t ke) {
   const int tid = threadIdx.x;
   double* As = st;
@@ -61,21 +62,33 @@ __device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_
       const int kk = p >> 5, i = (p & 31) * 2;
       const int64_t gi = m0 + i, gk = k0 + kk;
       const bool ok = gi < g.M && gk < ke;
-      cp16(As + kk * LDM + i, ok ? g.A + gi + gk * g.lda : g.A, ok);
+      if (CST) {   // complex-stacked A: row r >= rsplit is row r - rsplit of column k ^ 1 (sign in the fragment)
+        const bool lo = gi >= g.rsplit;
+        cp16(As + kk * LDM + i, ok ? g.A + (lo ? gi - g.rsplit : gi) + (lo ? (gk ^ 1) : gk) * g.lda : g.A, ok);
+      } else {
+        cp16(As + kk * LDM + i, ok ? g.A + gi + gk * g.lda : g.A, ok);
+      }
     }
   }
   // B: TBN columns x 16 k-contiguous doubles = 8 TBN pieces, TBN / 32 per thread
 #pragma unroll
   for (int q = 0; q < TBN / 32; ++q) {
     const int p = tid + q * NT;
-    const int j = p >> 3, kk = (p & 7) * 2;
-    const int64_t gk = k0 + kk;
-    const bool ok = j < g.N && gk < ke;
-    cp16(Bs + j * LDK + kk, ok ? g.B + gk + int64_t(j) * g.ldb : g.B, ok);
+    if (BROW) {                      // k-row kk: TBN n-contiguous doubles = TBN / 2 pieces
+      const int kk = p / (TBN / 2), j = (p % (TBN / 2)) * 2;
+      const int64_t gk = k0 + kk;
+      const int nv = (gk < ke) ? (g.N - j >= 2 ? 2 : (g.N - j > 0 ? int(g.N - j) : 0)) : 0;
+      cp16n(Bs + kk * (TBN + 4) + j, nv ? g.B + gk * g.ldb + j : g.B, 8 * nv);
+    } else {
+      const int j = p >> 3, kk = (p & 7) * 2;
+      const int64_t gk = k0 + kk;
+      const bool ok = j < g.N && gk < ke;
+      cp16(Bs + j * LDK + kk, ok ? g.B + gk + int64_t(j) * g.ldb : g.B, ok);
+    }
   }
 }
 
-template <bool AROW, int TBN>
+template <bool AROW, bool BROW, int TBN, bool CST = false>
 __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
   constexpr int WN = TBN / 4;          // warp tile N (56 / 32 / 16)
   constexpr int NJ = WN / 8;           // m8n8k4 tiles per warp along N
@@ -112,6 +125,11 @@ __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
   const int64_t ke = kb + g.kchunk < g.K ? kb + g.kchunk : g.K;
   const int nst = int((ke - kb + BK - 1) / BK);
 
+  // CST: rows >= rsplit of the stacked operand carry [-Im, Re] of the complex column pair
+  // (2s, 2s+1): the loaded value is negated at even k (k = lane & 3 in the fragment).
+  bool neg[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) neg[i] = CST && (m0 + wm + 8 * i + (lane >> 2) >= g.rsplit) && !(lane & 1);
   double acc[4][NJ][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -120,7 +138,7 @@ __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nst) load_stage<AROW, TBN>(g, sm + s * STAGE_ELEMS, m0, kb + s * BK, ke);
+    if (s < nst) load_stage<AROW, BROW, TBN, CST>(g, sm + s * STAGE_ELEMS, m0, kb + s * BK, ke);
     cp_commit();
   }
   for (int it = 0; it < nst; ++it) {
@@ -128,7 +146,7 @@ __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
     __syncthreads();
     {
       const int nx = it + STAGES - 1;
-      if (nx < nst) load_stage<AROW, TBN>(g, sm + (nx % STAGES) * STAGE_ELEMS, m0, kb + int64_t(nx) * BK, ke);
+      if (nx < nst) load_stage<AROW, BROW, TBN, CST>(g, sm + (nx % STAGES) * STAGE_ELEMS, m0, kb + int64_t(nx) * BK, ke);
       cp_commit();
     }
     const double* As = sm + (it % STAGES) * STAGE_ELEMS;
@@ -138,10 +156,12 @@ __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
       double af[4], bf[NJ];
       const int kq = k4 + (lane & 3), r8 = lane >> 2;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 4; ++i) {
         af[i] = AROW ? As[(wm + 8 * i + r8) * LDK + kq] : As[kq * LDM + wm + 8 * i + r8];
+        if (CST) af[i] = neg[i] ? -af[i] : af[i];
+      }
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) bf[j] = Bs[(wn + 8 * j + r8) * LDK + kq];
+      for (int j = 0; j < NJ; ++j) bf[j] = BROW ? Bs[kq * (TBN + 4) + wn + 8 * j + r8] : Bs[(wn + 8 * j + r8) * LDK + kq];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -157,7 +177,10 @@ __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
       for (int e = 0; e < 2; ++e) {
         const int64_t r = m0 + wm + 8 * i + (lane >> 2);
         const int64_t c = wn + 8 * j + 2 * (lane & 3) + e;
-        if (r < g.M && c < g.N) out[r + c * g.ldo] = acc[i][j][e];
+        if (r < g.M && c < g.N) {
+          if (g.rsplit > 0 && r >= g.rsplit) out[(r - g.rsplit) + c * g.ldo + g.roff] = acc[i][j][e];
+          else out[r + c * g.ldo] = acc[i][j][e];
+        }
       }
 }
 
@@ -171,11 +194,11 @@ __global__ void tall_reduce(int64_t M, int64_t N, int splits, const double* __re
   }
 }
 
-template <bool AROW, int TBN>
+template <bool AROW, int TBN, bool BROW = false, bool CST = false>
 ssi_status launch_one(dim3 grid, const TallArgs& g, cudaStream_t s) {
   constexpr size_t smem = tall_smem<TBN>();
-  cudaFuncSetAttribute(gemm_tall_kernel<AROW, TBN>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  gemm_tall_kernel<AROW, TBN><<<grid, NT, smem, s>>>(g);
+  cudaFuncSetAttribute(gemm_tall_kernel<AROW, BROW, TBN, CST>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  gemm_tall_kernel<AROW, BROW, TBN, CST><<<grid, NT, smem, s>>>(g);
   return launch_check("gemm_tall_kernel");
 }
 
@@ -202,6 +225,30 @@ int tall_splits(int64_t M, int64_t K) {
 }
 
 }  // namespace
+
+// Cross-spectral product (SSI_COV_SPECTRAL): per frequency z, C_z (M x N, M = 2 rsplit) =
+// A_z (M x K) * B_z (K x N, ROW-major: B(k, j) = B[k*ldb + j]) with A_z complex-stacked: the
+// caller stores only rows [0, rsplit) (col-major, column pairs (2s, 2s+1) = Re, Im), rows
+// r >= rsplit read as (-Im, Re) of row r - rsplit; output rows r >= rsplit are written at
+// (r - rsplit) + c*ldc + roff (the imaginary half of the complex product).
+ssi_status gemm_tall_batched_brow(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int64_t sA,
+                                  const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
+                                  int batch, int64_t rsplit, int64_t roff, cudaStream_t s) {
+  if (N > 192 || batch < 1 || batch > 65535 || (ldb & 1) || (lda & 1)) {
+    set_last_error("gemm_tall_batched_brow: N = %lld > 192, bad batch %d or odd ld", (long long)N, batch);
+    return SSI_ERR_INVALID_ARG;
+  }
+  const int64_t kchunk = (K + BK - 1) / BK * BK;
+  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, sA, sB, sC, 0, rsplit, roff};
+  const dim3 grid(unsigned((M + BM - 1) / BM), 1u, unsigned(batch));
+  if (M != 2 * rsplit || (K & 1)) {
+    set_last_error("gemm_tall_batched_brow: need M = 2 rsplit and even K");
+    return SSI_ERR_INVALID_ARG;
+  }
+  if (N <= 64) return launch_one<false, 64, true, true>(grid, g, s);
+  if (N <= 128) return launch_one<false, 128, true, true>(grid, g, s);
+  return launch_one<false, 192, true, true>(grid, g, s);
+}
 
 size_t gemm_tall_partial_elems(int64_t M, int64_t N, int64_t K) {
   const int s = tall_splits(M, K);

@@ -107,3 +107,21 @@ def test_rsvd_toeplitz_workspace_and_validation(lib):
     assert lib.ssi_rsvd_toeplitz(dummy, 6, 20, 40, 2, 1, 1, 41, dummy, 120, dummy, dummy, 1 << 30, None) == 1
     assert lib.ssi_rsvd_toeplitz(dummy, 6, 20, 40, 2, 1, 1, 30, dummy, 119, dummy, dummy, 1 << 30, None) == 2
     assert lib.ssi_rsvd_toeplitz(dummy, 6, 20, 40, 2, 1, 1, 30, dummy, 120, dummy, dummy, 64, None) == 4
+
+
+def test_spectral_covariance_workspace_and_validation(lib):
+    """SSI_COV_SPECTRAL (= 2): host-side plan / workspace query, lag limit, shard monotonicity."""
+    b = C.c_size_t(0)
+    assert lib.ssi_covariances_ws(360000, 192, 1, 119, 2, C.byref(b)) == 0
+    full = b.value
+    # segment spectra of the c3 record: X and Ye, each (F/2+1) x 2S x lp doubles (F = 1024, S = 398)
+    assert full >= 513 * 2 * 398 * 2 * 192 * 8
+    assert lib.ssi_covariances_ws(360000, 192, 1, 2048, 2, C.byref(b)) == 3     # lag_hi >= 2048
+    F, S = C.c_int32(0), C.c_int64(0)
+    assert lib.ssi_cov_spectral_plan(360000, 192, 1, 119, C.byref(F), C.byref(S)) == 0
+    assert (F.value, S.value) == (1024, 398)          # flop model minimum at c3 (DESIGN.md)
+    assert lib.ssi_cov_spectral_plan(360000, 192, 1, 159, C.byref(F), C.byref(S)) == 0
+    assert F.value > 159 and S.value == -(-360000 // (F.value - 159))
+    assert lib.ssi_covariances_ws(6000, 7, 1, 39, 2, C.byref(b)) == 0 and b.value > 0   # odd l
+    dummy = C.c_void_p(16)
+    assert lib.ssi_covariances(dummy, 0, 360000, 192, 192, 1, 119, 2, 0, 360000, 1, dummy, dummy, 8, None) == 4

@@ -114,6 +114,68 @@ def test_covariance_nonfinite_is_flagged(ssi):
     assert e.value.code == 6
 
 
+# ------------------------------------------------------------------ A1 spectral (NEXT-3)
+def _rel_scale(R, Ro):
+    """max over lags of ||R_k - Ro_k||_F relative to the largest ||Ro_k||_F: the segment
+    cross-spectral path's rounding is relative to the record's energy, not to each lag."""
+    scale = max(np.linalg.norm(Ro[k]) for k in range(Ro.shape[0]))
+    return max(np.linalg.norm(R[k] - Ro[k]) for k in range(Ro.shape[0])) / scale
+
+
+@pytest.mark.parametrize("name", ["c1", "c2"])
+def test_covariances_spectral_match_oracle(ssi, name):
+    api, _ = ssi
+    cfg = synth.config(name)
+    Y, _ = synth.make_record(cfg)
+    L = 2 * cfg.i - 1
+    R = api.covariances(_dev(Y), L, mode="spectral", check=True).cpu().numpy()
+    Ro = oracle.covariances(Y, L)
+    assert _rel(R, Ro) <= 1e-6                # contract (north star)
+    assert _rel(R, Ro) <= 1e-12               # internal FP64 tripwire
+    assert _rel_scale(R, Ro) <= 1e-12
+
+
+def test_covariance_spectral_edge_cases(ssi):
+    """Ragged / odd channel counts (padding channel), one channel, max lag = N-1 (segments of
+    one sample), lag_lo > 1, FP64 and strided records, lags past one GEMM N tile (> 224)."""
+    api, _ = ssi
+    rng = np.random.default_rng(31)
+    for (N, l, lo, hi, dt) in ((1013, 7, 1, 40, np.float32), (50, 3, 1, 49, np.float64),
+                               (3000, 65, 3, 17, np.float32), (129, 1, 1, 128, np.float64),
+                               (7000, 4, 1, 300, np.float32), (20000, 33, 5, 5, np.float64)):
+        Y = rng.standard_normal((N, l)).astype(dt)
+        R = api.covariances(_dev(Y), hi, lo, mode="spectral", check=True).cpu().numpy()
+        Ro = oracle.covariances(Y, hi, lo)
+        assert _rel_scale(R, Ro) <= 1e-12, (N, l, lo, hi)
+    Ywide = rng.standard_normal((800, 12))
+    Yd = _dev(Ywide)[:, :9]
+    R = api.covariances(Yd, 11, mode="spectral", check=True).cpu().numpy()
+    assert _rel_scale(R, oracle.covariances(Ywide[:, :9], 11)) <= 1e-12
+
+
+def test_covariance_spectral_time_shards_sum_to_full(ssi):
+    api, drivers = ssi
+    rng = np.random.default_rng(32)
+    Y = rng.standard_normal((5000, 10)).astype(np.float32)
+    Yd = _dev(Y)
+    tot = 0
+    for tb, te in list(drivers.time_shards(5000, 3)) + [(5000, 5000)]:   # + an empty shard
+        tot = tot + api.covariances(Yd, 25, 1, mode="spectral", t_begin=tb, t_end=te,
+                                    normalize=False).cpu().numpy()
+    ref = oracle.covariance_partial_sums(Y, 1, 25)
+    assert np.max(np.abs(tot - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_covariance_spectral_nonfinite_is_flagged(ssi):
+    api, _ = ssi
+    from paper_2411_05510_b200._lib import SSIError
+    Y = np.ones((100, 4), np.float32)
+    Y[37, 2] = np.inf
+    with pytest.raises(SSIError) as e:
+        api.covariances(_dev(Y), 5, mode="spectral", check=True)
+    assert e.value.code == 6
+
+
 # ------------------------------------------------------------------ A2 Toeplitz
 def test_toeplitz_bit_exact(ssi):
     api, _ = ssi
