@@ -20,6 +20,7 @@
 // 2 l^2 sum_k (N-k) for direct summation — about 1/3.4 of the FP64 product count at c3,
 // and the products run at FP64 accuracy (no slicing).
 #include <cmath>
+#include <cstdlib>
 
 #include "cov_spectral.cuh"
 #include "gemm_f64.cuh"
@@ -433,14 +434,19 @@ ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY,
   cov_spec_carve(c, N, t_end - t_begin, l, lag_lo, lag_hi, b);
   const SpecPlan p = spec_plan(N, t_end - t_begin, l, lag_lo, lag_hi);
   const int64_t nf = p.F / 2 + 1, lp2 = int64_t(p.lp) * p.lp;
-  {
+  // Measurement hook (bench.py times the product kernel alone with CUDA events): SSI_SPEC_PHASES
+  // = bit mask of 1 tables + FFT, 2 cross-spectral product, 4 inverse; default all. A partial
+  // mask re-runs phases on the spectra an earlier full call left in the same workspace.
+  const char* ph = getenv("SSI_SPEC_PHASES");
+  const int phases = ph ? atoi(ph) : 7;
+  if (phases & 1) {
     const int64_t total = p.F + int64_t(p.F + 2) * p.n_lags;
     int blocks = int((total + 255) / 256);
     if (blocks > 148 * 4) blocks = 148 * 4;
     spec_tables_kernel<<<blocks, 256, 0, s>>>(p.F, p.n_lags, lag_lo, N, normalize, b.tw, b.W);
     SSI_TRY(launch_check("spec_tables_kernel"));
   }
-  if (t_end > t_begin) {
+  if (t_end > t_begin && (phases & 1)) {
     FftArgs g{Y, dtype, N, ldY, t_begin, t_end, l, p.lp, p.F, p.B, p.S, b.tw, b.A, b.Bs, status};
     if (p.F == kF && p.lp % 4 == 0) {
       const size_t smem = size_t(4) * kFP * sizeof(double2);
@@ -455,13 +461,16 @@ ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY,
       case 1024: SSI_TRY(launch_fft<1024>(g, l, s)); break;
       default: SSI_TRY(launch_fft<2048>(g, l, s)); break;
     }
+  }
+  if (t_end > t_begin && (phases & 2)) {
     // C_f (2lp x lp) = A_f (2lp x 2S) * B_f (2S x lp); imaginary half to G + lp^2
     SSI_TRY(gemm_tall_batched_brow(2 * p.lp, p.lp, 2 * p.S, b.A, p.lp, 2 * p.S * p.lp, b.Bs, p.lp,
                                    2 * p.S * p.lp, b.G, p.lp, 2 * lp2, int(nf), p.lp, lp2, s));
-  } else {
+  } else if (t_end <= t_begin) {
     if (cudaMemsetAsync(b.G, 0, sizeof(double) * nf * 2 * lp2, s) != cudaSuccess) return launch_check("memset G");
   }
   // R (lp^2 x n_lags) = G (lp^2 x (F+2), col-major, ld lp^2) * W ((F+2) x n_lags)
+  if (!(phases & 4)) return SSI_OK;
   double* Rout = b.Rp ? b.Rp : R;
   for (int c0 = 0; c0 < p.n_lags; c0 += kTallMaxN) {
     const int nc = p.n_lags - c0 < kTallMaxN ? p.n_lags - c0 : kTallMaxN;

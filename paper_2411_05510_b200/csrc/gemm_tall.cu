@@ -13,11 +13,17 @@ namespace {
 // N-tile widths: 224 (the RSVD panels, k <= 224), 128 and 64 (the narrow DFT products; a
 // smaller tile also fits 2-3 CTAs per SM).
 constexpr int BM = 64, BN = 224, BK = 16, NT = 256, STAGES = 3;
+#ifndef TALL_CST_ST
+#define TALL_CST_ST 2
+#endif
+#ifndef TALL_CST_MINB
+#define TALL_CST_MINB 2
+#endif
 constexpr int LDK = BK + 4;            // k-contiguous rows (A row-major, B): 20 doubles
 constexpr int LDM = BM + 4;            // m-contiguous rows (A col-major): 68 doubles
 constexpr int A_ELEMS = BM * LDK > BK * LDM ? BM * LDK : BK * LDM;   // 1280
 template <int TBN> constexpr int stage_elems() { return A_ELEMS + TBN * LDK; }
-template <int TBN> constexpr size_t tall_smem() { return size_t(STAGES) * stage_elems<TBN>() * sizeof(double); }
+template <int TBN, int ST = STAGES> constexpr size_t tall_smem() { return size_t(ST) * stage_elems<TBN>() * sizeof(double); }
 
 __device__ __forceinline__ void cp16n(double* dst, const double* src, int nbytes) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -88,8 +94,8 @@ __device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_
   }
 }
 
-template <bool AROW, bool BROW, int TBN, bool CST = false>
-__global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
+template <bool AROW, bool BROW, int TBN, bool CST = false, int ST = STAGES, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
   constexpr int WN = TBN / 4;          // warp tile N (56 / 32 / 16)
   constexpr int NJ = WN / 8;           // m8n8k4 tiles per warp along N
   constexpr int STAGE_ELEMS = stage_elems<TBN>();
@@ -127,9 +133,11 @@ __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
 
   // CST: rows >= rsplit of the stacked operand carry [-Im, Re] of the complex column pair
   // (2s, 2s+1): the loaded value is negated at even k (k = lane & 3 in the fragment).
-  bool neg[4];
+  // The sign flip is an integer XOR of the high word (keeps the FP64 pipe free for DMMA).
+  int negmask[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) neg[i] = CST && (m0 + wm + 8 * i + (lane >> 2) >= g.rsplit) && !(lane & 1);
+  for (int i = 0; i < 4; ++i)
+    negmask[i] = (CST && (m0 + wm + 8 * i + (lane >> 2) >= g.rsplit) && !(lane & 1)) ? int(0x80000000u) : 0;
   double acc[4][NJ][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -137,19 +145,19 @@ __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
+  for (int s = 0; s < ST - 1; ++s) {
     if (s < nst) load_stage<AROW, BROW, TBN, CST>(g, sm + s * STAGE_ELEMS, m0, kb + s * BK, ke);
     cp_commit();
   }
   for (int it = 0; it < nst; ++it) {
-    cp_wait<STAGES - 2>();
+    cp_wait<ST - 2>();
     __syncthreads();
     {
-      const int nx = it + STAGES - 1;
-      if (nx < nst) load_stage<AROW, BROW, TBN, CST>(g, sm + (nx % STAGES) * STAGE_ELEMS, m0, kb + int64_t(nx) * BK, ke);
+      const int nx = it + ST - 1;
+      if (nx < nst) load_stage<AROW, BROW, TBN, CST>(g, sm + (nx % ST) * STAGE_ELEMS, m0, kb + int64_t(nx) * BK, ke);
       cp_commit();
     }
-    const double* As = sm + (it % STAGES) * STAGE_ELEMS;
+    const double* As = sm + (it % ST) * STAGE_ELEMS;
     const double* Bs = As + A_ELEMS;
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(NT) gemm_tall_kernel(TallArgs g) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         af[i] = AROW ? As[(wm + 8 * i + r8) * LDK + kq] : As[kq * LDM + wm + 8 * i + r8];
-        if (CST) af[i] = neg[i] ? -af[i] : af[i];
+        if (CST) af[i] = __hiloint2double(__double2hiint(af[i]) ^ negmask[i], __double2loint(af[i]));
       }
 #pragma unroll
       for (int j = 0; j < NJ; ++j) bf[j] = BROW ? Bs[kq * (TBN + 4) + wn + 8 * j + r8] : Bs[(wn + 8 * j + r8) * LDK + kq];
@@ -194,11 +202,11 @@ __global__ void tall_reduce(int64_t M, int64_t N, int splits, const double* __re
   }
 }
 
-template <bool AROW, int TBN, bool BROW = false, bool CST = false>
+template <bool AROW, int TBN, bool BROW = false, bool CST = false, int ST = STAGES, int MINB = 1>
 ssi_status launch_one(dim3 grid, const TallArgs& g, cudaStream_t s) {
-  constexpr size_t smem = tall_smem<TBN>();
-  cudaFuncSetAttribute(gemm_tall_kernel<AROW, BROW, TBN, CST>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  gemm_tall_kernel<AROW, BROW, TBN, CST><<<grid, NT, smem, s>>>(g);
+  constexpr size_t smem = tall_smem<TBN, ST>();
+  cudaFuncSetAttribute(gemm_tall_kernel<AROW, BROW, TBN, CST, ST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  gemm_tall_kernel<AROW, BROW, TBN, CST, ST, MINB><<<grid, NT, smem, s>>>(g);
   return launch_check("gemm_tall_kernel");
 }
 
@@ -247,7 +255,7 @@ ssi_status gemm_tall_batched_brow(int64_t M, int64_t N, int64_t K, const double*
   }
   if (N <= 64) return launch_one<false, 64, true, true>(grid, g, s);
   if (N <= 128) return launch_one<false, 128, true, true>(grid, g, s);
-  return launch_one<false, 192, true, true>(grid, g, s);
+  return launch_one<false, 192, true, true, TALL_CST_ST, TALL_CST_MINB>(grid, g, s);
 }
 
 size_t gemm_tall_partial_elems(int64_t M, int64_t N, int64_t K) {

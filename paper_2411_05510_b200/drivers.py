@@ -29,7 +29,7 @@ class SweepParams:
     n_min: int = 2
     n_step: int = 2
     seed: int = 0
-    cov_mode: str = "fp64"
+    cov_mode: str = "spectral"
     structured: bool = True     # RSVD through the block structure of T (T never formed)
 
     @property

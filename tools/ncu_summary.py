@@ -7,7 +7,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_active",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
         "launch__registers_per_thread", "launch__grid_size", "launch__block_size", "sm__cycles_elapsed.avg.per_second",
-        "sm__warps_active.avg.pct_of_peak_sustained_active"]
+        "sm__warps_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
 
 rep, out = sys.argv[1], sys.argv[2]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
@@ -16,6 +18,8 @@ hdr, units = rows[0], rows[1]
 res = json.load(open(out)) if "--merge" in sys.argv else {}
 for r in rows[2:]:
     name = r[hdr.index("Kernel Name")].split("(")[0].split("::")[-1]
+    if name in res and "--merge" not in sys.argv:
+        name = name + "#2"
     d = {}
     for k in KEYS:
         if k in hdr:
