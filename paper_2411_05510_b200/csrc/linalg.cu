@@ -128,49 +128,56 @@ constexpr unsigned FULLM = 0xffffffffu;
 
 __device__ __forceinline__ int tri(int r) { return r * (r + 1) / 2; }
 
-// One warp, left-looking: Cholesky of the 32 x 32 diagonal block at (j0, j0) of the packed P
-// in place (lane i computes row i). Reciprocal square roots inline (no slow-path calls).
-// (A register-resident right-looking variant with shuffles measured slower: 600k vs 400k
-// cycles for the seven blocks at k = 220.)
-__device__ __forceinline__ void chol32(double* P, int j0, int lane, int& bad) {
+// One warp, register-resident right-looking Cholesky of the 32 x 32 diagonal block at (j0, j0)
+// of the packed P (lane i holds row i; every index is a compile-time constant, so the row stays
+// in registers): per column one shuffle of the pivot, an inline rsqrt, and the rank-1 update
+// with the column entries broadcast lane to lane.
+__device__ __noinline__ void chol32(double* P, int j0, int lane, int& bad) {
   double* Li = P + tri(j0 + lane) + j0;
+  double a[CB];
+#pragma unroll
+  for (int c = 0; c < CB; ++c) a[c] = (c <= lane) ? Li[c] : 0.0;
+#pragma unroll
   for (int j = 0; j < CB; ++j) {
-    const double* Lj = P + tri(j0 + j) + j0;
-    double s = 0.0;
-    if (lane >= j) {
-      double s1 = 0.0;
-      s = Li[j];
-      int q = 0;
-      for (; q + 1 < j; q += 2) { s = fma(-Li[q], Lj[q], s); s1 = fma(-Li[q + 1], Lj[q + 1], s1); }
-      if (q < j) s = fma(-Li[q], Lj[q], s);
-      s += s1;
-    }
-    double d = __shfl_sync(FULLM, s, j);
+    double d = __shfl_sync(FULLM, a[j], j);
     if (!(d > 0.0) || !isfinite(d)) { bad = 1; d = 1.0; }
-    const double inv = fast_rsqrt(d);
-    if (lane == j) Li[j] = d * inv;
-    else if (lane > j) Li[j] = s * inv;
-    __syncwarp();
+    const double r = fast_rsqrt(d);
+    a[j] = (lane == j) ? d * r : a[j] * r;          // lanes < j hold 0 in a[j]
+#pragma unroll
+    for (int c = j + 1; c < CB; ++c) {
+      const double lcj = __shfl_sync(FULLM, a[j], c);
+      if (lane >= c) a[c] = fma(-a[j], lcj, a[c]);
+    }
   }
+#pragma unroll
+  for (int c = 0; c < CB; ++c)
+    if (c <= lane) Li[c] = a[c];
+  __syncwarp();
 }
 
-// One warp: X = L^{-1} of the lower-triangular 32 x 32 block at (j0, j0) of P, row by row
-// (lane c computes X[p][c]) into Xd (ld CB + 1).
-__device__ __forceinline__ void inv32(const double* P, int j0, double* Xd, int lane) {
+// One warp: X = L^{-1} of the lower-triangular 32 x 32 block at (j0, j0) of P into Xd (ld CB + 1),
+// lane c computing column c by forward substitution in registers (L entries are warp-wide
+// broadcasts from shared memory; X[q][c] = 0 for q < c falls out of the recurrence).
+__device__ __noinline__ void inv32(const double* P, int j0, double* Xd, int lane) {
+  const double myr = fast_rcp(P[tri(j0 + lane) + j0 + lane]);
+  double x[CB];
+#pragma unroll
   for (int p = 0; p < CB; ++p) {
     const double* Lp = P + tri(j0 + p) + j0;
-    double s = 0.0;
-    if (lane <= p) {
-      s = lane == p ? 1.0 : 0.0;
-      double s1 = 0.0;
-      int q = lane;
-      for (; q + 1 < p; q += 2) { s = fma(-Lp[q], Xd[q * (CB + 1) + lane], s); s1 = fma(-Lp[q + 1], Xd[(q + 1) * (CB + 1) + lane], s1); }
-      if (q < p) s = fma(-Lp[q], Xd[q * (CB + 1) + lane], s);
-      s = (s + s1) * fast_rcp(Lp[p]);
+    double s0 = (lane == p) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int q = 0; q < p; ++q) {
+      const double l = Lp[q];
+      if ((q & 3) == 0) s0 = fma(-l, x[q], s0);
+      else if ((q & 3) == 1) s1 = fma(-l, x[q], s1);
+      else if ((q & 3) == 2) s2 = fma(-l, x[q], s2);
+      else s3 = fma(-l, x[q], s3);
     }
-    Xd[p * (CB + 1) + lane] = s;
-    __syncwarp();
+    x[p] = ((s0 + s1) + (s2 + s3)) * __shfl_sync(FULLM, myr, p);
   }
+#pragma unroll
+  for (int p = 0; p < CB; ++p) Xd[p * (CB + 1) + lane] = x[p];
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const double* __restrict__ W, int k,
@@ -200,6 +207,8 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
       chol32(P, j0, lane, bad);
       if (bad && lane == 0) fail = 1;
       inv32(P, j0, Xd, lane);
+      // keep L_JJ^{-1} for the inverse phase (L2-resident scratch; saves recomputing it)
+      for (int e = lane; e < CB * (CB + 1); e += 32) X[J * CB * (CB + 1) + e] = Xd[e];
     }
     __syncthreads();
     tc = clock64(); tdiag += tc - t0c; t0c = tc;
@@ -266,15 +275,18 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
   // (rows above i0 of P already hold X; all T of a block row are formed before any write)
   for (int I = 0; I < nb; ++I) {
     const int i0 = I * CB;
-    if (warp == 0) inv32(P, i0, Xd, lane);
+    if (warp == 0)
+      for (int e = lane; e < CB * (CB + 1); e += 32) Xd[e] = X[I * CB * (CB + 1) + e];
     const int ntask = I * CB;
     const int col = tid;                                   // one column of X_I* per thread
     double T[CB];
 #pragma unroll
     for (int i = 0; i < CB; ++i) T[i] = 0.0;
     if (col < ntask) {
-      for (int q = col; q < i0; ++q) {                      // X[q][col] = 0 for q < col
-        const double xq = P[tri(q) + col];
+      // q runs warp-uniformly from the warp's first column, so the L_I* entries are shared-memory
+      // broadcasts; X[q][col] = 0 for q < col (masked: the packed row q ends at column q)
+      for (int q = col & ~31; q < i0; ++q) {
+        const double xq = (q >= col) ? P[tri(q) + col] : 0.0;
 #pragma unroll
         for (int i = 0; i < CB; ++i) T[i] = fma(P[tri(i0 + i) + q], xq, T[i]);
       }
