@@ -73,19 +73,40 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 // seg (a row segment for right updates, a column segment for left updates: element u is index
 // w0 + u) <- seg after the window's reflectors 0..nsteps-1, reflector t acting on u = t..t+BS-1
 // (refl: v_1..v_{BS-1}, tau per reflector; v_j = 0 past the reflector's length).
-__device__ __forceinline__ void apply_window(double (&seg)[WIN], const double* refl, int nsteps) {
+// Branch-free: the window's unused reflector slots (u >= nsteps) hold zeros (tau = 0, v = 0),
+// which leave seg bit-for-bit unchanged, so every slot is applied and the loop is one basic
+// block the scheduler can pipeline.
+__device__ __forceinline__ void apply_window(double (&seg)[WIN], const double* refl) {
 #pragma unroll
   for (int u = 0; u < SPW; ++u) {
-    if (u < nsteps) {
-      const double* rf = refl + BS * u;
-      double sum = seg[u];
+    const double* rf = refl + BS * u;
+    double sum = seg[u];
 #pragma unroll
-      for (int j = 1; j < BS; ++j) sum = fma(rf[j - 1], seg[u + j], sum);
-      sum *= rf[BS - 1];
-      seg[u] -= sum;
+    for (int j = 1; j < BS; ++j) sum = fma(rf[j - 1], seg[u + j], sum);
+    sum *= rf[BS - 1];
+    seg[u] -= sum;
 #pragma unroll
-      for (int j = 1; j < BS; ++j) seg[u + j] = fma(-sum, rf[j - 1], seg[u + j]);
-    }
+    for (int j = 1; j < BS; ++j) seg[u + j] = fma(-sum, rf[j - 1], seg[u + j]);
+  }
+}
+
+// apply_window on two independent segments, the two update chains interleaved
+__device__ __forceinline__ void apply_window2(double (&sa)[WIN], double (&sb)[WIN], const double* refl) {
+#pragma unroll
+  for (int u = 0; u < SPW; ++u) {
+    const double* rf = refl + BS * u;
+    double r[BS];
+#pragma unroll
+    for (int j = 0; j < BS; ++j) r[j] = rf[j];
+    double xa = sa[u], xb = sb[u];
+#pragma unroll
+    for (int j = 1; j < BS; ++j) { xa = fma(r[j - 1], sa[u + j], xa); xb = fma(r[j - 1], sb[u + j], xb); }
+    xa *= r[BS - 1];
+    xb *= r[BS - 1];
+    sa[u] -= xa;
+    sb[u] -= xb;
+#pragma unroll
+    for (int j = 1; j < BS; ++j) { sa[u + j] = fma(-xa, r[j - 1], sa[u + j]); sb[u + j] = fma(-xb, r[j - 1], sb[u + j]); }
   }
 }
 
@@ -776,6 +797,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
               }
               __syncwarp();
             }
+            for (int e = BS * nsteps + lane; e < BS * SPW; e += 32) refl[e] = 0.0;   // unused slots: no-ops
             if (lane == 0) { qe->type = QWIN; qe->w0 = w0; qe->nw = nw; qe->nsteps = nsteps; }
           }
           publish();                     // the C group may start on this window
@@ -791,26 +813,41 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
           // deferred parts: (L) columns c in [w1, n), rows [w0, w1); (R) rows r in [0, w0),
           // columns [w0, w1)
           const int nL = n - w1, nR = w0;
-          for (int task = htid; task < nL + nR; task += HG_T) {
-            double seg[WIN];
-            const bool isL = task < nL;
-            const int c = w1 + task;
-            double* row = s.H + (isL ? 0 : s.rowoff[task - nL] + w0);
-            if (isL) {
+          // two segments per thread, their reflector chains interleaved (independent: 2x ILP on
+          // the latency-bound update chain)
+          auto seg_load = [&](double (&seg)[WIN], int task) {
+            if (task >= nL + nR) {
+#pragma unroll
+              for (int u = 0; u < WIN; ++u) seg[u] = 0.0;
+            } else if (task < nL) {
+              const int c = w1 + task;
 #pragma unroll
               for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? s.H[s.rowoff[w0 + u] + c] : 0.0;
             } else {
+              const double* row = s.H + s.rowoff[task - nL] + w0;
 #pragma unroll
               for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? row[u] : 0.0;
             }
-            apply_window(seg, refl, nsteps);
-            if (isL) {
+          };
+          auto seg_store = [&](const double (&seg)[WIN], int task) {
+            if (task >= nL + nR) return;
+            if (task < nL) {
+              const int c = w1 + task;
 #pragma unroll
               for (int u = 0; u < WIN; ++u) if (u < nw) s.H[s.rowoff[w0 + u] + c] = seg[u];
             } else {
+              double* row = s.H + s.rowoff[task - nL] + w0;
 #pragma unroll
               for (int u = 0; u < WIN; ++u) if (u < nw) row[u] = seg[u];
             }
+          };
+          for (int t0 = htid; t0 < nL + nR; t0 += 2 * HG_T) {
+            double sa[WIN], sb[WIN];
+            seg_load(sa, t0);
+            seg_load(sb, t0 + HG_T);
+            apply_window2(sa, sb, refl);
+            seg_store(sa, t0);
+            seg_store(sb, t0 + HG_T);
           }
           hsync();
           t_wdef += clock64() - tw1;
@@ -848,7 +885,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
           double seg[WIN];
 #pragma unroll
           for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? cr[int64_t(u) * l] : 0.0;
-          apply_window(seg, e->r, nsteps);
+          apply_window(seg, e->r);
 #pragma unroll
           for (int u = 0; u < WIN; ++u) if (u < nw) cr[int64_t(u) * l] = seg[u];
         }
