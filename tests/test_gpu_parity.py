@@ -142,7 +142,8 @@ def test_covariance_spectral_edge_cases(ssi):
     rng = np.random.default_rng(31)
     for (N, l, lo, hi, dt) in ((1013, 7, 1, 40, np.float32), (50, 3, 1, 49, np.float64),
                                (3000, 65, 3, 17, np.float32), (129, 1, 1, 128, np.float64),
-                               (7000, 4, 1, 300, np.float32), (20000, 33, 5, 5, np.float64)):
+                               (7000, 4, 1, 300, np.float32), (20000, 33, 5, 5, np.float64),
+                               (30000, 6, 1, 1500, np.float32)):          # F = 2048 (two-channel FFT CTAs)
         Y = rng.standard_normal((N, l)).astype(dt)
         R = api.covariances(_dev(Y), hi, lo, mode="spectral", check=True).cpu().numpy()
         Ro = oracle.covariances(Y, hi, lo)
