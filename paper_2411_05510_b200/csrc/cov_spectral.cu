@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kFftThreads, 3) spec_fft_kernel(FftArgs g) {
 // quarter-warp hits distinct banks; a butterfly's 15 twiddles w^{rn} are formed from two table
 // entries (w^n, w^{4n}) by at most two complex products; spectra written as 32-byte vectors.
 __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
-constexpr int kF = 1024, kFP = kF + kF / 16;
+constexpr int kF = 1024, kFP = kF + kF / 16 + 1;   // odd row stride: the 4 channels on distinct banks
 
 // in-register radix-2 DIF DFT of length R (R = 16 or 4): x[bitrev(r)] = sum_m x[m] w_R^{rm}
 template <int R>
@@ -319,51 +319,65 @@ __global__ void __launch_bounds__(kFftThreads, 3) spec_fft1024_kernel(FftArgs g)
     store_twiddled(zc, base, 4, x, w1, w4);
   }
   __syncthreads();
-  // ---- pass 3: radix 4 over L = 4 (no twiddles), 4 butterflies per thread
+  // ---- pass 3 fused with the spectrum extraction. Position d0*64 + d1*4 + r holds frequency
+  // f = d0 + 16 d1 + 256 r after pass 3, and F - f sits in the partner group (d0', d1') =
+  // (16 - d0, 15 - d1) (d0 > 0) or (0, 16 - d1) (d0 = 0), at r' = 3 - r: a thread loads a group
+  // and its partner (the two radix-4 butterflies), transforms both in registers and writes the
+  // four conjugate couples' spectra. 127 group pairs + the self-paired groups (0, 0), (0, 8) per
+  // channel; lane = 4 * pair + channel, so 4 lanes write one 32-byte run.
+  {
+    const int cq = tid & 3;
+    const double2* zq = z + cq * kFP;
+    const int64_t sS = 2 * g.S * g.lp;
+    double* Ab = g.A + (2 * s) * g.lp + c0 + cq;
+    double* Bb = g.Bs + (2 * s) * g.lp + c0 + cq;
+    auto put = [&](int f, double2 zf, double2 zm) {
+      double* Af = Ab + f * sS;
+      double* Bf = Bb + f * sS;
+      __stcs(Af, 0.5 * (zf.x + zm.x));            // Re X
+      __stcs(Af + g.lp, 0.5 * (zf.y - zm.y));     // Im X
+      __stcs(Bf, 0.5 * (zf.y + zm.y));            // Re Ye
+      __stcs(Bf + g.lp, -0.5 * (zf.x - zm.x));    // Im Ye
+    };
+    auto group = [&](int d0, int d1, double2 (&y)[4]) {
+      const int base = d0 * 64 + d1 * 4;
+      double2 x[4];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    // butterfly index permuted (bit 3 of b to bit 1) so 8 consecutive lanes cover 8 banks
-    const int bp = (b & 1) | ((b >> 3) & 1) << 1 | ((b >> 1) & 3) << 2 | (b & 48);
-    const int base = 4 * (bp + 64 * u);
-    double2 x[4];
+      for (int m = 0; m < 4; ++m) x[m] = zq[pad16(base + m)];
+      dft_dif<4>(x);
 #pragma unroll
-    for (int m = 0; m < 4; ++m) x[m] = zc[pad16(base + m)];
-    dft_dif<4>(x);
+      for (int r = 0; r < 4; ++r) y[r] = x[bitrev<4>(r)];
+    };
 #pragma unroll
-    for (int r = 0; r < 4; ++r) zc[pad16(base + r)] = x[bitrev<4>(r)];
-  }
-  __syncthreads();
-  // ---- extraction: frequency f = d0 + 16 d1 + 256 d2 sits at d0*64 + d1*4 + d2. Positions with
-  // d2 < 2 are exactly f < 512 (f = 512 at position 2): thread p' -> position (p'>>1)*4 + (p'&1).
-  const int64_t sS = 2 * g.S * g.lp;
+    for (int u = 0; u < 3; ++u) {
+      const int pidx = (tid >> 2) + 64 * u;
+      if (pidx > 128) break;
+      int d0, d1;
+      if (pidx < 112) { d0 = 1 + (pidx >> 4); d1 = pidx & 15; }
+      else if (pidx < 120) { d0 = 8; d1 = pidx - 112; }
+      else if (pidx < 127) { d0 = 0; d1 = pidx - 119; }
+      else { d0 = 0; d1 = (pidx == 127) ? 0 : 8; }
+      double2 ya[4];
+      group(d0, d1, ya);
+      if (pidx < 127) {
+        const int e0 = d0 ? 16 - d0 : 0, e1 = d0 ? 15 - d1 : 16 - d1;
+        double2 yb[4];
+        group(e0, e1, yb);
 #pragma unroll
-  for (int u = 0; u < 3; ++u) {
-    int pf;
-    if (u < 2) {
-      const int pp = tid + u * kFftThreads;
-      pf = (pp >> 1) * 4 + (pp & 1);
-    } else {
-      if (tid != 0) break;
-      pf = 2;                                         // f = 512
+        for (int r = 0; r < 4; ++r) {
+          const int fa = d0 + 16 * d1 + 256 * r;     // partner frequency F - fa at (e0, e1, 3 - r)
+          if (fa <= kF / 2) put(fa, ya[r], yb[3 - r]);
+          else put(kF - fa, yb[3 - r], ya[r]);
+        }
+      } else if (d1 == 0) {                            // f = 0, 256 (with 768), 512
+        put(0, ya[0], ya[0]);
+        put(256, ya[1], ya[3]);
+        put(512, ya[2], ya[2]);
+      } else {                                         // f = 128 (with 896), 384 (with 640)
+        put(128, ya[0], ya[3]);
+        put(384, ya[1], ya[2]);
+      }
     }
-    const int f = (pf >> 6) + 16 * ((pf >> 2) & 15) + 256 * (pf & 3);
-    const int fm = (kF - f) & (kF - 1);
-    const int pm = (fm & 15) * 64 + ((fm >> 4) & 15) * 4 + (fm >> 8);
-    double xr[CH], xi[CH], yr[CH], yi[CH];
-#pragma unroll
-    for (int cc = 0; cc < CH; ++cc) {
-      const double2 zf = z[cc * kFP + pad16(pf)], zm = z[cc * kFP + pad16(pm)];
-      xr[cc] = 0.5 * (zf.x + zm.x);
-      xi[cc] = 0.5 * (zf.y - zm.y);
-      yr[cc] = 0.5 * (zf.y + zm.y);
-      yi[cc] = -0.5 * (zf.x - zm.x);
-    }
-    double* Af = g.A + f * sS + (2 * s) * g.lp + c0;
-    double* Bf = g.Bs + f * sS + (2 * s) * g.lp + c0;
-    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(Af), "d"(xr[0]), "d"(xr[1]), "d"(xr[2]), "d"(xr[3]) : "memory");
-    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(Af + g.lp), "d"(xi[0]), "d"(xi[1]), "d"(xi[2]), "d"(xi[3]) : "memory");
-    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(Bf), "d"(yr[0]), "d"(yr[1]), "d"(yr[2]), "d"(yr[3]) : "memory");
-    asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(Bf + g.lp), "d"(yi[0]), "d"(yi[1]), "d"(yi[2]), "d"(yi[3]) : "memory");
   }
 }
 
