@@ -71,7 +71,9 @@ enum { SSI_F32 = 0, SSI_F64 = 1 };
  *                   of the segment and of the segment plus its lag_hi halo, their cross-spectra
  *                   are summed over segments on the FP64 tensor cores (DMMA) and an inverse DFT
  *                   at the requested lags yields R_k exactly up to FP64 rounding (relative error
- *                   ~1e-15 of the lag-0 scale). Needs lag_hi < 2048. See DESIGN.md. */
+ *                   ~1e-15 of the lag-0 scale). Segments are processed in chunks of at most
+ *                   512, so the workspace is bounded independently of N. Needs lag_hi < 2048.
+ *                   See DESIGN.md. */
 enum { SSI_COV_FP64 = 0, SSI_COV_INT8X3 = 1, SSI_COV_SPECTRAL = 2 };
 
 /* ------------------------------------------------------------------------------

@@ -75,7 +75,8 @@ struct FftArgs {
   int dtype;
   int64_t N, ldY, t_begin, t_end;
   int l, lp, F, B;
-  int64_t S;
+  int64_t S;    // segment capacity of the spectra buffers (per-frequency stride 2 S lp)
+  int64_t s0;   // first segment of this chunk (blockIdx.y = segment within the chunk)
   const double2* tw;
   double* A;   // [F/2+1][2S][lp]: column 2s = Re X_s, 2s+1 = Im X_s (channel contiguous)
   double* Bs;  // [F/2+1][2S][lp]: row 2s = Re Ye_s, 2s+1 = Im Ye_s
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kFftThreads, 3) spec_fft_kernel(FftArgs g) {
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * CH;
   const int64_t s = blockIdx.y;
-  const int64_t t0 = g.t_begin + s * g.B;
+  const int64_t t0 = g.t_begin + (g.s0 + s) * g.B;
   bool bad = false;
   // ---- load: row r of the segment, CH channels per row
   constexpr int RPT = (F + kFftThreads - 1) / kFftThreads;   // rows per thread
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(kFftThreads, 3) spec_fft1024_kernel(FftArgs g)
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * CH;
   const int64_t s = blockIdx.y;
-  const int64_t t0 = g.t_begin + s * g.B;
+  const int64_t t0 = g.t_begin + (g.s0 + s) * g.B;
   // ---- load (rows tid + 256u), CH channels per row
   {
     const bool vec = g.dtype == SSI_F32 && c0 + 4 <= g.l &&
@@ -392,11 +393,11 @@ __global__ void spec_compact_kernel(const double* __restrict__ Rp, int l, int lp
 }
 
 template <int F>
-ssi_status launch_fft(const FftArgs& g, int l, cudaStream_t s) {
+ssi_status launch_fft(const FftArgs& g, int l, int64_t nseg, cudaStream_t s) {
   constexpr int CH = F <= 1024 ? 4 : 2;
   const size_t smem = size_t(CH) * (F + 2) * sizeof(double2);
   cudaFuncSetAttribute(spec_fft_kernel<F>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  spec_fft_kernel<F><<<dim3(unsigned((l + CH - 1) / CH), unsigned(g.S)), kFftThreads, smem, s>>>(g);
+  spec_fft_kernel<F><<<dim3(unsigned((l + CH - 1) / CH), unsigned(nseg)), kFftThreads, smem, s>>>(g);
   return launch_check("spec_fft_kernel");
 }
 
@@ -422,6 +423,11 @@ SpecPlan spec_plan(int64_t N, int64_t span, int l, int lag_lo, int lag_hi) {
     }
   }
   p.S = span > 0 ? (span + p.B - 1) / p.B : 1;
+  // segments are processed in chunks of at most kSpecChunk (the cross-spectral product
+  // accumulates over chunks), so the workspace does not grow with the record length
+  const int64_t Sfull = (N + p.B - 1) / p.B;
+  p.Sc = Sfull < kSpecChunk ? Sfull : kSpecChunk;
+  if (p.Sc < 1) p.Sc = 1;
   return p;
 }
 
@@ -430,8 +436,8 @@ void cov_spec_carve(Carver& c, int64_t N, int64_t span, int l, int lag_lo, int l
   const int64_t nf = p.F / 2 + 1;
   b.tw = c.take<double2>(size_t(p.F));
   b.W = c.take<double>(size_t(p.F + 2) * p.n_lags);
-  b.A = c.take<double>(size_t(nf) * 2 * p.S * p.lp);
-  b.Bs = c.take<double>(size_t(nf) * 2 * p.S * p.lp);
+  b.A = c.take<double>(size_t(nf) * 2 * p.Sc * p.lp);
+  b.Bs = c.take<double>(size_t(nf) * 2 * p.Sc * p.lp);
   b.G = c.take<double>(size_t(nf) * 2 * p.lp * p.lp);
   const int chunk = p.n_lags < kTallMaxN ? p.n_lags : kTallMaxN;
   b.partial = c.take<double>(gemm_tall_partial_elems(int64_t(p.lp) * p.lp, chunk, p.F + 2) + 1);
@@ -460,27 +466,32 @@ ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY,
     spec_tables_kernel<<<blocks, 256, 0, s>>>(p.F, p.n_lags, lag_lo, N, normalize, b.tw, b.W);
     SSI_TRY(launch_check("spec_tables_kernel"));
   }
-  if (t_end > t_begin && (phases & 1)) {
-    FftArgs g{Y, dtype, N, ldY, t_begin, t_end, l, p.lp, p.F, p.B, p.S, b.tw, b.A, b.Bs, status};
-    if (p.F == kF && p.lp % 4 == 0) {
-      const size_t smem = size_t(4) * kFP * sizeof(double2);
-      cudaFuncSetAttribute(spec_fft1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      spec_fft1024_kernel<<<dim3(unsigned((l + 3) / 4), unsigned(p.S)), kFftThreads, smem, s>>>(g);
-      SSI_TRY(launch_check("spec_fft1024_kernel"));
-    } else switch (p.F) {
-      case 64: SSI_TRY(launch_fft<64>(g, l, s)); break;
-      case 128: SSI_TRY(launch_fft<128>(g, l, s)); break;
-      case 256: SSI_TRY(launch_fft<256>(g, l, s)); break;
-      case 512: SSI_TRY(launch_fft<512>(g, l, s)); break;
-      case 1024: SSI_TRY(launch_fft<1024>(g, l, s)); break;
-      default: SSI_TRY(launch_fft<2048>(g, l, s)); break;
+  for (int64_t s0 = 0; t_end > t_begin && s0 < p.S; s0 += p.Sc) {
+    const int64_t nseg = (p.S - s0 < p.Sc) ? p.S - s0 : p.Sc;
+    if (phases & 1) {
+      FftArgs g{Y, dtype, N, ldY, t_begin, t_end, l, p.lp, p.F, p.B, p.Sc, s0, b.tw, b.A, b.Bs, status};
+      if (p.F == kF && p.lp % 4 == 0) {
+        const size_t smem = size_t(4) * kFP * sizeof(double2);
+        cudaFuncSetAttribute(spec_fft1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        spec_fft1024_kernel<<<dim3(unsigned((l + 3) / 4), unsigned(nseg)), kFftThreads, smem, s>>>(g);
+        SSI_TRY(launch_check("spec_fft1024_kernel"));
+      } else switch (p.F) {
+        case 64: SSI_TRY(launch_fft<64>(g, l, nseg, s)); break;
+        case 128: SSI_TRY(launch_fft<128>(g, l, nseg, s)); break;
+        case 256: SSI_TRY(launch_fft<256>(g, l, nseg, s)); break;
+        case 512: SSI_TRY(launch_fft<512>(g, l, nseg, s)); break;
+        case 1024: SSI_TRY(launch_fft<1024>(g, l, nseg, s)); break;
+        default: SSI_TRY(launch_fft<2048>(g, l, nseg, s)); break;
+      }
+    }
+    if (phases & 2) {
+      // C_f (2lp x lp) (+)= A_f (2lp x 2 nseg) * B_f (2 nseg x lp); imaginary half to G + lp^2
+      SSI_TRY(gemm_tall_batched_brow(2 * p.lp, p.lp, 2 * nseg, b.A, p.lp, 2 * p.Sc * p.lp, b.Bs, p.lp,
+                                     2 * p.Sc * p.lp, b.G, p.lp, 2 * lp2, int(nf), p.lp, lp2, s0 > 0, s));
     }
   }
-  if (t_end > t_begin && (phases & 2)) {
-    // C_f (2lp x lp) = A_f (2lp x 2S) * B_f (2S x lp); imaginary half to G + lp^2
-    SSI_TRY(gemm_tall_batched_brow(2 * p.lp, p.lp, 2 * p.S, b.A, p.lp, 2 * p.S * p.lp, b.Bs, p.lp,
-                                   2 * p.S * p.lp, b.G, p.lp, 2 * lp2, int(nf), p.lp, lp2, s));
-  } else if (t_end <= t_begin) {
+  if (t_end <= t_begin) {
+
     if (cudaMemsetAsync(b.G, 0, sizeof(double) * nf * 2 * lp2, s) != cudaSuccess) return launch_check("memset G");
   }
   // R (lp^2 x n_lags) = G (lp^2 x (F+2), col-major, ld lp^2) * W ((F+2) x n_lags)

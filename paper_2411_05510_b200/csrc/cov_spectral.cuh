@@ -5,10 +5,12 @@ namespace ssi {
 
 // SSI_COV_SPECTRAL (cov_spectral.cu): segment cross-spectra, FP64.
 constexpr int kSpecMaxF = 2048;   // FFT length limit (lag_hi < kSpecMaxF)
+constexpr int kSpecChunk = 512;   // segments per chunk (bounds the spectra workspace)
 
 struct SpecPlan {
   int F, B, lp, n_lags;   // FFT length, segment length F - lag_hi, l rounded up to even, lags
   int64_t S;              // segments covering the time shard
+  int64_t Sc;             // segments per chunk (spectra buffer capacity)
 };
 struct SpecBufs {
   double2* tw;

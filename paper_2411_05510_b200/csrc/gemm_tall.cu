@@ -48,6 +48,7 @@ struct TallArgs {
                         // = triangular tile index, TBN = BM); 2 upper-triangular B (N tile
                         // blockIdx.z only needs K rows [0, n0 + TBN))
   int64_t rsplit, roff; // rsplit > 0: output rows r >= rsplit go to (r - rsplit) + c*ldo + roff
+  int accum;            // 1: out += product (chunked K, fixed order); 0: out = product
 };
 
 template <bool AROW, bool BROW, int TBN, bool CST = false>
@@ -186,8 +187,8 @@ __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
         const int64_t r = m0 + wm + 8 * i + (lane >> 2);
         const int64_t c = wn + 8 * j + 2 * (lane & 3) + e;
         if (r < g.M && c < g.N) {
-          if (g.rsplit > 0 && r >= g.rsplit) out[(r - g.rsplit) + c * g.ldo + g.roff] = acc[i][j][e];
-          else out[r + c * g.ldo] = acc[i][j][e];
+          double* o = (g.rsplit > 0 && r >= g.rsplit) ? out + (r - g.rsplit) + c * g.ldo + g.roff : out + r + c * g.ldo;
+          *o = g.accum ? *o + acc[i][j][e] : acc[i][j][e];
         }
       }
 }
@@ -241,13 +242,13 @@ int tall_splits(int64_t M, int64_t K) {
 // (r - rsplit) + c*ldc + roff (the imaginary half of the complex product).
 ssi_status gemm_tall_batched_brow(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int64_t sA,
                                   const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
-                                  int batch, int64_t rsplit, int64_t roff, cudaStream_t s) {
+                                  int batch, int64_t rsplit, int64_t roff, bool accumulate, cudaStream_t s) {
   if (N > 192 || batch < 1 || batch > 65535 || (ldb & 1) || (lda & 1)) {
     set_last_error("gemm_tall_batched_brow: N = %lld > 192, bad batch %d or odd ld", (long long)N, batch);
     return SSI_ERR_INVALID_ARG;
   }
   const int64_t kchunk = (K + BK - 1) / BK * BK;
-  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, sA, sB, sC, 0, rsplit, roff};
+  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, sA, sB, sC, 0, rsplit, roff, accumulate ? 1 : 0};
   const dim3 grid(unsigned((M + BM - 1) / BM), 1u, unsigned(batch));
   if (M != 2 * rsplit || (K & 1)) {
     set_last_error("gemm_tall_batched_brow: need M = 2 rsplit and even K");

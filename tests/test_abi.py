@@ -125,3 +125,6 @@ def test_spectral_covariance_workspace_and_validation(lib):
     assert lib.ssi_covariances_ws(6000, 7, 1, 39, 2, C.byref(b)) == 0 and b.value > 0   # odd l
     dummy = C.c_void_p(16)
     assert lib.ssi_covariances(dummy, 0, 360000, 192, 192, 1, 119, 2, 0, 360000, 1, dummy, dummy, 8, None) == 4
+    # segments are processed in chunks: a day-long record needs no more spectra workspace
+    assert lib.ssi_covariances_ws(8_640_000, 192, 1, 119, 2, C.byref(b)) == 0
+    assert b.value < 4 * full

@@ -154,6 +154,19 @@ def test_covariance_spectral_edge_cases(ssi):
     assert _rel_scale(R, oracle.covariances(Ywide[:, :9], 11)) <= 1e-12
 
 
+def test_covariance_spectral_long_record_chunks(ssi):
+    """A record long enough that its segments are processed in several chunks (the product
+    accumulates over chunks in a fixed order), against the oracle."""
+    api, _ = ssi
+    N, l, hi = 1_200_000, 8, 60
+    F, S = api.cov_spectral_plan(N, l, hi)
+    assert S > 512                                   # more than one chunk of segments
+    rng = np.random.default_rng(33)
+    Y = rng.standard_normal((N, l)).astype(np.float32)
+    R = api.covariances(_dev(Y), hi, mode="spectral", check=True).cpu().numpy()
+    assert _rel_scale(R, oracle.covariances(Y, hi)) <= 1e-12
+
+
 def test_covariance_spectral_time_shards_sum_to_full(ssi):
     api, drivers = ssi
     rng = np.random.default_rng(32)
