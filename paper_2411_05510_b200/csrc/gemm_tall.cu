@@ -21,9 +21,14 @@ constexpr int BM = 64, BN = 224, BK = 16, NT = 256, STAGES = 3;
 #endif
 constexpr int LDK = BK + 4;            // k-contiguous rows (A row-major, B): 20 doubles
 constexpr int LDM = BM + 4;            // m-contiguous rows (A col-major): 68 doubles
-constexpr int A_ELEMS = BM * LDK > BK * LDM ? BM * LDK : BK * LDM;   // 1280
-template <int TBN> constexpr int stage_elems() { return A_ELEMS + TBN * LDK; }
-template <int TBN, int ST = STAGES> constexpr size_t tall_smem() { return size_t(ST) * stage_elems<TBN>() * sizeof(double); }
+// per-stage tile sizes: A is BM x BK (k-contiguous rows) or BK x BM (m-contiguous rows); B is
+// TBN x BK (k-contiguous) or BK x TBN (BROW: n-contiguous, row pitch TBN + 4)
+template <bool AROW> constexpr int a_elems() { return AROW ? BM * LDK : BK * LDM; }
+template <bool BROW, int TBN> constexpr int b_elems() { return BROW ? BK * (TBN + 4) : TBN * LDK; }
+template <bool AROW, bool BROW, int TBN> constexpr int stage_elems() { return a_elems<AROW>() + b_elems<BROW, TBN>(); }
+template <bool AROW, bool BROW, int TBN, int ST> constexpr size_t tall_smem() {
+  return size_t(ST) * stage_elems<AROW, BROW, TBN>() * sizeof(double);
+}
 
 __device__ __forceinline__ void cp16n(double* dst, const double* src, int nbytes) {
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
@@ -55,7 +60,7 @@ template <bool AROW, bool BROW, int TBN, bool CST = false>
 __device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_t m0, int64_t k0, int64_t ke) {
   const int tid = threadIdx.x;
   double* As = st;
-  double* Bs = st + A_ELEMS;
+  double* Bs = st + a_elems<AROW>();
   // A: 64 x 16 doubles = 512 16-byte pieces, 2 per thread
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
@@ -99,7 +104,7 @@ template <bool AROW, bool BROW, int TBN, bool CST = false, int ST = STAGES, int 
 __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
   constexpr int WN = TBN / 4;          // warp tile N (56 / 32 / 16)
   constexpr int NJ = WN / 8;           // m8n8k4 tiles per warp along N
-  constexpr int STAGE_ELEMS = stage_elems<TBN>();
+  constexpr int STAGE_ELEMS = stage_elems<AROW, BROW, TBN>();
   extern __shared__ __align__(16) double sm[];
   int64_t m0 = int64_t(blockIdx.x) * BM, n0 = 0;
   double* out = g.out + int64_t(blockIdx.y) * g.M * g.N;   // split-K slab (or C)
@@ -159,7 +164,7 @@ __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
       cp_commit();
     }
     const double* As = sm + (it % ST) * STAGE_ELEMS;
-    const double* Bs = As + A_ELEMS;
+    const double* Bs = As + a_elems<AROW>();
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
       double af[4], bf[NJ];
@@ -205,7 +210,7 @@ __global__ void tall_reduce(int64_t M, int64_t N, int splits, const double* __re
 
 template <bool AROW, int TBN, bool BROW = false, bool CST = false, int ST = STAGES, int MINB = 1>
 ssi_status launch_one(dim3 grid, const TallArgs& g, cudaStream_t s) {
-  constexpr size_t smem = tall_smem<TBN, ST>();
+  constexpr size_t smem = tall_smem<AROW, BROW, TBN, ST>();
   cudaFuncSetAttribute(gemm_tall_kernel<AROW, BROW, TBN, CST, ST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   gemm_tall_kernel<AROW, BROW, TBN, CST, ST, MINB><<<grid, NT, smem, s>>>(g);
   return launch_check("gemm_tall_kernel");
