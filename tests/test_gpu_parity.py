@@ -133,6 +133,10 @@ def test_covariances_spectral_match_oracle(ssi, name):
     assert _rel(R, Ro) <= 1e-6                # contract (north star)
     assert _rel(R, Ro) <= 1e-12               # internal FP64 tripwire
     assert _rel_scale(R, Ro) <= 1e-12
+    if name == "c2":                          # c2 plans F = 1024 (fast kernel): its FP64-record branch
+        assert api.cov_spectral_plan(cfg.N, cfg.l, L)[0] == 1024
+        R64 = api.covariances(_dev(Y.astype(np.float64)), L, mode="spectral", check=True).cpu().numpy()
+        assert _rel_scale(R64, Ro) <= 1e-12
 
 
 def test_covariance_spectral_edge_cases(ssi):
