@@ -32,7 +32,7 @@ UNIT = "records/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=80)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cov", default=os.environ.get("SSI_COV_MODE", "spectral"), choices=["fp64", "int8x3", "spectral"])
