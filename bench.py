@@ -371,7 +371,7 @@ def main():
     traffic = None
     try:
         nsum = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")))
-        key = {"int8x3": "cov_i8_kernel", "spectral": "gemm_tall_kernel<0, 1, 192, 1, 2, 2>"}.get(args.cov)
+        key = {"int8x3": "cov_i8_kernel", "spectral": "cross3m_kernel"}.get(args.cov)
         if key and key in nsum:
             mb = lambda d: d["value"] * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[d["unit"]]
             traffic = mb(nsum[key]["dram__bytes_read.sum"]) + mb(nsum[key]["dram__bytes_write.sum"])
@@ -380,7 +380,7 @@ def main():
     stage = None
     if args.cov == "spectral":
         # dominant kernel: the cross-spectral product (FP64 DMMA), its algorithmic flops
-        # 8 lp^2 S (F/2+1) over its own live duration; the whole covariance stage beside it
+        # 6 lp^2 S (F/2+1) over its own live duration; the whole covariance stage beside it
         f_main, f_inv = api.cov_spectral_flops(cfg.N, cfg.l, 2 * cfg.i - 1)
         F, S = api.cov_spectral_plan(cfg.N, cfg.l, 2 * cfg.i - 1)
         peak = extra["fp64_dgemm_tflops_burst"]
@@ -414,7 +414,7 @@ def main():
         share = None
     kname = {"int8x3": "covariance A1 (int8x3: chan_max + slice + tcgen05 contraction + reduce)",
              "fp64": "covariance A1 (fp64 DMMA)",
-             "spectral": "cross-spectral product of A1 (gemm_tall_kernel, FP64 DMMA, complex-stacked operand)"}
+             "spectral": "cross-spectral product of A1 (cross3m_kernel: FP64 DMMA, three real products per complex one)"}
     roof = {"bound": "tensor", "step_share": share, "kernel": kname[args.cov],
             "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": traffic,
             "peak_source": peak_src, "kernel_ms": iso_k, "stage_ms_in_pipeline": cov_ms,

@@ -100,7 +100,7 @@ SSI_API ssi_status ssi_covariances_ws(int64_t N, int32_t l, int32_t lag_lo, int3
                               int32_t cov_mode, size_t* bytes);
 /* SSI_COV_SPECTRAL plan for a record of N samples (pure host function): FFT length F (the
  * segment length is F - lag_hi) and the number of segments S covering the full record. The
- * cross-spectral product then costs 8 lp^2 S (F/2 + 1) flops and the inverse transform
+ * cross-spectral product then costs 6 lp^2 S (F/2 + 1) flops and the inverse transform
  * 2 lp^2 (lag_hi - lag_lo + 1) (F + 2), lp = l rounded up to even. */
 SSI_API ssi_status ssi_cov_spectral_plan(int64_t N, int32_t l, int32_t lag_lo, int32_t lag_hi,
                                  int32_t* F, int64_t* S);

@@ -70,10 +70,11 @@ def cov_spectral_plan(N, l, lag_hi, lag_lo=1):
 
 
 def cov_spectral_flops(N, l, lag_hi, lag_lo=1):
-    """Algorithmic flops of SSI_COV_SPECTRAL: (cross-spectral product, inverse transform)."""
+    """Algorithmic flops of SSI_COV_SPECTRAL: (cross-spectral product -- three real products per
+    complex one, 6 lp^2 S (F/2+1) -- and the inverse transform)."""
     F, S = cov_spectral_plan(N, l, lag_hi, lag_lo)
     lp = l + (l & 1)
-    return 8.0 * lp * lp * S * (F // 2 + 1), 2.0 * lp * lp * (lag_hi - lag_lo + 1) * (F + 2)
+    return 6.0 * lp * lp * S * (F // 2 + 1), 2.0 * lp * lp * (lag_hi - lag_lo + 1) * (F + 2)
 
 
 def covariances(Y: torch.Tensor, lag_hi: int, lag_lo: int = 1, mode: str = "fp64",

@@ -10,15 +10,15 @@
 //   G_ab(f) = sum_s Ye_{s,a}(f) conj(X_{s,b}(f))
 // exactly (up to rounding). Per segment and channel ONE complex FFT of z = x + i*ye gives
 // both spectra (X = (Z(f) + conj Z(F-f))/2, Ye = (Z(f) - conj Z(F-f))/2i). The sum over
-// segments is, per frequency, a real GEMM of K-dimension 2S on the FP64 tensor cores:
-//   A_f (2l x 2S) = [Xr Xi ..; -Xi Xr ..] (complex-stacked: only the top half is stored, the
-//   GEMM forms the bottom half while loading), B_f (2S x l) = [Yr; Yi],
-//   C_f = A_f B_f  ->  C_f(b, a) = Re G_ab(f), C_f(l + b, a) = Im G_ab(f).
+// segments is, per frequency, three real products on the FP64 tensor cores (cross_spectral.cu):
+//   T1 = sum Xr Yr, T2 = sum Xi Yi, T3 = sum (Xr + Xi)(Yi - Yr); Re G = T1 + T2, Im G = T3 + T1 - T2
+// (6 lp^2 S flops per frequency; SSI_SPEC_STACKED=1 selects the 8 lp^2 S complex-stacked real
+// GEMM instead, for A/B measurement).
 // The inverse DFT at the K needed lags (hermitian half spectrum, weights 1 / 2 / 1, 1/(N-k)
 // folded in) is a second GEMM R (l^2 x n_lags) = G (l^2 x (F+2)) W ((F+2) x n_lags).
-// Work: 4 l^2 N F/B (cross-spectra) + 2 l^2 n_lags (F+2) (inverse) flops against
-// 2 l^2 sum_k (N-k) for direct summation — about 1/3.4 of the FP64 product count at c3,
-// and the products run at FP64 accuracy (no slicing).
+// Work: 3 l^2 N F/B (cross-spectra) + 2 l^2 n_lags (F+2) (inverse) flops against
+// 2 l^2 sum_k (N-k) for direct summation (60x fewer at c3), and the products run at FP64
+// accuracy (no slicing).
 #include <cmath>
 #include <cstdlib>
 
@@ -486,8 +486,12 @@ ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY,
     }
     if (phases & 2) {
       // C_f (2lp x lp) (+)= A_f (2lp x 2 nseg) * B_f (2 nseg x lp); imaginary half to G + lp^2
-      SSI_TRY(gemm_tall_batched_brow(2 * p.lp, p.lp, 2 * nseg, b.A, p.lp, 2 * p.Sc * p.lp, b.Bs, p.lp,
-                                     2 * p.Sc * p.lp, b.G, p.lp, 2 * lp2, int(nf), p.lp, lp2, s0 > 0, s));
+      static const bool stacked = getenv("SSI_SPEC_STACKED") != nullptr;   // A/B measurement only
+      if (stacked)
+        SSI_TRY(gemm_tall_batched_brow(2 * p.lp, p.lp, 2 * nseg, b.A, p.lp, 2 * p.Sc * p.lp, b.Bs, p.lp,
+                                       2 * p.Sc * p.lp, b.G, p.lp, 2 * lp2, int(nf), p.lp, lp2, s0 > 0, s));
+      else
+        SSI_TRY(cross_spectral_3m(b.A, b.Bs, 2 * p.Sc * p.lp, nseg, p.lp, int(nf), b.G, s0 > 0, s));
     }
   }
   if (t_end <= t_begin) {
