@@ -319,12 +319,16 @@ __device__ __forceinline__ double* order_C(const EigArgs& g, int o) {
 // C <- U[0:l, :n] Q_H. Left update: warp per column (coalesced, lanes over rows); right update:
 // 4 warps per 32-row block split the columns (coalesced, many loads in flight).
 constexpr int HT = 1024;
+#ifndef SSI_HESS_QS
+#define SSI_HESS_QS 2
+#endif
+constexpr int HQS = SSI_HESS_QS;   // warps sharing a 32-row block of the right update (column split)
 constexpr int HW = HT / 32;
 
 __global__ void __launch_bounds__(HT) hess_order_kernel(EigArgs g) {
   __shared__ double v[256 + 8];
   __shared__ double red[HW];
-  __shared__ double part[4][256];
+  __shared__ double part[HQS][(HW / HQS) * 32];
   __shared__ double sh_tau, sh_scal, sh_beta;
   const int o = blockIdx.x;
   const int n = g.n_min + o * g.n_step;
@@ -390,10 +394,10 @@ __global__ void __launch_bounds__(HT) hess_order_kernel(EigArgs g) {
       }
     }
     __syncthreads();
-    // right: rows of A (0..n-1) then rows of C (n..n+l-1); 4 warps share a 32-row block
-    const int q = warp & 3;
-    for (int rb0 = 0; rb0 < n + l; rb0 += (HW / 4) * 32) {   // uniform trip count (barriers)
-      const int rb = rb0 + (warp >> 2) * 32;
+    // right: rows of A (0..n-1) then rows of C (n..n+l-1); HQS warps share a 32-row block
+    const int q = warp % HQS;
+    for (int rb0 = 0; rb0 < n + l; rb0 += (HW / HQS) * 32) {   // uniform trip count (barriers)
+      const int rb = rb0 + (warp / HQS) * 32;
       const int r = rb + lane;
       const bool valid = r < n + l;
       double* base = nullptr;
@@ -407,30 +411,33 @@ __global__ void __launch_bounds__(HT) hess_order_kernel(EigArgs g) {
         // four independent partial sums, 16 loads in flight (L2 latency, not FMA, bounds this)
         double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
         int c = q;
-        for (; c + 12 < L; c += 16) {
-          const double x0 = base[(j + 1 + c) * ld], x1 = base[(j + 5 + c) * ld];
-          const double x2 = base[(j + 9 + c) * ld], x3 = base[(j + 13 + c) * ld];
-          w0 = fma(x0, v[c], w0); w1 = fma(x1, v[c + 4], w1);
-          w2 = fma(x2, v[c + 8], w2); w3 = fma(x3, v[c + 12], w3);
+        for (; c + 3 * HQS < L; c += 4 * HQS) {
+          const double x0 = base[(j + 1 + c) * ld], x1 = base[(j + 1 + HQS + c) * ld];
+          const double x2 = base[(j + 1 + 2 * HQS + c) * ld], x3 = base[(j + 1 + 3 * HQS + c) * ld];
+          w0 = fma(x0, v[c], w0); w1 = fma(x1, v[c + HQS], w1);
+          w2 = fma(x2, v[c + 2 * HQS], w2); w3 = fma(x3, v[c + 3 * HQS], w3);
         }
-        for (; c < L; c += 4) w0 = fma(base[(j + 1 + c) * ld], v[c], w0);
+        for (; c < L; c += HQS) w0 = fma(base[(j + 1 + c) * ld], v[c], w0);
         w = (w0 + w1) + (w2 + w3);
       }
-      part[q][(warp >> 2) * 32 + lane] = w;
+      part[q][(warp / HQS) * 32 + lane] = w;
       __syncthreads();
       if (valid) {
-        const int pi = (warp >> 2) * 32 + lane;
-        const double ws = ((part[0][pi] + part[1][pi]) + (part[2][pi] + part[3][pi])) * tau;
-        // 16 read-modify-writes in flight (the row does not fit the registers at 1024 threads)
+        const int pi = (warp / HQS) * 32 + lane;
+        double ws = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < HQS; ++qq) ws += part[qq][pi];
+        ws *= tau;
+        // read-modify-writes 4 in flight per thread (the row does not fit the registers)
         int c = q;
-        for (; c + 12 < L; c += 16) {
+        for (; c + 3 * HQS < L; c += 4 * HQS) {
           double* p0 = base + (j + 1 + c) * ld;
-          const int64_t d4 = 4 * ld;
+          const int64_t d4 = HQS * ld;
           const double x0 = p0[0], x1 = p0[d4], x2 = p0[2 * d4], x3 = p0[3 * d4];
-          p0[0] = fma(-ws, v[c], x0); p0[d4] = fma(-ws, v[c + 4], x1);
-          p0[2 * d4] = fma(-ws, v[c + 8], x2); p0[3 * d4] = fma(-ws, v[c + 12], x3);
+          p0[0] = fma(-ws, v[c], x0); p0[d4] = fma(-ws, v[c + HQS], x1);
+          p0[2 * d4] = fma(-ws, v[c + 2 * HQS], x2); p0[3 * d4] = fma(-ws, v[c + 3 * HQS], x3);
         }
-        for (; c < L; c += 4) base[(j + 1 + c) * ld] -= ws * v[c];
+        for (; c < L; c += HQS) base[(j + 1 + c) * ld] -= ws * v[c];
       }
       __syncthreads();
     }
