@@ -147,7 +147,8 @@ def test_covariance_spectral_edge_cases(ssi):
     for (N, l, lo, hi, dt) in ((1013, 7, 1, 40, np.float32), (50, 3, 1, 49, np.float64),
                                (3000, 65, 3, 17, np.float32), (129, 1, 1, 128, np.float64),
                                (7000, 4, 1, 300, np.float32), (20000, 33, 5, 5, np.float64),
-                               (30000, 6, 1, 1500, np.float32)):          # F = 2048 (two-channel FFT CTAs)
+                               (30000, 6, 1, 1500, np.float32),           # F = 2048 (two-channel FFT CTAs)
+                               (20000, 2, 1, 2000, np.float32)):          # lag_hi near the 2047 limit
         Y = rng.standard_normal((N, l)).astype(dt)
         R = api.covariances(_dev(Y), hi, lo, mode="spectral", check=True).cpu().numpy()
         Ro = oracle.covariances(Y, hi, lo)
@@ -181,6 +182,22 @@ def test_covariance_spectral_time_shards_sum_to_full(ssi):
         tot = tot + api.covariances(Yd, 25, 1, mode="spectral", t_begin=tb, t_end=te,
                                     normalize=False).cpu().numpy()
     ref = oracle.covariance_partial_sums(Y, 1, 25)
+    assert np.max(np.abs(tot - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_covariance_spectral_chunked_time_shards(ssi):
+    """Time shards of a record whose segments span several chunks: the raw shard sums add up to
+    the oracle's full sums (multi-GPU split of the spectral path)."""
+    api, drivers = ssi
+    N, l, hi = 600_000, 4, 100
+    assert api.cov_spectral_plan(N, l, hi)[1] > 512
+    rng = np.random.default_rng(34)
+    Y = rng.standard_normal((N, l)).astype(np.float32)
+    Yd = _dev(Y)
+    tot = 0
+    for tb, te in drivers.time_shards(N, 3):
+        tot = tot + api.covariances(Yd, hi, 1, mode="spectral", t_begin=tb, t_end=te, normalize=False).cpu().numpy()
+    ref = oracle.covariance_partial_sums(Y, 1, hi)
     assert np.max(np.abs(tot - ref)) <= 1e-12 * np.max(np.abs(ref))
 
 
