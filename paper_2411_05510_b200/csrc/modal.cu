@@ -886,7 +886,6 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       if (type == QEND) break;
       const int w0 = e->w0, nw = e->nw;
       if (type == QWIN) {
-        const int nsteps = e->nsteps;
         for (int a = ctid; a < l; a += CG_T) {
           double* cr = C + a + int64_t(w0) * l;
           double seg[WIN];
