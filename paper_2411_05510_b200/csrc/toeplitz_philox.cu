@@ -7,31 +7,28 @@ namespace {
 
 // T[r*l+a][c*l+b] = R[(i+r-c)-1][a][b]. One thread writes two adjacent columns of a
 // row (16-byte store when aligned); pure store-bandwidth kernel, R stays in L2.
-__global__ void toeplitz_kernel(const double* __restrict__ R, int l, int i, int64_t m,
-                                double* __restrict__ T, int64_t ldT) {
-  const int64_t pairs_per_row = (m + 1) / 2;
-  const int64_t total = m * pairs_per_row;
+// One CTA per row of T: row (r, a) is the concatenation over block columns c of the rows
+// R_{i+r-c}[a][:] (Eq. 6), i.e. i contiguous copies of l doubles -- streamed as 16-byte vectors
+// (l even and aligned rows; a scalar loop otherwise). Write-bound (m^2 doubles).
+__global__ void __launch_bounds__(256) toeplitz_kernel(const double* __restrict__ R, int l, int i,
+                                                       double* __restrict__ T, int64_t ldT, int vec) {
+  const int row = blockIdx.x;
+  const int r = row / l, a = row - r * l;
   const int64_t ll = int64_t(l) * l;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
-       e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t row = e / pairs_per_row;
-    const int64_t col = (e % pairs_per_row) * 2;
-    const int r = int(row / l), a = int(row % l);
-    double v[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      const int64_t cc = col + q;
-      if (cc < m) {
-        const int c = int(cc / l), b = int(cc % l);
-        v[q] = __ldg(R + int64_t(i + r - c - 1) * ll + int64_t(a) * l + b);
-      }
+  double* dst = T + int64_t(row) * ldT;
+  const double* src0 = R + int64_t(i + r - 1) * ll + int64_t(a) * l;   // block column c = 0
+  if (vec) {
+    const int hl = l >> 1, np = hl * i;
+    for (int e = threadIdx.x; e < np; e += blockDim.x) {
+      const int c = e / hl, k = e - c * hl;
+      const double2 v = __ldg(reinterpret_cast<const double2*>(src0 - int64_t(c) * ll) + k);
+      __stcs(reinterpret_cast<double2*>(dst + int64_t(c) * l) + k, v);
     }
-    double* dst = T + row * ldT + col;
-    if (col + 1 < m && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-      *reinterpret_cast<double2*>(dst) = make_double2(v[0], v[1]);
-    } else {
-      dst[0] = v[0];
-      if (col + 1 < m) dst[1] = v[1];
+  } else {
+    const int m = l * i;
+    for (int e = threadIdx.x; e < m; e += blockDim.x) {
+      const int c = e / l, b = e - c * l;
+      dst[e] = __ldg(src0 - int64_t(c) * ll + b);
     }
   }
 }
@@ -89,10 +86,12 @@ __global__ void sketch_kernel(int m, int k, uint64_t seed, uint64_t sid, double*
 
 ssi_status toeplitz_launch(const double* R, int l, int i, double* T, int64_t ldT, cudaStream_t s) {
   const int64_t m = int64_t(l) * i;
-  const int64_t total = m * ((m + 1) / 2);
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  toeplitz_kernel<<<int(blocks), 256, 0, s>>>(R, l, i, m, T, ldT);
+  if (m > 2147483647) {
+    set_last_error("ssi_toeplitz: m = %lld too large", (long long)m);
+    return SSI_ERR_INVALID_ARG;
+  }
+  const int vec = ((l & 1) == 0 && (ldT & 1) == 0 && ((reinterpret_cast<uintptr_t>(R) | reinterpret_cast<uintptr_t>(T)) & 15) == 0) ? 1 : 0;
+  toeplitz_kernel<<<unsigned(m), 256, 0, s>>>(R, l, i, T, ldT, vec);
   return launch_check("toeplitz_kernel");
 }
 
