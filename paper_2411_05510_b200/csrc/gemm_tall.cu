@@ -16,6 +16,12 @@ constexpr int BM = 64, BN = 224, BK = 16, NT = 256, STAGES = 3;
 #ifndef TALL_CST_ST
 #define TALL_CST_ST 2
 #endif
+#ifndef TALL224_ST
+#define TALL224_ST 2
+#endif
+#ifndef TALL224_MINB
+#define TALL224_MINB 2
+#endif
 #ifndef TALL_CST_MINB
 #define TALL_CST_MINB 2
 #endif
@@ -220,7 +226,8 @@ ssi_status launch_one(dim3 grid, const TallArgs& g, cudaStream_t s) {
 ssi_status launch_tall(bool arow, int64_t N, dim3 grid, const TallArgs& g, cudaStream_t s) {
   if (N <= 64) return arow ? launch_one<true, 64>(grid, g, s) : launch_one<false, 64>(grid, g, s);
   if (N <= 128) return arow ? launch_one<true, 128>(grid, g, s) : launch_one<false, 128>(grid, g, s);
-  return arow ? launch_one<true, 224>(grid, g, s) : launch_one<false, 224>(grid, g, s);
+  return arow ? launch_one<true, 224, false, false, TALL224_ST, TALL224_MINB>(grid, g, s)
+              : launch_one<false, 224, false, false, TALL224_ST, TALL224_MINB>(grid, g, s);
 }
 
 int tall_splits(int64_t M, int64_t K) {
