@@ -22,14 +22,15 @@ crit = api.Criteria(**oracle.SC_BRIDGE_3D.__dict__)
 drivers.lag_sweep_3d(Y, P, lags, crit)
 torch.cuda.synchronize()
 ts = []
-for _ in range(3):   # median of 3 after a warm-up (the first sweeps also populate the allocator)
+for _ in range(7):   # median of 7 after a warm-up (stream interleaving of 16 lags varies run to run)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     tables, flags, counts = drivers.lag_sweep_3d(Y, P, lags, crit)
     b.record()
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b))
-out["c4_sweep_ms"] = sorted(ts)[1]
+out["c4_sweep_ms"] = sorted(ts)[3]
+out["c4_sweep_ms_min"] = min(ts)
 out["c4_sweep_ms_all"] = ts
 out["c4_lags"] = len(lags)
 out["c4_stable_poles"] = int(counts.sum().item())
