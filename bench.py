@@ -407,8 +407,11 @@ def main():
         src = {"int8x3": "smtime_r01.json", "spectral": "smtime_spectral_r01.json"}[args.cov]
         sm = json.load(open(os.path.join(ROOT, "profiles", src)))
         a1 = sm["stages"]["A1"]
+        top = sorted(sm["kernels"].items(), key=lambda kv: -kv[1]["share_sm_time"])[:6]
         share = {"stage_sm_time_share_of_record": a1["share_sm_time"],
                  "stage_serial_share_of_record": a1["share_serial"],
+                 "top_kernels_sm_time_share": {k.split("(")[0].replace("ssi::<unnamed>::", ""):
+                                               round(v["share_sm_time"], 4) for k, v in top},
                  "source": f"profiles/{src} (ncu sm__cycles_active.sum over one c3 record)"}
     except Exception:
         share = None
