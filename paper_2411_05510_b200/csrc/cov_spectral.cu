@@ -77,6 +77,7 @@ struct FftArgs {
   int l, lp, F, B;
   int64_t S;    // segment capacity of the spectra buffers (per-frequency stride 2 S lp)
   int64_t s0;   // first segment of this chunk (blockIdx.y = segment within the chunk)
+  int64_t nseg; // segments in this chunk
   const double2* tw;
   double* A;   // [F/2+1][2S][lp]: column 2s = Re X_s, 2s+1 = Im X_s (channel contiguous)
   double* Bs;  // [F/2+1][2S][lp]: row 2s = Re Ye_s, 2s+1 = Im Ye_s
@@ -202,6 +203,10 @@ __global__ void __launch_bounds__(kFftThreads, 3) spec_fft_kernel(FftArgs g) {
 // quarter-warp hits distinct banks; a butterfly's 15 twiddles w^{rn} are formed from two table
 // entries (w^n, w^{4n}) by at most two complex products; spectra written as 32-byte vectors.
 __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+#ifndef SSI_FFT_SEGS
+#define SSI_FFT_SEGS 2
+#endif
+constexpr int kFftSegs = SSI_FFT_SEGS;   // segments per CTA of the F = 1024 kernel
 constexpr int kF = 1024, kFP = kF + kF / 16 + 1;   // odd row stride: the 4 channels on distinct banks
 
 // in-register radix-2 DIF DFT of length R (R = 16 or 4): x[bitrev(r)] = sum_m x[m] w_R^{rm}
@@ -252,26 +257,43 @@ __device__ __forceinline__ void store_twiddled(double2* zc, int base, int q, con
   }
 }
 
-__global__ void __launch_bounds__(kFftThreads, 3) spec_fft1024_kernel(FftArgs g) {
+template <int SEGS>
+__global__ void __launch_bounds__(kFftThreads, SEGS == 1 ? 3 : 2) spec_fft1024_kernel(FftArgs g) {
   constexpr int CH = 4;
   extern __shared__ __align__(16) double2 z[];     // [CH][kFP]
   const int tid = threadIdx.x;
   const int c0 = blockIdx.x * CH;
-  const int64_t s = blockIdx.y;
-  const int64_t t0 = g.t_begin + (g.s0 + s) * g.B;
-  // ---- load (rows tid + 256u), CH channels per row
-  {
-    const bool vec = g.dtype == SSI_F32 && c0 + 4 <= g.l &&
-                     ((reinterpret_cast<uintptr_t>(g.Y) | uintptr_t(g.ldY * 4)) & 15) == 0;
-    double v[4][CH];
+  const bool vec = g.dtype == SSI_F32 && c0 + 4 <= g.l &&
+                   ((reinterpret_cast<uintptr_t>(g.Y) | uintptr_t(g.ldY * 4)) & 15) == 0;
+  // SEGS > 1: a CTA handles SEGS consecutive segments; the next segment's rows are loaded into
+  // registers while the current one is transformed (the load latency leaves the critical path)
+  float4 pf[4];
+  auto fetch = [&](int64_t sg) {
+    const int64_t tq = g.t_begin + (g.s0 + sg) * g.B;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t t = t0 + tid + u * kFftThreads;
-      if (vec) {
-        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (t < g.N) q = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(g.Y) + t * g.ldY + c0));
-        v[u][0] = q.x; v[u][1] = q.y; v[u][2] = q.z; v[u][3] = q.w;
-      } else {
+      const int64_t t = tq + tid + u * kFftThreads;
+      pf[u] = t < g.N ? __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(g.Y) + t * g.ldY + c0))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  const int64_t sfirst = int64_t(blockIdx.y) * SEGS;
+  if (vec) fetch(sfirst);
+  for (int kseg = 0; kseg < SEGS; ++kseg) {
+  const int64_t s = sfirst + kseg;
+  if (s >= g.nseg) break;                          // uniform over the CTA
+  const int64_t t0 = g.t_begin + (g.s0 + s) * g.B;
+  // ---- rows tid + 256u, CH channels per row
+  {
+    double v[4][CH];
+    if (vec) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { v[u][0] = pf[u].x; v[u][1] = pf[u].y; v[u][2] = pf[u].z; v[u][3] = pf[u].w; }
+      if (kseg + 1 < SEGS && s + 1 < g.nseg) fetch(s + 1);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t t = t0 + tid + u * kFftThreads;
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
           const int ch = c0 + c;
@@ -380,6 +402,8 @@ __global__ void __launch_bounds__(kFftThreads, 3) spec_fft1024_kernel(FftArgs g)
       }
     }
   }
+  __syncthreads();                                 // z is reused by the next segment
+  }
 }
 
 // R[lag][a][b] (l x l blocks) <- Rp[lag][a][b] (lp x lp blocks) for odd l
@@ -469,11 +493,12 @@ ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY,
   for (int64_t s0 = 0; t_end > t_begin && s0 < p.S; s0 += p.Sc) {
     const int64_t nseg = (p.S - s0 < p.Sc) ? p.S - s0 : p.Sc;
     if (phases & 1) {
-      FftArgs g{Y, dtype, N, ldY, t_begin, t_end, l, p.lp, p.F, p.B, p.Sc, s0, b.tw, b.A, b.Bs, status};
+      FftArgs g{Y, dtype, N, ldY, t_begin, t_end, l, p.lp, p.F, p.B, p.Sc, s0, nseg, b.tw, b.A, b.Bs, status};
       if (p.F == kF && p.lp % 4 == 0) {
         const size_t smem = size_t(4) * kFP * sizeof(double2);
-        cudaFuncSetAttribute(spec_fft1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        spec_fft1024_kernel<<<dim3(unsigned((l + 3) / 4), unsigned(nseg)), kFftThreads, smem, s>>>(g);
+        cudaFuncSetAttribute(spec_fft1024_kernel<kFftSegs>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        spec_fft1024_kernel<kFftSegs><<<dim3(unsigned((l + 3) / 4), unsigned((nseg + kFftSegs - 1) / kFftSegs)),
+                                         kFftThreads, smem, s>>>(g);
         SSI_TRY(launch_check("spec_fft1024_kernel"));
       } else switch (p.F) {
         case 64: SSI_TRY(launch_fft<64>(g, l, nseg, s)); break;
