@@ -16,6 +16,18 @@ constexpr int BM = 64, BN = 224, BK = 16, NT = 256, STAGES = 3;
 #ifndef TALL_CST_ST
 #define TALL_CST_ST 2
 #endif
+#ifndef TALL64_ST
+#define TALL64_ST 3
+#endif
+#ifndef TALL64_MINB
+#define TALL64_MINB 4
+#endif
+#ifndef TALL128_ST
+#define TALL128_ST 3
+#endif
+#ifndef TALL128_MINB
+#define TALL128_MINB 2
+#endif
 #ifndef TALL224_ST
 #define TALL224_ST 2
 #endif
@@ -224,8 +236,12 @@ ssi_status launch_one(dim3 grid, const TallArgs& g, cudaStream_t s) {
 
 // narrowest N tile that covers N
 ssi_status launch_tall(bool arow, int64_t N, dim3 grid, const TallArgs& g, cudaStream_t s) {
-  if (N <= 64) return arow ? launch_one<true, 64>(grid, g, s) : launch_one<false, 64>(grid, g, s);
-  if (N <= 128) return arow ? launch_one<true, 128>(grid, g, s) : launch_one<false, 128>(grid, g, s);
+  if (N <= 64)
+    return arow ? launch_one<true, 64, false, false, TALL64_ST, TALL64_MINB>(grid, g, s)
+                : launch_one<false, 64, false, false, TALL64_ST, TALL64_MINB>(grid, g, s);
+  if (N <= 128)
+    return arow ? launch_one<true, 128, false, false, TALL128_ST, TALL128_MINB>(grid, g, s)
+                : launch_one<false, 128, false, false, TALL128_ST, TALL128_MINB>(grid, g, s);
   return arow ? launch_one<true, 224, false, false, TALL224_ST, TALL224_MINB>(grid, g, s)
               : launch_one<false, 224, false, false, TALL224_ST, TALL224_MINB>(grid, g, s);
 }
@@ -327,7 +343,7 @@ ssi_status gemm_tall_syrk_lower(int64_t n, int64_t K, const double* A, int64_t l
   const int z = int((K + kchunk - 1) / kchunk);
   TallArgs g{n, n, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? n : ldc, kchunk, 0, 0, 0, 1};
   {
-    const ssi_status st = launch_one<true, 64>(dim3(unsigned(tiles), unsigned(z)), g, s);
+    const ssi_status st = launch_one<true, 64, false, false, TALL64_ST, TALL64_MINB>(dim3(unsigned(tiles), unsigned(z)), g, s);
     if (st != SSI_OK) return st;
   }
   if (z > 1) {
@@ -346,7 +362,7 @@ ssi_status gemm_tall_triu(int64_t M, int64_t N, int64_t K, const double* A, int6
                           int64_t ldb, double* C, int64_t ldc, cudaStream_t s) {
   const int64_t kchunk = (K + BK - 1) / BK * BK;
   TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, 0, 0, 0, 2};
-  return launch_one<false, 64>(dim3(unsigned((M + BM - 1) / BM), 1u, unsigned((N + 63) / 64)), g, s);
+  return launch_one<false, 64, false, false, TALL64_ST, TALL64_MINB>(dim3(unsigned((M + BM - 1) / BM), 1u, unsigned((N + 63) / 64)), g, s);
 }
 
 ssi_status gemm_tall_batched(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
