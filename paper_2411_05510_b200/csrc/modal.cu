@@ -747,11 +747,26 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
               const bool refl_on = (yz != 0.0);
               // beta = -sign(x) sqrt(s); tau = 1 + |x|/sqrt(s); v = sign(x) y/(|x| + sqrt(s))
               const double ss = fma(x, x, yz);
-              const double rs = fast_rsqrt(refl_on ? ss : 1.0);
+              // rsqrt and the reciprocal of |x| + sqrt(ss) start together: the reciprocal's
+              // hardware estimate uses the estimated sqrt, and its two Newton steps run on the
+              // refined denominator (estimate error ~2^-21 -> ~2^-84)
+              const double ssr = refl_on ? ss : 1.0;
+              double rs, r0;
+              asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(ssr));
+              asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(fabs(x) + ssr * rs));
+              {
+                const double hx = 0.5 * ssr;
+                rs = rs * fma(-hx * rs, rs, 1.5);
+                rs = rs * fma(-hx * rs, rs, 1.5);
+                rs = rs * fma(-hx * rs, rs, 1.5);
+              }
               const double sq = ss * rs;
               const double beta = -copysign(sq, x);
               const double tau = refl_on ? fma(fabs(x), rs, 1.0) : 0.0;
-              const double inv = refl_on ? copysign(fast_rcp(fabs(x) + sq), x) : 0.0;
+              const double den = fabs(x) + sq;
+              r0 = fma(r0, fma(-den, r0, 1.0), r0);
+              r0 = fma(r0, fma(-den, r0, 1.0), r0);
+              const double inv = refl_on ? copysign(r0, x) : 0.0;
               double v[BS];
               v[0] = 1.0;
 #pragma unroll
