@@ -741,9 +741,9 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
                 xv[j] = j < nr ? dv : 0.0;
               }
               const double x = xv[0];
-              double yz = 0.0;
-#pragma unroll
-              for (int j = 1; j < BS; ++j) yz = fma(xv[j], xv[j], yz);
+              static_assert(BS == 5, "tree sums below assume a bulge of 5");
+              // two-level trees instead of 4-long FMA chains (the step is one dependent chain)
+              const double yz = fma(xv[1], xv[1], xv[2] * xv[2]) + fma(xv[3], xv[3], xv[4] * xv[4]);
               const bool refl_on = (yz != 0.0);
               // beta = -sign(x) sqrt(s); tau = 1 + |x|/sqrt(s); v = sign(x) y/(|x| + sqrt(s))
               const double ss = fma(x, x, yz);
@@ -790,9 +790,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
                   double b[BS];
 #pragma unroll
                   for (int j = 0; j < BS; ++j) b[j] = p0[j * TLD];
-                  double sum = b[0];
-#pragma unroll
-                  for (int j = 1; j < BS; ++j) sum = fma(v[j], b[j], sum);
+                  double sum = fma(v[1], b[1], b[0]) + fma(v[2], b[2], fma(v[3], b[3], v[4] * b[4]));
                   sum *= tau;
                   p0[0] = b[0] - sum;
 #pragma unroll
@@ -808,9 +806,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
                   double b[BS];
 #pragma unroll
                   for (int j = 0; j < BS; ++j) b[j] = p0[j];
-                  double sum = b[0];
-#pragma unroll
-                  for (int j = 1; j < BS; ++j) sum = fma(v[j], b[j], sum);
+                  double sum = fma(v[1], b[1], b[0]) + fma(v[2], b[2], fma(v[3], b[3], v[4] * b[4]));
                   sum *= tau;
                   p0[0] = b[0] - sum;
 #pragma unroll
