@@ -754,13 +754,16 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
               double rs, r0;
               asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(ssr));
               asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(fabs(x) + ssr * rs));
-              {
-                const double hx = 0.5 * ssr;
-                rs = rs * fma(-hx * rs, rs, 1.5);
-                rs = rs * fma(-hx * rs, rs, 1.5);
-                rs = rs * fma(-hx * rs, rs, 1.5);
+              // Goldschmidt: g -> sqrt(ssr), h -> 1 / (2 sqrt(ssr)); one dependent FMA per step
+              double g = ssr * rs, h = 0.5 * rs;
+#pragma unroll
+              for (int it = 0; it < 3; ++it) {
+                const double rr = fma(-g, h, 0.5);
+                g = fma(g, rr, g);
+                h = fma(h, rr, h);
               }
-              const double sq = ss * rs;
+              rs = h + h;
+              const double sq = g;                 // (only used when refl_on, where ssr = ss)
               const double beta = -copysign(sq, x);
               const double tau = refl_on ? fma(fabs(x), rs, 1.0) : 0.0;
               const double den = fabs(x) + sq;
