@@ -775,15 +775,14 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
 #pragma unroll
               for (int j = 1; j < BS; ++j) v[j] = xv[j] * inv;
               __syncwarp();
-              if (lane == 0 && refl_on && !first) {
-                D[t * TLD + t] = beta;
+              // one predicated store per lane (no divergent lane-0 blocks): lanes 0..BS-1 write the
+              // reduced column (beta, zeros), lanes 0..BS-1 the reflector (v_1..v_4, tau)
+              if (lane < BS) {
+                if (refl_on && !first && lane < nr) D[(t + lane) * TLD + t] = lane == 0 ? beta : 0.0;
+                double rv = tau;
 #pragma unroll
-                for (int j = 1; j < BS; ++j) if (j < nr) D[(t + j) * TLD + t] = 0.0;
-              }
-              if (lane == 0) {
-#pragma unroll
-                for (int j = 1; j < BS; ++j) refl[BS * t + j - 1] = v[j];
-                refl[BS * t + BS - 1] = tau;
+                for (int j = 1; j < BS; ++j) rv = (lane == j - 1) ? v[j] : rv;
+                refl[BS * t + lane] = rv;
               }
               // left: rows t..t+BS-1, columns k..w1-1 (local t+1 .. nw)
               {
