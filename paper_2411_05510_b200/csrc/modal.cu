@@ -272,10 +272,25 @@ __device__ bool eig_small(double (&G)[N][N], double (&wr)[N], double (&wi)[N]) {
       const double yz = y * y + z * z;
       if (yz == 0.0) continue;
       const double ss = fma(x, x, yz);
-      const double rs = fast_rsqrt(ss), sq = ss * rs;
+      // as in the bulge chase: rsqrt and the reciprocal estimated together, Goldschmidt refinement
+      double rs, r0;
+      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(ss));
+      asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(fabs(x) + ss * rs));
+      double gq = ss * rs, hq = 0.5 * rs;
+#pragma unroll
+      for (int it = 0; it < 3; ++it) {
+        const double rr = fma(-gq, hq, 0.5);
+        gq = fma(gq, rr, gq);
+        hq = fma(hq, rr, hq);
+      }
+      rs = hq + hq;
+      const double sq = gq;
       const double beta = -copysign(sq, x);
       const double tau = fma(fabs(x), rs, 1.0);
-      const double inv = copysign(fast_rcp(fabs(x) + sq), x);
+      const double den = fabs(x) + sq;
+      r0 = fma(r0, fma(-den, r0, 1.0), r0);
+      r0 = fma(r0, fma(-den, r0, 1.0), r0);
+      const double inv = copysign(r0, x);
       const double v1 = y * inv, v2 = z * inv;
       if (k > l) {
         G[k][k - 1] = beta; G[k + 1][k - 1] = 0.0;
