@@ -552,10 +552,25 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       hsync();
       return s.q + qslot;
     };
+    int npub = 0;
     auto publish = [&]() {
       hsync();
       if (htid == 0) mbar_arrive(&s.q_full[qslot]);
       if (++qslot == NSLOT) { qslot = 0; ++quse; }
+      ++npub;
+    };
+    // wait until the C group has finished every published entry (it also applies the windows'
+    // right updates to the rows above each window; the next sweep and the 2 x 2 handling read them)
+    auto drain = [&]() {
+      if (npub == 0) return;
+      if (htid == 0) {
+        const int ls = (qslot + NSLOT - 1) % NSLOT;
+        const int us = (qslot == 0) ? quse - 1 : quse;
+        const long long tq = clock64();
+        mbar_wait_parity(&s.q_empty[ls], us & 1);
+        t_cwait += clock64() - tq;
+      }
+      hsync();
     };
     while (ihi >= 0) {
       long long ta = clock64();
@@ -581,6 +596,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       t_scan += tb - ta;
       if (lo > 0 && htid == 0) H(lo, lo - 1) = 0.0;
       if (lo == ihi) { ihi -= 1; its = 0; hsync(); continue; }
+      drain();
       if (lo == ihi - 1) {
         const int p = ihi - 1, q = ihi;
         QEntry* e = acquire();
@@ -598,12 +614,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
           H(p, c) = cs * x + sn * y;
           H(q, c) = cs * y - sn * x;
         }
-        for (int r = htid; r < p; r += HG_T) {
-          const double x = H(r, p), y = H(r, q);
-          H(r, p) = cs * x + sn * y;
-          H(r, q) = cs * y - sn * x;
-        }
-        publish();
+        publish();                     // (rows above p are rotated by the C group)
         ihi -= 2; its = 0;
         t_2x2 += clock64() - tb;
         continue;
@@ -847,7 +858,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
           }
           // deferred parts: (L) columns c in [w1, n), rows [w0, w1); (R) rows r in [0, w0),
           // columns [w0, w1)
-          const int nL = n - w1, nR = w0;
+          const int nL = n - w1, nR = 0;   // rows above the window: the C group (queue order)
           // two segments per thread, their reflector chains interleaved (independent: 2x ILP on
           // the latency-bound update chain)
           auto seg_load = [&](double (&seg)[WIN], int task) {
@@ -914,22 +925,40 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       if (type == QEND) break;
       const int w0 = e->w0, nw = e->nw;
       if (type == QWIN) {
-        for (int a = ctid; a < l; a += CG_T) {
-          double* cr = C + a + int64_t(w0) * l;
-          double seg[WIN];
+        // rows of C and rows 0..w0-1 of H, columns [w0, w0 + nw): right-multiplied by the window
+        for (int a = ctid; a < l + w0; a += CG_T) {
+          if (a < l) {
+            double* cr = C + a + int64_t(w0) * l;
+            double seg[WIN];
 #pragma unroll
-          for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? cr[int64_t(u) * l] : 0.0;
-          apply_window(seg, e->r);
+            for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? cr[int64_t(u) * l] : 0.0;
+            apply_window(seg, e->r);
 #pragma unroll
-          for (int u = 0; u < WIN; ++u) if (u < nw) cr[int64_t(u) * l] = seg[u];
+            for (int u = 0; u < WIN; ++u) if (u < nw) cr[int64_t(u) * l] = seg[u];
+          } else {
+            double* row = s.H + s.rowoff[a - l] + w0;
+            double seg[WIN];
+#pragma unroll
+            for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? row[u] : 0.0;
+            apply_window(seg, e->r);
+#pragma unroll
+            for (int u = 0; u < WIN; ++u) if (u < nw) row[u] = seg[u];
+          }
         }
-      } else {   // QROT: columns p = w0, q = w0 + 1
+      } else {   // QROT: columns p = w0, q = w0 + 1 of C and of H rows above p
         const double cs = e->r[0], sn = e->r[1];
-        for (int a = ctid; a < l; a += CG_T) {
-          double* cr = C + a;
-          const double x = cr[int64_t(w0) * l], y = cr[int64_t(w0 + 1) * l];
-          cr[int64_t(w0) * l] = cs * x + sn * y;
-          cr[int64_t(w0 + 1) * l] = cs * y - sn * x;
+        for (int a = ctid; a < l + w0; a += CG_T) {
+          if (a < l) {
+            double* cr = C + a;
+            const double x = cr[int64_t(w0) * l], y = cr[int64_t(w0 + 1) * l];
+            cr[int64_t(w0) * l] = cs * x + sn * y;
+            cr[int64_t(w0 + 1) * l] = cs * y - sn * x;
+          } else {
+            double* row = s.H + s.rowoff[a - l];
+            const double x = row[w0], y = row[w0 + 1];
+            row[w0] = cs * x + sn * y;
+            row[w0 + 1] = cs * y - sn * x;
+          }
         }
       }
       csync();
