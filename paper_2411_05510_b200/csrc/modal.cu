@@ -37,6 +37,7 @@ constexpr int NSLOT = 8;        // H -> C queue depth
 enum { QWIN = 0, QROT = 1, QEND = 2 };
 struct QEntry {
   int type, w0, nw, nsteps;
+  int chi;                      // columns > chi (deflated, never read again by the H group) are the C group's
   double r[BS * SPW];           // window reflectors (v_1..v_{BS-1}, tau) or rotation (cs, sn)
 };
 constexpr double kUlp = 2.220446049250313e-16;
@@ -141,6 +142,7 @@ struct Smem {
   QEntry* q;      // NSLOT queue entries (H group -> C group)
   uint64_t* q_full;
   uint64_t* q_empty;
+  uint64_t* q_rdone;   // C group finished an entry's rows above the block
   double* cre; double* cim; double* cf; double* cxi;  // cap each
 };
 
@@ -518,11 +520,12 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
     s.q = reinterpret_cast<QEntry*>(p);      p += sizeof(QEntry) * NSLOT;
     s.q_full = reinterpret_cast<uint64_t*>(p); p += sizeof(uint64_t) * NSLOT;
     s.q_empty = reinterpret_cast<uint64_t*>(p); p += sizeof(uint64_t) * NSLOT;
+    s.q_rdone = reinterpret_cast<uint64_t*>(p); p += sizeof(uint64_t) * NSLOT;
     s.rowoff = reinterpret_cast<int*>(p);    p += sizeof(int) * (nm + 1);
     s.cj = reinterpret_cast<int*>(p);
   }
   if (tid == 0) {
-    for (int i = 0; i < NSLOT; ++i) { mbar_init1(&s.q_full[i]); mbar_init1(&s.q_empty[i]); }
+    for (int i = 0; i < NSLOT; ++i) { mbar_init1(&s.q_full[i]); mbar_init1(&s.q_empty[i]); mbar_init1(&s.q_rdone[i]); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const Band H{s.H, n};
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
         const int ls = (qslot + NSLOT - 1) % NSLOT;
         const int us = (qslot == 0) ? quse - 1 : quse;
         const long long tq = clock64();
-        mbar_wait_parity(&s.q_empty[ls], us & 1);
+        mbar_wait_parity(&s.q_rdone[ls], us & 1);
         t_cwait += clock64() - tq;
       }
       hsync();
@@ -605,16 +608,11 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
           dlanv2(a, b, c, d, cs, sn);
           H(p, p) = a; H(p, q) = b; H(q, p) = c; H(q, q) = d;
           sh_cs = cs; sh_sn = sn;
-          e->type = QROT; e->w0 = p; e->nw = 2; e->nsteps = 0; e->r[0] = cs; e->r[1] = sn;
+          e->type = QROT; e->w0 = p; e->nw = 2; e->nsteps = 0; e->chi = q; e->r[0] = cs; e->r[1] = sn;
         }
         hsync();
         const double cs = sh_cs, sn = sh_sn;
-        for (int c = q + 1 + htid; c < n; c += HG_T) {
-          const double x = H(p, c), y = H(q, c);
-          H(p, c) = cs * x + sn * y;
-          H(q, c) = cs * y - sn * x;
-        }
-        publish();                     // (rows above p are rotated by the C group)
+        publish();                     // (rows above p and columns > q are rotated by the C group)
         ihi -= 2; its = 0;
         t_2x2 += clock64() - tb;
         continue;
@@ -844,7 +842,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
               __syncwarp();
             }
             for (int e = BS * nsteps + lane; e < BS * SPW; e += 32) refl[e] = 0.0;   // unused slots: no-ops
-            if (lane == 0) { qe->type = QWIN; qe->w0 = w0; qe->nw = nw; qe->nsteps = nsteps; }
+            if (lane == 0) { qe->type = QWIN; qe->w0 = w0; qe->nw = nw; qe->nsteps = nsteps; qe->chi = ihi; }
           }
           publish();                     // the C group may start on this window
           const long long tw1 = clock64();
@@ -858,7 +856,9 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
           }
           // deferred parts: (L) columns c in [w1, n), rows [w0, w1); (R) rows r in [0, w0),
           // columns [w0, w1)
-          const int nL = n - w1, nR = 0;   // rows above the window: the C group (queue order)
+          // columns beyond ihi (deflated: the H group never reads them again) and the rows above
+          // the window are the C group's, in queue order
+          const int nL = ihi + 1 - w1 > 0 ? ihi + 1 - w1 : 0, nR = 0;
           // two segments per thread, their reflector chains interleaved (independent: 2x ILP on
           // the latency-bound update chain)
           auto seg_load = [&](double (&seg)[WIN], int task) {
@@ -924,41 +924,61 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
       const int type = e->type;
       if (type == QEND) break;
       const int w0 = e->w0, nw = e->nw;
+      const int chi = e->chi;
+      // (1) H rows above the block (read by the H group's next sweep / 2 x 2 block): first, then
+      // signal q_rdone so the H group's drain does not wait for (2)
       if (type == QWIN) {
-        // rows of C and rows 0..w0-1 of H, columns [w0, w0 + nw): right-multiplied by the window
-        for (int a = ctid; a < l + w0; a += CG_T) {
-          if (a < l) {
-            double* cr = C + a + int64_t(w0) * l;
-            double seg[WIN];
+        for (int r = ctid; r < w0; r += CG_T) {
+          double* row = s.H + s.rowoff[r] + w0;
+          double seg[WIN];
 #pragma unroll
-            for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? cr[int64_t(u) * l] : 0.0;
-            apply_window(seg, e->r);
+          for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? row[u] : 0.0;
+          apply_window(seg, e->r);
 #pragma unroll
-            for (int u = 0; u < WIN; ++u) if (u < nw) cr[int64_t(u) * l] = seg[u];
-          } else {
-            double* row = s.H + s.rowoff[a - l] + w0;
-            double seg[WIN];
-#pragma unroll
-            for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? row[u] : 0.0;
-            apply_window(seg, e->r);
-#pragma unroll
-            for (int u = 0; u < WIN; ++u) if (u < nw) row[u] = seg[u];
-          }
+          for (int u = 0; u < WIN; ++u) if (u < nw) row[u] = seg[u];
         }
-      } else {   // QROT: columns p = w0, q = w0 + 1 of C and of H rows above p
+      } else {
         const double cs = e->r[0], sn = e->r[1];
-        for (int a = ctid; a < l + w0; a += CG_T) {
-          if (a < l) {
-            double* cr = C + a;
-            const double x = cr[int64_t(w0) * l], y = cr[int64_t(w0 + 1) * l];
-            cr[int64_t(w0) * l] = cs * x + sn * y;
-            cr[int64_t(w0 + 1) * l] = cs * y - sn * x;
-          } else {
-            double* row = s.H + s.rowoff[a - l];
-            const double x = row[w0], y = row[w0 + 1];
-            row[w0] = cs * x + sn * y;
-            row[w0 + 1] = cs * y - sn * x;
-          }
+        for (int r = ctid; r < w0; r += CG_T) {
+          double* row = s.H + s.rowoff[r];
+          const double x = row[w0], y = row[w0 + 1];
+          row[w0] = cs * x + sn * y;
+          row[w0 + 1] = cs * y - sn * x;
+        }
+      }
+      csync();
+      if (ctid == 0) mbar_arrive(&s.q_rdone[slot]);
+      // (2) rows of C (right) and H columns beyond chi (left; deflated, never read by the H group)
+      if (type == QWIN) {
+        for (int a = ctid; a < l; a += CG_T) {
+          double* cr = C + a + int64_t(w0) * l;
+          double seg[WIN];
+#pragma unroll
+          for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? cr[int64_t(u) * l] : 0.0;
+          apply_window(seg, e->r);
+#pragma unroll
+          for (int u = 0; u < WIN; ++u) if (u < nw) cr[int64_t(u) * l] = seg[u];
+        }
+        for (int c = chi + 1 + ctid; c < n; c += CG_T) {
+          double seg[WIN];
+#pragma unroll
+          for (int u = 0; u < WIN; ++u) seg[u] = (u < nw) ? s.H[s.rowoff[w0 + u] + c] : 0.0;
+          apply_window(seg, e->r);
+#pragma unroll
+          for (int u = 0; u < WIN; ++u) if (u < nw) s.H[s.rowoff[w0 + u] + c] = seg[u];
+        }
+      } else {   // QROT: columns p = w0, q = w0 + 1 of C; rows p, q of H beyond q
+        const double cs = e->r[0], sn = e->r[1];
+        for (int a = ctid; a < l; a += CG_T) {
+          double* cr = C + a;
+          const double x = cr[int64_t(w0) * l], y = cr[int64_t(w0 + 1) * l];
+          cr[int64_t(w0) * l] = cs * x + sn * y;
+          cr[int64_t(w0 + 1) * l] = cs * y - sn * x;
+        }
+        for (int c = chi + 1 + ctid; c < n; c += CG_T) {
+          const double x = s.H[s.rowoff[w0] + c], y = s.H[s.rowoff[w0 + 1] + c];
+          s.H[s.rowoff[w0] + c] = cs * x + sn * y;
+          s.H[s.rowoff[w0 + 1] + c] = cs * y - sn * x;
         }
       }
       csync();
@@ -1128,7 +1148,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
 }  // namespace
 
 size_t modal_smem_bytes(int n_max, int cap) {
-  return sizeof(QEntry) * NSLOT + 2 * sizeof(uint64_t) * NSLOT +
+  return sizeof(QEntry) * NSLOT + 3 * sizeof(uint64_t) * NSLOT +
          sizeof(double) * (band_elems(n_max) + x_elems(n_max) +
                            4 * size_t(cap)) +
          sizeof(int) * (size_t(n_max) + 1 + cap) + 64;
