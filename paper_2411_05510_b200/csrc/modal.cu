@@ -758,6 +758,12 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
               const int t = k - w0;
               const int nr = (ihi - k + 1) < BS ? (ihi - k + 1) : BS;
               const bool first = (k == lo);
+              // the left update's operands are final once the previous step's right update is done:
+              // load them with x, so their latency overlaps the reflector's
+              const int lc = t + 1 + lane;
+              double bL[BS];
+#pragma unroll
+              for (int j = 0; j < BS; ++j) bL[j] = D[(t + j) * TLD + (lc <= nw ? lc : t + 1)];
               double xv[BS];
 #pragma unroll
               for (int j = 0; j < BS; ++j) {
@@ -810,12 +816,9 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
               }
               // left: rows t..t+BS-1, columns k..w1-1 (local t+1 .. nw)
               {
-                const int lc = t + 1 + lane;
                 if (lc <= nw) {
                   double* p0 = D + t * TLD + lc;
-                  double b[BS];
-#pragma unroll
-                  for (int j = 0; j < BS; ++j) b[j] = p0[j * TLD];
+                  const double (&b)[BS] = bL;
                   double sum = fma(v[1], b[1], b[0]) + fma(v[2], b[2], fma(v[3], b[3], v[4] * b[4]));
                   sum *= tau;
                   p0[0] = b[0] - sum;
