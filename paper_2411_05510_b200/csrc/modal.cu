@@ -31,7 +31,10 @@ constexpr int TLD = WIN + BS + 2;   // tile row stride (doubles): columns w0-1 .
 constexpr int TROWS = WIN + BS;     // tile rows (zero-padded rows below the window)
 constexpr int HG_WARPS = 4;     // H group (band QR) warps; the rest form the C group
 constexpr int HG_T = HG_WARPS * 32;
-constexpr int CG_W0 = HG_WARPS + 1;   // C group: warps 5..7 (warp 4 would share warp 0's SMSP)
+#ifndef SSI_EIG_CG_W0
+#define SSI_EIG_CG_W0 (HG_WARPS + 1)
+#endif
+constexpr int CG_W0 = SSI_EIG_CG_W0;   // C group: warps CG_W0..7 (warp 4 shares warp 0's SMSP)
 constexpr int CG_T = NT - CG_W0 * 32;
 constexpr int NSLOT = 8;        // H -> C queue depth
 enum { QWIN = 0, QROT = 1, QEND = 2 };
