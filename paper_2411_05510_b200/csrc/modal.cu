@@ -36,7 +36,10 @@ constexpr int HG_T = HG_WARPS * 32;
 #endif
 constexpr int CG_W0 = SSI_EIG_CG_W0;   // C group: warps CG_W0..7 (warp 4 shares warp 0's SMSP)
 constexpr int CG_T = NT - CG_W0 * 32;
-constexpr int NSLOT = 8;        // H -> C queue depth
+#ifndef SSI_EIG_NSLOT
+#define SSI_EIG_NSLOT 8
+#endif
+constexpr int NSLOT = SSI_EIG_NSLOT;        // H -> C queue depth
 enum { QWIN = 0, QROT = 1, QEND = 2 };
 struct QEntry {
   int type, w0, nw, nsteps;
