@@ -1038,12 +1038,21 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   }
   __syncthreads();
   const int nc = sh_ncand;
+  if (tid == 0) sh_l = 0;               // reused as the pole counter of the vectors phase
   zero_shapes(nc);
 
   // ---------------- eigenvectors (warp per pole): back substitution on T, Phi = C x
   double* xr = s.x + warp * 2 * g.n_max;
   double* xim = xr + g.n_max;
-  for (int c = warp; c < nc; c += NW) {
+  __syncthreads();
+  // poles handed out dynamically, largest block index first (the back substitution and Phi cost
+  // grow with it): the slowest warp no longer sets the phase length
+  while (true) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(&sh_l, 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= nc) break;
+    c = nc - 1 - c;
     const int j = s.cj[c];
     const double wr = s.cre[c], wi = s.cim[c];
     const double smin = fmax(kUlp * hypot(wr, wi), kSafeMin);
