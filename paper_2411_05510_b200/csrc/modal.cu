@@ -21,6 +21,10 @@ namespace ssi {
 namespace {
 
 constexpr int NT = 256;
+#ifndef SSI_ORDER_REV
+#define SSI_ORDER_REV 1
+#endif
+constexpr bool kOrderRev = SSI_ORDER_REV != 0;   // CTAs of the largest orders launch first
 constexpr int NW = NT / 32;
 constexpr int WIN = 32;        // bulge-chase window (rows/cols) of the windowed Francis sweep
 constexpr int BS = 5;          // reflector length: a bulge of BS - 1 shifts (6 shifts measured slower: per-sweep overhead)
@@ -353,7 +357,7 @@ __global__ void __launch_bounds__(HT) hess_order_kernel(EigArgs g) {
   __shared__ double red[HW];
   __shared__ double part[HQS][(HW / HQS) * 32];
   __shared__ double sh_tau, sh_scal, sh_beta;
-  const int o = blockIdx.x;
+  const int o = kOrderRev ? int(gridDim.x) - 1 - int(blockIdx.x) : int(blockIdx.x);   // largest order first
   const int n = g.n_min + o * g.n_step;
   if (order_truncated(g, n)) return;
   const int l = g.l;
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   __shared__ int sh_ok4;
   __shared__ int sh_l, sh_fail, sh_ncand;
 
-  const int o = blockIdx.x;
+  const int o = kOrderRev ? int(gridDim.x) - 1 - int(blockIdx.x) : int(blockIdx.x);   // largest order first
   const int n = g.n_min + o * g.n_step;
   const int l = g.l;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
