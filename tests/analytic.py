@@ -34,3 +34,19 @@ def shear_frame_10dof(m=100.0, k=5.0e6, xi=0.01):
     A = np.array([[1 / (2 * w[0]), w[0] / 2], [1 / (2 * w[3]), w[3] / 2]])
     a, b = np.linalg.solve(A, [xi, xi])
     return M, K, a * M + b * K, w, (a, b)
+
+
+def shear_frame_modes(fs: float):
+    """The 10-DOF shear frame (Table 1 model) as synth.Modes: undamped modes of
+    (M, K) (proportional damping keeps them real), natural frequencies ω/2π, Rayleigh ξ_i =
+    a/(2ω_i) + b ω_i/2, unit-norm shapes with the largest component positive. The E2/E3 workload
+     is this model sampled at 200 Hz."""
+    import synth
+    M, K, C, w, (a, b) = shear_frame_10dof()
+    w2, V = np.linalg.eigh(np.linalg.solve(np.sqrt(M), np.linalg.solve(np.sqrt(M), K).T))
+    order = np.argsort(w2)
+    V = np.linalg.solve(np.sqrt(M), V[:, order])
+    om = np.sqrt(w2[order])
+    phi = V.T / np.linalg.norm(V.T, axis=1, keepdims=True)
+    phi *= np.sign(phi[np.arange(10), np.argmax(np.abs(phi), axis=1)])[:, None]
+    return synth.Modes(om / (2 * np.pi), a / (2 * om) + b * om / 2, phi, fs)

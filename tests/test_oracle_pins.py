@@ -438,3 +438,20 @@ def test_stab3d_axis_disjunction_and_hard_criteria():
     assert list(flags[1, 0]) == [2, 0, 0]          # lag axis match; ξ>10% and MPC=0.6 rejected
     assert list(flags[1, 1]) == [2, 2, 0]          # order axis (2.0 ↔ 2.01) and lag axis (5.01 ↔ 5.0)
     assert counts.tolist() == [[0, 0], [1, 2]]
+
+
+def test_shear_frame_modes_reproduce_table1():
+    """The E2/E3 input model (tests/analytic.shear_frame_modes, used by test_gpu_e3.py) carries
+    the paper's Table 1 frequencies and damping ratios, and its shapes are
+    M-orthogonal undamped modes of the shear frame (K φ = ω² M φ)."""
+    from tests.analytic import shear_frame_modes
+    modes = shear_frame_modes(200.0)
+    gold = np.array([[float(x) for x in r[1:]] for r in _rows("table1_10dof.txt")])
+    np.testing.assert_allclose(modes.f, gold[:, 0], atol=5e-4)
+    np.testing.assert_allclose(100 * modes.xi, gold[:, 1], atol=5e-4)
+    M, K, *_ = shear_frame_10dof()
+    w = 2 * np.pi * modes.f
+    for j in range(10):
+        np.testing.assert_allclose(K @ modes.phi[j], w[j] ** 2 * (M @ modes.phi[j]), atol=1e-6 * w[j] ** 2 * 100)
+    G = modes.phi @ M @ modes.phi.T
+    np.testing.assert_allclose(G - np.diag(np.diag(G)), 0, atol=1e-9)
