@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(kCholThreads) chol_inv_kernel(const double* __
 // formed by block rows, X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ (one thread per column of X_IJ),
 // into a kp x kp col-major scratch (kp = k rounded up to 32; the padding is an identity block).
 constexpr int CB = 32;
-constexpr int kCholBlkMax = 224;
+constexpr int kCholBlkMax = 224;    // packed triangle in shared memory
+constexpr int kCholBlkGMax = 512;   // packed triangle in the L2-resident scratch
 constexpr int kCholBlkThreads = 256;
 constexpr unsigned FULLM = 0xffffffffu;
 
@@ -180,6 +181,11 @@ __device__ __noinline__ void inv32(const double* P, int j0, double* Xd, int lane
   __syncwarp();
 }
 
+// GLOBALP (kCholBlkMax < k <= kCholBlkGMax): the packed triangle (1.05 MB at k = 512) does not
+// fit shared memory and lives in the L2-resident scratch instead (X + the diagonal-inverse
+// cache); the algorithm is the same, and each thread forms up to two columns of a block row
+// of the inverse (block rows are up to kp - 32 = 480 columns wide).
+template <bool GLOBALP>
 __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const double* __restrict__ W, int k,
                                                                    double* __restrict__ L,
                                                                    double* __restrict__ Linv,
@@ -189,8 +195,11 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
   long long tdiag = 0, tpanel = 0, ttrail = 0, tinv = 0, t0c = clock64(), tc;
   extern __shared__ __align__(16) double sm[];
   const int kp = (k + CB - 1) / CB * CB, nb = kp / CB;
-  double* P = sm;                              // packed lower triangle, tri(kp) doubles
-  double* Xd = sm + tri(kp);                   // CB x (CB + 1): inverse of the current diagonal block
+  constexpr int NCOL = GLOBALP ? 2 : 1;        // inverse columns per thread
+  // packed lower triangle, tri(kp) doubles; the diagonal-inverse cache follows it when global
+  double* P = GLOBALP ? X + size_t(nb) * CB * (CB + 1) : sm;
+  double* Xd = GLOBALP ? sm : sm + tri(kp);    // CB x (CB + 1): inverse of the current diagonal block
+  double* Z = GLOBALP ? P + tri(kp) : nullptr; // CB x kp staging of a block row of the inverse
   __shared__ int fail;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
@@ -278,27 +287,40 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
     if (warp == 0)
       for (int e = lane; e < CB * (CB + 1); e += 32) Xd[e] = X[I * CB * (CB + 1) + e];
     const int ntask = I * CB;
-    const int col = tid;                                   // one column of X_I* per thread
-    double T[CB];
+    if (GLOBALP) __syncthreads();                          // Xd ready (read before the T loop)
+#pragma unroll 1
+    for (int u = 0; u < NCOL; ++u) {
+      const int col = tid + u * nt;                        // columns tid, tid + nt of X_I*
+      double T[CB];
 #pragma unroll
-    for (int i = 0; i < CB; ++i) T[i] = 0.0;
-    if (col < ntask) {
-      // q runs warp-uniformly from the warp's first column, so the L_I* entries are shared-memory
-      // broadcasts; X[q][col] = 0 for q < col (masked: the packed row q ends at column q)
-      for (int q = col & ~31; q < i0; ++q) {
-        const double xq = (q >= col) ? P[tri(q) + col] : 0.0;
+      for (int i = 0; i < CB; ++i) T[i] = 0.0;
+      if (col < ntask) {
+        // q runs warp-uniformly from the warp's first column, so the L_I* entries are
+        // broadcasts; X[q][col] = 0 for q < col (masked: the packed row q ends at column q)
+        for (int q = col & ~31; q < i0; ++q) {
+          const double xq = (q >= col) ? P[tri(q) + col] : 0.0;
 #pragma unroll
-        for (int i = 0; i < CB; ++i) T[i] = fma(P[tri(i0 + i) + q], xq, T[i]);
+          for (int i = 0; i < CB; ++i) T[i] = fma(P[tri(i0 + i) + q], xq, T[i]);
+        }
+      }
+      if (!GLOBALP) __syncthreads();                       // Xd ready, every L_I* read
+      if (col < ntask) {
+#pragma unroll
+        for (int i = 0; i < CB; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int p = 0; p <= i; ++p) acc = fma(Xd[i * (CB + 1) + p], T[p], acc);
+          // global variant: staged in Z (other threads still read L_I*), copied after the barrier
+          if (GLOBALP) Z[i * int64_t(kp) + col] = -acc;
+          else P[tri(i0 + i) + col] = -acc;
+        }
       }
     }
-    __syncthreads();                                       // Xd ready, every L_I* read
-    if (col < ntask) {
-#pragma unroll
-      for (int i = 0; i < CB; ++i) {
-        double acc = 0.0;
-#pragma unroll
-        for (int p = 0; p <= i; ++p) acc = fma(Xd[i * (CB + 1) + p], T[p], acc);
-        P[tri(i0 + i) + col] = -acc;
+    if (GLOBALP) {
+      __syncthreads();                                     // every L_I* read
+      for (int e = tid; e < CB * ntask; e += nt) {
+        const int i = e / ntask, col = e - i * ntask;
+        P[tri(i0 + i) + col] = Z[i * int64_t(kp) + col];
       }
     }
     if (warp == 0) {
@@ -456,7 +478,10 @@ void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w) {
   w.LinvT2 = c.take<double>(size_t(k) * k);
   w.Q1 = c.take<double>(size_t(m) * k);
   const size_t kp = size_t(k + 31) / 32 * 32;
-  w.chol_g = c.take<double>(k <= kCholBlkMax ? kp * kp : size_t(k) * (k + 1) / 2);
+  const size_t nbk = kp / 32;
+  w.chol_g = c.take<double>(k <= kCholBlkMax ? kp * kp
+                            : k <= kCholBlkGMax ? nbk * 32 * 33 + kp * (kp + 1) / 2 + 32 * kp
+                                                : size_t(k) * (k + 1) / 2);
   w.partial = c.take<double>(cholqr_partial_elems(m, k) + 1);
   // gemm_tall uses s <= min(64, K/64) splits: upper bounds, non-decreasing in m
   const size_t s2 = size_t(k / 64 > 1 ? (k / 64 < 64 ? k / 64 : 64) : 1);
@@ -473,9 +498,15 @@ ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* Lin
   if (k <= kCholBlkMax) {
     const int kp = (k + CB - 1) / CB * CB;
     const size_t smem = (size_t(kp) * (kp + 1) / 2 + size_t(CB) * (CB + 1)) * sizeof(double);
-    cudaFuncSetAttribute(chol_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(chol_blk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     static const int profile = getenv("SSI_CHOL_PROFILE") ? 1 : 0;
-    chol_blk_kernel<<<1, kCholBlkThreads, smem, s>>>(W, k, L, Linv, LinvT, gscratch, status, profile);
+    chol_blk_kernel<false><<<1, kCholBlkThreads, smem, s>>>(W, k, L, Linv, LinvT, gscratch, status, profile);
+    return launch_check("chol_blk_kernel");
+  }
+  if (k <= kCholBlkGMax) {
+    const size_t smem = size_t(CB) * (CB + 1) * sizeof(double);
+    static const int profile = getenv("SSI_CHOL_PROFILE") ? 1 : 0;
+    chol_blk_kernel<true><<<1, kCholBlkThreads, smem, s>>>(W, k, L, Linv, LinvT, gscratch, status, profile);
     return launch_check("chol_blk_kernel");
   }
   const size_t smem_full = chol_smem_bytes(k);
