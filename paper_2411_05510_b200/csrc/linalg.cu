@@ -11,7 +11,7 @@ namespace {
 
 constexpr int kCholThreads = 512;
 constexpr int kJacThreads = 512;
-constexpr int JC = 8;                // Jacobi cluster size (CTAs)
+constexpr int JC = 8;                // Jacobi cluster size (CTAs); 16 (non-portable) for k > 256
 constexpr int kJacMaxSweeps = 60;
 
 
@@ -358,7 +358,7 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
-template <int KPL>   // column elements per lane (k <= 32 * KPL)
+template <int KPL, int JCT>   // column elements per lane (k <= 32 * KPL), cluster size
 __global__ void __launch_bounds__(kJacThreads, 1) jacobi_kernel(double* __restrict__ G, int k,
                                                              double* __restrict__ Ut,
                                                              double* __restrict__ S,
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(kJacThreads, 1) jacobi_kernel(double* __restri
   const int n = (k + 1) & ~1;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int cr = int(cluster_rank());
-  const int gw = cr * nw + warp, gnw = JC * nw;         // warp index / count over the cluster
+  const int gw = cr * nw + warp, gnw = JCT * nw;         // warp index / count over the cluster
   const double tol = sqrt(double(k)) * 1.1102230246251565e-16;
   if (cr == 0)
     for (int i = tid; i < kJacMaxSweeps; i += blockDim.x) gflag[i] = 0;
@@ -542,28 +542,36 @@ ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, Ch
   return trmul(w.Q1, m, w.Linv2, w.LinvT2, Q);
 }
 
-template <int KPL>
+template <int KPL, int JCT>
 static ssi_status jacobi_launch(double* G, int k, double* Ut, double* S, double* scratch, int32_t* status,
                                 cudaStream_t s) {
   const size_t smem = size_t(k) * (sizeof(double) + sizeof(int));
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(jacobi_kernel<KPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    cudaFuncSetAttribute(jacobi_kernel<KPL, JCT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (JCT > 8) cudaFuncSetAttribute(jacobi_kernel<KPL, JCT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   static const int profile = getenv("SSI_JAC_PROFILE") ? 1 : 0;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(JC);
+  cfg.gridDim = dim3(JCT);
   cfg.blockDim = dim3(kJacThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = JC;
+  attr[0].val.clusterDim.x = JCT;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (JCT > 8) {   // a 16-CTA cluster is opt-in: fall back to the portable 8 when it cannot be placed
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, jacobi_kernel<KPL, JCT>, &cfg) != cudaSuccess || nc < 1) {
+      cudaGetLastError();
+      return jacobi_launch<KPL, 8>(G, k, Ut, S, scratch, status, s);
+    }
+  }
   double* gnrm = scratch;
   int* gflag = reinterpret_cast<int*>(scratch + k);
-  if (cudaLaunchKernelEx(&cfg, jacobi_kernel<KPL>, G, k, Ut, S, gnrm, gflag, status, profile) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, jacobi_kernel<KPL, JCT>, G, k, Ut, S, gnrm, gflag, status, profile) != cudaSuccess)
     return launch_check("jacobi_kernel (cluster launch)");
   return SSI_OK;
 }
@@ -572,10 +580,10 @@ size_t jacobi_scratch_elems(int k) { return size_t(k) + kJacMaxSweeps / 2 + 1; }
 
 ssi_status jacobi_svd(double* G, int k, double* Ut, double* S, double* scratch, int32_t* status, cudaStream_t s) {
   ssi_status st;
-  if (k <= 64) st = jacobi_launch<2>(G, k, Ut, S, scratch, status, s);
-  else if (k <= 128) st = jacobi_launch<4>(G, k, Ut, S, scratch, status, s);
-  else if (k <= 256) st = jacobi_launch<8>(G, k, Ut, S, scratch, status, s);
-  else if (k <= 512) st = jacobi_launch<16>(G, k, Ut, S, scratch, status, s);
+  if (k <= 64) st = jacobi_launch<2, JC>(G, k, Ut, S, scratch, status, s);
+  else if (k <= 128) st = jacobi_launch<4, JC>(G, k, Ut, S, scratch, status, s);
+  else if (k <= 256) st = jacobi_launch<8, JC>(G, k, Ut, S, scratch, status, s);
+  else if (k <= 512) st = jacobi_launch<16, 16>(G, k, Ut, S, scratch, status, s);
   else {
     set_last_error("jacobi_svd: k = %d > 512 unsupported", k);
     return SSI_ERR_INVALID_ARG;
