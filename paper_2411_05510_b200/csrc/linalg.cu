@@ -200,6 +200,10 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
   double* P = GLOBALP ? X + size_t(nb) * CB * (CB + 1) : sm;
   double* Xd = GLOBALP ? sm : sm + tri(kp);    // CB x (CB + 1): inverse of the current diagonal block
   double* Z = GLOBALP ? P + tri(kp) : nullptr; // CB x kp staging of a block row of the inverse
+  // global variant: shared-memory copies of what the inner loops re-read — the panel below the
+  // diagonal block (rows j0 + CB.., CB columns, pitch CB + 1) for the trailing update, and the
+  // block row L_I* (CB x i0) for the inverse; both fit in (kp - CB) (CB + 1) doubles
+  double* Ps = GLOBALP ? sm + CB * (CB + 1) : nullptr;
   __shared__ int fail;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
@@ -233,6 +237,7 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
 #pragma unroll
         for (int p = 0; p <= c; ++p) acc = fma(av[p], Xd[c * (CB + 1) + p], acc);
         rowp[c] = acc;
+        if (GLOBALP) Ps[(r - j0 - CB) * (CB + 1) + c] = acc;
       }
     }
     __syncthreads();
@@ -249,7 +254,15 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
       const double* lr[4];
       const double* lc[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) { lr[u] = P + tri(r0 + u) + j0; lc[u] = P + tri(c0 + u) + j0; }
+      for (int u = 0; u < 4; ++u) {
+        if (GLOBALP) {
+          lr[u] = Ps + (r0 + u - j0 - CB) * (CB + 1);
+          lc[u] = Ps + (c0 + u - j0 - CB) * (CB + 1);
+        } else {
+          lr[u] = P + tri(r0 + u) + j0;
+          lc[u] = P + tri(c0 + u) + j0;
+        }
+      }
       double acc[4][4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -287,7 +300,13 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
     if (warp == 0)
       for (int e = lane; e < CB * (CB + 1); e += 32) Xd[e] = X[I * CB * (CB + 1) + e];
     const int ntask = I * CB;
-    if (GLOBALP) __syncthreads();                          // Xd ready (read before the T loop)
+    if (GLOBALP) {
+      for (int e = tid; e < CB * i0; e += nt) {            // L_I* -> shared (row-major CB x i0)
+        const int i = e / i0, q = e - i * i0;
+        Ps[e] = P[tri(i0 + i) + q];
+      }
+      __syncthreads();                                     // Xd and L_I* ready
+    }
 #pragma unroll 1
     for (int u = 0; u < NCOL; ++u) {
       const int col = tid + u * nt;                        // columns tid, tid + nt of X_I*
@@ -297,10 +316,11 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
       if (col < ntask) {
         // q runs warp-uniformly from the warp's first column, so the L_I* entries are
         // broadcasts; X[q][col] = 0 for q < col (masked: the packed row q ends at column q)
+#pragma unroll (GLOBALP ? 4 : 1)
         for (int q = col & ~31; q < i0; ++q) {
           const double xq = (q >= col) ? P[tri(q) + col] : 0.0;
 #pragma unroll
-          for (int i = 0; i < CB; ++i) T[i] = fma(P[tri(i0 + i) + q], xq, T[i]);
+          for (int i = 0; i < CB; ++i) T[i] = fma(GLOBALP ? Ps[i * i0 + q] : P[tri(i0 + i) + q], xq, T[i]);
         }
       }
       if (!GLOBALP) __syncthreads();                       // Xd ready, every L_I* read
@@ -504,7 +524,9 @@ ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* Lin
     return launch_check("chol_blk_kernel");
   }
   if (k <= kCholBlkGMax) {
-    const size_t smem = size_t(CB) * (CB + 1) * sizeof(double);
+    const int kp = (k + CB - 1) / CB * CB;
+    const size_t smem = (size_t(CB) * (CB + 1) + size_t(kp - CB) * (CB + 1)) * sizeof(double);
+    cudaFuncSetAttribute(chol_blk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     static const int profile = getenv("SSI_CHOL_PROFILE") ? 1 : 0;
     chol_blk_kernel<true><<<1, kCholBlkThreads, smem, s>>>(W, k, L, Linv, LinvT, gscratch, status, profile);
     return launch_check("chol_blk_kernel");
