@@ -455,3 +455,26 @@ def test_shear_frame_modes_reproduce_table1():
         np.testing.assert_allclose(K @ modes.phi[j], w[j] ** 2 * (M @ modes.phi[j]), atol=1e-6 * w[j] ** 2 * 100)
     G = modes.phi @ M @ modes.phi.T
     np.testing.assert_allclose(G - np.diag(np.diag(G)), 0, atol=1e-9)
+
+
+def test_e3_algorithm1_verbatim_recovers_table1():
+    """The paper's E3 setting: Algorithm 1 verbatim (q = p = 0) with
+    k = ⌈k̄(T) %·T⌉ = 512 at j_b = 189 (T = 1890) on a 5-min, 200 Hz, SNR 20 dB record of the
+    Table 1 shear frame identifies all ten Table 1 modes at order 30 (frequency within 1 %,
+    damping within 1 percentage point) — end-to-end statistical pin of the oracle chain on the
+    paper's own workload, independent of the c1-c5 generator settings."""
+    from synth.records import _simulate
+    from tests.analytic import shear_frame_modes
+    modes = shear_frame_modes(200.0)
+    Y = _simulate(modes, 60000, 0.1, np.random.default_rng([27, 0xE3]))
+    l, i = 10, 189
+    k = oracle.sample_count(oracle.min_rank_percent(l * i), l * i)
+    assert k == 512
+    U, S, _ = oracle.rsvd(oracle.toeplitz(oracle.covariances(Y, 2 * i - 1), i), k, 0, 0xE3, i, 30)
+    cell = oracle.modal_sweep(U, S, l, i, [30], 1 / 200.0)[0]
+    f_id = np.array([p.f for p in cell.poles])
+    xi_id = np.array([p.xi for p in cell.poles])
+    for f, xi in zip(modes.f, modes.xi):
+        j = np.argmin(np.abs(f_id - f))
+        assert abs(f_id[j] - f) / f < 0.01
+        assert abs(xi_id[j] - xi) < 0.01
