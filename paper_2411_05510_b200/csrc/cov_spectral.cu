@@ -258,7 +258,10 @@ __device__ __forceinline__ void store_twiddled(double2* zc, int base, int q, con
 }
 
 template <int SEGS>
-__global__ void __launch_bounds__(kFftThreads, SEGS == 1 ? 3 : 2) spec_fft1024_kernel(FftArgs g) {
+#ifndef SSI_FFT_MINB
+#define SSI_FFT_MINB 2   // resident CTAs per SM declared for the 2-segment kernel
+#endif
+__global__ void __launch_bounds__(kFftThreads, SEGS == 1 ? 3 : SSI_FFT_MINB) spec_fft1024_kernel(FftArgs g) {
   constexpr int CH = 4;
   extern __shared__ __align__(16) double2 z[];     // [CH][kFP]
   const int tid = threadIdx.x;
