@@ -201,8 +201,9 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
   double* Xd = GLOBALP ? sm : sm + tri(kp);    // CB x (CB + 1): inverse of the current diagonal block
   double* Z = GLOBALP ? P + tri(kp) : nullptr; // CB x kp staging of a block row of the inverse
   // global variant: shared-memory copies of what the inner loops re-read — the panel below the
-  // diagonal block (rows j0 + CB.., CB columns, pitch CB + 1) for the trailing update, and the
-  // block row L_I* (CB x i0) for the inverse; both fit in (kp - CB) (CB + 1) doubles
+  // diagonal block (CB columns of up to kp - CB rows, column-major, so a 4 x 4 tile reads its
+  // rows with 16-byte loads) for the trailing update, and the block row L_I* (CB x i0) for the
+  // inverse; both fit in (kp - CB) (CB + 1) doubles
   double* Ps = GLOBALP ? sm + CB * (CB + 1) : nullptr;
   __shared__ int fail;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
 #pragma unroll
         for (int p = 0; p <= c; ++p) acc = fma(av[p], Xd[c * (CB + 1) + p], acc);
         rowp[c] = acc;
-        if (GLOBALP) Ps[(r - j0 - CB) * (CB + 1) + c] = acc;
+        if (GLOBALP) Ps[c * (kp - CB) + (r - j0 - CB)] = acc;   // column-major panel
       }
     }
     __syncthreads();
@@ -254,15 +255,7 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
       const double* lr[4];
       const double* lc[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (GLOBALP) {
-          lr[u] = Ps + (r0 + u - j0 - CB) * (CB + 1);
-          lc[u] = Ps + (c0 + u - j0 - CB) * (CB + 1);
-        } else {
-          lr[u] = P + tri(r0 + u) + j0;
-          lc[u] = P + tri(c0 + u) + j0;
-        }
-      }
+      for (int u = 0; u < 4; ++u) { lr[u] = P + tri(r0 + u) + j0; lc[u] = P + tri(c0 + u) + j0; }
       double acc[4][4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -271,8 +264,16 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
 #pragma unroll 4
       for (int p = 0; p < CB; ++p) {
         double xr[4], xc[4];
+        if (GLOBALP) {   // column-major panel: the tile's 4 rows are two 16-byte loads
+          const double2* pr = reinterpret_cast<const double2*>(Ps + p * (kp - CB) + (r0 - j0 - CB));
+          const double2* pc = reinterpret_cast<const double2*>(Ps + p * (kp - CB) + (c0 - j0 - CB));
+          const double2 r01 = pr[0], r23 = pr[1], c01 = pc[0], c23 = pc[1];
+          xr[0] = r01.x; xr[1] = r01.y; xr[2] = r23.x; xr[3] = r23.y;
+          xc[0] = c01.x; xc[1] = c01.y; xc[2] = c23.x; xc[3] = c23.y;
+        } else {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) { xr[u] = lr[u][p]; xc[u] = lc[u][p]; }
+          for (int u = 0; u < 4; ++u) { xr[u] = lr[u][p]; xc[u] = lc[u][p]; }
+        }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
 #pragma unroll
