@@ -3,14 +3,23 @@
 
   CoV-SSI records/s (cov + Toeplitz + RSVD + modal sweep) at l=192, i=60 (config c3:
   N=360000 FP32 samples, k = n_max + p = 220, q = 2, orders 2..200 step 2), plus the
-  dominant kernel's fraction of the B200 roofline.
+  roofline fractions of its kernels.
 
-A "step" is one record through A1 (covariances) -> A2 (Toeplitz) -> A3-A8 (RSVD) ->
-A9-A11 (modal sweep). Records are device-resident (4 distinct records rotated, each
-276 MB > the 126 MB L2). Multi-GPU (torchrun): each rank processes its own records
-(weak scaling, no data-path collective); time = max over ranks.
+A "step" is one record through A1 (covariances) -> A2 (Toeplitz, applied through its block
+structure) -> A3-A8 (RSVD) -> A9-A11 (modal sweep). Records are device-resident (2 distinct
+276 MB records rotated per rank, each > the 126 MB L2), 8 in flight. Multi-GPU (torchrun): each
+rank processes its own records (weak scaling, no data-path collective); time = max over ranks.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--cov fp64|int8x3|spectral] [--impl reference]
+Two more workloads are timed in every run (keys "lag_sweep_c4" and "record_batch_c5"; the
+north star's scaling targets), at the launch's N GPUs:
+  * c4 — the 3D stabilization sweep on the c3 record, i = 20..80 step 4: time-sharded spectral
+    covariances to lag 159 (ssi_covariances, normalize=0) -> one NCCL all_reduce ->
+    ssi_cov_normalize -> lags by LPT on 8 high-priority streams per rank -> one packed all_gather
+    of the pole tables -> ssi_stab3d (strong scaling: one sweep, fixed work);
+  * c5 — the continuous-monitoring batch: 64 records of 180000 samples (i = 50) round-robin over
+    the ranks, 8 in flight per rank, then one packed all_gather of the 64 tables (strong scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c3|c4|c5] [--impl reference]
 """
 import argparse
 import json
@@ -27,6 +36,9 @@ sys.path.insert(0, ROOT)
 
 METRIC = "CoV-SSI records/sec (cov+RSVD+modal sweep), l=192,i=60; % of B200 roofline"
 UNIT = "records/s"
+C4_LAGS = tuple(range(20, 81, 4))          # BASELINE.json configs[3]
+C5_RECORDS = 64                            # BASELINE.json configs[4]
+FP64_ALU_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 148 SMs x 64 FP64 FMA lanes x 2 x 1965 MHz
 
 
 def parse():
@@ -35,17 +47,19 @@ def parse():
     ap.add_argument("--steps", type=int, default=80)
     ap.add_argument("--warmup", type=int, default=8)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4", "c5"],
+                    help="headline workload: c3 records (the metric), c4 lag sweeps or c5 record batches")
     ap.add_argument("--cov", default=os.environ.get("SSI_COV_MODE", "spectral"), choices=["fp64", "int8x3", "spectral"])
     ap.add_argument("--explicit-t", action="store_true",
                     help="materialize T (A2) and stream it through the RSVD GEMMs instead of "
                          "applying it through its block structure")
-    ap.add_argument("--config", default="c3")
     ap.add_argument("--records", type=int, default=2)
     ap.add_argument("--streams", type=int, default=8, help="records in flight (one engine per stream)")
     ap.add_argument("--no-priority", action="store_true",
                     help="one stream per record (no low-priority covariance streams)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-legs", action="store_true", help="skip the c4 / c5 legs")
     return ap.parse_args()
 
 
@@ -58,6 +72,28 @@ def workload_desc(cfg):
 def cov_flops(cfg):
     L = 2 * cfg.i - 1
     return 2.0 * cfg.l * cfg.l * sum(cfg.N - k for k in range(1, L + 1))
+
+
+def record_flops(cfg, api):
+    """Algorithmic flops of one record through the path as built, by stage:
+    A1 spectral: cross-spectral product 6 lp^2 S (F/2+1) + inverse DFT 2 lp^2 L (F+2);
+    A4/A6/A7 (2q+2 passes through the block DFT): per pass 2 i (2l)^2 k (block products) +
+    2 x 2 l (2i) i k (forward and inverse DFT);  A5/A8: 2q+2 CholeskyQR2 + the one of B^T, each
+    2 x (m k^2) (symmetric Gram, triangular Y L^-T) + Cholesky/inverse (2 k^3/3), U = Q U~
+    (2 m k n_max), Jacobi (~9 sweeps x k^2/2 pairs x 6k); A9-A11: CholeskyQR2 of U^up + Q^T U^down
+    (~6 m n_max^2) and per order n: Hessenberg (10/3 n^3) with C_n = U[0:l,:n] Q_H (2 l n^2), and
+    the Francis QR (~10 n^3) with its l-row Schur vectors (~15 l n^2; LAPACK's 25 n^3 for an
+    n-row Z scaled to l rows)."""
+    l, i, k, n_max, m, q = cfg.l, cfg.i, cfg.k, cfg.n_max, cfg.m, cfg.q
+    f_prod, f_inv = api.cov_spectral_flops(cfg.N, l, 2 * i - 1)
+    passes = 2 * q + 2                       # Y = T Omega, 2q power-iteration passes, B^T = T^T Q
+    rsvd_passes = passes * (2 * i * (2 * l) ** 2 * k + 2 * 2 * l * (2 * i) * i * k)
+    nqr = 2 * q + 2                          # qr(Y), 2q in the power iterations, qr(B^T)
+    qr = nqr * (4.0 * m * k * k + 2.0 * k ** 3 / 3)
+    small = 2.0 * m * k * n_max + 9 * (k * k / 2) * 6 * k
+    modal = 6.0 * m * n_max ** 2 + sum(10.0 / 3 * n ** 3 + 2.0 * l * n * n + 10.0 * n ** 3 + 15.0 * l * n * n
+                                       for n in cfg.orders)
+    return {"A1": f_prod + f_inv, "A4_A6_A7": rsvd_passes, "A5_A8": qr + small, "A9_A11": modal}
 
 
 # ------------------------------------------------------------------ clocks sampler
@@ -104,51 +140,6 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU oracle (reported baseline)
-def oracle_sample(cfg, Y, orders=(100, 200), cov_lags=None, R_full=None):
-    """Times the unmodified oracle on one c3 record: the covariances (all 2i-1 lags, or
-    `cov_lags` evenly spaced lags scaled to all of them: each lag is one independent matmul of
-    the same size), the full Toeplitz, the full RSVD (same Philox sketch), and the literal
-    pinv+eig modal identification at the given orders only (per-order cost fitted as
-    a + b n^2 and summed over all orders). With cov_lags the Toeplitz / RSVD / modal stages run on
-    `R_full` (the record's full covariances, computed once outside the timing).
-    Returns (seconds per record, stage seconds, description)."""
-    import oracle
-    t = {}
-    L = 2 * cfg.i - 1
-    t0 = time.perf_counter()
-    if cov_lags is None:
-        R = oracle.covariances(Y, L)
-        t["cov"] = time.perf_counter() - t0
-    else:
-        ks = sorted(set(int(round(x)) for x in np.linspace(1, L, cov_lags)))
-        for k in ks:
-            oracle.covariances(Y, k, k)
-        t["cov"] = (time.perf_counter() - t0) * L / len(ks)
-        R = R_full
-    t0 = time.perf_counter()
-    T = oracle.toeplitz(R, cfg.i)
-    t["toeplitz"] = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    U, S, _ = oracle.rsvd(T, cfg.k, cfg.q, cfg.philox_key, cfg.i, cfg.n_max)
-    t["rsvd"] = time.perf_counter() - t0
-    per = []
-    for n in orders:
-        t0 = time.perf_counter()
-        oracle.modal_sweep(U, S, cfg.l, cfg.i, [n], cfg.dt)
-        per.append((n, time.perf_counter() - t0))
-    (n1, a1), (n2, a2) = per[0], per[-1]
-    b = (a2 - a1) / (n2 ** 2 - n1 ** 2) if n2 != n1 else 0.0
-    a = a1 - b * n1 ** 2
-    t["modal"] = sum(max(a + b * n * n, 0.0) for n in cfg.orders)
-    total = sum(t.values())
-    cov_desc = f"full covariances ({L} lags)" if cov_lags is None else \
-        f"covariances timed on {cov_lags} of the {L} lags and scaled to all {L}"
-    sample = (f"one {cfg.name} record: {cov_desc}, full Toeplitz, full RSVD "
-              f"(k={cfg.k}, q={cfg.q}), modal sweep timed at orders {list(orders)} and fitted a+b*n^2 "
-              f"over the {len(cfg.orders)} orders")
-    return total, t, sample
-
-
 def cores_used():
     try:
         return len(os.sched_getaffinity(0))
@@ -156,30 +147,141 @@ def cores_used():
         return os.cpu_count()
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+class OracleRecord:
+    """One record through the UNMODIFIED oracle (oracle/, FP64 numpy/LAPACK), cut into `n`
+    pieces that run in order and together are exactly one record: the covariances as time shards
+    of the direct sum (oracle.covariance_partial_sums; the last shard divides by N - k), then the
+    Toeplitz + RSVD (same Philox sketch), then the literal pinv + eig modal sweep over every
+    order, in chunks of orders. Nothing is fitted or extrapolated: timing all n pieces times one
+    whole record. The FP32 record is converted to FP64 once, outside the timing."""
+
+    def __init__(self, cfg, Y, n: int):
+        import oracle
+        self.oracle = oracle
+        self.cfg = cfg
+        self.Y = np.asarray(Y, dtype=np.float64)
+        self.L = 2 * cfg.i - 1
+        n = max(3, n)
+        n_mod = max(1, n // 5)
+        n_cov = n - 1 - n_mod
+        N = self.Y.shape[0]
+        bounds = np.linspace(0, N, n_cov + 1).round().astype(int)
+        self.pieces = [("cov", int(a), int(b)) for a, b in zip(bounds[:-1], bounds[1:])]
+        self.pieces.append(("rsvd",))
+        w = np.cumsum([o ** 3 for o in cfg.orders]).astype(float)    # equal-cost chunks of orders
+        cut = np.searchsorted(w, w[-1] * np.arange(1, n_mod) / n_mod)
+        chunks = np.split(np.array(cfg.orders), cut)
+        self.pieces += [("modal", [int(o) for o in c]) for c in chunks if len(c)]
+        self.stage_s = {"cov": 0.0, "toeplitz": 0.0, "rsvd": 0.0, "modal": 0.0}
+        self.S = None
+        self.cells = []
+
+    def __len__(self):
+        return len(self.pieces)
+
+    def run(self, j):
+        o, cfg = self.oracle, self.cfg
+        pc = self.pieces[j]
+        t0 = time.perf_counter()
+        if pc[0] == "cov":
+            part = o.covariance_partial_sums(self.Y, 1, self.L, pc[1], pc[2])
+            self.S = part if self.S is None else self.S + part
+            if pc[2] == self.Y.shape[0]:
+                N = self.Y.shape[0]
+                for k in range(1, self.L + 1):
+                    self.S[k - 1] /= (N - k)
+            self.stage_s["cov"] += time.perf_counter() - t0
+        elif pc[0] == "rsvd":
+            T = o.toeplitz(self.S, cfg.i)
+            t1 = time.perf_counter()
+            self.stage_s["toeplitz"] += t1 - t0
+            self.U, self.Sv, _ = o.rsvd(T, cfg.k, cfg.q, cfg.philox_key, cfg.i, cfg.n_max)
+            self.stage_s["rsvd"] += time.perf_counter() - t1
+        else:
+            self.cells += o.modal_sweep(self.U, self.Sv, cfg.l, cfg.i, pc[1], cfg.dt)
+            self.stage_s["modal"] += time.perf_counter() - t0
+        return time.perf_counter() - t0
+
+    def describe(self):
+        n_cov = sum(1 for p in self.pieces if p[0] == "cov")
+        n_mod = sum(1 for p in self.pieces if p[0] == "modal")
+        return (f"one whole {self.cfg.name} record through the unmodified FP64 oracle, cut into {len(self)} "
+                f"pieces run in order: covariances by direct summation over all {self.L} lags in {n_cov} "
+                f"time shards, full Toeplitz + RSVD (k={self.cfg.k}, q={self.cfg.q}, same Philox sketch), "
+                f"literal pinv+eig modal sweep over all {len(self.cfg.orders)} orders in {n_mod} chunks; "
+                f"nothing fitted or extrapolated")
+
+
+def cpu_extras(cfg, cells):
+    """Beside the record: O-5 (one full dgesdd of the Toeplitz, timed at c2 size, 2880^2; the c3
+    11520^2 one takes minutes — profiles/), O-8 (oracle stab3d over the record's table), and a
+    single-thread direct-sum covariance rate (GFLOP/s)."""
+    import oracle
+    import synth
+    out = {}
+    c2 = synth.config("c2")
+    Y2, _ = synth.make_record(c2)
+    T2 = oracle.toeplitz(oracle.covariances(Y2, 2 * c2.i - 1), c2.i)
+    t0 = time.perf_counter()
+    oracle.full_svd(T2)
+    out["o5_full_svd_c2_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.stab3d([cells], oracle.SC_BRIDGE_3D, cfg.n_max // 2)
+    out["o8_stab3d_s"] = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_limits
+        Y, _ = synth.make_record(cfg, N=3000)
+        Y = np.asarray(Y, dtype=np.float64)
+        L = 2 * cfg.i - 1
+        with threadpool_limits(limits=1):
+            t0 = time.perf_counter()
+            oracle.covariance_partial_sums(Y, 1, L)
+            dt = time.perf_counter() - t0
+        out["cov_gflops_1thread"] = 2.0 * cfg.l ** 2 * sum(Y.shape[0] - k for k in range(1, L + 1)) / dt / 1e9
+    except Exception as e:            # threadpoolctl missing: report why
+        out["cov_gflops_1thread"] = None
+        out["cov_1thread_error"] = str(e)[:100]
+    return out
+
+
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """The oracle as the reference arm (this tier has no reference code; /root/reference is a
+    paper): rank 0 only; each of the K timed steps is one piece of ONE whole c3 record (so the K
+    steps together are exactly one record, timed piece by piece, nothing extrapolated); the W
+    warm-up steps run pieces of a tiny c1 record."""
     import synth
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import oracle
-    cfg = synth.config(args.config)
+    cfg = synth.config("c3")
     Y, _ = synth.make_record(cfg)
-    for _ in range(max(0, min(args.warmup, 1))):
-        oracle_sample(synth.config("c1"), synth.make_record(synth.config("c1"))[0], (10, 20))
-    # each step is a bounded sample (about 3 s of CPU work) so K steps finish in minutes
-    R_full = oracle.covariances(Y, 2 * cfg.i - 1)
-    secs = []
-    for _ in range(args.steps):
-        tot, _, sample = oracle_sample(cfg, Y, cov_lags=8, R_full=R_full)
-        secs.append(tot)
-    v = 1.0 / float(np.mean(secs))
+    c1 = synth.config("c1")
+    warm = OracleRecord(c1, synth.make_record(c1)[0], max(args.warmup, 3))
+    for j in range(args.warmup):
+        warm.run(j % len(warm))
+    rec = OracleRecord(cfg, Y, args.steps)
+    secs = [rec.run(j) for j in range(len(rec))]
+    total = float(np.sum(secs))
+    v = 1.0 / total
+    steps = len(rec)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(secs)),
+            "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": workload_desc(cfg)},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores_used(), "kind": "oracle",
-                             "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores_used(), "cpu_model": cpu_model(),
+                             "kind": "oracle", "sample": rec.describe(),
+                             "stage_s": {k: round(t, 3) for k, t in rec.stage_s.items()}},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -187,18 +289,85 @@ def run_reference(args):
 
 # ------------------------------------------------------------------ our arm
 def count_launches(fn):
-    """Kernels of libssi launched by fn() (CUPTI through torch.profiler)."""
+    """Kernels of libssi launched by fn() (CUPTI through torch.profiler); torch's own kernels
+    (the status-word bookkeeping, copies) are excluded."""
     import torch
     from torch.profiler import profile, ProfilerActivity
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         fn()
         torch.cuda.synchronize()
     names = [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
-    ours = [n for n in names if any(s in n for s in ("ssi::", "kernel", "cov_", "splitk", "toeplitz",
-                                                     "sketch", "jacobi", "chol", "eig_order", "gemm",
-                                                     "stab_", "i8"))
-            and "Memset" not in n and "Memcpy" not in n]
+    ours = [n for n in names if "ssi::" in n and "at::" not in n]
     return len(ours), names
+
+
+def _max_over_ranks(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(x, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def sweep_leg(api, drivers, synth, torch, dist, Y, world, rank, dev, reps=3, warm=2):
+    """c4: the whole 3D stabilization sweep (strong scaling over ranks), device time (events on
+    the current stream, which every phase joins), max over ranks."""
+    cfg = synth.config("c4")
+    P = drivers.SweepParams(l=cfg.l, i=cfg.i, n_max=cfg.n_max, p=cfg.p, q=cfg.q, fs=cfg.fs,
+                            n_min=cfg.n_min, n_step=cfg.n_step, seed=cfg.philox_key)
+    crit = api.CRITERIA_BRIDGE_3D
+    for _ in range(warm):
+        drivers.lag_sweep_3d(Y, P, C4_LAGS, crit, rank, world)
+    torch.cuda.synchronize()
+    rows = []
+    for _ in range(reps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        tm = {}
+        tabs, flags, counts = drivers.lag_sweep_3d(Y, P, C4_LAGS, crit, rank, world, timing=tm)
+        torch.cuda.synchronize()
+        ph = [tm["start"].elapsed_time(tm["cov"]), tm["cov"].elapsed_time(tm["lags"]),
+              tm["lags"].elapsed_time(tm["gather"]), tm["gather"].elapsed_time(tm["stab"]),
+              tm["start"].elapsed_time(tm["stab"])]
+        rows.append(_max_over_ranks(ph, world, dev))
+    best = min(rows, key=lambda r: r[-1])
+    med = sorted(r[-1] for r in rows)[len(rows) // 2]
+    return {"workload": "c4: c3 record, i = 20..80 step 4 (16 lags, T up to 15360^2), k=220, q=2, orders 2..200",
+            "ms_per_sweep": med, "ms_best": best[-1],
+            "phase_ms_best": {"cov_allreduce_normalize": best[0], "lags": best[1], "gather": best[2],
+                              "stab3d": best[3]},
+            "sweeps_per_s": 1e3 / med, "n_gpus": world, "reps": reps, "scaling": "strong",
+            "stable_poles": int(counts.sum().item()),
+            "lag_assignment": drivers.lpt_assign(list(C4_LAGS), world)}
+
+
+def batch_leg(api, drivers, synth, torch, dist, world, rank, dev, streams):
+    """c5: 64 records of 180000 samples over all ranks (strong scaling), 8 in flight per rank,
+    one packed all_gather of the 64 tables; device time, max over ranks."""
+    cfg = synth.config("c5")
+    P = drivers.SweepParams(l=cfg.l, i=cfg.i, n_max=cfg.n_max, p=cfg.p, q=cfg.q, fs=cfg.fs,
+                            n_min=cfg.n_min, n_step=cfg.n_step, seed=cfg.philox_key)
+    # two distinct drifted records per rank, device-resident, rotated (each 138 MB > L2)
+    Ys = [torch.from_numpy(synth.make_record(cfg, record=2 * rank + j)[0]).to(dev) for j in range(2)]
+    recs = [Ys[j % 2] for j in range(C5_RECORDS)]
+    drivers.record_batch(recs, P, rank, world, n_streams=streams)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    drivers.record_batch(recs, P, rank, world, n_streams=streams)
+    b.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks([a.elapsed_time(b)], world, dev)[0]
+    return {"workload": f"c5: {C5_RECORDS} records x 180000 F32 samples, l=192, i=50, k=220, q=2, orders 2..200 "
+                        "(2 distinct drifted records per rank rotated)",
+            "ms_per_batch": ms, "records_per_s": C5_RECORDS / (ms / 1e3), "n_gpus": world, "scaling": "strong",
+            "records_per_rank": len(drivers.record_assignment(C5_RECORDS, world)[0])}
 
 
 def main():
@@ -222,16 +391,18 @@ def main():
     if world > 1:
         dist.barrier()
 
-    cfg = synth.config(args.config)
+    cfg = synth.config("c3")
     P = drivers.SweepParams(l=cfg.l, i=cfg.i, n_max=cfg.n_max, p=cfg.p, q=cfg.q, fs=cfg.fs,
                             n_min=cfg.n_min, n_step=cfg.n_step, seed=cfg.philox_key, cov_mode=args.cov,
                             structured=not args.explicit_t)
-    # distinct records per rank (weak scaling): record index = rank * R + j
+    # distinct records per rank (weak scaling): record index = rank * R + j; the c3 record itself
+    # (seed cfg.seed) is also the c4 sweep's input on every rank
     host = []
     for j in range(args.records):
-        Yh, _ = synth.make_record(synth.config(args.config, seed=cfg.seed + 100 * (rank * args.records + j) if j or rank else cfg.seed))
+        Yh, _ = synth.make_record(synth.config("c3", seed=cfg.seed + 100 * (rank * args.records + j) if j or rank else cfg.seed))
         host.append(Yh)
     Ys = [torch.from_numpy(h).to(dev) for h in host]
+    Y_c3 = Ys[0] if rank == 0 else torch.from_numpy(synth.make_record(cfg)[0]).to(dev)
     pipe = drivers.RecordPipeline(P, cfg.N, dev, n_streams=args.streams, split_priority=not args.no_priority)
     eng = pipe.engines[0]
     stream = torch.cuda.current_stream()
@@ -244,11 +415,7 @@ def main():
         step(j)
     pipe.join()
     torch.cuda.synchronize()
-    for e in pipe.engines:
-        for ws in (e.ws_cov, e.ws_rsvd, e.ws_modal):
-            code = api.device_status(ws)
-            if code != 0:
-                raise RuntimeError(f"device status {code} after warm-up")
+    pipe.check()
     n_launch, _ = count_launches(lambda: (step(0), pipe.join()))
 
     # per-stage breakdown (one extra untimed record on one stream, events between stages)
@@ -289,14 +456,12 @@ def main():
     t_end.record(stream)
     torch.cuda.synchronize()
     clocks = clk.stop()
+    pipe.check()
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
     cov_ms = float(np.mean([a.elapsed_time(b) for a, b in cov_ev]))
-    if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = _max_over_ranks([ms], world, dev)[0]
     value = world * args.steps / (ms / 1e3)
 
     # ---------------- end to end through the public API with host buffers
@@ -321,24 +486,28 @@ def main():
             st = pipe.streams[slot]
             with torch.cuda.stream(st):
                 Ydev[slot].copy_(pinned[j % 2], non_blocking=True)       # H2D inside the step
-            tab, _ = pipe.submit(Ydev[slot], (j << 32) | cfg.i)
+                tab, _ = pipe.submit(Ydev[slot], (j << 32) | cfg.i)
             with torch.cuda.stream(st):
                 for hst, d in zip(tab_host[slot], tab.tensors()):      # D2H of the result
                     hst.copy_(d, non_blocking=True)
         pipe.join(stream)
         b.record(stream)
         torch.cuda.synchronize()
-        ems = a.elapsed_time(b)
-        if world > 1:
-            tt = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ems = float(tt.item())
+        pipe.check()
+        ems = _max_over_ranks([a.elapsed_time(b)], world, dev)[0]
         e2e = {"value": world * args.steps / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h)}
 
-    # ---------------- roofline of the dominant tensor-core kernel (covariance contraction)
-    # Timed in isolation (the pipelined timed region overlaps streams, so a launch's event
-    # span there includes other records' kernels; that span is reported for context).
+    # ---------------- the c4 sweep and the c5 batch at this N
+    legs = {}
+    if not args.no_legs:
+        legs["lag_sweep_c4"] = sweep_leg(api, drivers, synth, torch, dist, Y_c3, world, rank, dev)
+        legs["record_batch_c5"] = batch_leg(api, drivers, synth, torch, dist, world, rank, dev, args.streams)
+
+    # ---------------- roofline
+    # The covariance stage alone (CUDA events around one record's A1 on the current stream) and
+    # its dominant kernel, the cross-spectral product, re-run alone on the spectra the call left
+    # in the engine's workspace (measurement entry point ssi_cov_spectral_phases).
     iso = []
     for _ in range(3):
         a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
@@ -346,88 +515,86 @@ def main():
         torch.cuda.synchronize()
         iso.append(a.elapsed_time(b))
     iso_ms = float(np.median(iso))
-    prod_ms = None
-    if args.cov == "spectral":
-        # the dominant kernel alone: the cross-spectral product re-run on the spectra the call
-        # above left in the engine's workspace (library measurement hook SSI_SPEC_PHASES=2)
-        os.environ["SSI_SPEC_PHASES"] = "2"
-        try:
-            pt = []
-            for _ in range(3):
-                a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
-                a.record(stream); eng.covariances(Ys[0]); b.record(stream)
-                torch.cuda.synchronize()
-                pt.append(a.elapsed_time(b))
-            prod_ms = float(np.median(pt))
-        finally:
-            del os.environ["SSI_SPEC_PHASES"]
+    extra = json.load(open(os.path.join(ROOT, "profiles", "peaks_extra_r01.json")))
+    dgemm = extra["fp64_dgemm_tflops_burst"]
+    dgemm_sus = extra["fp64_dgemm_tflops_sustained"]
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         pass
-    extra = json.load(open(os.path.join(ROOT, "profiles", "peaks_extra_r01.json")))
-    flops = cov_flops(cfg)                  # 2 l^2 sum_k (N - k) per record
-    traffic = None
-    try:
-        nsum = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")))
-        key = {"int8x3": "cov_i8_kernel", "spectral": "cross3m_kernel"}.get(args.cov)
-        if key and key in nsum:
-            mb = lambda d: d["value"] * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[d["unit"]]
-            traffic = mb(nsum[key]["dram__bytes_read.sum"]) + mb(nsum[key]["dram__bytes_write.sum"])
-    except Exception:
-        traffic = None
-    stage = None
+    roof = None
+    stage_cov = None
     if args.cov == "spectral":
-        # dominant kernel: the cross-spectral product (FP64 DMMA), its algorithmic flops
-        # 6 lp^2 S (F/2+1) over its own live duration; the whole covariance stage beside it
+        pt = []
+        for _ in range(3):
+            a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+            a.record(stream); api.cov_spectral_phases(Ys[0], eng.lag_hi, 2, eng.R, eng.ws_cov); b.record(stream)
+            torch.cuda.synchronize()
+            pt.append(a.elapsed_time(b))
+        prod_ms = float(np.median(pt))
         f_main, f_inv = api.cov_spectral_flops(cfg.N, cfg.l, 2 * cfg.i - 1)
-        F, S = api.cov_spectral_plan(cfg.N, cfg.l, 2 * cfg.i - 1)
-        peak = extra["fp64_dgemm_tflops_burst"]
-        peak_src = "measured cuBLAS DGEMM 8192^3 on this pool's B200 (profiles/peaks_extra_r01.json)"
-        work, unit = f_main, "TFLOP/s"
-        stage = {"stage_ms": iso_ms, "plan": {"F": F, "S": S}, "stage_dmma_flop": f_main + f_inv,
-                 "stage_tflops": (f_main + f_inv) / (iso_ms / 1e3) / 1e12,
-                 "stage_frac": (f_main + f_inv) / (iso_ms / 1e3) / 1e12 / peak,
-                 "direct_sum_flop_equiv": flops}
-        iso_k = prod_ms
-    elif args.cov == "fp64":
-        peak = extra["fp64_dgemm_tflops_burst"]
-        peak_src = "measured cuBLAS DGEMM 8192^3 on this pool's B200 (profiles/peaks_extra_r01.json)"
-        work, unit = flops, "TFLOP/s"
+        F, S_ = api.cov_spectral_plan(cfg.N, cfg.l, 2 * cfg.i - 1)
+        stage_cov = {"stage_ms": iso_ms, "plan": {"F": F, "S": S_}, "stage_dmma_flop": f_main + f_inv,
+                     "stage_tflops": (f_main + f_inv) / (iso_ms / 1e3) / 1e12,
+                     "stage_frac": (f_main + f_inv) / (iso_ms / 1e3) / 1e12 / dgemm,
+                     "direct_sum_flop_equiv": cov_flops(cfg)}
+        traffic = None
+        try:
+            nsum = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary_r01.json")))
+            mb = lambda d: d["value"] * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[d["unit"]]
+            traffic = mb(nsum["cross3m_kernel"]["dram__bytes_read.sum"]) + mb(nsum["cross3m_kernel"]["dram__bytes_write.sum"])
+        except Exception:
+            traffic = None
+        achieved = f_main / (prod_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": "cross3m_kernel (A1 cross-spectral product, FP64 DMMA, three real "
+                                              "products per complex one)",
+                "achieved": achieved, "peak": dgemm, "unit": "TFLOP/s", "frac": achieved / dgemm,
+                "traffic": traffic, "peak_source": "measured cuBLAS DGEMM 8192^3 burst on this pool's B200 "
+                                                   "(profiles/peaks_extra_r01.json); MEASURED_PEAKS.json has no FP64 entry",
+                "kernel_ms": prod_ms, "algorithmic_flop_per_launch": f_main,
+                "stage_ms_in_pipeline": cov_ms, "covariance_stage": stage_cov}
     else:
-        peak = 2.0 * peaks.get("bf16_tflops", 1644.3)
-        peak_src = "of measured: 2 x bf16 dense burst (MEASURED_PEAKS.json) = nominal int8:bf16 ratio"
-        work, unit = 8.0 * flops, "TOP/s"   # each multiply-add runs as eight int8 slice products
-    if args.cov != "spectral":
-        iso_k = iso_ms
-    achieved = work / (iso_k / 1e3) / 1e12
-    share = None
-    try:   # the covariance stage's share of one record's SM-time, from the committed ncu pass
-        src = {"int8x3": "smtime_r01.json", "spectral": "smtime_spectral_r01.json"}[args.cov]
-        sm = json.load(open(os.path.join(ROOT, "profiles", src)))
-        a1 = sm["stages"]["A1"]
+        flops = cov_flops(cfg)
+        if args.cov == "fp64":
+            peak, work, unit = dgemm, flops, "TFLOP/s"
+        else:
+            peak, work, unit = 2.0 * peaks.get("bf16_tflops", 1644.3), 8.0 * flops, "TOP/s"
+        achieved = work / (iso_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": f"covariance A1 ({args.cov})", "achieved": achieved, "peak": peak,
+                "unit": unit, "frac": achieved / peak, "traffic": None, "kernel_ms": iso_ms,
+                "algorithmic_flop_per_launch": work}
+    # whole record: the path's own algorithmic flops (record_flops) per ms_per_step against the
+    # sustained DGEMM peak (every stage is FP64 DMMA or FP64 ALU), and per stage (one record alone)
+    rf = record_flops(cfg, api) if args.cov == "spectral" and P.structured else None
+    if rf is not None:
+        tot = sum(rf.values())
+        roof["record"] = {"algorithmic_flop": tot, "flop_by_stage": rf,
+                          "achieved_tflops": tot / (ms / args.steps / 1e3) / 1e12 / world,
+                          "peak": dgemm_sus, "frac": tot / (ms / args.steps / 1e3) / 1e12 / world / dgemm_sus,
+                          "peak_source": "measured cuBLAS DGEMM sustained (profiles/peaks_extra_r01.json)"}
+        roof["stage_frac_alone"] = {
+            "A1": rf["A1"] / (stage["cov"] / 1e3) / 1e12 / dgemm,
+            "A2_A8": (rf["A4_A6_A7"] + rf["A5_A8"]) / (stage["rsvd"] / 1e3) / 1e12 / dgemm,
+            "A9_A11": rf["A9_A11"] / (stage["modal"] / 1e3) / 1e12 / FP64_ALU_TFLOPS,
+            "note": "one record alone on one stream (no overlap): latency-bound stages read low here; "
+                    "the 8-in-flight pipeline overlaps them (the record fraction above)"}
+    try:   # SM-time shares of one record's kernels, from the committed ncu pass
+        sm = json.load(open(os.path.join(ROOT, "profiles", "smtime_spectral_latest.json")))
         top = sorted(sm["kernels"].items(), key=lambda kv: -kv[1]["share_sm_time"])[:6]
-        share = {"stage_sm_time_share_of_record": a1["share_sm_time"],
-                 "stage_serial_share_of_record": a1["share_serial"],
-                 "top_kernels_sm_time_share": {k.split("(")[0].replace("ssi::<unnamed>::", ""):
-                                               round(v["share_sm_time"], 4) for k, v in top},
-                 "source": f"profiles/{src} (ncu sm__cycles_active.sum over one c3 record)"}
+        roof["sm_time_share"] = {"source": sm.get("source", "profiles/smtime_spectral_latest.json"),
+                                 "top_kernels": {k.split("(")[0].replace("ssi::<unnamed>::", ""):
+                                                 round(v["share_sm_time"], 4) for k, v in top}}
     except Exception:
-        share = None
-    kname = {"int8x3": "covariance A1 (int8x3: chan_max + slice + tcgen05 contraction + reduce)",
-             "fp64": "covariance A1 (fp64 DMMA)",
-             "spectral": "cross-spectral product of A1 (cross3m_kernel: FP64 DMMA, three real products per complex one)"}
-    roof = {"bound": "tensor", "step_share": share, "kernel": kname[args.cov],
-            "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak, "traffic": traffic,
-            "peak_source": peak_src, "kernel_ms": iso_k, "stage_ms_in_pipeline": cov_ms,
-            "algorithmic_flop_per_launch": work, "covariance_stage": stage}
+        pass
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline and world == 1:
-        tot, parts, sample = oracle_sample(cfg, host[0])
-        cpu = {"value": 1.0 / tot, "unit": UNIT, "cores": cores_used(), "kind": "oracle",
-               "sample": sample, "stage_s": parts}
+        rec = OracleRecord(cfg, host[0], 1)
+        tot = sum(rec.run(j) for j in range(len(rec)))
+        cpu = {"value": 1.0 / tot, "unit": UNIT, "cores": cores_used(), "cpu_model": cpu_model(), "kind": "oracle",
+               "sample": rec.describe(), "stage_s": {k: round(t, 3) for k, t in rec.stage_s.items()}}
+        cpu.update(cpu_extras(cfg, rec.cells))
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -441,6 +608,17 @@ def main():
                            "parallelism": f"records sharded over {world} GPU(s)"},
                 "stage_ms": stage, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": n_launch * args.steps, "clocks": clocks}
+        line.update(legs)
+        if args.workload != "c3" and legs:
+            # headline on another workload (manual runs): its unit of work per second
+            if args.workload == "c4":
+                lg = legs["lag_sweep_c4"]
+                line.update(metric="CoV-SSI 3D lag sweeps/sec (c4)", value=lg["sweeps_per_s"], unit="sweeps/s",
+                            ms_per_step=lg["ms_per_sweep"], scaling="strong")
+            else:
+                lg = legs["record_batch_c5"]
+                line.update(metric="CoV-SSI records/sec (c5 batch)", value=lg["records_per_s"], unit=UNIT,
+                            ms_per_step=lg["ms_per_batch"] / C5_RECORDS, scaling="strong")
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

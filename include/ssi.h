@@ -20,10 +20,22 @@
  *    NULL pointers / bad sizes -> SSI_ERR_INVALID_ARG, leading dimension too small ->
  *    SSI_ERR_SHAPE, unsupported dtype / mode -> SSI_ERR_DTYPE, workspace too small ->
  *    SSI_ERR_WORKSPACE, a failed launch -> SSI_ERR_CUDA (detail in ssi_last_error()).
- *  - Asynchronous numeric failures (Cholesky breakdown in CholeskyQR2 after its
- *    shifted retry, Jacobi or Francis-QR non-convergence, non-finite input) are
- *    recorded in a device status word at the start of `ws`; read it with
- *    ssi_fetch_device_status() after synchronizing the stream.
+ *  - Asynchronous numeric failures (a Cholesky breakdown that the shifted-CholeskyQR3
+ *    fallback below could not absorb, Jacobi or Francis-QR non-convergence, non-finite
+ *    input) are recorded in a device status word at the start of `ws` (its first 256 bytes
+ *    are a header). The word is STICKY: every call max-combines its failures into it and no
+ *    call clears it, so a workspace reused by many calls (a record pipeline, a lag sweep)
+ *    reports a failure of any of them; zero it once before first use (ssi_clear_status, or
+ *    zero the 256-byte header) and read it with ssi_fetch_device_status() after
+ *    synchronizing the stream.
+ *  - QR (CholeskyQR2, "qr(Y,0)") on a numerically rank-deficient panel
+ *    (e.g. a sketch width k above the rank of T): the first Cholesky of the Gram matrix
+ *    W = Y^T Y breaks down when a pivot falls below 64 k u times its diagonal entry; it is
+ *    then redone on W + s I, s = 11 (m k + k (k + 1)) u tr(W) (shifted CholeskyQR), and one
+ *    extra CholeskyQR pass runs before the usual second one (shifted CholeskyQR3). The
+ *    decision is taken on the device (conditional launches), so it costs no host
+ *    synchronisation; the status stays SSI_OK. Only a breakdown of the final pass, or a
+ *    non-finite Gram matrix, sets SSI_ERR_NUMERIC.
  *  - Determinism: fixed inputs, seed and launch configuration give bit-identical
  *    outputs run to run (fixed reduction orders, no floating-point atomics).
  */
@@ -104,6 +116,23 @@ SSI_API ssi_status ssi_covariances_ws(int64_t N, int32_t l, int32_t lag_lo, int3
  * 2 lp^2 (lag_hi - lag_lo + 1) (F + 2), lp = l rounded up to even. */
 SSI_API ssi_status ssi_cov_spectral_plan(int64_t N, int32_t l, int32_t lag_lo, int32_t lag_hi,
                                  int32_t* F, int64_t* S);
+/* A1 across time shards: in place R[k - lag_lo][a][b] /= (N - k), k = lag_lo .. lag_lo + n_lags - 1
+ * (reading A-6), turning the raw sums of time-sharded ssi_covariances(normalize = 0) calls,
+ * summed over the shards (e.g. one NCCL all-reduce across ranks), into the covariances of the
+ * whole N-sample record. R: [n_lags][l][l] FP64 device. Errors: lag_lo < 1, n_lags < 1, l < 1
+ * or lag_lo + n_lags - 1 >= N -> INVALID_ARG. */
+SSI_API ssi_status ssi_cov_normalize(double* R, int32_t l, int32_t lag_lo, int32_t n_lags, int64_t N,
+                                     void* stream);
+/* Measurement entry point of SSI_COV_SPECTRAL (not part of the method): runs the phases in the
+ * bit mask `phases` (1 = twiddle/weight tables + segment FFTs, 2 = cross-spectral product,
+ * 4 = inverse DFT at the lags) with the arguments of ssi_covariances. phases = 7 is
+ * ssi_covariances(cov_mode = SSI_COV_SPECTRAL); a partial mask re-runs those phases on the
+ * spectra an earlier full call left in the same workspace (bench.py times the product kernel
+ * alone this way). */
+SSI_API ssi_status ssi_cov_spectral_phases(const void* Y, int32_t dtype, int64_t N, int32_t l, int64_t ldY,
+                                           int32_t lag_lo, int32_t lag_hi, int64_t t_begin, int64_t t_end,
+                                           int32_t normalize, double* R, void* ws, size_t ws_bytes,
+                                           int32_t phases, void* stream);
 
 /* ------------------------------------------------------------------------------
  * A2. Block-Toeplitz matrix T_{1|i}, Eq. (6) (§2.1):
@@ -124,12 +153,15 @@ SSI_API ssi_status ssi_toeplitz(const double* R, int32_t l, int32_t i, double* T
  *   q times: Z = qr(T^T Q); Q = qr(T Z);
  *   B = Q^T T; small SVD B = U~ S V^T (CholeskyQR2 of B^T + one-sided Jacobi);
  *   U = Q U~.
- *  T : m x m row-major FP64, ldT >= m.   k : sketch width (n_max + p), 1 <= k <= m.
+ *  T : m x m row-major FP64, ldT >= m.   k : sketch width (n_max + p), 1 <= k <= min(m, 512)
+ *      (the small SVD runs on one thread-block cluster; larger k -> INVALID_ARG, synchronously).
  *  U : output m x n_keep col-major FP64 (leading left singular vectors), ldU >= m,
  *      1 <= n_keep <= k. Column signs are arbitrary (reading A-13).
  *  S : output [k] FP64, descending.
- *  Errors: k or n_keep out of range -> INVALID_ARG. CholeskyQR2 breakdown or Jacobi
- *  non-convergence -> SSI_ERR_NUMERIC in the device status word.
+ *  Errors: k or n_keep out of range -> INVALID_ARG. A rank-deficient sketch (k above the
+ *  numerical rank of T) is handled by the shifted-CholeskyQR3 fallback (see the conventions
+ *  above) and returns SSI_OK with S[j] ~ 0 beyond the rank. A final-pass Cholesky breakdown or
+ *  Jacobi non-convergence -> SSI_ERR_NUMERIC in the device status word.
  * ---------------------------------------------------------------------------- */
 SSI_API ssi_status ssi_rsvd(const double* T, int64_t ldT, int32_t m, int32_t k, int32_t q,
                     uint64_t seed, uint64_t stream_id, int32_t n_keep,
@@ -148,7 +180,7 @@ SSI_API ssi_status ssi_rsvd_ws(int32_t m, int32_t k, int32_t n_keep, size_t* byt
  * its block-Toeplitz structure"). Results equal ssi_rsvd's up to FP64 rounding order.
  *  R : [>= 2i-1][l][l] row-major FP64, R_k at block k-1 (ssi_covariances, lag_lo = 1).
  *  m = l*i; k, q, seed, stream_id, n_keep, U, ldU, S as in ssi_rsvd.
- *  Errors: as ssi_rsvd; i < 1 or l < 1 -> INVALID_ARG.
+ *  Errors: as ssi_rsvd (k <= min(l*i, 512)); i < 1 or l < 1 -> INVALID_ARG.
  * ---------------------------------------------------------------------------- */
 SSI_API ssi_status ssi_rsvd_toeplitz(const double* R, int32_t l, int32_t i, int32_t k, int32_t q,
                              uint64_t seed, uint64_t stream_id, int32_t n_keep,
@@ -227,6 +259,8 @@ SSI_API ssi_status ssi_stab3d(const ssi_pole_table* tables, int32_t n_lags, cons
 /* ------------------------------------------------------------------------------
  * Status helpers.
  * ---------------------------------------------------------------------------- */
+/* Zeroes the 256-byte header of ws (the sticky status word), enqueued on stream. */
+SSI_API ssi_status ssi_clear_status(void* ws, void* stream);
 /* Reads the device status word at the start of ws (synchronous copy; call after the
  * stream finished the work that used ws). */
 SSI_API ssi_status ssi_fetch_device_status(const void* ws, ssi_status* code);

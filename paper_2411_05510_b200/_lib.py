@@ -33,6 +33,8 @@ SIGNATURES = {
     "ssi_covariances": (I32, [P, I32, I64, I32, I64, I32, I32, I32, I64, I64, I32, P, P, SZ, P]),
     "ssi_covariances_ws": (I32, [I64, I32, I32, I32, I32, C.POINTER(SZ)]),
     "ssi_cov_spectral_plan": (I32, [I64, I32, I32, I32, C.POINTER(I32), C.POINTER(I64)]),
+    "ssi_cov_normalize": (I32, [P, I32, I32, I32, I64, P]),
+    "ssi_cov_spectral_phases": (I32, [P, I32, I64, I32, I64, I32, I32, I64, I64, I32, P, P, SZ, I32, P]),
     "ssi_toeplitz": (I32, [P, I32, I32, P, I64, P]),
     "ssi_rsvd": (I32, [P, I64, I32, I32, I32, U64, U64, I32, P, I64, P, P, SZ, P]),
     "ssi_rsvd_ws": (I32, [I32, I32, I32, C.POINTER(SZ)]),
@@ -44,6 +46,7 @@ SIGNATURES = {
     "ssi_modal_sweep_ws": (I32, [I32, I32, I32, I32, I32, C.POINTER(SZ)]),
     "ssi_stab3d": (I32, [C.POINTER(PoleTableC), I32, C.POINTER(CriteriaC), P, P, P]),
     "ssi_fetch_device_status": (I32, [P, C.POINTER(I32)]),
+    "ssi_clear_status": (I32, [P, P]),
     "ssi_status_string": (C.c_char_p, [I32]),
     "ssi_last_error": (C.c_char_p, []),
     "ssi_version": (C.c_char_p, []),

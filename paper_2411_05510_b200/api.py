@@ -38,7 +38,15 @@ def _require_cuda(*ts):
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
-    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+    """Workspace of nbytes with its status header cleared (the status word is sticky)."""
+    ws = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+    clear_status(ws)
+    return ws
+
+
+def clear_status(ws: torch.Tensor) -> None:
+    """Zero the sticky device status word of ws (ssi_clear_status), on the current stream."""
+    call("ssi_clear_status", _ptr(ws), _stream())
 
 
 def device_status(ws: torch.Tensor) -> int:
@@ -97,6 +105,29 @@ def covariances(Y: torch.Tensor, lag_hi: int, lag_lo: int = 1, mode: str = "fp64
          t_begin, t_end, 1 if normalize else 0, _ptr(R), _ptr(ws), ws.numel(), _stream())
     _check_device("ssi_covariances", ws, check)
     return R
+
+
+def cov_normalize(R: torch.Tensor, N: int, lag_lo: int = 1) -> torch.Tensor:
+    """In place R[k - lag_lo] /= (N - k) on the device (ssi_cov_normalize): the all-reduced raw sums
+    of time-sharded covariances(..., normalize=False) calls become the record's covariances."""
+    _require_cuda(R)
+    if R.dtype != torch.float64 or not R.is_contiguous() or R.dim() != 3:
+        raise ValueError("R must be contiguous FP64 [L][l][l]")
+    call("ssi_cov_normalize", _ptr(R), R.shape[1], lag_lo, R.shape[0], N, _stream())
+    return R
+
+
+def cov_spectral_phases(Y: torch.Tensor, lag_hi: int, phases: int, out: torch.Tensor, ws: torch.Tensor,
+                        lag_lo: int = 1) -> torch.Tensor:
+    """Measurement entry point (ssi_cov_spectral_phases): re-runs the SSI_COV_SPECTRAL phases in the
+    bit mask (1 FFT, 2 cross-spectral product, 4 inverse DFT) on the workspace of an earlier full
+    covariances(..., mode="spectral", ws=ws) call."""
+    _require_cuda(Y, out, ws)
+    dtype = {torch.float32: SSI_F32, torch.float64: SSI_F64}[Y.dtype]
+    N, l = Y.shape
+    call("ssi_cov_spectral_phases", _ptr(Y), dtype, N, l, Y.stride(0), lag_lo, lag_hi, 0, N, 1, _ptr(out),
+         _ptr(ws), ws.numel(), phases, _stream())
+    return out
 
 
 def toeplitz(R: torch.Tensor, i: int, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -263,12 +294,26 @@ def modal_sweep(U: torch.Tensor, S: torch.Tensor, l: int, i: int, n_min: int, n_
 
 @dataclass(frozen=True)
 class Criteria:
+    """Hard (xi_max, mpc_min, mpd_max; reading A-17) and soft (alpha_f, alpha_xi, alpha_mac;
+    readings A-18..A-21) stabilization criteria of ssi_stab3d. The default is the paper's 10-DOF
+    3D set; the presets below are the sets the paper states."""
     xi_max: float = 0.10
     mpc_min: float = 0.60
     mpd_max: float = 0.50
     alpha_f: float = 0.01
     alpha_xi: float = 0.03
     alpha_mac: float = 0.02
+
+
+# The paper's criteria sets (HC: xi > 10 %, MPC <= 60 %, MPD >= 50 % discarded everywhere).
+#  - 2D order-axis SC of the rank study (Fig. 3): 2 %, 2 %, 5 % (PAPER.md:356, §3.1.1)
+#  - 10-DOF 3D diagram: alpha_f, alpha_xi, alpha_MAC = 1 %, 3 %, 2 % (PAPER.md:402, §3.1.3)
+#  - San Faustino 2D continuous identification: 2 %, 3 %, 2 % (PAPER.md:518, §3.2.2)
+#  - San Faustino 3D diagram: 2.5 %, 5 %, 3 % (PAPER.md:541, §3.2.2)
+CRITERIA_2D_RANK_STUDY = Criteria(alpha_f=0.02, alpha_xi=0.02, alpha_mac=0.05)
+CRITERIA_10DOF_3D = Criteria(alpha_f=0.01, alpha_xi=0.03, alpha_mac=0.02)
+CRITERIA_BRIDGE_2D = Criteria(alpha_f=0.02, alpha_xi=0.03, alpha_mac=0.02)
+CRITERIA_BRIDGE_3D = Criteria(alpha_f=0.025, alpha_xi=0.05, alpha_mac=0.03)
 
 
 def stab3d(tables: list, crit: Criteria):

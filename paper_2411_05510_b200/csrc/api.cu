@@ -32,10 +32,6 @@ ssi_status launch_check(const char* what) {
 
 static cudaStream_t S(void* p) { return static_cast<cudaStream_t>(p); }
 
-static ssi_status reset_status(void* ws, cudaStream_t s) {
-  if (cudaMemsetAsync(ws, 0, kWsHeader, s) != cudaSuccess) return launch_check("status reset");
-  return SSI_OK;
-}
 
 static size_t cov_ws(int64_t N, int l, int lag_lo, int lag_hi, int mode, int64_t span) {
   Carver c(nullptr);
@@ -73,6 +69,12 @@ const char* ssi_status_string(ssi_status s) {
     case SSI_ERR_NUMERIC: return "numerical failure (CholeskyQR2 breakdown or non-convergence)";
     default: return "unknown status";
   }
+}
+
+ssi_status ssi_clear_status(void* ws, void* stream) {
+  SSI_REQUIRE(ws, SSI_ERR_INVALID_ARG, "ssi_clear_status: NULL ws");
+  if (cudaMemsetAsync(ws, 0, kWsHeader, S(stream)) != cudaSuccess) return launch_check("ssi_clear_status");
+  return SSI_OK;
 }
 
 ssi_status ssi_fetch_device_status(const void* ws, ssi_status* code) {
@@ -135,7 +137,6 @@ ssi_status ssi_covariances(const void* Y, int32_t dtype, int64_t N, int32_t l, i
   SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_covariances: workspace %zu < %zu",
               ws_bytes, need);
   cudaStream_t s = S(stream);
-  SSI_TRY(reset_status(ws, s));
   int32_t* st = static_cast<int32_t*>(ws);
   if (cov_mode == SSI_COV_FP64) {
     Carver c(ws);
@@ -146,6 +147,36 @@ ssi_status ssi_covariances(const void* Y, int32_t dtype, int64_t N, int32_t l, i
   if (cov_mode == SSI_COV_SPECTRAL)
     return cov_spectral(Y, dtype, N, l, ldY, lag_lo, lag_hi, t_begin, t_end, normalize, R, ws, st, s);
   return cov_i8(Y, dtype, N, l, ldY, lag_lo, lag_hi, t_begin, t_end, normalize, R, ws, st, s);
+}
+
+ssi_status ssi_cov_normalize(double* R, int32_t l, int32_t lag_lo, int32_t n_lags, int64_t N, void* stream) {
+  SSI_REQUIRE(R, SSI_ERR_INVALID_ARG, "ssi_cov_normalize: NULL R");
+  SSI_REQUIRE(l > 0 && lag_lo >= 1 && n_lags >= 1, SSI_ERR_INVALID_ARG, "ssi_cov_normalize: bad sizes");
+  SSI_REQUIRE(int64_t(lag_lo) + n_lags - 1 < N, SSI_ERR_INVALID_ARG,
+              "ssi_cov_normalize: record too short (N=%lld, lag %d)", (long long)N, lag_lo + n_lags - 1);
+  return cov_normalize(R, l, lag_lo, n_lags, N, S(stream));
+}
+
+ssi_status ssi_cov_spectral_phases(const void* Y, int32_t dtype, int64_t N, int32_t l, int64_t ldY,
+                                   int32_t lag_lo, int32_t lag_hi, int64_t t_begin, int64_t t_end,
+                                   int32_t normalize, double* R, void* ws, size_t ws_bytes, int32_t phases,
+                                   void* stream) {
+  SSI_REQUIRE(phases >= 1 && phases <= 7, SSI_ERR_INVALID_ARG, "ssi_cov_spectral_phases: phases must be 1..7");
+  SSI_REQUIRE(Y && R && ws, SSI_ERR_INVALID_ARG, "ssi_cov_spectral_phases: NULL pointer");
+  SSI_REQUIRE(N > 0 && l > 0 && lag_lo >= 1 && lag_hi >= lag_lo && lag_hi < N, SSI_ERR_INVALID_ARG,
+              "ssi_cov_spectral_phases: bad sizes");
+  SSI_REQUIRE(0 <= t_begin && t_begin <= t_end && t_end <= N, SSI_ERR_INVALID_ARG,
+              "ssi_cov_spectral_phases: bad time shard");
+  SSI_REQUIRE(!normalize || (t_begin == 0 && t_end == N), SSI_ERR_INVALID_ARG,
+              "ssi_cov_spectral_phases: normalize=1 requires the full record");
+  SSI_REQUIRE(ldY >= l, SSI_ERR_SHAPE, "ssi_cov_spectral_phases: ldY < l");
+  SSI_REQUIRE(dtype == SSI_F32 || dtype == SSI_F64, SSI_ERR_DTYPE, "ssi_cov_spectral_phases: bad dtype");
+  SSI_REQUIRE(cov_spec_supported(lag_hi), SSI_ERR_DTYPE, "ssi_cov_spectral_phases: lag_hi >= %d", kSpecMaxF);
+  const size_t need = cov_ws(N, l, lag_lo, lag_hi, SSI_COV_SPECTRAL, t_end - t_begin);
+  SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_cov_spectral_phases: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = S(stream);
+  return cov_spectral(Y, dtype, N, l, ldY, lag_lo, lag_hi, t_begin, t_end, normalize, R, ws,
+                      static_cast<int32_t*>(ws), s, phases);
 }
 
 ssi_status ssi_toeplitz(const double* R, int32_t l, int32_t i, double* T, int64_t ldT, void* stream) {
@@ -159,6 +190,7 @@ ssi_status ssi_rsvd_ws(int32_t m, int32_t k, int32_t n_keep, size_t* bytes) {
   SSI_REQUIRE(bytes, SSI_ERR_INVALID_ARG, "ssi_rsvd_ws: NULL bytes");
   SSI_REQUIRE(m > 0 && k >= 1 && k <= m && n_keep >= 1 && n_keep <= k, SSI_ERR_INVALID_ARG,
               "ssi_rsvd_ws: bad sizes");
+  SSI_REQUIRE(k <= kSvdMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd_ws: k = %d > %d unsupported", k, kSvdMaxK);
   *bytes = rsvd_ws_bytes(m, k);
   return SSI_OK;
 }
@@ -168,13 +200,13 @@ ssi_status ssi_rsvd(const double* T, int64_t ldT, int32_t m, int32_t k, int32_t 
                     void* ws, size_t ws_bytes, void* stream) {
   SSI_REQUIRE(T && U && S_ && ws, SSI_ERR_INVALID_ARG, "ssi_rsvd: NULL pointer");
   SSI_REQUIRE(m > 0 && k >= 1 && k <= m, SSI_ERR_INVALID_ARG, "ssi_rsvd: need 1 <= k <= m");
+  SSI_REQUIRE(k <= kSvdMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd: k = %d > %d unsupported", k, kSvdMaxK);
   SSI_REQUIRE(n_keep >= 1 && n_keep <= k, SSI_ERR_INVALID_ARG, "ssi_rsvd: need 1 <= n_keep <= k");
   SSI_REQUIRE(q >= 0, SSI_ERR_INVALID_ARG, "ssi_rsvd: q < 0");
   SSI_REQUIRE(ldT >= m && ldU >= m, SSI_ERR_SHAPE, "ssi_rsvd: ldT or ldU < m");
   const size_t need = rsvd_ws_bytes(m, k);
   SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_rsvd: workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = S(stream);
-  SSI_TRY(reset_status(ws, s));
   return rsvd_run(T, ldT, m, k, q, seed, stream_id, n_keep, U, ldU, S_, ws,
                   static_cast<int32_t*>(ws), s);
 }
@@ -183,6 +215,7 @@ ssi_status ssi_rsvd_toeplitz_ws(int32_t l, int32_t i, int32_t k, int32_t n_keep,
   SSI_REQUIRE(bytes, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz_ws: NULL bytes");
   SSI_REQUIRE(l > 0 && i > 0 && k >= 1 && int64_t(k) <= int64_t(l) * i && n_keep >= 1 && n_keep <= k,
               SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz_ws: bad sizes");
+  SSI_REQUIRE(k <= kSvdMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz_ws: k = %d > %d unsupported", k, kSvdMaxK);
   *bytes = rsvd_bt_ws_bytes(l, i, k);
   return SSI_OK;
 }
@@ -195,13 +228,13 @@ ssi_status ssi_rsvd_toeplitz(const double* R, int32_t l, int32_t i, int32_t k, i
   const int64_t m = int64_t(l) * i;
   SSI_REQUIRE(m <= INT32_MAX, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: l*i too large");
   SSI_REQUIRE(k >= 1 && k <= m, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: need 1 <= k <= l*i");
+  SSI_REQUIRE(k <= kSvdMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: k = %d > %d unsupported", k, kSvdMaxK);
   SSI_REQUIRE(n_keep >= 1 && n_keep <= k, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: need 1 <= n_keep <= k");
   SSI_REQUIRE(q >= 0, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: q < 0");
   SSI_REQUIRE(ldU >= m, SSI_ERR_SHAPE, "ssi_rsvd_toeplitz: ldU < l*i");
   const size_t need = rsvd_bt_ws_bytes(l, i, k);
   SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_rsvd_toeplitz: workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = S(stream);
-  SSI_TRY(reset_status(ws, s));
   return rsvd_bt_run(R, l, i, k, q, seed, stream_id, n_keep, U, ldU, S_, ws,
                      static_cast<int32_t*>(ws), s);
 }
@@ -230,6 +263,8 @@ ssi_status ssi_modal_sweep_ws(int32_t l, int32_t i, int32_t n_min, int32_t n_max
                               size_t* bytes) {
   SSI_REQUIRE(bytes && l > 0 && i >= 2, SSI_ERR_INVALID_ARG, "ssi_modal_sweep_ws: bad sizes");
   SSI_TRY(check_orders(n_min, n_max, n_step));
+  SSI_REQUIRE(modal_smem_bytes(n_max, n_max / 2) <= 227 * 1024, SSI_ERR_INVALID_ARG,
+              "ssi_modal_sweep_ws: n_max %d too large for the one-CTA eigen-solver", n_max);
   *bytes = modal_ws_bytes(l, i, n_min, n_max, n_step);
   return SSI_OK;
 }
@@ -255,7 +290,6 @@ ssi_status ssi_modal_sweep(const double* U, int64_t ldU, const double* S_, int32
   const size_t need = modal_ws_bytes(l, i, n_min, n_max, n_step);
   SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_modal_sweep: workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = S(stream);
-  SSI_TRY(reset_status(ws, s));
   return modal_run(U, ldU, S_, l, i, n_min, n_max, n_step, dt, *out, ws, static_cast<int32_t*>(ws), s);
 }
 

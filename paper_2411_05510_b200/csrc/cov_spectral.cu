@@ -475,17 +475,16 @@ bool cov_spec_supported(int lag_hi) { return lag_hi < kSpecMaxF; }
 
 ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY, int lag_lo, int lag_hi,
                         int64_t t_begin, int64_t t_end, int normalize, double* R, void* ws, int32_t* status,
-                        cudaStream_t s) {
+                        cudaStream_t s, int phases) {
   Carver c(ws);
   SpecBufs b;
   cov_spec_carve(c, N, t_end - t_begin, l, lag_lo, lag_hi, b);
   const SpecPlan p = spec_plan(N, t_end - t_begin, l, lag_lo, lag_hi);
   const int64_t nf = p.F / 2 + 1, lp2 = int64_t(p.lp) * p.lp;
-  // Measurement hook (bench.py times the product kernel alone with CUDA events): SSI_SPEC_PHASES
-  // = bit mask of 1 tables + FFT, 2 cross-spectral product, 4 inverse; default all. A partial
-  // mask re-runs phases on the spectra an earlier full call left in the same workspace.
-  const char* ph = getenv("SSI_SPEC_PHASES");
-  const int phases = ph ? atoi(ph) : 7;
+  // phases: bit mask of 1 tables + FFT, 2 cross-spectral product, 4 inverse. ssi_covariances
+  // always runs all three; the measurement entry point ssi_cov_spectral_phases re-runs a subset
+  // on the spectra an earlier full call left in the same workspace (bench.py times the product
+  // kernel alone that way).
   if (phases & 1) {
     const int64_t total = p.F + int64_t(p.F + 2) * p.n_lags;
     int blocks = int((total + 255) / 256);
@@ -514,8 +513,11 @@ ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY,
     }
     if (phases & 2) {
       // C_f (2lp x lp) (+)= A_f (2lp x 2 nseg) * B_f (2 nseg x lp); imaginary half to G + lp^2
-      static const bool stacked = getenv("SSI_SPEC_STACKED") != nullptr;   // A/B measurement only
-      if (stacked)
+#ifdef SSI_SPEC_STACKED   // complex-stacked single GEMM, kept for A/B measurement (SSI_NVCC_EXTRA)
+      if (true)
+#else
+      if (false)
+#endif
         SSI_TRY(gemm_tall_batched_brow(2 * p.lp, p.lp, 2 * nseg, b.A, p.lp, 2 * p.Sc * p.lp, b.Bs, p.lp,
                                        2 * p.Sc * p.lp, b.G, p.lp, 2 * lp2, int(nf), p.lp, lp2, s0 > 0, s));
       else

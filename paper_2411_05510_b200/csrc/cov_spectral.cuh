@@ -26,6 +26,6 @@ ssi_status cross_spectral_3m(const double* A, const double* B, int64_t sF, int64
                              double* G, bool accumulate, cudaStream_t s);
 ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY, int lag_lo, int lag_hi,
                         int64_t t_begin, int64_t t_end, int normalize, double* R, void* ws, int32_t* status,
-                        cudaStream_t s);
+                        cudaStream_t s, int phases = 7);
 
 }  // namespace ssi

@@ -166,6 +166,23 @@ ssi_status cov_fp64(const void* Y, int dtype, int64_t N, int l, int64_t ldY, int
   return launch_check("cov_finalize");
 }
 
+// R[k - lag_lo][a][b] /= (N - k) in place (reading A-6): the raw sums of time-sharded calls,
+// all-reduced over ranks, become the covariances of the whole record.
+__global__ void cov_normalize_kernel(double* __restrict__ R, int l, int lag_lo, int64_t n_lags, int64_t N) {
+  const int64_t per = int64_t(l) * l, total = n_lags * per;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x)
+    R[e] /= double(N - (lag_lo + e / per));
+}
+
+ssi_status cov_normalize(double* R, int l, int lag_lo, int n_lags, int64_t N, cudaStream_t s) {
+  const int64_t tot = int64_t(n_lags) * l * l;
+  int blocks = int((tot + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  cov_normalize_kernel<<<blocks, 256, 0, s>>>(R, l, lag_lo, n_lags, N);
+  return launch_check("cov_normalize_kernel");
+}
+
 size_t cov_fp64_partial_elems(int64_t span, int rows, int l) {
   return size_t(cov_fp64_splits(span, rows, l)) * size_t(rows) * size_t(l);
 }

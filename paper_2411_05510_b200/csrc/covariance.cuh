@@ -9,6 +9,8 @@ ssi_status cov_fp64(const void* Y, int dtype, int64_t N, int l, int64_t ldY, int
                     double* partial, int32_t* status, cudaStream_t s);
 size_t cov_fp64_partial_elems(int64_t span, int rows, int l);
 int cov_fp64_splits(int64_t span, int rows, int l);
+// In-place R[k - lag_lo] /= (N - k) for k = lag_lo .. lag_lo + n_lags - 1.
+ssi_status cov_normalize(double* R, int l, int lag_lo, int n_lags, int64_t N, cudaStream_t s);
 
 // Toeplitz assembly (A2).
 ssi_status toeplitz_launch(const double* R, int l, int i, double* T, int64_t ldT, cudaStream_t s);

@@ -118,8 +118,9 @@ __device__ __forceinline__ void store_acc(const double (&acc)[4][4][2], int64_t 
 template <bool AKC, bool BKC>
 __global__ void __launch_bounds__(NT) gemm_kernel(int64_t M, int64_t N, int64_t K, double alpha,
                                                   Operand A, Operand B, double* C, int64_t ldc,
-                                                  int64_t kchunk, double* partial) {
+                                                  int64_t kchunk, double* partial, const int* run_if) {
   __shared__ __align__(16) double smem[4 * BK * LDS];
+  if (!run_enabled(run_if)) return;
   const int64_t m0 = int64_t(blockIdx.x) * BM, n0 = int64_t(blockIdx.y) * BN;
   TileArgs t{M, N, int64_t(blockIdx.z) * kchunk, 0, A, B};
   t.ke = t.kb + kchunk < K ? t.kb + kchunk : K;
@@ -132,7 +133,8 @@ __global__ void __launch_bounds__(NT) gemm_kernel(int64_t M, int64_t N, int64_t 
 }
 
 __global__ void splitk_reduce(int64_t M, int64_t N, int splits, const double* __restrict__ part,
-                              double alpha, double* __restrict__ C, int64_t ldc) {
+                              double alpha, double* __restrict__ C, int64_t ldc, const int* run_if) {
+  if (!run_enabled(run_if)) return;
   const int64_t total = M * N;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
        e += int64_t(gridDim.x) * blockDim.x) {
@@ -179,7 +181,7 @@ size_t gemm_partial_elems(int64_t M, int64_t N, int splits) {
 }
 
 ssi_status gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, Operand A, Operand B,
-                    double* C, int64_t ldc, int splits, double* partial, cudaStream_t s) {
+                    double* C, int64_t ldc, int splits, double* partial, cudaStream_t s, const int* run_if) {
   if (M <= 0 || N <= 0) return SSI_OK;
   const bool akc = (A.s_c == 1), bkc = (B.s_r == 1);
   if (splits < 1) splits = 1;
@@ -189,16 +191,16 @@ ssi_status gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, Operand A, Op
   const int z = int((K + kchunk - 1) / kchunk > 0 ? (K + kchunk - 1) / kchunk : 1);
   double* part = (z > 1) ? partial : nullptr;
   dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, z);
-  if (akc && bkc) gemm_kernel<true, true><<<grid, NT, 0, s>>>(M, N, K, alpha, A, B, C, ldc, kchunk, part);
-  else if (akc)   gemm_kernel<true, false><<<grid, NT, 0, s>>>(M, N, K, alpha, A, B, C, ldc, kchunk, part);
-  else if (bkc)   gemm_kernel<false, true><<<grid, NT, 0, s>>>(M, N, K, alpha, A, B, C, ldc, kchunk, part);
-  else            gemm_kernel<false, false><<<grid, NT, 0, s>>>(M, N, K, alpha, A, B, C, ldc, kchunk, part);
+  if (akc && bkc) gemm_kernel<true, true><<<grid, NT, 0, s>>>(M, N, K, alpha, A, B, C, ldc, kchunk, part, run_if);
+  else if (akc)   gemm_kernel<true, false><<<grid, NT, 0, s>>>(M, N, K, alpha, A, B, C, ldc, kchunk, part, run_if);
+  else if (bkc)   gemm_kernel<false, true><<<grid, NT, 0, s>>>(M, N, K, alpha, A, B, C, ldc, kchunk, part, run_if);
+  else            gemm_kernel<false, false><<<grid, NT, 0, s>>>(M, N, K, alpha, A, B, C, ldc, kchunk, part, run_if);
   SSI_TRY(launch_check("gemm_f64"));
   if (z > 1) {
     const int64_t tot = M * N;
     int blocks = int((tot + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    splitk_reduce<<<blocks, 256, 0, s>>>(M, N, z, partial, alpha, C, ldc);
+    splitk_reduce<<<blocks, 256, 0, s>>>(M, N, z, partial, alpha, C, ldc, run_if);
     SSI_TRY(launch_check("splitk_reduce"));
   }
   return SSI_OK;

@@ -13,12 +13,20 @@ struct Operand {
   int64_t s_r, s_c;
 };
 
+// Conditional launches: a kernel given run_if != nullptr returns at once unless *run_if != 0
+// (a device flag written by an earlier kernel on the same stream; used by the CholeskyQR
+// breakdown fallback, whose extra pass must not cost a host synchronisation).
+__device__ __forceinline__ bool run_enabled(const int* run_if) {
+  return run_if == nullptr || *reinterpret_cast<const volatile int*>(run_if) != 0;
+}
+
 // C (M x N, col-major, ldc) = alpha * A (M x K) * B (K x N).
 // A is "k-contiguous" when s_c == 1 (row-major), otherwise s_r must be 1 (col-major);
 // likewise B is k-contiguous when s_r == 1. splits > 1 partitions K, writes partials to
 // `partial` ([splits][M*N]) and reduces them in fixed order (deterministic).
 ssi_status gemm_f64(int64_t M, int64_t N, int64_t K, double alpha, Operand A, Operand B,
-                    double* C, int64_t ldc, int splits, double* partial, cudaStream_t s);
+                    double* C, int64_t ldc, int splits, double* partial, cudaStream_t s,
+                    const int* run_if = nullptr);
 
 // Heuristic split count so that tiles*splits fills the 148 SMs a few times over.
 int gemm_pick_splits(int64_t M, int64_t N, int64_t K);
@@ -47,11 +55,12 @@ constexpr int kTallMaxN = 224;
 // A[i*lda + k]); the strictly-upper off-diagonal tiles of C are not written. partial: at least
 // 64 n^2 doubles (split-K slabs).
 ssi_status gemm_tall_syrk_lower(int64_t n, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
-                                double* C, int64_t ldc, double* partial, cudaStream_t s);
+                                double* C, int64_t ldc, double* partial, cudaStream_t s,
+                                const int* run_if = nullptr);
 // C (M x N) = A (M x K, col-major) B (K x N, col-major upper triangular, K == N): the N tile at
 // j0 reads only K rows [0, j0 + 64).
 ssi_status gemm_tall_triu(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
-                          int64_t ldb, double* C, int64_t ldc, cudaStream_t s);
+                          int64_t ldb, double* C, int64_t ldc, cudaStream_t s, const int* run_if = nullptr);
 ssi_status gemm_tall_batched(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
                              int64_t sA, const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
                              int64_t sC, int batch, cudaStream_t s);

@@ -72,6 +72,7 @@ struct TallArgs {
                         // blockIdx.z only needs K rows [0, n0 + TBN))
   int64_t rsplit, roff; // rsplit > 0: output rows r >= rsplit go to (r - rsplit) + c*ldo + roff
   int accum;            // 1: out += product (chunked K, fixed order); 0: out = product
+  const int* run_if;    // conditional launch (run_enabled), nullptr = always
 };
 
 template <bool AROW, bool BROW, int TBN, bool CST = false>
@@ -124,6 +125,7 @@ __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
   constexpr int NJ = WN / 8;           // m8n8k4 tiles per warp along N
   constexpr int STAGE_ELEMS = stage_elems<AROW, BROW, TBN>();
   extern __shared__ __align__(16) double sm[];
+  if (!run_enabled(g.run_if)) return;
   int64_t m0 = int64_t(blockIdx.x) * BM, n0 = 0;
   double* out = g.out + int64_t(blockIdx.y) * g.M * g.N;   // split-K slab (or C)
   if (g.mode == 0) {
@@ -217,7 +219,8 @@ __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
 }
 
 __global__ void tall_reduce(int64_t M, int64_t N, int splits, const double* __restrict__ part, double* __restrict__ C,
-                            int64_t ldc) {
+                            int64_t ldc, const int* run_if = nullptr) {
+  if (!run_enabled(run_if)) return;
   const int64_t total = M * N;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
     double s = 0.0;
@@ -329,7 +332,7 @@ ssi_status gemm_tall(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const dou
 // C (n x n, col-major, ldc) lower triangle (64 x 64 tiles on and below the diagonal) of
 // op(A) (n x K) * B (K x n); split-K over whole waves with a fixed-order reduction.
 ssi_status gemm_tall_syrk_lower(int64_t n, int64_t K, const double* A, int64_t lda, const double* B, int64_t ldb,
-                                double* C, int64_t ldc, double* partial, cudaStream_t s) {
+                                double* C, int64_t ldc, double* partial, cudaStream_t s, const int* run_if) {
   const int nt = int((n + BM - 1) / BM);
   const int tiles = nt * (nt + 1) / 2;
   int splits = 1;
@@ -341,7 +344,7 @@ ssi_status gemm_tall_syrk_lower(int64_t n, int64_t K, const double* A, int64_t l
   int64_t kchunk = (K + splits - 1) / splits;
   kchunk = (kchunk + BK - 1) / BK * BK;
   const int z = int((K + kchunk - 1) / kchunk);
-  TallArgs g{n, n, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? n : ldc, kchunk, 0, 0, 0, 1};
+  TallArgs g{n, n, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? n : ldc, kchunk, 0, 0, 0, 1, 0, 0, 0, run_if};
   {
     const ssi_status st = launch_one<true, 64, false, false, TALL64_ST, TALL64_MINB>(dim3(unsigned(tiles), unsigned(z)), g, s);
     if (st != SSI_OK) return st;
@@ -350,7 +353,7 @@ ssi_status gemm_tall_syrk_lower(int64_t n, int64_t K, const double* A, int64_t l
     const int64_t tot = n * n;
     int blocks = int((tot + 255) / 256);
     if (blocks > 148 * 8) blocks = 148 * 8;
-    tall_reduce<<<blocks, 256, 0, s>>>(n, n, z, partial, C, ldc);
+    tall_reduce<<<blocks, 256, 0, s>>>(n, n, z, partial, C, ldc, run_if);
     SSI_TRY(launch_check("tall_reduce"));
   }
   return SSI_OK;
@@ -359,9 +362,9 @@ ssi_status gemm_tall_syrk_lower(int64_t n, int64_t K, const double* A, int64_t l
 // C (M x N, col-major) = A (M x K, col-major) * B (K x N, col-major, upper triangular: B(k, j) = 0
 // for k > j): N tiles of 64, tile j0 reads only K rows [0, j0 + 64); no split-K.
 ssi_status gemm_tall_triu(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
-                          int64_t ldb, double* C, int64_t ldc, cudaStream_t s) {
+                          int64_t ldb, double* C, int64_t ldc, cudaStream_t s, const int* run_if) {
   const int64_t kchunk = (K + BK - 1) / BK * BK;
-  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, 0, 0, 0, 2};
+  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, 0, 0, 0, 2, 0, 0, 0, run_if};
   return launch_one<false, 64, false, false, TALL64_ST, TALL64_MINB>(dim3(unsigned((M + BM - 1) / BM), 1u, unsigned((N + 63) / 64)), g, s);
 }
 

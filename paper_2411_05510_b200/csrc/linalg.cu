@@ -9,118 +9,18 @@
 namespace ssi {
 namespace {
 
-constexpr int kCholThreads = 512;
 constexpr int kJacThreads = 512;
 constexpr int JC = 8;                // Jacobi cluster size (CTAs); 16 (non-portable) for k > 256
 constexpr int kJacMaxSweeps = 60;
 
-
-// W (k x k col-major, lower part read) -> L (lower) and Linv = L^{-1} (lower), both
-// col-major ld k with zeros above the diagonal. Packed row-major lower triangle P
-// (P[i(i+1)/2 + c], c <= i) in shared memory when it fits, else in gscratch.
-// Inverse: row i of X = L^{-1} overwrites row i of L; the dot products over p are split
-// into kGroups interleaved chunks (independent accumulators, unrolled) and reduced
-// through shared memory, so the per-row chain is short instead of k-long.
-constexpr int kGroups = 4;
-
-__global__ void __launch_bounds__(kCholThreads) chol_inv_kernel(const double* __restrict__ W, int k,
-                                                                double* __restrict__ L,
-                                                                double* __restrict__ Linv,
-                                                                double* __restrict__ LinvT,
-                                                                double* gscratch, int use_smem,
-                                                                int32_t* status) {
-  extern __shared__ __align__(16) double sm[];
-  double* vec = sm;                          // k: scaled column j / row i of L
-  double* part = sm + k;                     // kGroups * k partial sums
-  double* P = use_smem ? sm + k + kGroups * k : gscratch;
-  __shared__ int fail;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-  if (tid == 0) fail = 0;
-  for (int i = warp; i < k; i += nw) {
-    const int b = i * (i + 1) / 2;
-    for (int c = lane; c <= i; c += 32) P[b + c] = W[i + int64_t(c) * k];
-  }
-  __syncthreads();
-  // Right-looking Cholesky, column by column.
-  for (int j = 0; j < k; ++j) {
-    const int bj = j * (j + 1) / 2;
-    if (tid == 0) {
-      const double d = P[bj + j];
-      if (!(d > 0.0) || !isfinite(d)) { fail = 1; P[bj + j] = 1.0; }
-      else P[bj + j] = sqrt(d);
-    }
-    __syncthreads();
-    const double djj = P[bj + j];
-    for (int i = j + 1 + tid; i < k; i += nt) {
-      const double v = P[i * (i + 1) / 2 + j] / djj;
-      P[i * (i + 1) / 2 + j] = v;
-      vec[i] = v;
-    }
-    __syncthreads();
-    for (int i = j + 1 + warp; i < k; i += nw) {   // trailing update, warp per row
-      const double li = vec[i];
-      double* row = P + i * (i + 1) / 2;
-      for (int c = j + 1 + lane; c <= i; c += 32) row[c] -= li * vec[c];
-    }
-    __syncthreads();
-  }
-  if (fail) set_status(status, SSI_ERR_NUMERIC);
-  for (int64_t e = tid; e < int64_t(k) * k; e += nt) {
-    const int r = int(e % k), c = int(e / k);
-    L[e] = (c <= r) ? P[r * (r + 1) / 2 + c] : 0.0;
-  }
-  __syncthreads();
-  //   X[i][j] = (delta_ij - sum_{p=j}^{i-1} L[i][p] X[p][j]) / L[i][i]
-  const int g = tid / (nt / kGroups);           // p-chunk of this thread
-  const int jt = tid % (nt / kGroups);
-  const int jstride = nt / kGroups;
-  for (int i = 0; i < k; ++i) {
-    const int bi = i * (i + 1) / 2;
-    for (int p = tid; p <= i; p += nt) vec[p] = P[bi + p];
-    __syncthreads();
-    for (int j = jt; j < i; j += jstride) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int p = j + g;
-      int bp = p * (p + 1) / 2;                  // tri(p), advanced incrementally
-      for (; p + 3 * kGroups < i; p += 4 * kGroups) {
-        const int b1 = bp + (p + 1) + (p + 2) + (p + 3) + (p + 4);          // tri(p+4)
-        const int b2 = b1 + (p + 5) + (p + 6) + (p + 7) + (p + 8);          // tri(p+8)
-        const int b3 = b2 + (p + 9) + (p + 10) + (p + 11) + (p + 12);       // tri(p+12)
-        a0 += vec[p] * P[bp + j];
-        a1 += vec[p + 4] * P[b1 + j];
-        a2 += vec[p + 8] * P[b2 + j];
-        a3 += vec[p + 12] * P[b3 + j];
-        bp = b3 + (p + 13) + (p + 14) + (p + 15) + (p + 16);
-      }
-      for (; p < i; p += kGroups) {
-        a0 += vec[p] * P[bp + j];
-        bp += (p + 1) + (p + 2) + (p + 3) + (p + 4);
-      }
-      part[g * k + j] = (a0 + a1) + (a2 + a3);
-    }
-    __syncthreads();
-    const double lii = vec[i];
-    for (int j = tid; j <= i; j += nt) {
-      double s = (j == i) ? 1.0 : 0.0;
-      if (j < i) s -= (part[j] + part[k + j]) + (part[2 * k + j] + part[3 * k + j]);
-      P[bi + j] = s / lii;
-    }
-    __syncthreads();
-  }
-  for (int64_t e = tid; e < int64_t(k) * k; e += nt) {
-    const int r = int(e % k), c = int(e / k);
-    Linv[e] = (c <= r) ? P[r * (r + 1) / 2 + c] : 0.0;
-    if (LinvT) LinvT[e] = (r <= c) ? P[c * (c + 1) / 2 + r] : 0.0;
-  }
-}
 
 // Blocked variant (k <= 224): 32-wide block columns; the diagonal block is factored and
 // inverted by one warp in registers (shuffles, no barriers), the panel below is L_IJ = A_IJ L_JJ^-T
 // (one thread per row), the trailing lower triangle gets a rank-32 update in 4 x 4 register
 // tiles; three barriers per block column instead of three per column. The inverse is then
 // formed by block rows, X_IJ = -X_II sum_{K=J}^{I-1} L_IK X_KJ (one thread per column of X_IJ),
-// into a kp x kp col-major scratch (kp = k rounded up to 32; the padding is an identity block).
+// (kp = k rounded up to 32; the padding is an identity block). The nb diagonal-block inverses are
+// cached in the scratch X (nb CB x (CB + 1) blocks; for k > 224 the packed triangle follows them).
 constexpr int CB = 32;
 constexpr int kCholBlkMax = 224;    // packed triangle in shared memory
 constexpr int kCholBlkGMax = 512;   // packed triangle in the L2-resident scratch
@@ -133,7 +33,9 @@ __device__ __forceinline__ int tri(int r) { return r * (r + 1) / 2; }
 // of the packed P (lane i holds row i; every index is a compile-time constant, so the row stays
 // in registers): per column one shuffle of the pivot, an inline rsqrt, and the rank-1 update
 // with the column entries broadcast lane to lane.
-__device__ __noinline__ void chol32(double* P, int j0, int lane, int& bad) {
+// Breakdown test: pivot j must exceed thr_j = tau * (diagonal of the Gram matrix at row j), lane j
+// holding thr_j; a smaller pivot means column j is numerically in the span of the previous ones.
+__device__ __noinline__ void chol32(double* P, int j0, int lane, double thr, int& bad) {
   double* Li = P + tri(j0 + lane) + j0;
   double a[CB];
 #pragma unroll
@@ -141,7 +43,8 @@ __device__ __noinline__ void chol32(double* P, int j0, int lane, int& bad) {
 #pragma unroll
   for (int j = 0; j < CB; ++j) {
     double d = __shfl_sync(FULLM, a[j], j);
-    if (!(d > 0.0) || !isfinite(d)) { bad = 1; d = 1.0; }
+    const double tj = __shfl_sync(FULLM, thr, j);
+    if (!(d > tj) || !isfinite(d)) { bad = 1; d = 1.0; }
     const double r = fast_rsqrt(d);
     a[j] = (lane == j) ? d * r : a[j] * r;          // lanes < j hold 0 in a[j]
 #pragma unroll
@@ -185,13 +88,24 @@ __device__ __noinline__ void inv32(const double* P, int j0, double* Xd, int lane
 // fit shared memory and lives in the L2-resident scratch instead (X + the diagonal-inverse
 // cache); the algorithm is the same, and each thread forms up to two columns of a block row
 // of the inverse (block rows are up to kp - 32 = 480 columns wide).
+//
+// Breakdown fallback (shifted CholeskyQR, Fukaya et al.'s shift): when a pivot fails the relative
+// test of chol32 (tau = 64 k u of the row's Gram diagonal, i.e. Y is numerically rank-deficient or
+// kappa(Y) >~ 1e6), the factorization restarts once on W + s I with s = 11 (m k + k (k + 1)) u tr(W),
+// which always factors; *shifted_out = 1 then tells cholqr2 to run its extra (third) pass. A
+// failure of the shifted attempt (non-finite input), or any shift in the final pass of a QR
+// (final != 0), sets SSI_ERR_NUMERIC.
 template <bool GLOBALP>
 __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const double* __restrict__ W, int k,
+                                                                   int64_t m,
                                                                    double* __restrict__ L,
                                                                    double* __restrict__ Linv,
                                                                    double* __restrict__ LinvT,
-                                                                   double* __restrict__ X,   // kp x kp scratch
-                                                                   int32_t* status, int profile) {
+                                                                   double* __restrict__ X,   // diagonal-inverse cache (+ packed triangle)
+                                                                   int32_t* status, int profile,
+                                                                   const int* run_if, int* shifted_out,
+                                                                   int final) {
+  if (!run_enabled(run_if)) return;
   long long tdiag = 0, tpanel = 0, ttrail = 0, tinv = 0, t0c = clock64(), tc;
   extern __shared__ __align__(16) double sm[];
   const int kp = (k + CB - 1) / CB * CB, nb = kp / CB;
@@ -206,19 +120,25 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
   // inverse; both fit in (kp - CB) (CB + 1) doubles
   double* Ps = GLOBALP ? sm + CB * (CB + 1) : nullptr;
   __shared__ int fail;
+  __shared__ double shift;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  const double tau = 64.0 * double(k) * 1.1102230246251565e-16;
+  int attempt = 0;
+  for (;; ++attempt) {
+  const double sh = attempt ? shift : 0.0;
   if (tid == 0) fail = 0;
   for (int i = warp; i < kp; i += nw)
     for (int c = lane; c <= i; c += 32)
-      P[tri(i) + c] = (i < k) ? W[i + int64_t(c) * k] : (i == c ? 1.0 : 0.0);
+      P[tri(i) + c] = (i < k) ? W[i + int64_t(c) * k] + (i == c ? sh : 0.0) : (i == c ? 1.0 : 0.0);
   __syncthreads();
   // ---------------- factorization
   for (int J = 0; J < nb; ++J) {
     const int j0 = J * CB;
     if (warp == 0) {
       int bad = 0;
-      chol32(P, j0, lane, bad);
+      const int r = j0 + lane;
+      chol32(P, j0, lane, tau * (r < k ? W[r + int64_t(r) * k] + sh : 1.0), bad);
       if (bad && lane == 0) fail = 1;
       inv32(P, j0, Xd, lane);
       // keep L_JJ^{-1} for the inverse phase (L2-resident scratch; saves recomputing it)
@@ -288,7 +208,19 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
     __syncthreads();
     tc = clock64(); ttrail += tc - t0c; t0c = tc;
   }
-  if (fail && tid == 0) set_status(status, SSI_ERR_NUMERIC);
+  if (!fail || attempt == 1) break;               // fail is read after the loop's last barrier
+  if (warp == 0) {                                // s = 11 (m k + k (k + 1)) u tr(W)
+    double t = 0.0;
+    for (int c = lane; c < k; c += 32) t += W[c + int64_t(c) * k];
+    t = warp_sum(t);
+    if (lane == 0) shift = 11.0 * (double(m) * k + double(k) * (k + 1)) * 1.1102230246251565e-16 * t;
+  }
+  __syncthreads();
+  }
+  if (tid == 0) {
+    if (shifted_out) *shifted_out = attempt;
+    if (fail || (final && attempt)) set_status(status, SSI_ERR_NUMERIC);
+  }
   // L out (col-major k x k, zeros above the diagonal) before P is overwritten by the inverse
   for (int64_t e = tid; e < int64_t(k) * k; e += nt) {
     const int r = int(e % k), c = int(e / k);
@@ -497,10 +429,16 @@ void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w) {
   w.Linv2 = c.take<double>(size_t(k) * k);
   w.LinvT1 = c.take<double>(size_t(k) * k);
   w.LinvT2 = c.take<double>(size_t(k) * k);
+  w.Lb = c.take<double>(size_t(k) * k);
+  w.Linvb = c.take<double>(size_t(k) * k);
+  w.LinvTb = c.take<double>(size_t(k) * k);
+  w.flag = c.take<int>(1);
   w.Q1 = c.take<double>(size_t(m) * k);
   const size_t kp = size_t(k + 31) / 32 * 32;
   const size_t nbk = kp / 32;
-  w.chol_g = c.take<double>(k <= kCholBlkMax ? kp * kp
+  // k <= kCholBlkMax: chol_blk_kernel<false> keeps the packed triangle in shared memory and
+  // caches the nb diagonal-block inverses (CB x (CB + 1) each) here
+  w.chol_g = c.take<double>(k <= kCholBlkMax ? nbk * 32 * 33
                             : k <= kCholBlkGMax ? nbk * 32 * 33 + kp * (kp + 1) / 2 + 32 * kp
                                                 : size_t(k) * (k + 1) / 2);
   w.partial = c.take<double>(cholqr_partial_elems(m, k) + 1);
@@ -510,59 +448,107 @@ void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w) {
   w.tallp = c.take<double>((t1 > t2 ? t1 : t2) + 1);
 }
 
-static size_t chol_smem_bytes(int k) {
-  return (size_t(k) * (1 + kGroups) + size_t(k) * (k + 1) / 2) * sizeof(double);
-}
-
-ssi_status chol_inv(const double* W, int k, double* L, double* Linv, double* LinvT, double* gscratch,
-                    int32_t* status, cudaStream_t s) {
+ssi_status chol_inv(const double* W, int k, int64_t m, double* L, double* Linv, double* LinvT, double* gscratch,
+                    int32_t* status, cudaStream_t s, const int* run_if, int* shifted_out, int final) {
+  static const int profile = getenv("SSI_CHOL_PROFILE") ? 1 : 0;
+  const int kp = (k + CB - 1) / CB * CB;
   if (k <= kCholBlkMax) {
-    const int kp = (k + CB - 1) / CB * CB;
     const size_t smem = (size_t(kp) * (kp + 1) / 2 + size_t(CB) * (CB + 1)) * sizeof(double);
     cudaFuncSetAttribute(chol_blk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    static const int profile = getenv("SSI_CHOL_PROFILE") ? 1 : 0;
-    chol_blk_kernel<false><<<1, kCholBlkThreads, smem, s>>>(W, k, L, Linv, LinvT, gscratch, status, profile);
+    chol_blk_kernel<false><<<1, kCholBlkThreads, smem, s>>>(W, k, m, L, Linv, LinvT, gscratch, status, profile,
+                                                           run_if, shifted_out, final);
     return launch_check("chol_blk_kernel");
   }
   if (k <= kCholBlkGMax) {
-    const int kp = (k + CB - 1) / CB * CB;
     const size_t smem = (size_t(CB) * (CB + 1) + size_t(kp - CB) * (CB + 1)) * sizeof(double);
     cudaFuncSetAttribute(chol_blk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    static const int profile = getenv("SSI_CHOL_PROFILE") ? 1 : 0;
-    chol_blk_kernel<true><<<1, kCholBlkThreads, smem, s>>>(W, k, L, Linv, LinvT, gscratch, status, profile);
+    chol_blk_kernel<true><<<1, kCholBlkThreads, smem, s>>>(W, k, m, L, Linv, LinvT, gscratch, status, profile,
+                                                          run_if, shifted_out, final);
     return launch_check("chol_blk_kernel");
   }
-  const size_t smem_full = chol_smem_bytes(k);
-  const bool use_smem = smem_full <= 220 * 1024;
-  const size_t smem = use_smem ? smem_full : size_t(k) * (1 + kGroups) * sizeof(double);
-  if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  }
-  chol_inv_kernel<<<1, kCholThreads, smem, s>>>(W, k, L, Linv, LinvT, gscratch, use_smem ? 1 : 0, status);
-  return launch_check("chol_inv_kernel");
+  set_last_error("chol_inv: k = %d > %d unsupported", k, kCholBlkGMax);
+  return SSI_ERR_INVALID_ARG;
 }
 
+namespace {
+// Q1 <- Q (m x k, both ld m) when *run_if (the extra pass of the breakdown fallback wrote Q).
+__global__ void cq_copy_kernel(const int* run_if, int64_t n, const double* __restrict__ src, double* __restrict__ dst) {
+  if (!run_enabled(run_if)) return;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+    dst[e] = src[e];
+}
+
+// After a fallback QR, Y = Q L2^T Lb^T L1^T: fold the extra pass's factor into the second one so
+// R^T = L1 L2 and R^{-1} = Linv1^T Linv2^T keep holding for the callers:
+//   L2 <- Lb L2 (CTA c < k: column c, which only reads column c of L2), and
+//   Linv2 <- Linv2 Linvb (CTA k + r: row r, which only reads row r of Linv2);
+// each CTA forms its whole column / row before writing it back, so the update is in place.
+__global__ void cq_fold_kernel(const int* run_if, int k, const double* __restrict__ Lb,
+                               const double* __restrict__ Linvb, double* L2, double* Linv2) {
+  if (!run_enabled(run_if)) return;
+  extern __shared__ double v[];
+  const int b = blockIdx.x;
+  if (b < k) {
+    const int c = b;
+    for (int r = threadIdx.x; r < k; r += blockDim.x) {
+      double a = 0.0;
+      for (int p = c; p <= r; ++p) a = fma(Lb[r + int64_t(p) * k], L2[p + int64_t(c) * k], a);
+      v[r] = a;
+    }
+    __syncthreads();
+    for (int r = c + threadIdx.x; r < k; r += blockDim.x) L2[r + int64_t(c) * k] = v[r];
+  } else {
+    const int r = b - k;
+    for (int c = threadIdx.x; c <= r; c += blockDim.x) {
+      double a = 0.0;
+      for (int p = c; p <= r; ++p) a = fma(Linv2[r + int64_t(p) * k], Linvb[p + int64_t(c) * k], a);
+      v[c] = a;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c <= r; c += blockDim.x) Linv2[r + int64_t(c) * k] = v[c];
+  }
+}
+}  // namespace
+
+// CholeskyQR2 with the shifted-CholeskyQR3 fallback: pass 1 (shift on breakdown) -> [extra pass,
+// launched always, run only when pass 1 shifted] -> pass 2. The conditional launches read a
+// device flag, so a healthy QR costs no host synchronisation and no arithmetic for the fallback.
 ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, CholQRWork& w,
                    int32_t* status, cudaStream_t s) {
   // tall-skinny DMMA kernels (cp.async 16-byte pieces) when the shapes and alignment allow
   const bool tall = k <= kTallMaxN && ldy % 2 == 0 && m % 2 == 0 && k % 2 == 0 &&
                     (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0;
   const int splits = gemm_pick_splits(k, k, m);
-  auto gram = [&](const double* X, int64_t ldx) -> ssi_status {   // W = X^T X (lower triangle read)
-    if (tall) return gemm_tall_syrk_lower(k, m, X, ldx, X, ldx, w.W, k, w.tallp, s);
-    return gemm_f64(k, k, m, 1.0, Operand{X, ldx, 1}, Operand{X, 1, ldx}, w.W, k, splits, w.partial, s);
+  auto gram = [&](const double* X, int64_t ldx, const int* run_if) -> ssi_status {   // W = X^T X (lower)
+    if (tall) return gemm_tall_syrk_lower(k, m, X, ldx, X, ldx, w.W, k, w.tallp, s, run_if);
+    return gemm_f64(k, k, m, 1.0, Operand{X, ldx, 1}, Operand{X, 1, ldx}, w.W, k, splits, w.partial, s, run_if);
   };
-  auto trmul = [&](const double* X, int64_t ldx, const double* Linv, const double* LinvT, double* out) {
+  auto trmul = [&](const double* X, int64_t ldx, const double* Linv, const double* LinvT, double* out,
+                   const int* run_if) {
     // out = X Linv^T  (B(kk, j) = Linv(j, kk) = LinvT[kk + j k])
-    if (tall) return gemm_tall_triu(m, k, k, X, ldx, LinvT, k, out, m, s);
-    return gemm_f64(m, k, k, 1.0, Operand{X, 1, ldx}, Operand{Linv, k, 1}, out, m, 1, nullptr, s);
+    if (tall) return gemm_tall_triu(m, k, k, X, ldx, LinvT, k, out, m, s, run_if);
+    return gemm_f64(m, k, k, 1.0, Operand{X, 1, ldx}, Operand{Linv, k, 1}, out, m, 1, nullptr, s, run_if);
   };
-  SSI_TRY(gram(Y, ldy));
-  SSI_TRY(chol_inv(w.W, k, w.L1, w.Linv1, w.LinvT1, w.chol_g, status, s));
-  SSI_TRY(trmul(Y, ldy, w.Linv1, w.LinvT1, w.Q1));
-  SSI_TRY(gram(w.Q1, m));
-  SSI_TRY(chol_inv(w.W, k, w.L2, w.Linv2, w.LinvT2, w.chol_g, status, s));
-  return trmul(w.Q1, m, w.Linv2, w.LinvT2, Q);
+  const int* shifted = w.flag;
+  SSI_TRY(gram(Y, ldy, nullptr));
+  SSI_TRY(chol_inv(w.W, k, m, w.L1, w.Linv1, w.LinvT1, w.chol_g, status, s, nullptr, w.flag, 0));
+  SSI_TRY(trmul(Y, ldy, w.Linv1, w.LinvT1, w.Q1, nullptr));
+#ifndef SSI_NO_CQ_FALLBACK
+  // fallback pass: Q1 = Q_b Lb^T (CholeskyQR of the shifted pass's output), result through Q
+  SSI_TRY(gram(w.Q1, m, shifted));
+  SSI_TRY(chol_inv(w.W, k, m, w.Lb, w.Linvb, w.LinvTb, w.chol_g, status, s, shifted, nullptr, 0));
+  SSI_TRY(trmul(w.Q1, m, w.Linvb, w.LinvTb, Q, shifted));
+  cq_copy_kernel<<<148 * 4, 256, 0, s>>>(shifted, m * k, Q, w.Q1);
+  SSI_TRY(launch_check("cq_copy_kernel"));
+#endif
+  SSI_TRY(gram(w.Q1, m, nullptr));
+  SSI_TRY(chol_inv(w.W, k, m, w.L2, w.Linv2, w.LinvT2, w.chol_g, status, s, nullptr, nullptr, 1));
+  SSI_TRY(trmul(w.Q1, m, w.Linv2, w.LinvT2, Q, nullptr));
+#ifdef SSI_NO_CQ_FALLBACK
+  return SSI_OK;
+#endif
+  cq_fold_kernel<<<2 * k, 128, size_t(k) * sizeof(double), s>>>(shifted, k, w.Lb, w.Linvb, w.L2, w.Linv2);
+  return launch_check("cq_fold_kernel");
 }
 
 template <int KPL, int JCT>

@@ -45,6 +45,16 @@ class SweepParams:
         return 1.0 / self.fs
 
 
+def check_status(workspaces, what: str) -> None:
+    """Raise if any call that used one of `workspaces` reported a device-side numeric failure
+    (the status word accumulates across calls; reading it synchronises the current stream)."""
+    for ws in workspaces:
+        code = api.device_status(ws)
+        if code != 0:
+            from . import _lib
+            raise _lib.SSIError(what + " (device status)", code)
+
+
 class Engine:
     """Reusable device buffers for identify(); one Engine per (device, stream) user."""
 
@@ -95,10 +105,16 @@ class Engine:
         U, S = api.rsvd(T, P.k, P.q, P.seed, stream_id, P.n_max, ws=self.ws_rsvd)
         return api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=self.ws_modal), (U, S)
 
-    def identify(self, Y, stream_id=0):
-        """A1-A11 for one record (the metric's unit of work)."""
+    def workspaces(self):
+        return (self.ws_cov, self.ws_rsvd, self.ws_modal)
+
+    def identify(self, Y, stream_id=0, check: bool = True):
+        """A1-A11 for one record (the metric's unit of work). check: synchronise and raise if any
+        call so far on this engine reported a device-side numeric failure."""
         R = self.covariances(Y)
         tab, _ = self.decompose(R, self.P.i, stream_id)
+        if check:
+            check_status(self.workspaces(), "identify")
         return tab
 
 
@@ -130,8 +146,10 @@ class RecordPipeline:
         k = self.j % len(self.engines)
         e, st, cst = self.engines[k], self.streams[k], self.cov_streams[k]
         self.j += 1
+        st.wait_stream(torch.cuda.current_stream(Y.device))   # Y was produced on the caller's stream
         if self.split:
             cst.wait_stream(st)            # the engine's buffers are free; Y is ready on st
+        Y.record_stream(cst)               # the caching allocator must not reuse Y before A1 read it
         with torch.cuda.stream(cst):
             if events is not None:
                 events[0].record(cst)
@@ -143,6 +161,11 @@ class RecordPipeline:
         with torch.cuda.stream(st):
             tab, _ = e.decompose(R, e.P.i, stream_id)
         return tab, st
+
+    def check(self):
+        """Raise if any record so far reported a device-side numeric failure (synchronises)."""
+        for e in self.engines:
+            check_status(e.workspaces(), "RecordPipeline")
 
     def join(self, stream=None):
         """Make `stream` (default: current) wait for all pipeline streams."""
@@ -178,23 +201,31 @@ def lpt_assign(lags, world: int):
     return [sorted(x) for x in out]
 
 
-def allreduce_covariance_sums(S: torch.Tensor, N: int, lag_lo: int, group=None) -> torch.Tensor:
-    """Sum time-sharded raw covariance sums over ranks, then divide by (N - k)
-    (reading A-6). S: [L][l][l] FP64 on any backend's device."""
+def allreduce_sums(S: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum time-sharded raw covariance sums over ranks in place (one all-reduce; the lag sweep's
+    only exchange). When the process group's backend cannot reduce device tensors (gloo), the
+    sums are staged through host memory. No arithmetic of the method runs here."""
     import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1):
+        return S
+    if S.is_cuda and dist.get_backend(group) != "nccl":
+        h = S.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        S.copy_(h)
+    else:
         dist.all_reduce(S, op=dist.ReduceOp.SUM, group=group)
-    k = torch.arange(lag_lo, lag_lo + S.shape[0], dtype=torch.float64, device=S.device)
-    return S / (N - k).view(-1, 1, 1)
+    return S
 
 
 def sharded_covariances(Y: torch.Tensor, lag_hi: int, rank: int, world: int, mode="fp64",
-                        group=None) -> torch.Tensor:
-    """Time-sharded A1 across ranks + one all-reduce (the lag sweep's only exchange)."""
+                        group=None, out: torch.Tensor | None = None, ws: torch.Tensor | None = None) -> torch.Tensor:
+    """Time-sharded A1 across ranks: raw sums over this rank's shard (ssi_covariances, normalize=0),
+    one all-reduce, then 1/(N - k) on the device (ssi_cov_normalize)."""
     N = Y.shape[0]
     tb, te = time_shards(N, world)[rank]
-    S = api.covariances(Y, lag_hi, 1, mode, t_begin=tb, t_end=te, normalize=False)
-    return allreduce_covariance_sums(S, N, 1, group)
+    S = api.covariances(Y, lag_hi, 1, mode, t_begin=tb, t_end=te, normalize=False, out=out, ws=ws)
+    allreduce_sums(S, group)
+    return api.cov_normalize(S, N, 1)
 
 
 def record_assignment(n_records: int, world: int):
@@ -202,38 +233,95 @@ def record_assignment(n_records: int, world: int):
     return [list(range(r, n_records, world)) for r in range(world)]
 
 
+def _segments(t: api.PoleTable):
+    """Byte layout of one pole table in a packed buffer: (tensor, offset, nbytes), 16-byte aligned."""
+    out, off = [], 0
+    for x in t.tensors():
+        nb = x.numel() * x.element_size()
+        out.append((x, off, nb))
+        off += (nb + 15) // 16 * 16
+    return out, off
+
+
+def pack_tables(tables, device) -> torch.Tensor:
+    """Tables -> one contiguous uint8 buffer [len(tables)][table bytes] (byte copies only)."""
+    tb = _segments(tables[0])[1] if tables else 0
+    buf = torch.zeros(len(tables) * tb, dtype=torch.uint8, device=device)
+    for j, t in enumerate(tables):
+        for x, off, nb in _segments(t)[0]:
+            buf[j * tb + off: j * tb + off + nb].copy_(x.contiguous().view(-1).view(torch.uint8))
+    return buf
+
+
+def unpack_table(buf: torch.Tensor, t: api.PoleTable) -> api.PoleTable:
+    for x, off, nb in _segments(t)[0]:
+        x.view(-1).view(torch.uint8).copy_(buf[off: off + nb])
+    return t
+
+
 def gather_tables(local: dict, assignment, make_empty, rank: int, world: int, group=None) -> dict:
     """All ranks receive every pole table: table key -> owner from `assignment` (a list of key
-    lists, one per rank); the owner broadcasts its fixed-size tensors (the sweep's/batch's
-    second and last collective). make_empty() allocates a receive table of the same shape."""
+    lists, one per rank). Each rank packs its tables into one byte buffer, padded to the largest
+    per-rank count, and ONE all_gather exchanges them (the sweep's / batch's last collective;
+    ~31 MB per c3-sized table). Over gloo the buffer is staged through host memory.
+    make_empty() allocates a table of the common shape."""
     if world == 1:
         return dict(local)
     import torch.distributed as dist
+    proto = make_empty()
+    tb = _segments(proto)[1]
+    cap = max(len(k) for k in assignment)
+    dev = proto.count.device
+    mine = [local[key] for key in assignment[rank]]
+    send = torch.zeros(cap * tb, dtype=torch.uint8, device=dev)
+    if mine:
+        send[: len(mine) * tb].copy_(pack_tables(mine, dev))
+    if dist.get_backend(group) == "nccl":
+        recv = torch.empty(world * cap * tb, dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(recv, send, group=group)
+    else:
+        parts = [torch.empty(cap * tb, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(parts, send.cpu(), group=group)
+        recv = torch.cat(parts).to(dev)
     out = {}
     for r, keys in enumerate(assignment):
-        for key in keys:
-            t = local[key] if r == rank else make_empty()
-            for x in t.tensors():
-                dist.broadcast(x, src=r, group=group)
-            out[key] = t
+        for j, key in enumerate(keys):
+            if r == rank:
+                out[key] = local[key]
+            else:
+                base = (r * cap + j) * tb
+                out[key] = unpack_table(recv[base: base + tb], make_empty())
     return out
 
 
 def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank: int = 0, world: int = 1,
-                 group=None, n_streams: int = 8):
+                 group=None, n_streams: int = 8, timing: dict | None = None):
     """3D stabilization diagram (steps i-ii) for the time-lag steps `lags`:
     covariances once up to lag 2 max(i) - 1 (time-sharded over ranks + one all-reduce),
     Toeplitz + RSVD + modal sweep per lag (lags assigned by LPT; on a rank the lags are
     independent and run on `n_streams` CUDA streams, largest first, each stream with its own
     workspaces), all tables gathered, ssi_stab3d over the lag axis.
+    timing: optional dict that receives CUDA events recorded on the current stream at the phase
+    boundaries ("start", "cov" = covariances + all-reduce + normalisation, "lags", "gather",
+    "stab").
     Returns ({i: PoleTable}, flags, stable_count)."""
     lags = sorted(lags)
     lag_hi = 2 * lags[-1] - 1
-    R = sharded_covariances(Y, lag_hi, rank, world, P.cov_mode, group)
-    assign = lpt_assign(lags, world)
     dev = Y.device
+
+    def mark(name):
+        if timing is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(torch.cuda.current_stream(dev))
+            timing[name] = ev
+
+    mark("start")
+    ws_c = api._workspace(api.covariances_ws_bytes(Y.shape[0], P.l, lag_hi, 1, P.cov_mode), dev)
+    R = sharded_covariances(Y, lag_hi, rank, world, P.cov_mode, group, ws=ws_c)
+    mark("cov")
+    assign = lpt_assign(lags, world)
     mine = sorted(assign[rank], reverse=True)            # largest lags first (longest chains)
-    ns = max(1, min(n_streams, len(mine)))
+    ns = min(n_streams, len(mine))                       # 0 when this rank got no lag
     cur = torch.cuda.current_stream(dev)
     lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
     streams = [torch.cuda.Stream(device=dev, priority=hi) for _ in range(ns)]
@@ -266,9 +354,13 @@ def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank
             local[i] = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=ws_m)
     for st in streams:
         cur.wait_stream(st)
+    mark("lags")
+    check_status([ws_c] + [w for sl in slots for w in (sl[0], sl[2])], "lag_sweep_3d")
     tables = gather_tables(local, assign, lambda: api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, dev),
                            rank, world, group)
+    mark("gather")
     flags, counts = api.stab3d([tables[i] for i in lags], crit)
+    mark("stab")
     return tables, flags, counts
 
 
@@ -289,6 +381,7 @@ def record_batch(records, P: SweepParams, rank: int = 0, world: int = 1, n_strea
             local[j] = api.PoleTable(tab.n_min, tab.n_step, tab.l, tab.cap, *[t.clone() for t in tab.tensors()])
     pipe.join()
     torch.cuda.current_stream().synchronize()
+    pipe.check()
     if not gather:
         return local
     return gather_tables(local, assign, lambda: api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, first.device),

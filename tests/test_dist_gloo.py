@@ -1,8 +1,10 @@
 """Multi-GPU host logic on CPU (-m "not gpu"): world-size-2 gloo process groups exercise the
 exchange steps of the lag sweep and the record batch without a GPU. The covariance shards
 are computed here by the oracle (test infrastructure) standing in for ssi_covariances'
-raw-sum mode; the product code under test is drivers.allreduce_covariance_sums,
-drivers.gather_tables and the assignment helpers."""
+raw-sum mode; the product code under test is drivers.allreduce_sums (the one exchange of
+the time-sharded covariances; the 1/(N-k) that follows runs in libssi, ssi_cov_normalize,
+covered by the GPU tests), drivers.gather_tables (one packed all_gather) and the
+assignment helpers."""
 import os
 import socket
 
@@ -56,18 +58,18 @@ def _cov_rank(rank, world):
     Y = _record()
     tb, te = drivers.time_shards(Y.shape[0], world)[rank]
     S = torch.from_numpy(oracle.covariance_partial_sums(Y, 1, 17, tb, te))
-    R = drivers.allreduce_covariance_sums(S, Y.shape[0], 1)
-    return R.numpy()
+    return drivers.allreduce_sums(S).numpy()
 
 
 def test_time_sharded_covariance_allreduce_gloo():
     """Lag sweep exchange step: per-rank time shards (halo read by the kernel), one
-    all-reduce of raw FP64 sums, then 1/(N-k) — equals the full-record covariances."""
+    all-reduce of raw FP64 sums — equals the full-record raw sums on every rank."""
     out = _spawn(_cov_rank)
-    ref = oracle.covariances(_record(), 17)
+    Y = _record()
+    ref = oracle.covariance_partial_sums(Y, 1, 17, 0, Y.shape[0])
     for r in (0, 1):
-        np.testing.assert_allclose(out[r], ref, rtol=1e-12, atol=1e-14)
-    assert np.array_equal(out[0], out[1])          # every rank holds identical R
+        np.testing.assert_allclose(out[r], ref, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(out[0], out[1])          # every rank holds identical sums
 
 
 def _fake_table(key, n_min=2, n_max=10, l=3):
@@ -92,6 +94,39 @@ def test_gather_tables_gloo():
     for r in (0, 1):
         assert sorted(out[r]) == lags
         assert all(out[r][i] == float(i) for i in lags)
+
+
+def _gather_uneven_rank(rank, world):
+    # 3 tables over 2 ranks: rank 0 owns two, rank 1 one (padding of the packed buffer)
+    assign = [[0, 2], [1]]
+    local = {}
+    for key in assign[rank]:
+        t = api.PoleTable.empty(2, 8, 2, 3, "cpu")
+        g = torch.Generator().manual_seed(key)
+        for x in t.tensors():
+            x.copy_((torch.rand(x.shape, generator=g, dtype=torch.float64) * 1000).to(x.dtype))
+        local[key] = t
+    tabs = drivers.gather_tables(local, assign, lambda: api.PoleTable.empty(2, 8, 2, 3, "cpu"), rank, world)
+    return {k: [x.numpy().copy() for x in tabs[k].tensors()] for k in (0, 1, 2)}
+
+
+def test_gather_tables_bytes_exact_gloo():
+    """The packed all_gather moves every array of every table bit for bit (int32 counts too)."""
+    out = _spawn(_gather_uneven_rank)
+    for k in (0, 1, 2):
+        for a, b in zip(out[0][k], out[1][k]):
+            assert a.dtype == b.dtype and np.array_equal(a, b)
+    assert out[0][1][0].dtype == np.int32
+
+
+def test_pack_unpack_roundtrip():
+    t = api.PoleTable.empty(2, 6, 2, 2, "cpu")
+    for j, x in enumerate(t.tensors()):
+        x.copy_(torch.arange(x.numel()).reshape(x.shape).to(x.dtype) + j)
+    buf = drivers.pack_tables([t, t], "cpu")
+    u = drivers.unpack_table(buf[: buf.numel() // 2], api.PoleTable.empty(2, 6, 2, 2, "cpu"))
+    for a, b in zip(t.tensors(), u.tensors()):
+        assert torch.equal(a, b)
 
 
 def test_assignment_helpers():
