@@ -26,6 +26,9 @@ from .indicators import mac, mpc, mpd, normalize_shape
 from .stab import stab3d, Criteria, HC_DEFAULT, SC_10DOF_3D, SC_BRIDGE_3D
 from .params import (time_lag_step, lag_of_step, lag_grid, min_rank_percent,
                      sample_count)
+from .cluster import (stable_pole_features, fuzzy_cmeans, fcm_memberships, select_physical,
+                      pole_distances, hierarchical_clusters, cluster_3d)
+from .track import track_session, success_ratio
 
 __all__ = [
     "covariances", "covariance_partial_sums", "toeplitz", "philox4x32_10", "philox_words",
@@ -33,4 +36,6 @@ __all__ = [
     "modal_sweep", "poles_from_eigs", "Pole", "OrderCell", "mac", "mpc", "mpd",
     "normalize_shape", "stab3d", "Criteria", "HC_DEFAULT", "SC_10DOF_3D", "SC_BRIDGE_3D",
     "time_lag_step", "lag_of_step", "lag_grid", "min_rank_percent", "sample_count",
+    "stable_pole_features", "fuzzy_cmeans", "fcm_memberships", "select_physical", "pole_distances",
+    "hierarchical_clusters", "cluster_3d", "track_session", "success_ratio",
 ]
