@@ -257,6 +257,92 @@ SSI_API ssi_status ssi_stab3d(const ssi_pole_table* tables, int32_t n_lags, cons
                       uint8_t* flags, int32_t* stable_count, void* stream);
 
 /* ------------------------------------------------------------------------------
+ * NEXT-2. Two-stage clustering of the stable poles of a 3D stabilization diagram
+ * (§2.3 step iii; §3.1.3; §3.2.2) and modal
+ * tracking (§3.2.2, Table 4). Readings C-1..C-5 of DESIGN.md §3:
+ *  Stage I  (ssi_cluster_stage1): every pole with flag 2 (stable) gets the features of its
+ *           best soft-criteria neighbour (order axis (g, o-1) first, then lag axis (g-1, o),
+ *           slots ascending, least d_f + d_xi + (1-MAC), first on ties):
+ *           x = (d_f, d_xi, 1-MAC, 1-MPC, MPD) (C-1). Fuzzy C-means with c = 2, m = 2,
+ *           centroids initialised at the feature-wise min and max, until the largest centroid
+ *           move is < fcm_tol or fcm_max_iter iterations (C-2). The "possibly physical"
+ *           cluster is the one whose centroid is nearer the origin; a pole is
+ *           retained iff its membership there is >= 0.5 (C-3).
+ *  Stage II (ssi_cluster_stage2): d(i, j) = d_f + d_xi + (1 - MAC) between retained poles
+ *           (PAPER.md:293, :405); average linkage (UPGMA); flat clusters = merges at height
+ *           <= cutoff; clusters with < min_size members are dropped; per cluster the lower
+ *           median f and xi and the medoid's shape (least summed distance, lowest index on
+ *           ties); clusters ordered by (f, smallest member index) (C-4).
+ *  Tracking (ssi_track): a session mode c is a candidate for reference mode r iff
+ *           |f_c - f_r| / max(f_c, f_r) <= df_max and 1 - MAC <= macd_max; candidates are
+ *           assigned one-to-one in ascending d_f + (1 - MAC) order (ties: lower r, then lower
+ *           c); success[r] = 100 * (sessions where r was matched) / n_sess (C-5).
+ * The pole table layout is the one of ssi_modal_sweep; tables as for ssi_stab3d, at most
+ * SSI_MAX_LAGS lags. All arrays are device memory. Indices of stable poles ("pole rows") are
+ * in (lag, order, slot) lexicographic order; "retained rows" index the retained poles in
+ * increasing pole-row order.
+ * ---------------------------------------------------------------------------- */
+#define SSI_MAX_LAGS 64
+
+typedef struct {
+  int32_t n_stable;      /* stable poles (flag 2) in the diagram */
+  int32_t n_retained;    /* poles with membership >= 0.5 in the physical FCM cluster */
+  int32_t fcm_iters;     /* fuzzy C-means iterations run */
+  int32_t phys;          /* index (0 / 1) of the possibly-physical FCM cluster */
+  int32_t n_components;  /* stage II: connected components of {d <= cutoff} (diagnostic) */
+  int32_t n_clusters;    /* stage II: clusters with >= min_size members */
+  int32_t n_merges;      /* stage II: average-linkage merges at height <= cutoff */
+  int32_t overflow;      /* 1: n_stable > max_poles or n_clusters > max_clusters (truncated) */
+  double V[2][5];        /* FCM centroids */
+} ssi_cluster_info;
+
+/* Stage I. flags: [n_lags][n_orders][cap] from ssi_stab3d with the same crit.
+ *  pole_idx [max_poles][3] int32 (lag, order index, slot); X [max_poles][5] features;
+ *  U [max_poles][2] final memberships; retained [max_poles] int32 pole rows of the retained
+ *  poles; info: device struct (all fields of stage I written). Rows past info.n_stable (or
+ *  max_poles) are not written.
+ *  Errors: n_lags outside [1, SSI_MAX_LAGS], tables of different shape, max_poles < 1,
+ *  fcm_tol < 0 or fcm_max_iter < 0 -> INVALID_ARG; ws_bytes below ssi_cluster_stage1_ws ->
+ *  WORKSPACE. A flag-2 pole without a qualifying neighbour (flags made with other criteria)
+ *  gets NaN features and sets SSI_ERR_NUMERIC in the device status word. */
+SSI_API ssi_status ssi_cluster_stage1(const ssi_pole_table* tables, int32_t n_lags, const ssi_criteria* crit,
+                                      const uint8_t* flags, int32_t max_poles, double fcm_tol,
+                                      int32_t fcm_max_iter, int32_t* pole_idx, double* X, double* U,
+                                      int32_t* retained, ssi_cluster_info* info, void* ws, size_t ws_bytes,
+                                      void* stream);
+SSI_API ssi_status ssi_cluster_stage1_ws(int32_t n_lags, int32_t n_orders, size_t* bytes);
+
+/* Stage II on the n_retained poles listed by stage I (n_retained = info.n_retained, read by the
+ * caller after stage I; the workspace, O(n_retained^2) doubles, depends on it).
+ *  labels [n_retained] int32: cluster of each retained row (0..), -1 if its cluster was dropped.
+ *  cl_f, cl_xi [max_clusters], cl_size, cl_medoid (retained row) [max_clusters] int32,
+ *  cl_shape [max_clusters][l][2]: the clusters in output order; info.n_clusters of them.
+ *  merges_ab [n_retained][2] int32 (retained rows; the surviving cluster keeps the larger
+ *  row) and merges_h [n_retained]: the merges at height <= cutoff, component by component,
+ *  padded with -1 / NaN; either may be NULL.
+ *  Errors: n_retained < 0, min_size < 1, max_clusters < 1, cutoff not finite -> INVALID_ARG;
+ *  ws_bytes below ssi_cluster_stage2_ws -> WORKSPACE. */
+SSI_API ssi_status ssi_cluster_stage2(const ssi_pole_table* tables, int32_t n_lags, const int32_t* pole_idx,
+                                      const int32_t* retained, int32_t n_retained, double cutoff,
+                                      int32_t min_size, int32_t max_clusters, int32_t* labels, double* cl_f,
+                                      double* cl_xi, int32_t* cl_size, int32_t* cl_medoid, double* cl_shape,
+                                      int32_t* merges_ab, double* merges_h, ssi_cluster_info* info, void* ws,
+                                      size_t ws_bytes, void* stream);
+SSI_API ssi_status ssi_cluster_stage2_ws(int32_t n_retained, int32_t l, size_t* bytes);
+
+/* Tracking over n_sess sessions against n_ref reference modes.
+ *  ref_f [n_ref], ref_shape [n_ref][l][2]; f [n_sess][max_modes], shape
+ *  [n_sess][max_modes][l][2], count [n_sess] int32 (modes of each session; clamped to
+ *  [0, max_modes]). match [n_sess][n_ref] int32: the session mode assigned to r, or -1.
+ *  success [n_ref] (may be NULL): percentage of sessions in which r was matched.
+ *  Errors: n_ref < 1, n_sess < 1, max_modes < 1, l < 1, n_ref * max_modes > 16384 ->
+ *  INVALID_ARG. */
+SSI_API ssi_status ssi_track(const double* ref_f, const double* ref_shape, int32_t n_ref, const double* f,
+                             const double* shape, const int32_t* count, int32_t n_sess, int32_t max_modes,
+                             int32_t l, double df_max, double macd_max, int32_t* match, double* success,
+                             void* stream);
+
+/* ------------------------------------------------------------------------------
  * Status helpers.
  * ---------------------------------------------------------------------------- */
 /* Zeroes the 256-byte header of ws (the sticky status word), enqueued on stream. */

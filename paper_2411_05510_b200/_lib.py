@@ -27,6 +27,14 @@ class CriteriaC(C.Structure):
                 ("alpha_f", C.c_double), ("alpha_xi", C.c_double), ("alpha_mac", C.c_double)]
 
 
+class ClusterInfoC(C.Structure):
+    _fields_ = [("n_stable", C.c_int32), ("n_retained", C.c_int32), ("fcm_iters", C.c_int32),
+                ("phys", C.c_int32), ("n_components", C.c_int32), ("n_clusters", C.c_int32),
+                ("n_merges", C.c_int32), ("overflow", C.c_int32), ("V", C.c_double * 10)]
+
+
+SSI_MAX_LAGS = 64
+
 # name -> (restype, argtypes)
 P, I32, I64, U64, SZ, D = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_size_t, C.c_double
 SIGNATURES = {
@@ -45,6 +53,13 @@ SIGNATURES = {
     "ssi_modal_sweep": (I32, [P, I64, P, I32, I32, I32, I32, I32, D, C.POINTER(PoleTableC), P, SZ, P]),
     "ssi_modal_sweep_ws": (I32, [I32, I32, I32, I32, I32, C.POINTER(SZ)]),
     "ssi_stab3d": (I32, [C.POINTER(PoleTableC), I32, C.POINTER(CriteriaC), P, P, P]),
+    "ssi_cluster_stage1": (I32, [C.POINTER(PoleTableC), I32, C.POINTER(CriteriaC), P, I32, D, I32, P, P, P, P, P,
+                                 P, SZ, P]),
+    "ssi_cluster_stage1_ws": (I32, [I32, I32, C.POINTER(SZ)]),
+    "ssi_cluster_stage2": (I32, [C.POINTER(PoleTableC), I32, P, P, I32, D, I32, I32, P, P, P, P, P, P, P, P, P, P,
+                                 SZ, P]),
+    "ssi_cluster_stage2_ws": (I32, [I32, I32, C.POINTER(SZ)]),
+    "ssi_track": (I32, [P, P, I32, P, P, P, I32, I32, I32, D, D, P, P, P]),
     "ssi_fetch_device_status": (I32, [P, C.POINTER(I32)]),
     "ssi_clear_status": (I32, [P, P]),
     "ssi_status_string": (C.c_char_p, [I32]),

@@ -9,6 +9,9 @@ runs in the library's sm_100a kernels. Functions mirror the C entry points:
     rsvd_toeplitz(R, l, i, k, ...)   -> same RSVD, T applied through its block structure (A2-A8)
     modal_sweep(U, S, l, i, ...)     -> PoleTable                   (A9-A11, Eqs. 9-12)
     stab3d(tables, criteria)         -> flags, stable_count         (A13)
+    cluster3d(tables, flags, crit)   -> Clustering (two-stage: fuzzy C-means + average linkage)
+                                                                    (NEXT-2, PAPER.md:293, :402-415)
+    track(ref_f, ref_shape, f, shape, count) -> match, success      (NEXT-2, PAPER.md:544)
 """
 from __future__ import annotations
 
@@ -18,7 +21,7 @@ from dataclasses import dataclass
 import torch
 
 from . import _lib
-from ._lib import PoleTableC, CriteriaC, call, SSI_F32, SSI_F64, SSI_COV_FP64, SSI_COV_INT8X3, SSI_COV_SPECTRAL
+from ._lib import PoleTableC, CriteriaC, ClusterInfoC, call, SSI_F32, SSI_F64, SSI_COV_FP64, SSI_COV_INT8X3, SSI_COV_SPECTRAL
 
 COV_MODES = {"fp64": SSI_COV_FP64, "int8x3": SSI_COV_INT8X3, "spectral": SSI_COV_SPECTRAL}
 
@@ -327,3 +330,116 @@ def stab3d(tables: list, crit: Criteria):
     cc = CriteriaC(crit.xi_max, crit.mpc_min, crit.mpd_max, crit.alpha_f, crit.alpha_xi, crit.alpha_mac)
     call("ssi_stab3d", arr, G, C.byref(cc), _ptr(flags), _ptr(counts), _stream())
     return flags, counts
+
+
+# ------------------------------------------------------------------ NEXT-2: clustering + tracking
+@dataclass
+class Clustering:
+    """Result of cluster3d (device tensors; readings C-1..C-4, include/ssi.h NEXT-2).
+    pole_idx [n_stable][3] (lag, order index, slot) of the stable poles; X [n_stable][5] stage-I
+    features; U [n_stable][2] fuzzy memberships; V [2][5] centroids; phys: index of the possibly-
+    physical FCM cluster; retained [n_retained] rows of pole_idx kept for stage II; labels
+    [n_retained] cluster of each retained pole (-1: dropped); f, xi, size, medoid (retained row),
+    shape [K][l][2] of the K clusters ordered by (f, first member); merges_ab / merges_h: the
+    average-linkage merges at height <= cutoff."""
+    n_stable: int
+    n_retained: int
+    fcm_iters: int
+    phys: int
+    n_components: int
+    n_merges: int
+    overflow: int
+    pole_idx: torch.Tensor
+    X: torch.Tensor
+    U: torch.Tensor
+    V: torch.Tensor
+    retained: torch.Tensor
+    labels: torch.Tensor
+    f: torch.Tensor
+    xi: torch.Tensor
+    size: torch.Tensor
+    medoid: torch.Tensor
+    shape: torch.Tensor
+    merges_ab: torch.Tensor
+    merges_h: torch.Tensor
+
+    @property
+    def n_clusters(self):
+        return int(self.f.shape[0])
+
+
+def _table_array(tables):
+    if not 1 <= len(tables) <= _lib.SSI_MAX_LAGS:
+        raise ValueError(f"1..{_lib.SSI_MAX_LAGS} pole tables expected")
+    return (PoleTableC * len(tables))(*[t.as_c() for t in tables])
+
+
+def cluster3d(tables: list, flags: torch.Tensor, crit: Criteria, cutoff: float = 0.10, min_size: int = 1,
+              max_clusters: int = 4096, fcm_tol: float = 1e-10, fcm_max_iter: int = 1000,
+              check: bool = True) -> Clustering:
+    """Two-stage clustering of the stable poles (flag 2) of the diagram `tables` (lags in increasing
+    i) with `flags` from stab3d(tables, crit) (ssi_cluster_stage1 + ssi_cluster_stage2). Stage I
+    reads back the retained-pole count (one synchronisation) to size stage II's O(n^2) workspace."""
+    t0 = tables[0]
+    dev = t0.count.device
+    _require_cuda(flags)
+    arr = _table_array(tables)
+    G = len(tables)
+    cc = CriteriaC(crit.xi_max, crit.mpc_min, crit.mpd_max, crit.alpha_f, crit.alpha_xi, crit.alpha_mac)
+    max_poles = max(1, G * t0.n_orders * t0.cap)
+    pole_idx = torch.empty((max_poles, 3), dtype=torch.int32, device=dev)
+    X = torch.empty((max_poles, 5), dtype=torch.float64, device=dev)
+    U = torch.empty((max_poles, 2), dtype=torch.float64, device=dev)
+    retained = torch.empty(max_poles, dtype=torch.int32, device=dev)
+    info = torch.zeros(C.sizeof(ClusterInfoC), dtype=torch.uint8, device=dev)
+    b = C.c_size_t(0)
+    call("ssi_cluster_stage1_ws", G, t0.n_orders, C.byref(b))
+    ws1 = _workspace(b.value, dev)
+    call("ssi_cluster_stage1", arr, G, C.byref(cc), _ptr(flags), max_poles, float(fcm_tol), int(fcm_max_iter),
+         _ptr(pole_idx), _ptr(X), _ptr(U), _ptr(retained), _ptr(info), _ptr(ws1), ws1.numel(), _stream())
+    if check:
+        _check_device("ssi_cluster_stage1", ws1, True)
+    h = ClusterInfoC.from_buffer_copy(bytes(info.cpu().numpy()))
+    n_ret = h.n_retained
+    call("ssi_cluster_stage2_ws", n_ret, t0.l, C.byref(b))
+    ws2 = _workspace(b.value, dev)
+    labels = torch.empty(max(n_ret, 1), dtype=torch.int32, device=dev)
+    cl_f = torch.empty(max_clusters, dtype=torch.float64, device=dev)
+    cl_xi = torch.empty_like(cl_f)
+    cl_size = torch.empty(max_clusters, dtype=torch.int32, device=dev)
+    cl_med = torch.empty_like(cl_size)
+    cl_shape = torch.empty((max_clusters, t0.l, 2), dtype=torch.float64, device=dev)
+    m_ab = torch.empty((max(n_ret, 1), 2), dtype=torch.int32, device=dev)
+    m_h = torch.empty(max(n_ret, 1), dtype=torch.float64, device=dev)
+    call("ssi_cluster_stage2", arr, G, _ptr(pole_idx), _ptr(retained), n_ret, float(cutoff), int(min_size),
+         int(max_clusters), _ptr(labels), _ptr(cl_f), _ptr(cl_xi), _ptr(cl_size), _ptr(cl_med), _ptr(cl_shape),
+         _ptr(m_ab), _ptr(m_h), _ptr(info), _ptr(ws2), ws2.numel(), _stream())
+    if check:
+        _check_device("ssi_cluster_stage2", ws2, True)
+    h = ClusterInfoC.from_buffer_copy(bytes(info.cpu().numpy()))
+    K = min(h.n_clusters, max_clusters)
+    ns = min(h.n_stable, max_poles)
+    return Clustering(h.n_stable, n_ret, h.fcm_iters, h.phys, h.n_components, h.n_merges, h.overflow,
+                      pole_idx[:ns], X[:ns], U[:ns], torch.tensor(list(h.V), dtype=torch.float64).view(2, 5),
+                      retained[:n_ret], labels[:n_ret], cl_f[:K], cl_xi[:K], cl_size[:K], cl_med[:K],
+                      cl_shape[:K], m_ab[:h.n_merges], m_h[:h.n_merges])
+
+
+def track(ref_f: torch.Tensor, ref_shape: torch.Tensor, f: torch.Tensor, shape: torch.Tensor,
+          count: torch.Tensor, df_max: float = 0.05, macd_max: float = 0.15):
+    """Modal tracking (ssi_track, reading C-5): ref_f [R], ref_shape [R][l][2]; f [S][M],
+    shape [S][M][l][2], count [S] int32 modes per session. Returns (match [S][R] int32 with the
+    session mode assigned to each reference mode or -1, success [R] percentages)."""
+    _require_cuda(ref_f, ref_shape, f, shape, count)
+    R, l = ref_shape.shape[0], ref_shape.shape[1]
+    S, M = f.shape
+    for t in (ref_f, ref_shape, f, shape):
+        if t.dtype != torch.float64 or not t.is_contiguous():
+            raise ValueError("ref_f, ref_shape, f, shape must be contiguous FP64")
+    if count.dtype != torch.int32 or shape.shape != (S, M, l, 2) or ref_shape.shape != (R, l, 2):
+        raise ValueError("shape mismatch")
+    match = torch.empty((S, R), dtype=torch.int32, device=f.device)
+    success = torch.empty(R, dtype=torch.float64, device=f.device)
+    call("ssi_track", _ptr(ref_f), _ptr(ref_shape), R, _ptr(f), _ptr(shape), _ptr(count), S, M, l,
+         float(df_max), float(macd_max), _ptr(match), _ptr(success), _stream())
+    return match, success

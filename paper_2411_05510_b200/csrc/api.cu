@@ -9,6 +9,7 @@
 #include "cov_spectral.cuh"
 #include "linalg.cuh"
 #include "rsvd.cuh"
+#include "cluster.cuh"
 
 namespace ssi {
 
@@ -303,6 +304,77 @@ ssi_status ssi_stab3d(const ssi_pole_table* tables, int32_t n_lags, const ssi_cr
                     tables[g].n_step == tables[0].n_step,
                 SSI_ERR_INVALID_ARG, "ssi_stab3d: pole tables differ in shape");
   return stab3d_run(tables, n_lags, *crit, flags, stable_count, S(stream));
+}
+
+static ssi_status table_set(const ssi_pole_table* tables, int32_t n_lags, const char* fn, TableSet& ts) {
+  SSI_REQUIRE(tables && n_lags >= 1 && n_lags <= SSI_MAX_LAGS, SSI_ERR_INVALID_ARG,
+              "%s: need 1 <= n_lags <= %d tables", fn, SSI_MAX_LAGS);
+  for (int g = 0; g < n_lags; ++g) {
+    const ssi_pole_table& t = tables[g];
+    SSI_REQUIRE(t.count && t.f && t.xi && t.mpc && t.mpd && t.shape && t.n_orders >= 1 && t.cap >= 1 && t.l >= 1,
+                SSI_ERR_INVALID_ARG, "%s: bad pole table %d", fn, g);
+    SSI_REQUIRE(t.n_orders == tables[0].n_orders && t.cap == tables[0].cap && t.l == tables[0].l &&
+                    t.n_min == tables[0].n_min && t.n_step == tables[0].n_step,
+                SSI_ERR_INVALID_ARG, "%s: pole tables differ in shape", fn);
+    ts.t[g] = t;
+  }
+  for (int g = n_lags; g < SSI_MAX_LAGS; ++g) ts.t[g] = tables[0];
+  return SSI_OK;
+}
+
+ssi_status ssi_cluster_stage1_ws(int32_t n_lags, int32_t n_orders, size_t* bytes) {
+  SSI_REQUIRE(bytes && n_lags >= 1 && n_orders >= 1, SSI_ERR_INVALID_ARG, "ssi_cluster_stage1_ws: bad arguments");
+  *bytes = cluster_stage1_ws_bytes(n_lags, n_orders);
+  return SSI_OK;
+}
+
+ssi_status ssi_cluster_stage1(const ssi_pole_table* tables, int32_t n_lags, const ssi_criteria* crit,
+                              const uint8_t* flags, int32_t max_poles, double fcm_tol, int32_t fcm_max_iter,
+                              int32_t* pole_idx, double* X, double* U, int32_t* retained,
+                              ssi_cluster_info* info, void* ws, size_t ws_bytes, void* stream) {
+  TableSet ts;
+  SSI_TRY(table_set(tables, n_lags, "ssi_cluster_stage1", ts));
+  SSI_REQUIRE(crit && flags && pole_idx && X && U && retained && info && ws, SSI_ERR_INVALID_ARG,
+              "ssi_cluster_stage1: NULL pointer");
+  SSI_REQUIRE(max_poles >= 1 && fcm_tol >= 0.0 && fcm_max_iter >= 0, SSI_ERR_INVALID_ARG,
+              "ssi_cluster_stage1: need max_poles >= 1, fcm_tol >= 0, fcm_max_iter >= 0");
+  const size_t need = cluster_stage1_ws_bytes(n_lags, tables[0].n_orders);
+  SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_cluster_stage1: workspace %zu < %zu", ws_bytes, need);
+  return cluster_stage1_run(ts, n_lags, *crit, flags, max_poles, fcm_tol, fcm_max_iter, pole_idx, X, U, retained,
+                            info, ws, static_cast<int32_t*>(ws), S(stream));
+}
+
+ssi_status ssi_cluster_stage2_ws(int32_t n_retained, int32_t l, size_t* bytes) {
+  SSI_REQUIRE(bytes && n_retained >= 0 && l >= 1, SSI_ERR_INVALID_ARG, "ssi_cluster_stage2_ws: bad arguments");
+  *bytes = cluster_stage2_ws_bytes(n_retained, l);
+  return SSI_OK;
+}
+
+ssi_status ssi_cluster_stage2(const ssi_pole_table* tables, int32_t n_lags, const int32_t* pole_idx,
+                              const int32_t* retained, int32_t n_retained, double cutoff, int32_t min_size,
+                              int32_t max_clusters, int32_t* labels, double* cl_f, double* cl_xi, int32_t* cl_size,
+                              int32_t* cl_medoid, double* cl_shape, int32_t* merges_ab, double* merges_h,
+                              ssi_cluster_info* info, void* ws, size_t ws_bytes, void* stream) {
+  TableSet ts;
+  SSI_TRY(table_set(tables, n_lags, "ssi_cluster_stage2", ts));
+  SSI_REQUIRE(pole_idx && retained && labels && cl_f && cl_xi && cl_size && cl_medoid && cl_shape && info && ws,
+              SSI_ERR_INVALID_ARG, "ssi_cluster_stage2: NULL pointer");
+  SSI_REQUIRE(n_retained >= 0 && min_size >= 1 && max_clusters >= 1 && isfinite(cutoff), SSI_ERR_INVALID_ARG,
+              "ssi_cluster_stage2: need n_retained >= 0, min_size >= 1, max_clusters >= 1, finite cutoff");
+  const size_t need = cluster_stage2_ws_bytes(n_retained, tables[0].l);
+  SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_cluster_stage2: workspace %zu < %zu", ws_bytes, need);
+  return cluster_stage2_run(ts, pole_idx, retained, n_retained, cutoff, min_size, max_clusters, labels, cl_f, cl_xi,
+                            cl_size, cl_medoid, cl_shape, merges_ab, merges_h, info, ws, S(stream));
+}
+
+ssi_status ssi_track(const double* ref_f, const double* ref_shape, int32_t n_ref, const double* f,
+                     const double* shape, const int32_t* count, int32_t n_sess, int32_t max_modes, int32_t l,
+                     double df_max, double macd_max, int32_t* match, double* success, void* stream) {
+  SSI_REQUIRE(ref_f && ref_shape && f && shape && count && match, SSI_ERR_INVALID_ARG, "ssi_track: NULL pointer");
+  SSI_REQUIRE(n_ref >= 1 && n_sess >= 1 && max_modes >= 1 && l >= 1 && int64_t(n_ref) * max_modes <= 16384,
+              SSI_ERR_INVALID_ARG, "ssi_track: need n_ref, n_sess, max_modes, l >= 1 and n_ref * max_modes <= 16384");
+  return track_run(ref_f, ref_shape, n_ref, f, shape, count, n_sess, max_modes, l, df_max, macd_max, match, success,
+                   S(stream));
 }
 
 }  // extern "C"

@@ -386,3 +386,59 @@ def record_batch(records, P: SweepParams, rank: int = 0, world: int = 1, n_strea
         return local
     return gather_tables(local, assign, lambda: api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, first.device),
                          rank, world, group)
+
+
+# ------------------------------------------------------------------ NEXT-2: step iii + tracking
+def identify_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, cutoff: float = 0.10,
+                min_size: int | None = None, rank: int = 0, world: int = 1, group=None, n_streams: int = 8,
+                timing: dict | None = None):
+    """The whole 3D-RSVD identification (§2.3 steps i-iii): lag sweep and 3D
+    stabilization (lag_sweep_3d), then the two-stage clustering of the stable poles (api.cluster3d;
+    every rank clusters the gathered diagram). min_size defaults to 20 % of the diagram's
+    (lag, order) cells, the share used for the paper's frame in tests/test_oracle_cluster.py.
+    Returns (tables, flags, stable_count, Clustering)."""
+    lags = sorted(lags)
+    tables, flags, counts = lag_sweep_3d(Y, P, lags, crit, rank, world, group, n_streams, timing)
+    O = tables[lags[0]].n_orders
+    ms = min_size if min_size is not None else max(1, int(0.2 * O * len(lags)))
+    cl = api.cluster3d([tables[i] for i in lags], flags, crit, cutoff=cutoff, min_size=ms)
+    if timing is not None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(torch.cuda.current_stream(Y.device))
+        timing["cluster"] = ev
+    return tables, flags, counts, cl
+
+
+def session_modes(tab: api.PoleTable, crit: api.Criteria, cutoff: float = 0.10, min_size: int | None = None):
+    """Modes of one monitoring session from its (single-lag) stabilization diagram: stab3d with
+    one lag (the 2D order-axis criteria), then the two-stage clustering."""
+    flags, _ = api.stab3d([tab], crit)
+    ms = min_size if min_size is not None else max(1, int(0.2 * tab.n_orders))
+    return api.cluster3d([tab], flags, crit, cutoff=cutoff, min_size=ms)
+
+
+def track_campaign(tables, crit: api.Criteria, max_modes: int = 64, df_max: float = 0.05,
+                   macd_max: float = 0.15, cutoff: float = 0.10, min_size: int | None = None, ref=None):
+    """Modal tracking over a campaign (§3.2.2; Table 4): every session's modes from
+    session_modes(); reference modes = those of the first session unless `ref` = (f, shape) is
+    given ("The reference modal properties are those identified ... from the first acquisition
+    record", PAPER.md Table 4). Returns (match [S][R], success [R] in %, ref_f, ref_shape)."""
+    dev = tables[0].count.device
+    sess = [session_modes(t, crit, cutoff, min_size) for t in tables]
+    l = tables[0].l
+    S = len(sess)
+    f = torch.zeros((S, max_modes), dtype=torch.float64, device=dev)
+    sh = torch.zeros((S, max_modes, l, 2), dtype=torch.float64, device=dev)
+    cnt = torch.zeros(S, dtype=torch.int32, device=dev)
+    for s, c in enumerate(sess):
+        k = min(c.n_clusters, max_modes)
+        f[s, :k] = c.f[:k]
+        sh[s, :k] = c.shape[:k]
+        cnt[s] = k
+    if ref is None:
+        k0 = int(cnt[0])
+        ref_f, ref_shape = f[0, :k0].contiguous(), sh[0, :k0].contiguous()
+    else:
+        ref_f, ref_shape = ref
+    match, success = api.track(ref_f, ref_shape, f, sh, cnt, df_max, macd_max)
+    return match, success, ref_f, ref_shape

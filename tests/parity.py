@@ -60,3 +60,85 @@ def compare_tables(gpu, ora, stable_flags=None):
                 st["max_dxi_stable"] = max(st["max_dxi_stable"], dxi)
                 st["min_mac_stable"] = min(st["min_mac_stable"], oracle.mac(p.shape, q.shape))
     return st
+
+
+def cells_to_table(cells, api, device, cap=None, l=None):
+    """Oracle cells of one lag (list of OrderCell, orders with a constant step) -> device
+    PoleTable (upload only; slots past count are zero)."""
+    import torch
+    n = [c.n for c in cells]
+    step = n[1] - n[0] if len(n) > 1 else 2
+    cap = cap or max(1, max(max(c.count, 0) for c in cells))
+    l = l or next(len(p.shape) for c in cells for p in c.poles)
+    t = api.PoleTable.empty(n[0], n[-1], step, l, "cpu", cap=cap)
+    for o, c in enumerate(cells):
+        t.count[o] = c.count
+        for s, p in enumerate(c.poles):
+            t.f[o, s], t.xi[o, s] = p.f, p.xi
+            t.mu_re[o, s], t.mu_im[o, s] = p.mu.real, p.mu.imag
+            t.mpc[o, s], t.mpd[o, s] = p.mpc, p.mpd
+            sh = np.asarray(p.shape)
+            t.shape[o, s, :, 0] = torch.from_numpy(sh.real.copy())
+            t.shape[o, s, :, 1] = torch.from_numpy(sh.imag.copy())
+    return t.to(device)
+
+
+def diagram_cells(d):
+    """synth.poles.Diagram -> per lag, list of oracle OrderCell."""
+    G, O = d.count.shape
+    out = []
+    for g in range(G):
+        cells = []
+        for o, n in enumerate(d.orders):
+            ps = [oracle.Pole(float(d.f[g, o, s]), float(d.xi[g, o, s]), 0j, d.shape[g, o, s].copy(),
+                              float(d.mpc[g, o, s]), float(d.mpd[g, o, s])) for s in range(d.count[g, o])]
+            cells.append(oracle.OrderCell(n, int(d.count[g, o]), ps))
+        out.append(cells)
+    return out
+
+
+def compare_clustering(gc, oc, cutoff):
+    """GPU Clustering vs oracle.cluster_3d output; returns a dict of statistics and asserts the
+    exact parts (stable-pole list, FCM cluster choice, retained set, cluster memberships)."""
+    from scipy.cluster.hierarchy import linkage
+    from scipy.spatial.distance import squareform
+    st = {}
+    idx = gc.pole_idx.cpu().numpy()
+    assert gc.n_stable == len(oc["idx"]) and np.array_equal(idx, oc["idx"])
+    X = gc.X.cpu().numpy()
+    st["max_dX"] = float(np.abs(X - oc["X"]).max()) if len(X) else 0.0
+    U = gc.U.cpu().numpy()
+    st["max_dU"] = float(np.abs(U - oc["U"]).max()) if len(U) else 0.0
+    st["max_dV"] = float(np.abs(gc.V.numpy() - oc["V"]).max()) if len(X) else 0.0
+    st["fcm_iters"] = (gc.fcm_iters, oc["iters"])
+    if len(X):
+        st["min_margin_P"] = float(np.abs(oc["U"][:, oc["phys"]] - 0.5).min())
+        assert gc.phys == oc["phys"]
+    ret = gc.retained.cpu().numpy()
+    assert np.array_equal(ret, np.flatnonzero(oc["keep"]))
+    labels = gc.labels.cpu().numpy()
+    assert np.array_equal(labels, oc["labels"]), (labels, oc["labels"])
+    cl = oc["clusters"]
+    assert gc.n_clusters == len(cl)
+    assert np.array_equal(gc.size.cpu().numpy(), [c["size"] for c in cl])
+    assert np.array_equal(gc.f.cpu().numpy(), [c["f"] for c in cl])
+    assert np.array_equal(gc.xi.cpu().numpy(), [c["xi"] for c in cl])
+    n = len(ret)
+    st["n_retained"], st["n_clusters"], st["n_components"] = n, len(cl), gc.n_components
+    if n >= 2:
+        D = oracle.pole_distances(oc["f"], oc["xi"], oc["shapes"])
+        # medoids: equal, or a tie within rounding of the oracle's summed distances
+        med = gc.medoid.cpu().numpy()
+        for k, c in enumerate(cl):
+            if med[k] != c["medoid"]:
+                sums = D[np.ix_(c["members"], c["members"])].sum(axis=1)
+                a, b = sums[c["members"].index(med[k])], sums[c["members"].index(c["medoid"])]
+                assert abs(a - b) <= 1e-12 * max(abs(b), 1e-300), (k, a, b)
+        Z = linkage(squareform(D, checks=False), method="average")
+        h_o = np.sort(Z[Z[:, 2] <= cutoff, 2])
+        h_g = np.sort(gc.merges_h.cpu().numpy())
+        assert len(h_o) == len(h_g) == gc.n_merges
+        st["max_dh"] = float(np.abs(h_o - h_g).max()) if len(h_o) else 0.0
+        above = Z[:, 2][Z[:, 2] > cutoff]
+        st["cut_margin"] = float(min(np.abs(Z[:, 2] - cutoff).min(), 1.0))
+    return st
