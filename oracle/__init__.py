@@ -29,6 +29,8 @@ from .params import (time_lag_step, lag_of_step, lag_grid, min_rank_percent,
 from .cluster import (stable_pole_features, fuzzy_cmeans, fcm_memberships, select_physical,
                       pole_distances, hierarchical_clusters, cluster_3d)
 from .track import track_session, success_ratio
+from .preprocess import detrend, preprocess, lowpass_sos, filtfilt_zero_state, rate_ratio
+from .frame import frame_matrices, discretize, simulate as simulate_frame
 
 __all__ = [
     "covariances", "covariance_partial_sums", "toeplitz", "philox4x32_10", "philox_words",
@@ -38,4 +40,6 @@ __all__ = [
     "time_lag_step", "lag_of_step", "lag_grid", "min_rank_percent", "sample_count",
     "stable_pole_features", "fuzzy_cmeans", "fcm_memberships", "select_physical", "pole_distances",
     "hierarchical_clusters", "cluster_3d", "track_session", "success_ratio",
+    "detrend", "preprocess", "lowpass_sos", "filtfilt_zero_state", "rate_ratio",
+    "frame_matrices", "discretize", "simulate_frame",
 ]
