@@ -395,7 +395,7 @@ def identify_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, cutof
     """The whole 3D-RSVD identification (§2.3 steps i-iii): lag sweep and 3D
     stabilization (lag_sweep_3d), then the two-stage clustering of the stable poles (api.cluster3d;
     every rank clusters the gathered diagram). min_size defaults to 20 % of the diagram's
-    (lag, order) cells, the share used for the paper's frame in tests/test_oracle_cluster.py.
+    (lag, order) cells (the share used in the NEXT-2 tests of the paper's frame).
     Returns (tables, flags, stable_count, Clustering)."""
     lags = sorted(lags)
     tables, flags, counts = lag_sweep_3d(Y, P, lags, crit, rank, world, group, n_streams, timing)
