@@ -343,6 +343,56 @@ SSI_API ssi_status ssi_track(const double* ref_f, const double* ref_shape, int32
                              void* stream);
 
 /* ------------------------------------------------------------------------------
+ * NEXT-4. Upstream preprocessing of raw acceleration records (§3.2): "elimination
+ * of linear trends and downsampling to 40 Hz (eighth-order low-pass Chebyshev Type I filter with
+ * a cut-off frequency of 0.8·20 Hz followed by a decimation to 40 Hz)". Readings P-1..P-3 of
+ * DESIGN.md §3:
+ *  P-1 per channel, subtract the least-squares line alpha + beta h (h = 0..N-1);
+ *  P-2 Chebyshev-I low-pass of the given even order (2..16) and passband ripple rp_db, passband
+ *      edge fc_hz, designed by the bilinear transform (prewarped) for the rate L fs_in, applied
+ *      zero-phase: forward, then backward, zero initial state, no padding;
+ *  P-3 upsample by L (L x[n] at n L, zeros between), filter (P-2), keep every M-th sample
+ *      starting with the first: Z has N_out = floor(N L / M) rows (125 -> 40 Hz: L = 8, M = 25;
+ *      an integer decimation by q: L = 1, M = q).
+ *  Y : [N][ldY] SSI_F32 / SSI_F64, ldY >= l. Z : [N_out][ldZ] of out_dtype, ldZ >= l.
+ *  Errors: N < 2, l < 1, L < 1, M < 1, fs_in <= 0, odd order or order outside 2..16, rp_db <= 0,
+ *  fc_hz outside (0, L fs_in / 2), N_out < 1 -> INVALID_ARG; ld too small -> SHAPE; workspace
+ *  (O(N L l) doubles: the forward-filtered signal at the high rate) too small -> WORKSPACE.
+ * ---------------------------------------------------------------------------- */
+SSI_API ssi_status ssi_preprocess(const void* Y, int32_t dtype, int64_t N, int32_t l, int64_t ldY, double fs_in,
+                                  int32_t L, int32_t M, int32_t order, double rp_db, double fc_hz, void* Z,
+                                  int32_t out_dtype, int64_t ldZ, void* ws, size_t ws_bytes, void* stream);
+SSI_API ssi_status ssi_preprocess_ws(int64_t N, int32_t l, int32_t L, int32_t order, size_t* bytes);
+/* The filter of P-2 as second-order sections: sos [order/2][5] = (b0, b1, b2, a1, a2) with
+ * a0 = 1 (verification entry point; same design kernel as ssi_preprocess). */
+SSI_API ssi_status ssi_lowpass_design(int32_t order, double rp_db, double fc_hz, double fs_hz, double* sos,
+                                      void* stream);
+
+/* ------------------------------------------------------------------------------
+ * NEXT-4. The paper's shear-type frame generator (§3.1; §3.1.2;
+ * readings F-1..F-4 of DESIGN.md §3): n_dof storeys of mass m and stiffness k (K tridiagonal:
+ * 2k on the diagonal except k at the roof, -k off it), Rayleigh damping C = a M + b K with
+ * damping ratio xi at undamped modes mode_a and mode_b; state x = (q, dq/dt), a Gaussian force
+ * at every DOF held over each step (zero-order hold: [[A_d, B_d], [0, I]] = exp([[A_c, B_c],
+ * [0, 0]] / fs)); x_0 = 0, x_{h+1} = A_d x_h + B_d u_h; outputs the accelerations
+ * y_h = C_o x_h, C_o = [-M^-1 K, -M^-1 C]; the first n_burn samples are discarded; channel c
+ * gets Gaussian noise of variance P_c / 10^(snr_db/10), P_c the mean square of the kept clean
+ * channel. u_h: column h of the reading-A-11 Philox Gaussian sketch n_dof x (n_burn + N) with
+ * (seed, stream 2 stream_id); v_h: column h of the l x N sketch with (seed, stream 2 stream_id + 1).
+ *  Y : [N][ldY] (dtype), clean (may be NULL): [N][n_dof] FP64 noise-free outputs.
+ *  Errors: n_dof outside 1..12, m, k, fs <= 0, xi outside (0, 1), modes outside 1..n_dof or
+ *  equal, N < 1, n_burn < 0, (N + n_burn) n_dof >= 2^31 -> INVALID_ARG; ldY < n_dof -> SHAPE.
+ * ssi_frame_model writes the model: Ad [2n][2n], Bd [2n][n], Co [n][2n] row-major, ab = (a, b).
+ * ---------------------------------------------------------------------------- */
+SSI_API ssi_status ssi_frame_simulate(int32_t n_dof, double m, double k, double xi, int32_t mode_a, int32_t mode_b,
+                                      double fs, int64_t N, int64_t n_burn, double snr_db, uint64_t seed,
+                                      uint64_t stream_id, void* Y, int32_t dtype, int64_t ldY, double* clean,
+                                      void* ws, size_t ws_bytes, void* stream);
+SSI_API ssi_status ssi_frame_simulate_ws(int32_t n_dof, int64_t N, int64_t n_burn, size_t* bytes);
+SSI_API ssi_status ssi_frame_model(int32_t n_dof, double m, double k, double xi, int32_t mode_a, int32_t mode_b,
+                                   double fs, double* Ad, double* Bd, double* Co, double* ab, void* stream);
+
+/* ------------------------------------------------------------------------------
  * Status helpers.
  * ---------------------------------------------------------------------------- */
 /* Zeroes the 256-byte header of ws (the sticky status word), enqueued on stream. */

@@ -60,6 +60,12 @@ SIGNATURES = {
                                  SZ, P]),
     "ssi_cluster_stage2_ws": (I32, [I32, I32, C.POINTER(SZ)]),
     "ssi_track": (I32, [P, P, I32, P, P, P, I32, I32, I32, D, D, P, P, P]),
+    "ssi_preprocess": (I32, [P, I32, I64, I32, I64, D, I32, I32, I32, D, D, P, I32, I64, P, SZ, P]),
+    "ssi_preprocess_ws": (I32, [I64, I32, I32, I32, C.POINTER(SZ)]),
+    "ssi_lowpass_design": (I32, [I32, D, D, D, P, P]),
+    "ssi_frame_simulate": (I32, [I32, D, D, D, I32, I32, D, I64, I64, D, U64, U64, P, I32, I64, P, P, SZ, P]),
+    "ssi_frame_simulate_ws": (I32, [I32, I64, I64, C.POINTER(SZ)]),
+    "ssi_frame_model": (I32, [I32, D, D, D, I32, I32, D, P, P, P, P, P]),
     "ssi_fetch_device_status": (I32, [P, C.POINTER(I32)]),
     "ssi_clear_status": (I32, [P, P]),
     "ssi_status_string": (C.c_char_p, [I32]),

@@ -12,6 +12,8 @@ runs in the library's sm_100a kernels. Functions mirror the C entry points:
     cluster3d(tables, flags, crit)   -> Clustering (two-stage: fuzzy C-means + average linkage)
                                                                     (NEXT-2, PAPER.md:293, :402-415)
     track(ref_f, ref_shape, f, shape, count) -> match, success      (NEXT-2, PAPER.md:544)
+    preprocess(Y, fs_in, fs_out)     -> detrended, low-passed, resampled record (NEXT-4)
+    frame_simulate(N, fs, snr_db, ...) -> shear-frame acceleration record      (NEXT-4)
 """
 from __future__ import annotations
 
@@ -443,3 +445,84 @@ def track(ref_f: torch.Tensor, ref_shape: torch.Tensor, f: torch.Tensor, shape: 
     call("ssi_track", _ptr(ref_f), _ptr(ref_shape), R, _ptr(f), _ptr(shape), _ptr(count), S, M, l,
          float(df_max), float(macd_max), _ptr(match), _ptr(success), _stream())
     return match, success
+
+
+# ------------------------------------------------------------------ NEXT-4: preprocessing + generator
+def rate_ratio(fs_in: float, fs_out: float):
+    """(L, M) with fs_out / fs_in = L / M in lowest terms (integral rates in Hz)."""
+    from fractions import Fraction
+    fr = Fraction(int(round(fs_out)), int(round(fs_in)))
+    return fr.numerator, fr.denominator
+
+
+def preprocess_ws_bytes(N, l, L, order=8) -> int:
+    b = C.c_size_t(0)
+    call("ssi_preprocess_ws", N, l, L, order, C.byref(b))
+    return b.value
+
+
+def preprocess(Y: torch.Tensor, fs_in: float, fs_out: float, order: int = 8, rp_db: float = 0.05,
+               fc_hz: float | None = None, out_dtype=torch.float64, out: torch.Tensor | None = None,
+               ws: torch.Tensor | None = None) -> torch.Tensor:
+    """ssi_preprocess (readings P-1..P-3): detrend, upsample by L, zero-phase Chebyshev-I low-pass
+    (edge 0.8 fs_out / 2 unless fc_hz is given) at L fs_in, keep every M-th sample."""
+    _require_cuda(Y)
+    if Y.dim() != 2 or Y.stride(1) != 1:
+        raise ValueError("Y must be [N][l] with unit channel stride")
+    dt = {torch.float32: SSI_F32, torch.float64: SSI_F64}
+    N, l = Y.shape
+    L, M = rate_ratio(fs_in, fs_out)
+    fc = 0.8 * fs_out / 2.0 if fc_hz is None else fc_hz
+    n_out = (N * L) // M
+    Z = out if out is not None else torch.empty((n_out, l), dtype=out_dtype, device=Y.device)
+    if ws is None:
+        ws = _workspace(preprocess_ws_bytes(N, l, L, order), Y.device)
+    call("ssi_preprocess", _ptr(Y), dt[Y.dtype], N, l, Y.stride(0), float(fs_in), L, M, order, float(rp_db),
+         float(fc), _ptr(Z), dt[Z.dtype], Z.stride(0), _ptr(ws), ws.numel(), _stream())
+    return Z
+
+
+def lowpass_design(order: int, rp_db: float, fc_hz: float, fs_hz: float, device="cuda") -> torch.Tensor:
+    """Second-order sections [order/2][5] = (b0, b1, b2, a1, a2) of ssi_preprocess's filter."""
+    sos = torch.empty((order // 2, 5), dtype=torch.float64, device=device)
+    call("ssi_lowpass_design", order, float(rp_db), float(fc_hz), float(fs_hz), _ptr(sos), _stream())
+    return sos
+
+
+@dataclass(frozen=True)
+class Frame:
+    """Shear-type frame of PAPER.md:314 (defaults: the paper's 10-DOF case)."""
+    n_dof: int = 10
+    m: float = 100.0
+    k: float = 5.0e6
+    xi: float = 0.01
+    mode_a: int = 1
+    mode_b: int = 4
+
+
+def frame_model(frame: Frame, fs: float, device="cuda"):
+    """(A_d [2n][2n], B_d [2n][n], C_o [n][2n], (a, b)) computed by ssi_frame_model."""
+    n = frame.n_dof
+    z = lambda *s: torch.empty(s, dtype=torch.float64, device=device)
+    Ad, Bd, Co, ab = z(2 * n, 2 * n), z(2 * n, n), z(n, 2 * n), z(2)
+    call("ssi_frame_model", n, frame.m, frame.k, frame.xi, frame.mode_a, frame.mode_b, float(fs), _ptr(Ad), _ptr(Bd),
+         _ptr(Co), _ptr(ab), _stream())
+    return Ad, Bd, Co, ab
+
+
+def frame_simulate(N: int, fs: float, snr_db: float, seed: int, stream_id: int = 0, frame: Frame = Frame(),
+                   n_burn: int | None = None, dtype=torch.float64, device="cuda", with_clean: bool = False):
+    """ssi_frame_simulate (readings F-1..F-4): an [N][n_dof] acceleration record of the frame at fs Hz
+    (burn-in 10 s unless n_burn is given); with_clean also returns the noise-free outputs."""
+    n = frame.n_dof
+    nb = int(round(10.0 * fs)) if n_burn is None else n_burn
+    Y = torch.empty((N, n), dtype=dtype, device=device)
+    clean = torch.empty((N, n), dtype=torch.float64, device=device) if with_clean else None
+    b = C.c_size_t(0)
+    call("ssi_frame_simulate_ws", n, N, nb, C.byref(b))
+    ws = _workspace(b.value, device)
+    call("ssi_frame_simulate", n, frame.m, frame.k, frame.xi, frame.mode_a, frame.mode_b, float(fs), N, nb,
+         float(snr_db), C.c_uint64(seed), C.c_uint64(stream_id), _ptr(Y),
+         {torch.float32: SSI_F32, torch.float64: SSI_F64}[dtype], Y.stride(0),
+         _ptr(clean) if clean is not None else None, _ptr(ws), ws.numel(), _stream())
+    return (Y, clean) if with_clean else Y

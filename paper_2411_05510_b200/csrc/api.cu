@@ -10,6 +10,7 @@
 #include "linalg.cuh"
 #include "rsvd.cuh"
 #include "cluster.cuh"
+#include "preprocess.cuh"
 
 namespace ssi {
 
@@ -375,6 +376,71 @@ ssi_status ssi_track(const double* ref_f, const double* ref_shape, int32_t n_ref
               SSI_ERR_INVALID_ARG, "ssi_track: need n_ref, n_sess, max_modes, l >= 1 and n_ref * max_modes <= 16384");
   return track_run(ref_f, ref_shape, n_ref, f, shape, count, n_sess, max_modes, l, df_max, macd_max, match, success,
                    S(stream));
+}
+
+ssi_status ssi_preprocess_ws(int64_t N, int32_t l, int32_t L, int32_t order, size_t* bytes) {
+  SSI_REQUIRE(bytes && N >= 2 && l >= 1 && L >= 1 && order >= 2 && order <= 16 && order % 2 == 0,
+              SSI_ERR_INVALID_ARG, "ssi_preprocess_ws: bad arguments");
+  *bytes = preprocess_ws_bytes(N, l, L, order);
+  return SSI_OK;
+}
+
+ssi_status ssi_preprocess(const void* Y, int32_t dtype, int64_t N, int32_t l, int64_t ldY, double fs_in, int32_t L,
+                          int32_t M, int32_t order, double rp_db, double fc_hz, void* Z, int32_t out_dtype,
+                          int64_t ldZ, void* ws, size_t ws_bytes, void* stream) {
+  SSI_REQUIRE(Y && Z && ws, SSI_ERR_INVALID_ARG, "ssi_preprocess: NULL pointer");
+  SSI_REQUIRE((dtype == SSI_F32 || dtype == SSI_F64) && (out_dtype == SSI_F32 || out_dtype == SSI_F64),
+              SSI_ERR_DTYPE, "ssi_preprocess: dtype must be SSI_F32 or SSI_F64");
+  SSI_REQUIRE(N >= 2 && l >= 1 && L >= 1 && M >= 1 && fs_in > 0.0 && order >= 2 && order <= 16 && order % 2 == 0 &&
+                  rp_db > 0.0 && fc_hz > 0.0 && fc_hz < 0.5 * L * fs_in && (N * L) / M >= 1,
+              SSI_ERR_INVALID_ARG, "ssi_preprocess: bad sizes, rates or filter parameters");
+  SSI_REQUIRE(ldY >= l && ldZ >= l, SSI_ERR_SHAPE, "ssi_preprocess: ldY or ldZ < l");
+  const size_t need = preprocess_ws_bytes(N, l, L, order);
+  SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_preprocess: workspace %zu < %zu", ws_bytes, need);
+  return preprocess_run(Y, dtype, N, l, ldY, fs_in, L, M, order, rp_db, fc_hz, Z, out_dtype, ldZ, ws, S(stream));
+}
+
+ssi_status ssi_lowpass_design(int32_t order, double rp_db, double fc_hz, double fs_hz, double* sos, void* stream) {
+  SSI_REQUIRE(sos && order >= 2 && order <= 16 && order % 2 == 0 && rp_db > 0.0 && fc_hz > 0.0 &&
+                  fc_hz < 0.5 * fs_hz,
+              SSI_ERR_INVALID_ARG, "ssi_lowpass_design: bad arguments");
+  return lowpass_design(order, rp_db, fc_hz, fs_hz, sos, S(stream));
+}
+
+static ssi_status frame_check(int32_t n_dof, double m, double k, double xi, int32_t mode_a, int32_t mode_b, double fs,
+                              const char* fn) {
+  SSI_REQUIRE(n_dof >= 1 && n_dof <= kFrameMaxDof && m > 0.0 && k > 0.0 && fs > 0.0 && xi > 0.0 && xi < 1.0 &&
+                  mode_a >= 1 && mode_a <= n_dof && mode_b >= 1 && mode_b <= n_dof && mode_a != mode_b,
+              SSI_ERR_INVALID_ARG, "%s: bad frame parameters", fn);
+  return SSI_OK;
+}
+
+ssi_status ssi_frame_simulate_ws(int32_t n_dof, int64_t N, int64_t n_burn, size_t* bytes) {
+  SSI_REQUIRE(bytes && n_dof >= 1 && n_dof <= kFrameMaxDof && N >= 1 && n_burn >= 0, SSI_ERR_INVALID_ARG,
+              "ssi_frame_simulate_ws: bad arguments");
+  *bytes = frame_ws_bytes(n_dof, N, n_burn);
+  return SSI_OK;
+}
+
+ssi_status ssi_frame_model(int32_t n_dof, double m, double k, double xi, int32_t mode_a, int32_t mode_b, double fs,
+                           double* Ad, double* Bd, double* Co, double* ab, void* stream) {
+  SSI_TRY(frame_check(n_dof, m, k, xi, mode_a, mode_b, fs, "ssi_frame_model"));
+  SSI_REQUIRE(Ad && Bd && Co && ab, SSI_ERR_INVALID_ARG, "ssi_frame_model: NULL pointer");
+  return frame_model_run(n_dof, m, k, xi, mode_a, mode_b, fs, Ad, Bd, Co, ab, S(stream));
+}
+
+ssi_status ssi_frame_simulate(int32_t n_dof, double m, double k, double xi, int32_t mode_a, int32_t mode_b, double fs,
+                              int64_t N, int64_t n_burn, double snr_db, uint64_t seed, uint64_t stream_id, void* Y,
+                              int32_t dtype, int64_t ldY, double* clean, void* ws, size_t ws_bytes, void* stream) {
+  SSI_TRY(frame_check(n_dof, m, k, xi, mode_a, mode_b, fs, "ssi_frame_simulate"));
+  SSI_REQUIRE(Y && ws && N >= 1 && n_burn >= 0 && (N + n_burn) * n_dof < (int64_t(1) << 31) && isfinite(snr_db),
+              SSI_ERR_INVALID_ARG, "ssi_frame_simulate: bad arguments");
+  SSI_REQUIRE(dtype == SSI_F32 || dtype == SSI_F64, SSI_ERR_DTYPE, "ssi_frame_simulate: dtype");
+  SSI_REQUIRE(ldY >= n_dof, SSI_ERR_SHAPE, "ssi_frame_simulate: ldY < n_dof");
+  const size_t need = frame_ws_bytes(n_dof, N, n_burn);
+  SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_frame_simulate: workspace %zu < %zu", ws_bytes, need);
+  return frame_simulate_run(n_dof, m, k, xi, mode_a, mode_b, fs, N, n_burn, snr_db, seed, stream_id, Y, dtype, ldY,
+                            clean, ws, S(stream));
 }
 
 }  // extern "C"
