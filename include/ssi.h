@@ -207,6 +207,8 @@ SSI_API ssi_status ssi_gaussian_sketch(int32_t m, int32_t k, uint64_t seed, uint
  *   Poles: Im(mu) > 0, 0 < xi < 1 (reading A-14), shapes unit-norm with the largest
  *   component real positive (A-15), MPC / MPD (A-16), sorted by (f, xi).
  *  U : m x n_max col-major (m = l*i, ldU >= m), S : [>= n_max] descending (ssi_rsvd).
+ *  n_max <= 512 (PAPER.md:518 sweeps orders up to 400); orders whose banded Schur matrix
+ *  exceeds shared memory (n_max above ~230) keep it in the workspace (L2-resident).
  *  out : caller-allocated pole table (device arrays) with n_orders = number of orders,
  *        cap >= n_max/2, l = channels. count[o] = number of poles, or -1 when
  *        S[n-1] < 1e-12 S[0] (order above the numerical rank) or when the

@@ -265,8 +265,8 @@ ssi_status ssi_modal_sweep_ws(int32_t l, int32_t i, int32_t n_min, int32_t n_max
                               size_t* bytes) {
   SSI_REQUIRE(bytes && l > 0 && i >= 2, SSI_ERR_INVALID_ARG, "ssi_modal_sweep_ws: bad sizes");
   SSI_TRY(check_orders(n_min, n_max, n_step));
-  SSI_REQUIRE(modal_smem_bytes(n_max, n_max / 2) <= 227 * 1024, SSI_ERR_INVALID_ARG,
-              "ssi_modal_sweep_ws: n_max %d too large for the one-CTA eigen-solver", n_max);
+  SSI_REQUIRE(n_max <= kModalMaxOrder && modal_smem_bytes(n_max, n_max / 2, modal_band_global(n_max)) <= kModalSmemMax,
+              SSI_ERR_INVALID_ARG, "ssi_modal_sweep_ws: n_max %d > %d", n_max, kModalMaxOrder);
   *bytes = modal_ws_bytes(l, i, n_min, n_max, n_step);
   return SSI_OK;
 }
@@ -287,8 +287,10 @@ ssi_status ssi_modal_sweep(const double* U, int64_t ldU, const double* S_, int32
   SSI_REQUIRE(out->count && out->f && out->xi && out->mu_re && out->mu_im && out->mpc && out->mpd &&
                   out->shape,
               SSI_ERR_INVALID_ARG, "ssi_modal_sweep: NULL pole-table array");
-  SSI_REQUIRE(modal_smem_bytes(n_max, out->cap) <= 227 * 1024, SSI_ERR_INVALID_ARG,
-              "ssi_modal_sweep: n_max %d too large for the one-CTA eigen-solver", n_max);
+  SSI_REQUIRE(n_max <= kModalMaxOrder &&
+                  modal_smem_bytes(n_max, out->cap, modal_band_global(n_max)) <= kModalSmemMax,
+              SSI_ERR_INVALID_ARG, "ssi_modal_sweep: n_max %d > %d or pole-table cap %d too large", n_max,
+              kModalMaxOrder, out->cap);
   const size_t need = modal_ws_bytes(l, i, n_min, n_max, n_step);
   SSI_REQUIRE(ws_bytes >= need, SSI_ERR_WORKSPACE, "ssi_modal_sweep: workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = S(stream);

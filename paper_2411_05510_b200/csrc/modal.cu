@@ -142,6 +142,8 @@ struct EigArgs {
   double dt;
   ssi_pole_table tab;
   int profile;          // development: print phase clocks of the largest order
+  double* band_g;       // non-null: the banded H of order o lives in global memory (L2) at
+                        // band_g + o * band_elems(n_max) (orders whose band exceeds shared memory)
 };
 
 struct Smem {
@@ -351,9 +353,10 @@ constexpr int HT = 1024;
 #endif
 constexpr int HQS = SSI_HESS_QS;   // warps sharing a 32-row block of the right update (column split)
 constexpr int HW = HT / 32;
+constexpr int kHessMaxN = 512;   // Householder vector in shared memory: orders up to 513
 
 __global__ void __launch_bounds__(HT) hess_order_kernel(EigArgs g) {
-  __shared__ double v[256 + 8];
+  __shared__ double v[kHessMaxN + 8];
   __shared__ double red[HW];
   __shared__ double part[HQS][(HW / HQS) * 32];
   __shared__ double sh_tau, sh_scal, sh_beta;
@@ -521,7 +524,11 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   {
     char* p = reinterpret_cast<char*>(dsm);
     const int nm = g.n_max;
-    s.H = reinterpret_cast<double*>(p);      p += sizeof(double) * band_elems(nm);
+    if (g.band_g) {
+      s.H = g.band_g + int64_t(o) * int64_t(band_elems(nm));
+    } else {
+      s.H = reinterpret_cast<double*>(p);    p += sizeof(double) * band_elems(nm);
+    }
     s.x = reinterpret_cast<double*>(p);      p += sizeof(double) * x_elems(nm);
     s.cre = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
     s.cim = reinterpret_cast<double*>(p);    p += sizeof(double) * cap;
@@ -1169,15 +1176,21 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
 
 }  // namespace
 
-size_t modal_smem_bytes(int n_max, int cap) {
+// dynamic shared memory of eig_order_kernel; band_global: the banded H is in global memory
+size_t modal_smem_bytes(int n_max, int cap, bool band_global) {
   return sizeof(QEntry) * NSLOT + 3 * sizeof(uint64_t) * NSLOT +
-         sizeof(double) * (band_elems(n_max) + x_elems(n_max) +
+         sizeof(double) * ((band_global ? 0 : band_elems(n_max)) + x_elems(n_max) +
                            4 * size_t(cap)) +
          sizeof(int) * (size_t(n_max) + 1 + cap) + 64;
 }
 
+// Orders up to ~230 keep the banded Hessenberg/Schur matrix in shared memory; beyond that (the
+// paper's bridge sweeps reach order 400) it lives in an L2-resident global slab per
+// order and the same kernel addresses it through generic pointers.
+bool modal_band_global(int n_max) { return modal_smem_bytes(n_max, n_max / 2, false) > kModalSmemMax; }
+
 struct ModalWork {
-  double *Rinv, *W, *M, *C, *Qup;
+  double *Rinv, *W, *M, *C, *Qup, *band;
   CholQRWork cq;
   double* partial;
 };
@@ -1192,6 +1205,7 @@ static void modal_carve(Carver& c, int l, int i, int n_min, int n_max, int n_ste
   w.M = c.take<double>(size_t(sq));
   w.C = c.take<double>(size_t(lin) * l);
   w.Qup = c.take<double>(size_t(mu) * n_max);
+  w.band = modal_band_global(n_max) ? c.take<double>(size_t(no) * band_elems(n_max)) : nullptr;
   w.partial = c.take<double>(gemm_partial_elems(n_max, n_max, gemm_pick_splits(n_max, n_max, mu)) + 1);
   cholqr_carve(c, mu, n_max, w.cq);
 }
@@ -1221,8 +1235,9 @@ ssi_status modal_run(const double* U, int64_t ldU, const double* S, int l, int i
                    n_max, splits, w.partial, st));
   // M_n = Rinv[:n,:n] W[:n,:n] for every order
   SSI_TRY(gemm_f64_orders(no, n_min, n_step, w.Rinv, n_max, w.W, n_max, w.M, st));
-  EigArgs g{w.M, w.C, U, ldU, S, l, n_min, n_step, no, n_max, tab.cap, dt, tab, getenv("SSI_EIG_PROFILE") ? atoi(getenv("SSI_EIG_PROFILE")) : 0};
-  const size_t smem = modal_smem_bytes(n_max, tab.cap);
+  EigArgs g{w.M, w.C, U, ldU, S, l, n_min, n_step, no, n_max, tab.cap, dt, tab,
+            getenv("SSI_EIG_PROFILE") ? atoi(getenv("SSI_EIG_PROFILE")) : 0, w.band};
+  const size_t smem = modal_smem_bytes(n_max, tab.cap, w.band != nullptr);
   cudaFuncSetAttribute(eig_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   hess_order_kernel<<<no, HT, 0, st>>>(g);
   SSI_TRY(launch_check("hess_order_kernel"));

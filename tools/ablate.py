@@ -10,13 +10,13 @@ cfg = synth.config("c3")
 Y, _ = synth.make_record(cfg)
 Ys = [torch.from_numpy(Y).cuda(), torch.from_numpy(synth.make_record(synth.config("c3", seed=103))[0]).cuda()]
 P = drivers.SweepParams(l=cfg.l, i=cfg.i, n_max=cfg.n_max, p=cfg.p, q=cfg.q, fs=cfg.fs, seed=cfg.philox_key,
-                        cov_mode="int8x3")
-ns = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+                        cov_mode=os.environ.get("SSI_COV_MODE", "spectral"))
+ns = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 engines = [drivers.Engine(P, cfg.N) for _ in range(ns)]
 streams = [torch.cuda.Stream() for _ in range(ns)]
 
 
-def run(stages, n=12):
+def run(stages, n=48):
     def one(j):
         e, st = engines[j % ns], streams[j % ns]
         with torch.cuda.stream(st):
@@ -36,6 +36,7 @@ def run(stages, n=12):
     return n / (time.perf_counter() - t0)
 
 
-for stages in (("cov", "rsvd", "modal"), ("cov",), ("rsvd",), ("modal",), ("cov", "rsvd"), ("rsvd", "modal"), ("cov", "modal")):
+for stages in (("cov", "rsvd", "modal"), ("cov",), ("rsvd",), ("modal",), ("cov", "rsvd"), ("rsvd", "modal"),
+               ("cov", "modal"), ("cov", "rsvd", "modal")):
     r = run(stages)
     print(f"{'+'.join(stages):20s} {r:7.2f} rec/s  {1e3 / r:7.2f} ms/rec")
