@@ -35,7 +35,9 @@
  *    extra CholeskyQR pass runs before the usual second one (shifted CholeskyQR3). The
  *    decision is taken on the device (conditional launches), so it costs no host
  *    synchronisation; the status stays SSI_OK. Only a breakdown of the final pass, or a
- *    non-finite Gram matrix, sets SSI_ERR_NUMERIC.
+ *    non-finite Gram matrix, sets SSI_ERR_NUMERIC. Sketch widths k > 512 (the paper's rank rule
+ *    at bridge sizes, blocked whole-GPU Cholesky) have no shifted retry: any breakdown sets
+ *    SSI_ERR_NUMERIC.
  *  - Determinism: fixed inputs, seed and launch configuration give bit-identical
  *    outputs run to run (fixed reduction orders, no floating-point atomics).
  */
@@ -153,8 +155,11 @@ SSI_API ssi_status ssi_toeplitz(const double* R, int32_t l, int32_t i, double* T
  *   q times: Z = qr(T^T Q); Q = qr(T Z);
  *   B = Q^T T; small SVD B = U~ S V^T (CholeskyQR2 of B^T + one-sided Jacobi);
  *   U = Q U~.
- *  T : m x m row-major FP64, ldT >= m.   k : sketch width (n_max + p), 1 <= k <= min(m, 512)
- *      (the small SVD runs on one thread-block cluster; larger k -> INVALID_ARG, synchronously).
+ *  T : m x m row-major FP64, ldT >= m.   k : sketch width (n_max + p, or the paper's rank rule
+ *      k = ceil(kbar(T) % T)), 1 <= k <= min(m, 4096): k <= 512 runs the small
+ *      SVD on one thread-block cluster, larger k the blocked whole-GPU Cholesky / triangular solve
+ *      and a block one-sided Jacobi (one persistent CTA per 32-column block pair); larger k ->
+ *      INVALID_ARG, synchronously.
  *  U : output m x n_keep col-major FP64 (leading left singular vectors), ldU >= m,
  *      1 <= n_keep <= k. Column signs are arbitrary (reading A-13).
  *  S : output [k] FP64, descending.
@@ -180,7 +185,7 @@ SSI_API ssi_status ssi_rsvd_ws(int32_t m, int32_t k, int32_t n_keep, size_t* byt
  * its block-Toeplitz structure"). Results equal ssi_rsvd's up to FP64 rounding order.
  *  R : [>= 2i-1][l][l] row-major FP64, R_k at block k-1 (ssi_covariances, lag_lo = 1).
  *  m = l*i; k, q, seed, stream_id, n_keep, U, ldU, S as in ssi_rsvd.
- *  Errors: as ssi_rsvd (k <= min(l*i, 512)); i < 1 or l < 1 -> INVALID_ARG.
+ *  Errors: as ssi_rsvd (k <= min(l*i, 4096)); i < 1 or l < 1 -> INVALID_ARG.
  * ---------------------------------------------------------------------------- */
 SSI_API ssi_status ssi_rsvd_toeplitz(const double* R, int32_t l, int32_t i, int32_t k, int32_t q,
                              uint64_t seed, uint64_t stream_id, int32_t n_keep,

@@ -192,7 +192,7 @@ ssi_status ssi_rsvd_ws(int32_t m, int32_t k, int32_t n_keep, size_t* bytes) {
   SSI_REQUIRE(bytes, SSI_ERR_INVALID_ARG, "ssi_rsvd_ws: NULL bytes");
   SSI_REQUIRE(m > 0 && k >= 1 && k <= m && n_keep >= 1 && n_keep <= k, SSI_ERR_INVALID_ARG,
               "ssi_rsvd_ws: bad sizes");
-  SSI_REQUIRE(k <= kSvdMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd_ws: k = %d > %d unsupported", k, kSvdMaxK);
+  SSI_REQUIRE(k <= kBigMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd_ws: k = %d > %d unsupported", k, kBigMaxK);
   *bytes = rsvd_ws_bytes(m, k);
   return SSI_OK;
 }
@@ -202,7 +202,7 @@ ssi_status ssi_rsvd(const double* T, int64_t ldT, int32_t m, int32_t k, int32_t 
                     void* ws, size_t ws_bytes, void* stream) {
   SSI_REQUIRE(T && U && S_ && ws, SSI_ERR_INVALID_ARG, "ssi_rsvd: NULL pointer");
   SSI_REQUIRE(m > 0 && k >= 1 && k <= m, SSI_ERR_INVALID_ARG, "ssi_rsvd: need 1 <= k <= m");
-  SSI_REQUIRE(k <= kSvdMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd: k = %d > %d unsupported", k, kSvdMaxK);
+  SSI_REQUIRE(k <= kBigMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd: k = %d > %d unsupported", k, kBigMaxK);
   SSI_REQUIRE(n_keep >= 1 && n_keep <= k, SSI_ERR_INVALID_ARG, "ssi_rsvd: need 1 <= n_keep <= k");
   SSI_REQUIRE(q >= 0, SSI_ERR_INVALID_ARG, "ssi_rsvd: q < 0");
   SSI_REQUIRE(ldT >= m && ldU >= m, SSI_ERR_SHAPE, "ssi_rsvd: ldT or ldU < m");
@@ -217,7 +217,7 @@ ssi_status ssi_rsvd_toeplitz_ws(int32_t l, int32_t i, int32_t k, int32_t n_keep,
   SSI_REQUIRE(bytes, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz_ws: NULL bytes");
   SSI_REQUIRE(l > 0 && i > 0 && k >= 1 && int64_t(k) <= int64_t(l) * i && n_keep >= 1 && n_keep <= k,
               SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz_ws: bad sizes");
-  SSI_REQUIRE(k <= kSvdMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz_ws: k = %d > %d unsupported", k, kSvdMaxK);
+  SSI_REQUIRE(k <= kBigMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz_ws: k = %d > %d unsupported", k, kBigMaxK);
   *bytes = rsvd_bt_ws_bytes(l, i, k);
   return SSI_OK;
 }
@@ -230,7 +230,7 @@ ssi_status ssi_rsvd_toeplitz(const double* R, int32_t l, int32_t i, int32_t k, i
   const int64_t m = int64_t(l) * i;
   SSI_REQUIRE(m <= INT32_MAX, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: l*i too large");
   SSI_REQUIRE(k >= 1 && k <= m, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: need 1 <= k <= l*i");
-  SSI_REQUIRE(k <= kSvdMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: k = %d > %d unsupported", k, kSvdMaxK);
+  SSI_REQUIRE(k <= kBigMaxK, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: k = %d > %d unsupported", k, kBigMaxK);
   SSI_REQUIRE(n_keep >= 1 && n_keep <= k, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: need 1 <= n_keep <= k");
   SSI_REQUIRE(q >= 0, SSI_ERR_INVALID_ARG, "ssi_rsvd_toeplitz: q < 0");
   SSI_REQUIRE(ldU >= m, SSI_ERR_SHAPE, "ssi_rsvd_toeplitz: ldU < l*i");

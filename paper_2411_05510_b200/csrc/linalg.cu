@@ -422,6 +422,21 @@ size_t cholqr_partial_elems(int64_t m, int k) {
 }
 
 void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w) {
+  if (k > kSvdMaxK) {   // blocked whole-GPU path (linalg_big.cu): no explicit inverses
+    w.W = c.take<double>(size_t(k) * k);
+    w.L1 = c.take<double>(size_t(k) * k);
+    w.L2 = c.take<double>(size_t(k) * k);
+    w.Linv1 = w.Linv2 = w.LinvT1 = w.LinvT2 = w.Lb = w.Linvb = w.LinvTb = nullptr;
+    w.flag = c.take<int>(1);
+    w.Q1 = c.take<double>(size_t(m) * k);
+    w.chol_g = nullptr;
+    w.partial = c.take<double>(cholqr_partial_elems(m, k) + 1);
+    w.tallp = nullptr;
+    w.Dp1 = c.take<double>(cholqr_big_panel_elems(k));
+    w.Dp2 = c.take<double>(cholqr_big_panel_elems(k));
+    return;
+  }
+  w.Dp1 = w.Dp2 = nullptr;
   w.W = c.take<double>(size_t(k) * k);
   w.L1 = c.take<double>(size_t(k) * k);
   w.Linv1 = c.take<double>(size_t(k) * k);
@@ -515,6 +530,7 @@ __global__ void cq_fold_kernel(const int* run_if, int k, const double* __restric
 // device flag, so a healthy QR costs no host synchronisation and no arithmetic for the fallback.
 ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, CholQRWork& w,
                    int32_t* status, cudaStream_t s) {
+  if (k > kSvdMaxK) return cholqr2_big(Y, ldy, m, k, Q, w, status, s);
   // tall-skinny DMMA kernels (cp.async 16-byte pieces) when the shapes and alignment allow
   const bool tall = k <= kTallMaxN && ldy % 2 == 0 && m % 2 == 0 && k % 2 == 0 &&
                     (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0;
@@ -585,7 +601,9 @@ static ssi_status jacobi_launch(double* G, int k, double* Ut, double* S, double*
   return SSI_OK;
 }
 
-size_t jacobi_scratch_elems(int k) { return size_t(k) + kJacMaxSweeps / 2 + 1; }
+size_t jacobi_scratch_elems(int k) {
+  return k > kSvdMaxK ? jacobi_big_scratch_elems(k) : size_t(k) + kJacMaxSweeps / 2 + 1;
+}
 
 ssi_status jacobi_svd(double* G, int k, double* Ut, double* S, double* scratch, int32_t* status, cudaStream_t s) {
   ssi_status st;
@@ -593,8 +611,9 @@ ssi_status jacobi_svd(double* G, int k, double* Ut, double* S, double* scratch, 
   else if (k <= 128) st = jacobi_launch<4, JC>(G, k, Ut, S, scratch, status, s);
   else if (k <= 256) st = jacobi_launch<8, JC>(G, k, Ut, S, scratch, status, s);
   else if (k <= 512) st = jacobi_launch<16, 16>(G, k, Ut, S, scratch, status, s);
+  else if (k <= kBigMaxK) return jacobi_big(G, k, Ut, S, scratch, status, s);
   else {
-    set_last_error("jacobi_svd: k = %d > 512 unsupported", k);
+    set_last_error("jacobi_svd: k = %d > %d unsupported", k, kBigMaxK);
     return SSI_ERR_INVALID_ARG;
   }
   if (st != SSI_OK) return st;

@@ -21,6 +21,8 @@ struct CholQRWork {
   double* chol_g;   // packed triangle when k is too large for shared memory
   double* partial;  // split-K partials
   double* tallp;    // split-K partials of the tall-skinny kernels
+  double* Dp1;      // k > kSvdMaxK (linalg_big.cu): 64 x 64 panel inverses of L1 / L2 and the
+  double* Dp2;      //   original Gram diagonal
 };
 size_t cholqr_partial_elems(int64_t m, int k);
 void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w);
@@ -38,9 +40,18 @@ ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, Ch
 ssi_status chol_inv(const double* W, int k, int64_t m, double* L, double* Linv, double* LinvT, double* gscratch,
                     int32_t* status, cudaStream_t s, const int* run_if, int* shifted_out, int final);
 
-// Largest sketch width the small SVD (one-sided Jacobi on one 8/16-CTA cluster) supports; the
-// RSVD entry points reject larger k synchronously, before any launch.
+// Largest sketch width of the one-SM kernels (Cholesky, one-sided Jacobi on one 8/16-CTA cluster);
+// above it the blocked whole-GPU kernels of linalg_big.cu take over, up to kBigMaxK. The RSVD
+// entry points reject larger k synchronously, before any launch.
 constexpr int kSvdMaxK = 512;
+constexpr int kBigMaxK = 4096;
+
+// linalg_big.cu (k > kSvdMaxK)
+size_t cholqr_big_panel_elems(int k);
+ssi_status cholqr2_big(const double* Y, int64_t ldy, int64_t m, int k, double* Q, CholQRWork& w, int32_t* status,
+                       cudaStream_t s);
+size_t jacobi_big_scratch_elems(int k);
+ssi_status jacobi_big(double* G, int k, double* Ut, double* S, double* scratch, int32_t* status, cudaStream_t s);
 
 // One-sided (Hestenes) Jacobi SVD of a k x k matrix G (col-major, overwritten):
 // G V = U Sigma; Ut = U sorted by descending sigma (col-major k x k), S = sigma.

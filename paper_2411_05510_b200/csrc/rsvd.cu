@@ -22,7 +22,7 @@ static void rsvd_carve(Carver& c, int64_t m, int k, RsvdWork& w) {
   w.Ut = c.take<double>(size_t(k) * k);
   w.Sk = c.take<double>(size_t(k));
   w.jac = c.take<double>(jacobi_scratch_elems(k));
-  w.tall = c.take<double>(gemm_tall_partial_elems_upto(m, k) + 1);
+  w.tall = c.take<double>((k <= kTallMaxN ? gemm_tall_partial_elems_upto(m, k) : 0) + 1);
   cholqr_carve(c, m, k, w.cq);
 }
 

@@ -6,7 +6,7 @@
   make every Gram matrix of the RSVD singular;
 * ssi_cov_normalize (reading A-6, 1/(N-k)) after time-sharded raw sums;
 * ssi_cov_spectral_phases (measurement entry point) reproducing ssi_covariances bit for bit;
-* synchronous rejection of k > 512 before any launch (ssi.h conventions);
+* synchronous rejection of k > 4096 (kBigMaxK) before any launch (ssi.h conventions);
 * the multi-rank drivers (time-sharded covariances + all-reduce + on-device normalisation,
   LPT lags, one packed all_gather, ssi_stab3d; round-robin record batch) run as two processes
   on one GPU over gloo (host-staged collectives: no kernel of one rank waits on the other)
@@ -82,11 +82,11 @@ def test_modal_sweep_after_rank_deficient_rsvd(ssi):
     np.testing.assert_allclose(f, np.sort(modes.f), rtol=1e-9)
 
 
-def test_rsvd_k_above_512_rejected_before_any_launch(ssi):
+def test_rsvd_k_above_4096_rejected_before_any_launch(ssi):
     api, _ = ssi
     from paper_2411_05510_b200 import _lib
     lib = _lib.get()
-    l, i, k = 20, 30, 513
+    l, i, k = 64, 70, 4097
     R = torch.zeros((2 * i - 1, l, l), dtype=torch.float64, device="cuda")
     U = torch.full((k * l * i,), -7.0, dtype=torch.float64, device="cuda")
     S = torch.full((k,), -7.0, dtype=torch.float64, device="cuda")
@@ -97,7 +97,7 @@ def test_rsvd_k_above_512_rejected_before_any_launch(ssi):
     code = lib.ssi_rsvd_toeplitz(C.c_void_p(R.data_ptr()), l, i, k, 1, C.c_uint64(1), C.c_uint64(1), k,
                                  C.c_void_p(U.data_ptr()), l * i, C.c_void_p(S.data_ptr()),
                                  C.c_void_p(ws.data_ptr()), ws.numel(), None)
-    assert code == 1 and b"512" in lib.ssi_last_error()
+    assert code == 1 and b"4096" in lib.ssi_last_error()
     torch.cuda.synchronize()
     assert torch.all(U == -7.0) and torch.all(S == -7.0) and torch.all(ws == 0x55)
 
