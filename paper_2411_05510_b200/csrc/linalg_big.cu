@@ -10,6 +10,8 @@
 //     rotations accumulated into V, and the pair's columns are replaced by X V (DMMA).
 // Same results as the one-CTA kernels of linalg.cu up to rounding; used for k > kSvdMaxK.
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 #include <math_constants.h>
 
 #include "linalg.cuh"
@@ -156,18 +158,44 @@ constexpr int JRC = 96;            // rows per staged chunk (static shared memor
 constexpr int JLD = JP + 4;        // 36: conflict-free m8n8k4 fragments
 constexpr int kBjThreads = 256;
 constexpr int kBjMaxSweeps = 40;
-constexpr int kBjInner = 8;
+#ifndef SSI_BJ_INNER
+#define SSI_BJ_INNER 1
+#endif
+constexpr int kBjInner = SSI_BJ_INNER;   // inner sweeps per pair and round (the outer sweeps revisit every pair)
 
 struct BjArgs {
   double* G;
   int k, nb;               // matrix size, blocks (even)
   int* sweep_rot;          // [kBjMaxSweeps]: pairs that rotated in each sweep
   int32_t* status;
+  int profile;
 };
 
 __device__ __forceinline__ int bj_col(int blk, int j, int k) {   // column of slot j of block blk, or -1
   const int c = blk * JB + j;
   return c < k ? c : -1;
+}
+
+constexpr int PRE = JRC * JP / kBjThreads;   // chunk elements per thread (12)
+static_assert(PRE * kBjThreads == JRC * JP, "chunk must split evenly over the threads");
+
+// chunk rows [r0, r0 + JRC) of the pair's 32 columns into registers (element e = tid + 256 u:
+// row e % JRC, pair column e / JRC; consecutive threads read consecutive rows of a column)
+__device__ __forceinline__ void bj_fetch(const double* G, int k, const int (&cols)[2], int r0, double (&pre)[PRE]) {
+#pragma unroll
+  for (int u = 0; u < PRE; ++u) {
+    const int e = threadIdx.x + u * kBjThreads;
+    const int rr = e % JRC, j = e / JRC;
+    const int c = bj_col(cols[j / JB], j % JB, k);
+    pre[u] = (c >= 0 && r0 + rr < k) ? __ldcg(G + int64_t(c) * k + r0 + rr) : 0.0;
+  }
+}
+__device__ __forceinline__ void bj_stage(const double (&pre)[PRE], double* X) {
+#pragma unroll
+  for (int u = 0; u < PRE; ++u) {
+    const int e = threadIdx.x + u * kBjThreads;
+    X[(e % JRC) * JLD + e / JRC] = pre[u];
+  }
 }
 
 __global__ void __launch_bounds__(kBjThreads) bjacobi_kernel(BjArgs a) {
@@ -176,12 +204,13 @@ __global__ void __launch_bounds__(kBjThreads) bjacobi_kernel(BjArgs a) {
   __shared__ double Gm[JP][JP + 1];    // pair Gram
   __shared__ double V[JP][JP + 1];     // accumulated rotation
   __shared__ double cs_c[JP / 2], cs_s[JP / 2];
-  __shared__ int cs_on[JP / 2];
-  __shared__ int any_rot, step_rot, sweep_done;
+  __shared__ int cs_p[JP / 2], cs_q[JP / 2];
+  __shared__ int any_rot, sweep_done;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k = a.k, nb = a.nb;
   const double tol = sqrt(double(k)) * 1.1102230246251565e-16;
   const int kq = lane & 3, r8 = lane >> 2;
+  long long t_gram = 0, t_inner = 0, t_apply = 0, t_sync = 0, tc = clock64();
   for (int sweep = 0; sweep < kBjMaxSweeps; ++sweep) {
     if (tid == 0) any_rot = 0;
     for (int round = 0; round < nb - 1; ++round) {
@@ -191,106 +220,109 @@ __global__ void __launch_bounds__(kBjThreads) bjacobi_kernel(BjArgs a) {
       const int bb = 1 + (pb - 1 + round) % (nb - 1);
       int cols[2] = {ba < bb ? ba : bb, ba < bb ? bb : ba};
       // ---- Gram of the pair's columns, row chunks through shared memory (DMMA, 16 tiles)
-      double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
-      const int t0 = 2 * warp, t1 = 2 * warp + 1;            // tiles (ti, tj) of the 4 x 4 grid
-      for (int r0 = 0; r0 < k; r0 += JRC) {
-        for (int e = tid; e < JRC * JP; e += kBjThreads) {
-          const int rr = e % JRC, j = e / JRC;
-          const int c = bj_col(cols[j / JB], j % JB, k);
-          X[rr * JLD + j] = (c >= 0 && r0 + rr < k) ? __ldcg(a.G + int64_t(c) * k + r0 + rr) : 0.0;
-        }
-        __syncthreads();
-#pragma unroll 4
-        for (int kk = 0; kk < JRC; kk += 4) {
-          // tile t: rows 8 (t / 4), cols 8 (t % 4); A = X^T (col index, row), B = X (row, col index)
-          const double a0 = X[(kk + kq) * JLD + 8 * (t0 / 4) + r8];
-          const double b0 = X[(kk + kq) * JLD + 8 * (t0 % 4) + r8];
-          const double b1 = X[(kk + kq) * JLD + 8 * (t1 % 4) + r8];
-          dmma884(g0[0], g0[1], a0, b0);
-          dmma884(g1[0], g1[1], a0, b1);          // t1 shares t0's row of tiles (t0 even)
-        }
-        __syncthreads();
-      }
+      // warp w: tile row ti = w & 3 (4 tiles of 8 x 8), row half w >> 2 of every chunk (4-way ILP);
+      // the two halves are summed in a fixed order
+      double g[4][2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        Gm[8 * (t0 / 4) + r8][8 * (t0 % 4) + 2 * kq + h] = g0[h];
-        Gm[8 * (t1 / 4) + r8][8 * (t1 % 4) + 2 * kq + h] = g1[h];
+      for (int tj = 0; tj < 4; ++tj) g[tj][0] = g[tj][1] = 0.0;
+      const int ti = warp & 3, kh = (warp >> 2) * (JRC / 2);
+      // row chunks staged through registers: the next chunk's loads are in flight while the
+      // current one is multiplied (PRE loads per thread, all issued together)
+      double pre[PRE];
+      bj_fetch(a.G, k, cols, 0, pre);
+      for (int r0 = 0; r0 < k; r0 += JRC) {
+        bj_stage(pre, X);
+        __syncthreads();
+        if (r0 + JRC < k) bj_fetch(a.G, k, cols, r0 + JRC, pre);
+#pragma unroll 4
+        for (int kk = kh; kk < kh + JRC / 2; kk += 4) {
+          // A = X^T (pair column, row), B = X (row, pair column)
+          const double a0 = X[(kk + kq) * JLD + 8 * ti + r8];
+#pragma unroll
+          for (int tj = 0; tj < 4; ++tj) dmma884(g[tj][0], g[tj][1], a0, X[(kk + kq) * JLD + 8 * tj + r8]);
+        }
+        __syncthreads();
       }
-      for (int e = tid; e < JP * JP; e += kBjThreads) V[e / JP][e % JP] = (e / JP == e % JP) ? 1.0 : 0.0;
-      if (tid == 0) step_rot = 0;
+      { const long long t = clock64(); t_gram += t - tc; tc = t; }
+      if (warp >= 4)
+#pragma unroll
+        for (int tj = 0; tj < 4; ++tj)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) Gm[8 * ti + r8][8 * tj + 2 * kq + h] = g[tj][h];
       __syncthreads();
-      // ---- diagonalise the pair Gram: parallel-ordered Jacobi sweeps (16 disjoint pairs a step)
+      if (warp < 4)
+#pragma unroll
+        for (int tj = 0; tj < 4; ++tj)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double& d = Gm[8 * ti + r8][8 * tj + 2 * kq + h];
+            d = g[tj][h] + d;
+          }
+      for (int e = tid; e < JP * JP; e += kBjThreads) V[e / JP][e % JP] = (e / JP == e % JP) ? 1.0 : 0.0;
+      __syncthreads();
+      // ---- diagonalise the pair Gram: parallel-ordered Jacobi sweeps (16 disjoint pairs a step:
+      // angles, then G <- J^T G, then G <- G J and V <- V J; a pair below the threshold keeps
+      // c = 1, s = 0, which leaves its rows and columns bit-for-bit unchanged)
       int rotated = 0;
       for (int inner = 0; inner < kBjInner; ++inner) {
         int inner_rot = 0;
         for (int st = 0; st < JP - 1; ++st) {
+          int on = 0;
           if (tid < JP / 2) {
             const int q0 = tid, q1 = JP - 1 - tid;
             int p = q0 == 0 ? 0 : 1 + (q0 - 1 + st) % (JP - 1);
             int q = 1 + (q1 - 1 + st) % (JP - 1);
             if (p > q) { const int t = p; p = q; q = t; }
             const double al = Gm[p][p], be = Gm[q][q], ga = Gm[p][q];
-            int on = 0;
             double c = 1.0, s = 0.0;
-            if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
-              const double zeta = (be - al) / (2.0 * ga);
-              const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-              c = 1.0 / sqrt(1.0 + t * t);
+            if (ga != 0.0 && ga * ga > tol * tol * (al * be)) {
+              // zeta = (be - al) / (2 ga); t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2));
+              // c = 1 / sqrt(1 + t^2), s = c t  (Newton-refined reciprocal / rsqrt: a few ulp)
+              const double zeta = (be - al) * fast_rcp(2.0 * ga);
+              const double r1 = fast_rsqrt(fma(zeta, zeta, 1.0));
+              const double hyp = fma(zeta, zeta, 1.0) * r1;          // sqrt(1 + zeta^2)
+              const double t = copysign(fast_rcp(fabs(zeta) + hyp), zeta);
+              c = fast_rsqrt(fma(t, t, 1.0));
               s = c * t;
               on = 1;
             }
-            cs_c[tid] = c; cs_s[tid] = s; cs_on[tid] = on;
-            if (on) atomicOr(&step_rot, 1);
+            cs_p[tid] = p; cs_q[tid] = q; cs_c[tid] = c; cs_s[tid] = s;
+          }
+          if (__syncthreads_or(on)) inner_rot = 1;
+          // rows: G <- J^T G (thread: (pair, column))
+          for (int e = tid; e < (JP / 2) * JP; e += kBjThreads) {
+            const int pr = e / JP, j = e % JP;
+            const int p = cs_p[pr], q = cs_q[pr];
+            const double c = cs_c[pr], s = cs_s[pr];
+            const double x = Gm[p][j], y = Gm[q][j];
+            Gm[p][j] = c * x - s * y;
+            Gm[q][j] = s * x + c * y;
           }
           __syncthreads();
-          if (step_rot) {
-            // rows: G <- J^T G (pair t on rows p, q; thread handles (pair, column))
-            for (int e = tid; e < (JP / 2) * JP; e += kBjThreads) {
-              const int pr = e / JP, j = e % JP;
-              if (!cs_on[pr]) continue;
-              const int q0 = pr, q1 = JP - 1 - pr;
-              int p = q0 == 0 ? 0 : 1 + (q0 - 1 + st) % (JP - 1);
-              int q = 1 + (q1 - 1 + st) % (JP - 1);
-              if (p > q) { const int t = p; p = q; q = t; }
-              const double c = cs_c[pr], s = cs_s[pr];
-              const double x = Gm[p][j], y = Gm[q][j];
-              Gm[p][j] = c * x - s * y;
-              Gm[q][j] = s * x + c * y;
-            }
-            __syncthreads();
-            // columns: G <- G J, V <- V J
-            for (int e = tid; e < (JP / 2) * JP * 2; e += kBjThreads) {
-              const int which = e / ((JP / 2) * JP), f = e % ((JP / 2) * JP);
-              const int pr = f / JP, j = f % JP;
-              if (!cs_on[pr]) continue;
-              const int q0 = pr, q1 = JP - 1 - pr;
-              int p = q0 == 0 ? 0 : 1 + (q0 - 1 + st) % (JP - 1);
-              int q = 1 + (q1 - 1 + st) % (JP - 1);
-              if (p > q) { const int t = p; p = q; q = t; }
-              const double c = cs_c[pr], s = cs_s[pr];
-              double (*Mx)[JP + 1] = which ? V : Gm;
-              const double x = Mx[j][p], y = Mx[j][q];
-              Mx[j][p] = c * x - s * y;
-              Mx[j][q] = s * x + c * y;
-            }
-            inner_rot = 1;
+          // columns: G <- G J, V <- V J
+          for (int e = tid; e < (JP / 2) * JP * 2; e += kBjThreads) {
+            const int which = e / ((JP / 2) * JP), f = e % ((JP / 2) * JP);
+            const int pr = f / JP, j = f % JP;
+            const int p = cs_p[pr], q = cs_q[pr];
+            const double c = cs_c[pr], s = cs_s[pr];
+            double (*Mx)[JP + 1] = which ? V : Gm;
+            const double x = Mx[j][p], y = Mx[j][q];
+            Mx[j][p] = c * x - s * y;
+            Mx[j][q] = s * x + c * y;
           }
-          __syncthreads();
-          if (tid == 0) step_rot = 0;
           __syncthreads();
         }
         rotated |= inner_rot;
         if (!inner_rot) break;
       }
+      { const long long t = clock64(); t_inner += t - tc; tc = t; }
       // ---- X <- X V for the pair's columns (row chunks, DMMA: chunk (JRC x 32) * V (32 x 32))
       if (rotated) {
+        bj_fetch(a.G, k, cols, 0, pre);
         for (int r0 = 0; r0 < k; r0 += JRC) {
-          for (int e = tid; e < JRC * JP; e += kBjThreads) {
-            const int rr = e % JRC, j = e / JRC;
-            const int c = bj_col(cols[j / JB], j % JB, k);
-            X[rr * JLD + j] = (c >= 0 && r0 + rr < k) ? __ldcg(a.G + int64_t(c) * k + r0 + rr) : 0.0;
-          }
+          bj_stage(pre, X);
           __syncthreads();
+          if (r0 + JRC < k) bj_fetch(a.G, k, cols, r0 + JRC, pre);
           // output tiles: (JRC/8) x 4, TPW per warp
           constexpr int TPW = JRC / 16;
           double acc[TPW][2];
@@ -321,13 +353,20 @@ __global__ void __launch_bounds__(kBjThreads) bjacobi_kernel(BjArgs a) {
         }
         if (tid == 0) any_rot = 1;
       }
+      { const long long t = clock64(); t_apply += t - tc; tc = t; }
       grid.sync();
+      { const long long t = clock64(); t_sync += t - tc; tc = t; }
     }
     if (tid == 0 && any_rot) atomicAdd(a.sweep_rot + sweep, 1);
     grid.sync();
     if (tid == 0) sweep_done = (__ldcg(a.sweep_rot + sweep) == 0);
     __syncthreads();
-    if (sweep_done) return;
+    if (sweep_done) {
+      if (a.profile && blockIdx.x == 0 && tid == 0)
+        printf("bjacobi k=%d: %d sweeps of %d rounds; cycles gram %lld inner %lld apply %lld sync %lld\n", k,
+               sweep + 1, nb - 1, t_gram, t_inner, t_apply, t_sync);
+      return;
+    }
   }
   if (blockIdx.x == 0 && tid == 0) set_status(a.status, SSI_ERR_NUMERIC);
 }
@@ -439,7 +478,7 @@ ssi_status jacobi_big(double* G, int k, double* Ut, double* S, double* scratch, 
   int* rank = reinterpret_cast<int*>(scratch + k);
   int* flags = reinterpret_cast<int*>(scratch + 2 * size_t(k));
   if (cudaMemsetAsync(flags, 0, sizeof(int) * kBjMaxSweeps, s) != cudaSuccess) return launch_check("memset flags");
-  BjArgs a{G, k, nb, flags, status};
+  BjArgs a{G, k, nb, flags, status, getenv("SSI_JAC_PROFILE") ? 1 : 0};
   void* args[] = {&a};
   if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bjacobi_kernel), dim3(unsigned(nb / 2)), dim3(kBjThreads),
                                   args, 0, s) != cudaSuccess)
