@@ -589,6 +589,19 @@ def main():
         roof["sm_time_share"] = {"source": sm.get("source", "profiles/smtime_spectral_latest.json"),
                                  "top_kernels": {k.split("(")[0].replace("ssi::<unnamed>::", ""):
                                                  round(v["share_sm_time"], 4) for k, v in top}}
+        # the kernel with the largest SM-time share: the per-order Francis QR (A10), one CTA per
+        # order, a latency-bound bulge chase; its algorithmic flops (~10 n^3 per order, LAPACK's
+        # count for the eigenvalues) over its SM-time, against the FP64 ALU peak
+        name, v = top[0]
+        if "eig_order_kernel" in name:
+            eig_flop = sum(10.0 * n ** 3 for n in cfg.orders)
+            ach = eig_flop / (v["gpu_ms_equiv"] / 1e3) / 1e12
+            roof["sm_time_dominant"] = {
+                "kernel": "eig_order_kernel (A10 per-order Francis QR + Schur vectors + poles)",
+                "bound": "latency (one warp's dependent FP64 chain per order)", "share_sm_time": v["share_sm_time"],
+                "gpu_ms_equiv": v["gpu_ms_equiv"], "algorithmic_flop": eig_flop, "achieved": ach,
+                "peak": FP64_ALU_TFLOPS, "unit": "TFLOP/s", "frac": ach / FP64_ALU_TFLOPS,
+                "peak_source": "148 SMs x 64 FP64 FMA lanes x 2 x 1965 MHz (B200_PROFILING.md unit counts)"}
     except Exception:
         pass
 

@@ -491,7 +491,13 @@ struct Band {
   }
 };
 
-__global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
+#ifndef SSI_EIG_MINB
+#define SSI_EIG_MINB 1
+#endif
+// BG: the banded matrix lives in global memory (orders beyond shared memory); a separate
+// instantiation so the shared-memory one addresses the band with LDS/STS, not generic accesses
+template <bool BG>
+__global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ double sh_cs, sh_sn, sh_pt[NSH / 2], sh_pd[NSH / 2];
   __shared__ int sh_ok4;
@@ -524,7 +530,7 @@ __global__ void __launch_bounds__(NT) eig_order_kernel(EigArgs g) {
   {
     char* p = reinterpret_cast<char*>(dsm);
     const int nm = g.n_max;
-    if (g.band_g) {
+    if (BG) {
       s.H = g.band_g + int64_t(o) * int64_t(band_elems(nm));
     } else {
       s.H = reinterpret_cast<double*>(p);    p += sizeof(double) * band_elems(nm);
@@ -1187,7 +1193,12 @@ size_t modal_smem_bytes(int n_max, int cap, bool band_global) {
 // Orders up to ~230 keep the banded Hessenberg/Schur matrix in shared memory; beyond that (the
 // paper's bridge sweeps reach order 400) it lives in an L2-resident global slab per
 // order and the same kernel addresses it through generic pointers.
-bool modal_band_global(int n_max) { return modal_smem_bytes(n_max, n_max / 2, false) > kModalSmemMax; }
+#ifndef SSI_EIG_BAND_GLOBAL
+#define SSI_EIG_BAND_GLOBAL 0
+#endif
+bool modal_band_global(int n_max) {
+  return SSI_EIG_BAND_GLOBAL || modal_smem_bytes(n_max, n_max / 2, false) > kModalSmemMax;
+}
 
 struct ModalWork {
   double *Rinv, *W, *M, *C, *Qup, *band;
@@ -1238,10 +1249,15 @@ ssi_status modal_run(const double* U, int64_t ldU, const double* S, int l, int i
   EigArgs g{w.M, w.C, U, ldU, S, l, n_min, n_step, no, n_max, tab.cap, dt, tab,
             getenv("SSI_EIG_PROFILE") ? atoi(getenv("SSI_EIG_PROFILE")) : 0, w.band};
   const size_t smem = modal_smem_bytes(n_max, tab.cap, w.band != nullptr);
-  cudaFuncSetAttribute(eig_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   hess_order_kernel<<<no, HT, 0, st>>>(g);
   SSI_TRY(launch_check("hess_order_kernel"));
-  eig_order_kernel<<<no, NT, smem, st>>>(g);
+  if (w.band) {
+    cudaFuncSetAttribute(eig_order_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    eig_order_kernel<true><<<no, NT, smem, st>>>(g);
+  } else {
+    cudaFuncSetAttribute(eig_order_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    eig_order_kernel<false><<<no, NT, smem, st>>>(g);
+  }
   return launch_check("eig_order_kernel");
 }
 
