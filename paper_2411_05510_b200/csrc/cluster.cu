@@ -12,12 +12,15 @@
 //                      retained iff membership >= 0.5              (C-2, C-3)
 // Stage II (ssi_cluster_stage2), on the n retained poles:
 //   gather_kernel      f, xi, shape planes (re / im, channel-padded) and |shape|^2
-//   dist_kernel        D[i][j] = d_f + d_xi + (1 - MAC), the complex Gram
-//                      S S^H on the FP64 tensor cores (DMMA), fused epilogue, symmetric tiles
-//   link_kernel        union-find over the edges D <= cutoff (single-linkage components). An
-//                      average-linkage merge at height <= cutoff needs one pair <= cutoff, so
-//                      every flat cluster lies inside one component and the components are
-//                      clustered independently and in parallel.
+//   rank_f_kernel      f order of the retained poles (rank by counting)
+//   band_link_kernel   union-find over the edges d <= cutoff (single-linkage components), with
+//                      d = d_f + d_xi + (1 - MAC) from the complex Gram
+//                      S S^H on the FP64 tensor cores (DMMA) with a fused epilogue. An edge needs
+//                      d_f <= cutoff, so only 64 x 64 tiles inside that f band (in f order) are
+//                      formed. An average-linkage merge at height <= cutoff needs one pair
+//                      <= cutoff, so every flat cluster lies inside one component and the
+//                      components are clustered independently and in parallel.
+//   comp_dist_kernel   each component's dense distance block (DMMA tiles from a tile list)
 //   nnchain_kernel     one CTA per component: average linkage (UPGMA) by the nearest-neighbour
 //                      chain with the Lance-Williams update, restricted to heights <= cutoff
 //                      (a cluster whose nearest neighbour is farther than the cutoff is final:
@@ -372,24 +375,20 @@ __global__ void __launch_bounds__(kGathNT) gather_kernel(TableSet ts, const int3
   }
 }
 
-// D tile kernel: 64 x 64 tile (ti <= tj) of D; 8 warps, warp w owns rows 16 (w>>1) .. +16 and
-// columns 32 (w&1) .. +32 of the tile as 2 x 4 DMMA 8x8 blocks (re and im accumulators).
+// Distance tile: d between 64 row poles ri[] and 64 column poles cj[] (retained indices, -1 =
+// none; shared arrays) into Ct [64][65] (shared, aliases the staging buffers). 8 warps, warp w owns
+// rows 16 (w>>1) .. +16 and columns 32 (w&1) .. +32 as 2 x 4 DMMA 8x8 blocks (re and im).
 constexpr int kDT = 64, kDK = 32, kDS = kDK + 4;   // stride 36 doubles: conflict-free fragments
 constexpr int kDistNT = 256;
+constexpr size_t kDistSmem = size_t(4) * kDT * kDS * sizeof(double);
 
-__global__ void __launch_bounds__(kDistNT) dist_kernel(const double* __restrict__ F, const double* __restrict__ XI,
-                                                       const double* __restrict__ Sre,
-                                                       const double* __restrict__ Sim,
-                                                       const double* __restrict__ NRM, int n, int lp,
-                                                       double* __restrict__ D, int64_t ldD) {
-  const int ti = blockIdx.y, tj = blockIdx.x;
-  if (tj < ti) return;
-  extern __shared__ double smem[];
+__device__ void dist_tile(const double* __restrict__ F, const double* __restrict__ XI,
+                          const double* __restrict__ Sre, const double* __restrict__ Sim,
+                          const double* __restrict__ NRM, int lp, const int* ri, const int* cj, double* smem) {
   double* Ar = smem;                 // [64][kDS]
   double* Ai = Ar + kDT * kDS;
   double* Br = Ai + kDT * kDS;
   double* Bi = Br + kDT * kDS;
-  const int i0 = ti * kDT, j0 = tj * kDT;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int wr = (warp >> 1) * 16, wc = (warp & 1) * 32;
   double cre[2][4][2], cim[2][4][2];
@@ -402,11 +401,11 @@ __global__ void __launch_bounds__(kDistNT) dist_kernel(const double* __restrict_
     for (int e = threadIdx.x; e < kDT * kDK; e += kDistNT) {
       const int r = e / kDK, k = e % kDK;
       const bool okk = k < kw;
-      const int gi = i0 + r, gj = j0 + r;
-      Ar[r * kDS + k] = okk && gi < n ? Sre[int64_t(gi) * lp + k0 + k] : 0.0;
-      Ai[r * kDS + k] = okk && gi < n ? Sim[int64_t(gi) * lp + k0 + k] : 0.0;
-      Br[r * kDS + k] = okk && gj < n ? Sre[int64_t(gj) * lp + k0 + k] : 0.0;
-      Bi[r * kDS + k] = okk && gj < n ? Sim[int64_t(gj) * lp + k0 + k] : 0.0;
+      const int gi = ri[r], gj = cj[r];
+      Ar[r * kDS + k] = okk && gi >= 0 ? Sre[int64_t(gi) * lp + k0 + k] : 0.0;
+      Ai[r * kDS + k] = okk && gi >= 0 ? Sim[int64_t(gi) * lp + k0 + k] : 0.0;
+      Br[r * kDS + k] = okk && gj >= 0 ? Sre[int64_t(gj) * lp + k0 + k] : 0.0;
+      Bi[r * kDS + k] = okk && gj >= 0 ? Sim[int64_t(gj) * lp + k0 + k] : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -438,8 +437,7 @@ __global__ void __launch_bounds__(kDistNT) dist_kernel(const double* __restrict_
     }
     __syncthreads();
   }
-  // epilogue: d = d_f + d_xi + (1 - MAC) into a shared 64 x 65 tile, then row-wise stores of
-  // D[i][j] and, for off-diagonal tiles, of the transposed tile D[j][i]
+  // d = d_f + d_xi + (1 - MAC); 0 on the diagonal (same pole)
   double* Ct = smem;   // [64][65]
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -448,9 +446,9 @@ __global__ void __launch_bounds__(kDistNT) dist_kernel(const double* __restrict_
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = wr + 8 * a + (lane >> 2), cc = wc + 8 * b + 2 * (lane & 3) + h;
-        const int gi = i0 + r, gj = j0 + cc;
+        const int gi = ri[r], gj = cj[cc];
         double d = 0.0;
-        if (gi < n && gj < n && gi != gj) {
+        if (gi >= 0 && gj >= 0 && gi != gj) {
           const double re = cre[a][b][h], im = cim[a][b][h];
           const double mac = (re * re + im * im) / (NRM[gi] * NRM[gj]);
           d = (rel_diff(F[gi], F[gj]) + rel_diff(XI[gi], XI[gj])) + (1.0 - mac);
@@ -458,15 +456,148 @@ __global__ void __launch_bounds__(kDistNT) dist_kernel(const double* __restrict_
         Ct[r * (kDT + 1) + cc] = d;
       }
   __syncthreads();
+}
+
+// f-order of the retained poles: rank by counting (ties by index), ord[rank] = i, fs[rank] = f_i.
+__global__ void __launch_bounds__(256) rank_f_kernel(const double* __restrict__ F, int n, int* __restrict__ ord,
+                                                     double* __restrict__ fs) {
+  __shared__ double fb[2048];
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  const double fi = i < n ? F[i] : 0.0;
+  int rk = 0;
+  for (int j0 = 0; j0 < n; j0 += 2048) {
+    const int nj = min(2048, n - j0);
+    for (int e = threadIdx.x; e < nj; e += 256) fb[e] = F[j0 + e];
+    __syncthreads();
+    if (i < n)
+      for (int e = 0; e < nj; ++e) rk += fb[e] < fi || (fb[e] == fi && j0 + e < i);
+    __syncthreads();
+  }
+  if (i < n) { ord[rk] = i; fs[rk] = fi; }
+}
+
+// Band of candidate edges: an edge needs d <= cutoff, hence d_f <= cutoff, hence (f ascending)
+// f_q <= f_p / (1 - cutoff); tile row ti needs column tiles whose first f is below
+// lim[ti] = f(last pole of ti) / (1 - cutoff), widened by 1e-12 relative (rounding of d).
+__global__ void band_lim_kernel(const double* __restrict__ fs, int n, double cutoff, double* __restrict__ lim) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nt = (n + kDT - 1) / kDT;
+  if (t >= nt) return;
+  const double fmax = fs[min(n - 1, t * kDT + kDT - 1)];
+  lim[t] = cutoff < 1.0 ? fmax / (1.0 - cutoff) * (1.0 + 1e-12) : CUDART_INF;
+}
+
+__device__ void uf_union(int* parent, int a, int b);
+
+// Edges of the band: tile (ti, tj), tj >= ti, in f order; pairs p < q (f order) with d <= cutoff
+// are joined in the union-find forest (retained indices).
+__global__ void __launch_bounds__(kDistNT) band_link_kernel(const double* __restrict__ F, const double* __restrict__ XI,
+                                                            const double* __restrict__ Sre,
+                                                            const double* __restrict__ Sim,
+                                                            const double* __restrict__ NRM, int n, int lp,
+                                                            const int* __restrict__ ord, const double* __restrict__ fs,
+                                                            const double* __restrict__ lim, double cutoff,
+                                                            int* parent) {
+  const int ti = blockIdx.y, tj = blockIdx.x;
+  if (tj < ti || fs[tj * kDT] > lim[ti]) return;
+  extern __shared__ double smem[];
+  __shared__ int ri[kDT], cj[kDT];
+  if (threadIdx.x < kDT) {
+    const int p = ti * kDT + threadIdx.x, q = tj * kDT + threadIdx.x;
+    ri[threadIdx.x] = p < n ? ord[p] : -1;
+    cj[threadIdx.x] = q < n ? ord[q] : -1;
+  }
+  __syncthreads();
+  dist_tile(F, XI, Sre, Sim, NRM, lp, ri, cj, smem);
+  const double* Ct = smem;
   for (int e = threadIdx.x; e < kDT * kDT; e += kDistNT) {
     const int r = e / kDT, cc = e % kDT;
-    if (i0 + r < n && j0 + cc < n) D[int64_t(i0 + r) * ldD + j0 + cc] = Ct[r * (kDT + 1) + cc];
+    const int p = ti * kDT + r, q = tj * kDT + cc;
+    if (p < q && q < n && Ct[r * (kDT + 1) + cc] <= cutoff) uf_union(parent, ri[r], cj[cc]);
   }
-  if (ti != tj)
-    for (int e = threadIdx.x; e < kDT * kDT; e += kDistNT) {
-      const int r = e / kDT, cc = e % kDT;      // D[j0 + r][i0 + cc] = tile[cc][r]
-      if (j0 + r < n && i0 + cc < n) D[int64_t(j0 + r) * ldD + i0 + cc] = Ct[cc * (kDT + 1) + r];
+}
+
+// Tile list of the per-component distance blocks: (component, ti, tj), tj >= ti, components of
+// >= 2 members. One CTA; the count goes to *ntiles.
+__global__ void __launch_bounds__(256) comp_tiles_kernel(const int* __restrict__ comp_size, const ssi_cluster_info* info,
+                                                         int* __restrict__ tiles, int* ntiles) {
+  __shared__ int sh[256 / 32 + 1];
+  const int K = info->n_components;
+  int base = 0;
+  for (int c0 = 0; c0 < K; c0 += 256) {
+    const int c = c0 + threadIdx.x;
+    const int s = c < K ? comp_size[c] : 0;
+    const int nt = s >= 2 ? (s + kDT - 1) / kDT : 0;
+    const int cnt = nt * (nt + 1) / 2;
+    int total;
+    const int ex = block_excl_scan<256>(cnt, sh, total);
+    int w = base + ex;
+    for (int a = 0; a < nt; ++a)
+      for (int b = a; b < nt; ++b, ++w) { tiles[3 * w] = c; tiles[3 * w + 1] = a; tiles[3 * w + 2] = b; }
+    base += total;
+  }
+  if (threadIdx.x == 0) *ntiles = base;
+}
+
+// Per-component distance blocks from the tile list: Dco (original distances, 0 diagonal, for the
+// medoids) and Dc (+inf diagonal, consumed by the nearest-neighbour chains), s x s row-major at
+// comp_doff[c], rows in the component's member order (ascending retained index).
+__global__ void __launch_bounds__(kDistNT) comp_dist_kernel(const double* __restrict__ F, const double* __restrict__ XI,
+                                                            const double* __restrict__ Sre,
+                                                            const double* __restrict__ Sim,
+                                                            const double* __restrict__ NRM, int lp,
+                                                            const int* __restrict__ tiles, const int* ntiles,
+                                                            const int* __restrict__ comp_off,
+                                                            const int* __restrict__ comp_size,
+                                                            const int64_t* __restrict__ comp_doff,
+                                                            const int* __restrict__ members, double* __restrict__ Dc,
+                                                            double* __restrict__ Dco) {
+  extern __shared__ double smem[];
+  __shared__ int ri[kDT], cj[kDT];
+  const int T = *ntiles;
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
+    const int c = tiles[3 * t], ti = tiles[3 * t + 1], tj = tiles[3 * t + 2];
+    const int s = comp_size[c], off = comp_off[c];
+    if (threadIdx.x < kDT) {
+      const int p = ti * kDT + threadIdx.x, q = tj * kDT + threadIdx.x;
+      ri[threadIdx.x] = p < s ? members[off + p] : -1;
+      cj[threadIdx.x] = q < s ? members[off + q] : -1;
     }
+    __syncthreads();
+    dist_tile(F, XI, Sre, Sim, NRM, lp, ri, cj, smem);
+    const double* Ct = smem;
+    double* D1 = Dc + comp_doff[c];
+    double* D0 = Dco + comp_doff[c];
+    for (int e = threadIdx.x; e < kDT * kDT; e += kDistNT) {
+      const int r = e / kDT, cc = e % kDT;
+      const int p = ti * kDT + r, q = tj * kDT + cc;
+      if (p < s && q < s) {
+        const double d = Ct[r * (kDT + 1) + cc];
+        D0[int64_t(p) * s + q] = d;
+        D1[int64_t(p) * s + q] = p == q ? CUDART_INF : d;
+      }
+    }
+    if (ti != tj)
+      for (int e = threadIdx.x; e < kDT * kDT; e += kDistNT) {
+        const int r = e / kDT, cc = e % kDT;     // (q, p) = tile[cc][r] transposed
+        const int q = tj * kDT + r, p = ti * kDT + cc;
+        if (p < s && q < s) {
+          const double d = Ct[cc * (kDT + 1) + r];
+          D0[int64_t(q) * s + p] = d;
+          D1[int64_t(q) * s + p] = d;
+        }
+      }
+    __syncthreads();
+  }
+}
+
+// local position of every retained pole inside its component's member list
+__global__ void local_index_kernel(const int* __restrict__ members, const int* __restrict__ key,
+                                   const int* __restrict__ comp_off, int n, int* __restrict__ g2l) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int i = members[p];
+  g2l[i] = p - comp_off[key[i]];
 }
 
 __device__ int uf_find(int* parent, int x) {
@@ -494,16 +625,6 @@ __device__ void uf_union(int* parent, int a, int b) {
 __global__ void uf_init_kernel(int* parent, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) parent[i] = i;
-}
-
-// Edges i < j with D[i][j] <= cutoff; one warp per row (coalesced row reads).
-__global__ void __launch_bounds__(256) link_kernel(const double* __restrict__ D, int64_t ldD, int n, double cutoff,
-                                                   int* parent) {
-  const int i = (blockIdx.x * 256 + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (i >= n) return;
-  const double* row = D + int64_t(i) * ldD;
-  for (int j = i + 1 + lane; j < n; j += 32)
-    if (row[j] <= cutoff) uf_union(parent, i, j);
 }
 
 __global__ void uf_flatten_kernel(int* parent, int n) {
@@ -576,26 +697,6 @@ __global__ void __launch_bounds__(kScanNT) components_kernel(const int* __restri
   }
   __syncthreads();
   if (threadIdx.x < 32) warp_stable_place(key, n, ctr, members);
-}
-
-// Per-component dense copy Dc = D[mem][mem] with +inf on the diagonal (the NN-chain works on
-// the copy; D keeps the original distances for the medoids).
-__global__ void __launch_bounds__(256) extract_kernel(const double* __restrict__ D, int64_t ldD,
-                                                      const int* __restrict__ comp_off, const int* __restrict__ comp_size,
-                                                      const int64_t* __restrict__ comp_doff,
-                                                      const int* __restrict__ members, const ssi_cluster_info* info,
-                                                      double* __restrict__ Dc) {
-  const int K = info->n_components;
-  for (int c = blockIdx.x; c < K; c += gridDim.x) {
-    const int s = comp_size[c];
-    if (s < 2) continue;
-    const int* mem = members + comp_off[c];
-    double* out = Dc + comp_doff[c];
-    for (int64_t e = threadIdx.x; e < int64_t(s) * s; e += 256) {
-      const int r = int(e / s), q = int(e % s);
-      out[e] = r == q ? CUDART_INF : D[int64_t(mem[r]) * ldD + mem[q]];
-    }
-  }
 }
 
 constexpr int kChainNT = 256;
@@ -768,7 +869,10 @@ __global__ void __launch_bounds__(kScanNT) flat_kernel(const int* __restrict__ r
 
 // Per kept cluster: lower median of f and xi (rank selection), medoid (least summed original
 // distance to the other members, lowest index on ties), first member.
-__global__ void __launch_bounds__(256) summary_kernel(const double* __restrict__ D, int64_t ldD,
+__global__ void __launch_bounds__(256) summary_kernel(const double* __restrict__ Dco,
+                                                      const int64_t* __restrict__ comp_doff,
+                                                      const int* __restrict__ comp_size, const int* __restrict__ key,
+                                                      const int* __restrict__ g2l,
                                                       const double* __restrict__ F, const double* __restrict__ XI,
                                                       const int* __restrict__ cl_off,
                                                       const int* __restrict__ cl_members, const ssi_cluster_info* info,
@@ -794,10 +898,17 @@ __global__ void __launch_bounds__(256) summary_kernel(const double* __restrict__
     }
     double best = CUDART_INF;
     int besti = 0x7fffffff;
+    // a flat cluster lies inside one component: its original distances are in that component's
+    // block (rows / columns in the component's member order)
+    const int comp = key[mem[0]];
+    const int cs = comp_size[comp];
+    const double* Db = Dco + comp_doff[comp];
     for (int a = threadIdx.x; a < s; a += 256) {
-      const double* row = D + int64_t(mem[a]) * ldD;
       double sum = 0.0;
-      for (int b = 0; b < s; ++b) sum += row[mem[b]];
+      if (cs >= 2) {
+        const double* row = Db + int64_t(g2l[mem[a]]) * cs;
+        for (int b = 0; b < s; ++b) sum += row[g2l[mem[b]]];
+      }
       if (sum < best || (sum == best && a < besti)) { best = sum; besti = a; }
     }
 #pragma unroll
@@ -976,8 +1087,9 @@ ssi_status cluster_stage1_run(const TableSet& ts, int n_lags, const ssi_criteria
 
 namespace {
 struct Stage2Bufs {
-  double *F, *XI, *Sre, *Sim, *NRM, *D, *Dc, *kf, *kxi, *m_h;
-  int *parent, *comp_id, *comp_off, *comp_size, *ctr, *members, *key, *csize, *chain, *par, *root, *rsize,
+  double *F, *XI, *Sre, *Sim, *NRM, *Dco, *Dc, *kf, *kxi, *m_h, *fs, *lim;
+  int *ord, *tiles, *ntiles, *g2l;
+  int *parent, *comp_id, *comp_off, *comp_size, *ctr, *members, *key, *key2, *csize, *chain, *par, *root, *rsize,
       *cid, *cl_root, *cl_off, *cl_members, *kmed, *kfirst, *ksize, *krank, *m_cnt, *m_ab;
   int64_t* comp_doff;
   uint8_t* act;
@@ -988,10 +1100,15 @@ void carve2(Carver& c, int n, int l, Stage2Bufs& b) {
   const size_t nn = size_t(n) * n;
   b.F = c.take<double>(n); b.XI = c.take<double>(n); b.NRM = c.take<double>(n);
   b.Sre = c.take<double>(size_t(n) * lp); b.Sim = c.take<double>(size_t(n) * lp);
-  b.D = c.take<double>(nn); b.Dc = c.take<double>(nn);
+  // per-component distance blocks: sum of squared component sizes <= n^2
+  b.Dco = c.take<double>(nn); b.Dc = c.take<double>(nn);
+  const size_t ntl = size_t((n + 63) / 64);
+  b.fs = c.take<double>(n); b.lim = c.take<double>(ntl);
+  b.ord = c.take<int>(n); b.g2l = c.take<int>(n);
+  b.tiles = c.take<int>(3 * (ntl * (ntl + 1) / 2 + ntl)); b.ntiles = c.take<int>(1);
   b.kf = c.take<double>(n); b.kxi = c.take<double>(n); b.m_h = c.take<double>(n);
   b.parent = c.take<int>(n); b.comp_id = c.take<int>(n); b.comp_off = c.take<int>(n + 1);
-  b.comp_size = c.take<int>(n); b.ctr = c.take<int>(n + 1); b.members = c.take<int>(n); b.key = c.take<int>(n);
+  b.comp_size = c.take<int>(n); b.ctr = c.take<int>(n + 1); b.members = c.take<int>(n); b.key = c.take<int>(n); b.key2 = c.take<int>(n);
   b.csize = c.take<int>(n); b.chain = c.take<int>(n); b.par = c.take<int>(n); b.root = c.take<int>(n);
   b.rsize = c.take<int>(n); b.cid = c.take<int>(n); b.cl_root = c.take<int>(n); b.cl_off = c.take<int>(n + 1);
   b.cl_members = c.take<int>(n); b.kmed = c.take<int>(n); b.kfirst = c.take<int>(n); b.ksize = c.take<int>(n);
@@ -1026,32 +1143,42 @@ ssi_status cluster_stage2_run(const TableSet& ts, const int32_t* pole_idx, const
                                                                     b.Sre, b.Sim, b.NRM);
   SSI_TRY(launch_check("gather_kernel"));
   const int nt = (n + kDT - 1) / kDT;
-  const size_t dsm = 4 * kDT * kDS * sizeof(double);
-  cudaFuncSetAttribute(dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsm));
-  dist_kernel<<<dim3(nt, nt), kDistNT, dsm, s>>>(b.F, b.XI, b.Sre, b.Sim, b.NRM, n, lp, b.D, n);
-  SSI_TRY(launch_check("dist_kernel"));
+  // components of {d <= cutoff}: only pairs inside the f band can be edges
+  rank_f_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.F, n, b.ord, b.fs);
+  SSI_TRY(launch_check("rank_f_kernel"));
+  band_lim_kernel<<<(nt + 127) / 128, 128, 0, s>>>(b.fs, n, cutoff, b.lim);
+  SSI_TRY(launch_check("band_lim_kernel"));
   uf_init_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.parent, n);
   SSI_TRY(launch_check("uf_init_kernel"));
-  link_kernel<<<(n * 32 + 255) / 256, 256, 0, s>>>(b.D, n, n, cutoff, b.parent);
-  SSI_TRY(launch_check("link_kernel"));
+  cudaFuncSetAttribute(band_link_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDistSmem));
+  band_link_kernel<<<dim3(nt, nt), kDistNT, kDistSmem, s>>>(b.F, b.XI, b.Sre, b.Sim, b.NRM, n, lp, b.ord, b.fs,
+                                                             b.lim, cutoff, b.parent);
+  SSI_TRY(launch_check("band_link_kernel"));
   uf_flatten_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.parent, n);
   SSI_TRY(launch_check("uf_flatten_kernel"));
   components_kernel<<<1, kScanNT, 0, s>>>(b.parent, n, b.comp_id, b.comp_off, b.comp_size, b.comp_doff, b.ctr,
                                           b.members, b.key, info);
   SSI_TRY(launch_check("components_kernel"));
+  local_index_kernel<<<(n + 255) / 256, 256, 0, s>>>(b.members, b.key, b.comp_off, n, b.g2l);
+  SSI_TRY(launch_check("local_index_kernel"));
+  // every component's dense distance block (original and chain copies)
+  comp_tiles_kernel<<<1, 256, 0, s>>>(b.comp_size, info, b.tiles, b.ntiles);
+  SSI_TRY(launch_check("comp_tiles_kernel"));
   const int grid = 148 * 4;
-  extract_kernel<<<grid, 256, 0, s>>>(b.D, n, b.comp_off, b.comp_size, b.comp_doff, b.members, info, b.Dc);
-  SSI_TRY(launch_check("extract_kernel"));
+  cudaFuncSetAttribute(comp_dist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kDistSmem));
+  comp_dist_kernel<<<grid, kDistNT, kDistSmem, s>>>(b.F, b.XI, b.Sre, b.Sim, b.NRM, lp, b.tiles, b.ntiles, b.comp_off,
+                                                    b.comp_size, b.comp_doff, b.members, b.Dc, b.Dco);
+  SSI_TRY(launch_check("comp_dist_kernel"));
   nnchain_kernel<<<grid, kChainNT, 0, s>>>(b.Dc, b.comp_off, b.comp_size, b.comp_doff, b.members, info, cutoff,
                                            b.csize, b.chain, b.par, b.act, b.m_ab, b.m_h, b.m_cnt);
   SSI_TRY(launch_check("nnchain_kernel"));
   roots_kernel<<<grid, 128, 0, s>>>(b.comp_off, b.comp_size, b.members, b.par, b.csize, info, b.root, b.rsize);
   SSI_TRY(launch_check("roots_kernel"));
-  flat_kernel<<<1, kScanNT, 0, s>>>(b.root, b.rsize, n, min_size, b.cid, b.cl_root, b.cl_off, b.ctr, b.key,
+  flat_kernel<<<1, kScanNT, 0, s>>>(b.root, b.rsize, n, min_size, b.cid, b.cl_root, b.cl_off, b.ctr, b.key2,
                                     b.cl_members, info);
   SSI_TRY(launch_check("flat_kernel"));
-  summary_kernel<<<grid, 256, 0, s>>>(b.D, n, b.F, b.XI, b.cl_off, b.cl_members, info, b.kf, b.kxi, b.kmed,
-                                      b.kfirst, b.ksize);
+  summary_kernel<<<grid, 256, 0, s>>>(b.Dco, b.comp_doff, b.comp_size, b.key, b.g2l, b.F, b.XI, b.cl_off,
+                                      b.cl_members, info, b.kf, b.kxi, b.kmed, b.kfirst, b.ksize);
   SSI_TRY(launch_check("summary_kernel"));
   order_kernel<<<1, 256, 0, s>>>(ts, pole_idx, retained, n, b.root, b.cid, b.kf, b.kxi, b.kmed, b.kfirst, b.ksize,
                                  b.krank, info, max_clusters, labels, cl_f, cl_xi, cl_size, cl_medoid, cl_shape);
