@@ -164,8 +164,8 @@ constexpr int kBjMaxSweeps = 40;
 constexpr int kBjInner = SSI_BJ_INNER;   // inner sweeps per pair and round (the outer sweeps revisit every pair)
 
 struct BjArgs {
-  double* G;
-  int k, nb;               // matrix size, blocks (even)
+  double* G;               // k x k, col-major, leading dimension ld (even: 16-byte row pairs)
+  int k, nb, ld;           // matrix size, blocks (even), leading dimension
   int* sweep_rot;          // [kBjMaxSweeps]: pairs that rotated in each sweep
   int32_t* status;
   int profile;
@@ -176,38 +176,45 @@ __device__ __forceinline__ int bj_col(int blk, int j, int k) {   // column of sl
   return c < k ? c : -1;
 }
 
-constexpr int PRE = JRC * JP / kBjThreads;   // chunk elements per thread (12)
-static_assert(PRE * kBjThreads == JRC * JP, "chunk must split evenly over the threads");
+// Row chunks of the pair's 32 columns go through a KST-stage ring of cp.async (16-byte pieces:
+// the matrix is copied to an even leading dimension first) into column-major chunks
+// Xc[pair column][row] (pitch XLD: m8n8k4 fragments conflict-free both ways).
+constexpr int XLD = JRC + 4;                 // 100 doubles
+constexpr int KST = 4;                       // ring stages
+constexpr int XCH = JP * XLD;                // doubles per chunk
+constexpr int PIECES = JP * (JRC / 2);       // 16-byte pieces per chunk (1536)
+static_assert(PIECES % kBjThreads == 0, "pieces must split evenly");
+constexpr size_t kBjSmem = size_t(KST) * XCH * sizeof(double);
 
-// chunk rows [r0, r0 + JRC) of the pair's 32 columns into registers (element e = tid + 256 u:
-// row e % JRC, pair column e / JRC; consecutive threads read consecutive rows of a column)
-__device__ __forceinline__ void bj_fetch(const double* G, int k, const int (&cols)[2], int r0, double (&pre)[PRE]) {
+__device__ __forceinline__ void bj_issue(const double* G, int k, int ld, const int (&cols)[2], int r0, double* Xc) {
 #pragma unroll
-  for (int u = 0; u < PRE; ++u) {
-    const int e = threadIdx.x + u * kBjThreads;
-    const int rr = e % JRC, j = e / JRC;
+  for (int u = 0; u < PIECES / kBjThreads; ++u) {
+    const int q = threadIdx.x + u * kBjThreads;
+    const int j = q / (JRC / 2), rr = (q % (JRC / 2)) * 2;
     const int c = bj_col(cols[j / JB], j % JB, k);
-    pre[u] = (c >= 0 && r0 + rr < k) ? __ldcg(G + int64_t(c) * k + r0 + rr) : 0.0;
+    const int rows = (c >= 0) ? min(2, k - (r0 + rr)) : 0;          // k - r0 - rr may be <= 0
+    const bool ok = rows > 0;
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(Xc + j * XLD + rr));
+    const double* src = ok ? G + int64_t(c) * ld + r0 + rr : G;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 * rows : 0)
+                 : "memory");
   }
 }
-__device__ __forceinline__ void bj_stage(const double (&pre)[PRE], double* X) {
-#pragma unroll
-  for (int u = 0; u < PRE; ++u) {
-    const int e = threadIdx.x + u * kBjThreads;
-    X[(e % JRC) * JLD + e / JRC] = pre[u];
-  }
-}
+__device__ __forceinline__ void bj_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bj_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 __global__ void __launch_bounds__(kBjThreads) bjacobi_kernel(BjArgs a) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double X[JRC * JLD];      // row chunk of the pair's 32 columns
+  extern __shared__ __align__(16) double xring[];   // KST chunks Xc[JP][XLD]
   __shared__ double Gm[JP][JP + 1];    // pair Gram
   __shared__ double V[JP][JP + 1];     // accumulated rotation
   __shared__ double cs_c[JP / 2], cs_s[JP / 2];
   __shared__ int cs_p[JP / 2], cs_q[JP / 2];
   __shared__ int any_rot, sweep_done;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int k = a.k, nb = a.nb;
+  const int k = a.k, nb = a.nb, ld = a.ld;
+  const int nch = (k + JRC - 1) / JRC;
   const double tol = sqrt(double(k)) * 1.1102230246251565e-16;
   const int kq = lane & 3, r8 = lane >> 2;
   long long t_gram = 0, t_inner = 0, t_apply = 0, t_sync = 0, tc = clock64();
@@ -226,23 +233,27 @@ __global__ void __launch_bounds__(kBjThreads) bjacobi_kernel(BjArgs a) {
 #pragma unroll
       for (int tj = 0; tj < 4; ++tj) g[tj][0] = g[tj][1] = 0.0;
       const int ti = warp & 3, kh = (warp >> 2) * (JRC / 2);
-      // row chunks staged through registers: the next chunk's loads are in flight while the
-      // current one is multiplied (PRE loads per thread, all issued together)
-      double pre[PRE];
-      bj_fetch(a.G, k, cols, 0, pre);
-      for (int r0 = 0; r0 < k; r0 += JRC) {
-        bj_stage(pre, X);
-        __syncthreads();
-        if (r0 + JRC < k) bj_fetch(a.G, k, cols, r0 + JRC, pre);
+#pragma unroll
+      for (int c0 = 0; c0 < KST - 1; ++c0) {
+        if (c0 < nch) bj_issue(a.G, k, ld, cols, c0 * JRC, xring + c0 * XCH);
+        bj_commit();
+      }
+      for (int ch = 0; ch < nch; ++ch) {
+        bj_wait<KST - 2>();
+        __syncthreads();                       // chunk ch landed; slot (ch - 1) % KST is free
+        if (ch + KST - 1 < nch) bj_issue(a.G, k, ld, cols, (ch + KST - 1) * JRC, xring + ((ch + KST - 1) % KST) * XCH);
+        bj_commit();
+        const double* Xc = xring + (ch % KST) * XCH;
 #pragma unroll 4
         for (int kk = kh; kk < kh + JRC / 2; kk += 4) {
-          // A = X^T (pair column, row), B = X (row, pair column)
-          const double a0 = X[(kk + kq) * JLD + 8 * ti + r8];
+          // A = X^T (pair column, row), B = X (row, pair column): both Xc[column][row]
+          const double a0 = Xc[(8 * ti + r8) * XLD + kk + kq];
 #pragma unroll
-          for (int tj = 0; tj < 4; ++tj) dmma884(g[tj][0], g[tj][1], a0, X[(kk + kq) * JLD + 8 * tj + r8]);
+          for (int tj = 0; tj < 4; ++tj) dmma884(g[tj][0], g[tj][1], a0, Xc[(8 * tj + r8) * XLD + kk + kq]);
         }
-        __syncthreads();
       }
+      bj_wait<0>();
+      __syncthreads();
       { const long long t = clock64(); t_gram += t - tc; tc = t; }
       if (warp >= 4)
 #pragma unroll
@@ -318,11 +329,18 @@ __global__ void __launch_bounds__(kBjThreads) bjacobi_kernel(BjArgs a) {
       { const long long t = clock64(); t_inner += t - tc; tc = t; }
       // ---- X <- X V for the pair's columns (row chunks, DMMA: chunk (JRC x 32) * V (32 x 32))
       if (rotated) {
-        bj_fetch(a.G, k, cols, 0, pre);
-        for (int r0 = 0; r0 < k; r0 += JRC) {
-          bj_stage(pre, X);
+#pragma unroll
+        for (int c0 = 0; c0 < KST - 1; ++c0) {
+          if (c0 < nch) bj_issue(a.G, k, ld, cols, c0 * JRC, xring + c0 * XCH);
+          bj_commit();
+        }
+        for (int ch = 0; ch < nch; ++ch) {
+          const int r0 = ch * JRC;
+          bj_wait<KST - 2>();
           __syncthreads();
-          if (r0 + JRC < k) bj_fetch(a.G, k, cols, r0 + JRC, pre);
+          if (ch + KST - 1 < nch) bj_issue(a.G, k, ld, cols, (ch + KST - 1) * JRC, xring + ((ch + KST - 1) % KST) * XCH);
+          bj_commit();
+          const double* Xc = xring + (ch % KST) * XCH;
           // output tiles: (JRC/8) x 4, TPW per warp
           constexpr int TPW = JRC / 16;
           double acc[TPW][2];
@@ -333,12 +351,11 @@ __global__ void __launch_bounds__(kBjThreads) bjacobi_kernel(BjArgs a) {
 #pragma unroll
             for (int u = 0; u < TPW; ++u) {
               const int t = warp * TPW + u, ti = t / 4, tj = t % 4;
-              const double af = X[(8 * ti + r8) * JLD + kk + kq];
+              const double af = Xc[(kk + kq) * XLD + 8 * ti + r8];
               const double bf = V[kk + kq][8 * tj + r8];
               dmma884(acc[u][0], acc[u][1], af, bf);
             }
           }
-          __syncthreads();
 #pragma unroll
           for (int u = 0; u < TPW; ++u) {
             const int t = warp * TPW + u, ti = t / 4, tj = t % 4;
@@ -346,11 +363,12 @@ __global__ void __launch_bounds__(kBjThreads) bjacobi_kernel(BjArgs a) {
             for (int h = 0; h < 2; ++h) {
               const int rr = 8 * ti + r8, j = 8 * tj + 2 * kq + h;
               const int c = bj_col(cols[j / JB], j % JB, k);
-              if (c >= 0 && r0 + rr < k) __stcg(a.G + int64_t(c) * k + r0 + rr, acc[u][h]);
+              if (c >= 0 && r0 + rr < k) __stcg(a.G + int64_t(c) * ld + r0 + rr, acc[u][h]);
             }
           }
-          __syncthreads();
         }
+        bj_wait<0>();
+        __syncthreads();
         if (tid == 0) any_rot = 1;
       }
       { const long long t = clock64(); t_apply += t - tc; tc = t; }
@@ -372,11 +390,11 @@ __global__ void __launch_bounds__(kBjThreads) bjacobi_kernel(BjArgs a) {
 }
 
 // singular values = column norms; ranks by counting (descending, ties by index); Ut columns
-__global__ void bj_norms_kernel(const double* __restrict__ G, int k, double* __restrict__ nrm) {
+__global__ void bj_norms_kernel(const double* __restrict__ G, int k, int ld, double* __restrict__ nrm) {
   const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (j >= k) return;
   double a = 0.0;
-  for (int r = lane; r < k; r += 32) { const double x = G[int64_t(j) * k + r]; a = fma(x, x, a); }
+  for (int r = lane; r < k; r += 32) { const double x = G[int64_t(j) * ld + r]; a = fma(x, x, a); }
   a = warp_sum(a);
   if (lane == 0) nrm[j] = sqrt(a);
 }
@@ -391,13 +409,19 @@ __global__ void bj_rank_kernel(const double* __restrict__ nrm, int k, int* __res
   S[rk] = v;
 }
 
-__global__ void bj_out_kernel(const double* __restrict__ G, int k, const double* __restrict__ nrm,
+__global__ void bj_out_kernel(const double* __restrict__ G, int k, int ld, const double* __restrict__ nrm,
                               const int* __restrict__ rank, double* __restrict__ Ut) {
   const int j = blockIdx.y;
   const double inv = nrm[j] > 0.0 ? 1.0 / nrm[j] : 0.0;
   const int dst = rank[j];
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < k; r += gridDim.x * blockDim.x)
-    Ut[int64_t(dst) * k + r] = G[int64_t(j) * k + r] * inv;
+    Ut[int64_t(dst) * k + r] = G[int64_t(j) * ld + r] * inv;
+}
+
+__global__ void bj_copy_kernel(const double* __restrict__ src, int k, int ld, double* __restrict__ dst) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < int64_t(k) * k;
+       e += int64_t(gridDim.x) * blockDim.x)
+    dst[(e % k) + (e / k) * ld] = src[e];
 }
 
 }  // namespace
@@ -463,7 +487,9 @@ ssi_status cholqr2_big(const double* Y, int64_t ldy, int64_t m, int k, double* Q
   return trsm_big(Q, m, k, w.L2, w.Dp2, s);
 }
 
-size_t jacobi_big_scratch_elems(int k) { return size_t(k) + size_t(k) + kBjMaxSweeps + 1; }
+size_t jacobi_big_scratch_elems(int k) {
+  return size_t(k) + size_t(k) + kBjMaxSweeps + 2 + size_t(k + (k & 1)) * k;
+}
 
 int jacobi_big_ctas(int k) {
   int nb = (k + JB - 1) / JB;
@@ -478,16 +504,23 @@ ssi_status jacobi_big(double* G, int k, double* Ut, double* S, double* scratch, 
   int* rank = reinterpret_cast<int*>(scratch + k);
   int* flags = reinterpret_cast<int*>(scratch + 2 * size_t(k));
   if (cudaMemsetAsync(flags, 0, sizeof(int) * kBjMaxSweeps, s) != cudaSuccess) return launch_check("memset flags");
-  BjArgs a{G, k, nb, flags, status, getenv("SSI_JAC_PROFILE") ? 1 : 0};
+  // working copy with an even leading dimension (16-byte cp.async pieces of two rows)
+  const int ld = k + (k & 1);
+  double* Gp = scratch + 2 * size_t(k) + kBjMaxSweeps + 2;
+  Gp = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(Gp) + 15) & ~uintptr_t(15));
+  bj_copy_kernel<<<148 * 8, 256, 0, s>>>(G, k, ld, Gp);
+  SSI_TRY(launch_check("bj_copy_kernel"));
+  BjArgs a{Gp, k, nb, ld, flags, status, getenv("SSI_JAC_PROFILE") ? 1 : 0};
   void* args[] = {&a};
+  cudaFuncSetAttribute(bjacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kBjSmem));
   if (cudaLaunchCooperativeKernel(reinterpret_cast<void*>(bjacobi_kernel), dim3(unsigned(nb / 2)), dim3(kBjThreads),
-                                  args, 0, s) != cudaSuccess)
+                                  args, kBjSmem, s) != cudaSuccess)
     return launch_check("bjacobi_kernel (cooperative launch)");
-  bj_norms_kernel<<<(k + 7) / 8, 256, 0, s>>>(G, k, nrm);
+  bj_norms_kernel<<<(k + 7) / 8, 256, 0, s>>>(Gp, k, ld, nrm);
   SSI_TRY(launch_check("bj_norms_kernel"));
   bj_rank_kernel<<<(k + 255) / 256, 256, 0, s>>>(nrm, k, rank, S);
   SSI_TRY(launch_check("bj_rank_kernel"));
-  bj_out_kernel<<<dim3(unsigned((k + 255) / 256), unsigned(k)), 256, 0, s>>>(G, k, nrm, rank, Ut);
+  bj_out_kernel<<<dim3(unsigned((k + 255) / 256), unsigned(k)), 256, 0, s>>>(Gp, k, ld, nrm, rank, Ut);
   return launch_check("bj_out_kernel");
 }
 
