@@ -175,10 +175,13 @@ def _world_job(rank, world, port, q):
         cfg, P = _params()
         Y, _ = synth.make_record(cfg, N=60000)
         Yd = _dev(Y)
-        tabs, flags, counts = drivers.lag_sweep_3d(Yd, P, LAGS, api.CRITERIA_BRIDGE_3D, rank, world)
+        tabs, flags, counts, cl = drivers.identify_3d(Yd, P, LAGS, api.CRITERIA_BRIDGE_3D, rank=rank, world=world)
         recs = [_dev(synth.make_record(synth.config("c2", seed=cfg.seed + 7 * r), N=20000)[0]) for r in range(3)]
         btabs = drivers.record_batch(recs, P, rank, world, n_streams=2)
-        q.put((rank, (_host_tables(tabs), flags.cpu().numpy(), counts.cpu().numpy(), _host_tables(btabs))))
+        match, succ, _, _ = drivers.track_campaign([btabs[j] for j in range(3)], api.CRITERIA_BRIDGE_3D)
+        clus = (cl.labels.cpu().numpy(), cl.f.cpu().numpy(), cl.size.cpu().numpy())
+        q.put((rank, (_host_tables(tabs), flags.cpu().numpy(), counts.cpu().numpy(), _host_tables(btabs), clus,
+                      match.cpu().numpy())))
     finally:
         if world > 1:
             dist.destroy_process_group()
@@ -202,13 +205,17 @@ def _run_world(world):
 def test_two_ranks_match_one_rank(ssi):
     """world = 2 (two processes on one GPU, gloo) vs world = 1: the lag sweep's tables agree to
     FP64 rounding of the re-associated covariance sum (1e-9 relative on every pole's f and xi,
-    identical pole counts, stab3d flags and stable counts); the record batch, whose records are
-    independent, is bit-identical; both ranks hold identical gathered tables."""
+    identical pole counts, stab3d flags and stable counts) and so does the clustering of the
+    gathered diagram (identical memberships); the record batch, whose records are independent, is
+    bit-identical, and so is its tracking; both ranks hold identical gathered tables."""
     one = _run_world(1)[0]
     two = _run_world(2)
     for r in (0, 1):
-        t1, f1, c1, b1 = one
-        t2, f2, c2, b2 = two[r]
+        t1, f1, c1, b1, k1, m1 = one
+        t2, f2, c2, b2, k2, m2 = two[r]
+        assert np.array_equal(k1[0], k2[0]) and np.array_equal(k1[2], k2[2])       # memberships, sizes
+        np.testing.assert_allclose(k2[1], k1[1], rtol=1e-9)                         # cluster f
+        assert np.array_equal(m1, m2)
         assert sorted(t2) == sorted(t1) == list(LAGS)
         for lag in LAGS:
             cnt1, cnt2 = t1[lag][0], t2[lag][0]
