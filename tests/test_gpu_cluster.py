@@ -194,3 +194,32 @@ def test_c5_campaign_tracking(api):
     assert np.array_equal(match.cpu().numpy(), m_o)
     np.testing.assert_array_equal(success.cpu().numpy(), oracle.success_ratio(m_o))
     print("c5 campaign: reference modes", len(ref[0]), "success", success.cpu().numpy().round(1).tolist())
+
+
+def test_cluster_degenerate_settings(api):
+    """Cutoff >= 1 (no f band pruning), a min_size above every cluster (nothing kept, all labels
+    -1), max_clusters below the cluster count (overflow flagged, outputs truncated), and orders
+    reported as truncated (count = -1) inside the diagram."""
+    d = make_diagram(31, 3, list(range(2, 41, 2)), 16, 10, 6)
+    d.count[1, 5] = -1                     # an order above the numerical rank (count = -1)
+    d.count[2, 7] = -1
+    cells = diagram_cells(d)
+    for c in (cells[1][5], cells[2][7]):
+        c.poles = []
+    crit = oracle.SC_10DOF_3D
+    gc, oc = _run_both(api, cells, crit, 1.5, 1, 16, 10)
+    compare_clustering(gc, oc, 1.5)
+    gc, oc = _run_both(api, cells, crit, 0.1, 10 ** 6, 16, 10)
+    compare_clustering(gc, oc, 0.1)
+    assert gc.n_clusters == 0 and (gc.labels.cpu().numpy() == -1).all()
+    flags, _ = oracle.stab3d(cells, crit, 16)
+    tabs = [cells_to_table(c, api, "cuda", cap=16, l=10) for c in cells]
+    full = api.cluster3d(tabs, torch.from_numpy(flags).cuda(), _crit(api, crit), cutoff=0.1, min_size=1)
+    few = api.cluster3d(tabs, torch.from_numpy(flags).cuda(), _crit(api, crit), cutoff=0.1, min_size=1,
+                        max_clusters=3)
+    assert full.n_clusters > 3 and full.overflow == 0
+    assert few.overflow == 1 and few.n_clusters == 3
+    np.testing.assert_array_equal(few.f.cpu().numpy(), full.f.cpu().numpy()[:3])
+    lab = few.labels.cpu().numpy()
+    lab_full = full.labels.cpu().numpy()
+    assert np.array_equal(lab[lab_full < 3], lab_full[lab_full < 3]) and (lab[lab_full >= 3] == -1).all()

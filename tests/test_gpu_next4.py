@@ -138,3 +138,33 @@ def test_raw_record_through_preprocess_and_identification(api):
         j = np.argmin(np.abs(f - f0))
         assert abs(f[j] - f0) / f0 <= 0.01, (f0, f[j])
     assert f.max() < 20.0
+
+
+@pytest.mark.parametrize("order,rp", [(2, 0.5), (16, 0.05)])
+def test_preprocess_other_orders(api, order, rp):
+    """Orders at the ends of the supported range (2 and 16 poles) through the same chunked passes."""
+    Y, _ = make_raw_record(l=4, fs=125.0, N=12000, seed=order, dtype=np.float64)
+    Z = api.preprocess(torch.from_numpy(Y).cuda(), 125.0, 40.0, order=order, rp_db=rp)
+    _check(Z.cpu().numpy(), oracle.preprocess(Y, 125.0, 40.0, order=order, rp_db=rp))
+
+
+def test_preprocess_and_frame_reject_bad_arguments(api):
+    """Synchronous checks (ssi.h): odd order, edge at/above Nyquist, no output sample, bad frame."""
+    import ctypes as C
+    from paper_2411_05510_b200 import _lib
+    lib = _lib.get()
+    Y = torch.zeros((100, 3), dtype=torch.float32, device="cuda")
+    Z = torch.zeros((100, 3), dtype=torch.float32, device="cuda")
+    ws = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    p = lambda t: C.c_void_p(t.data_ptr())
+    call = lambda *a: lib.ssi_preprocess(p(Y), 0, 100, 3, 3, *a, p(Z), 0, 3, p(ws), ws.numel(), None)
+    assert call(125.0, 8, 25, 7, 0.05, 16.0) == 1                 # odd order
+    assert call(125.0, 8, 25, 8, 0.05, 500.0) == 1                # edge >= L fs / 2
+    assert call(125.0, 1, 1000, 8, 0.05, 16.0) == 1               # N L / M < 1
+    assert lib.ssi_preprocess(p(Y), 0, 100, 3, 2, 125.0, 8, 25, 8, 0.05, 16.0, p(Z), 0, 3, p(ws), ws.numel(),
+                              None) == 2                          # ldY < l
+    b = C.c_size_t(0)
+    assert lib.ssi_frame_simulate_ws(13, 100, 0, C.byref(b)) == 1  # n_dof > 12
+    assert lib.ssi_frame_model(10, 100.0, 5e6, 0.01, 4, 4, 200.0, p(ws), p(ws), p(ws), p(ws), None) == 1  # equal modes
+    torch.cuda.synchronize()
+    assert torch.all(Z == 0)
