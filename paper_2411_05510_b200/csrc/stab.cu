@@ -1,7 +1,8 @@
 // A13: hard criteria + 3D soft criteria (§2.1; Eq. (stabcriteria3D),
-// PAPER.md:283-291 §2.3 step ii; readings A-17..A-21). One launch per lag, one CTA
+// PAPER.md:283-291 §2.3 step ii; readings A-17..A-21). One launch for all lags, one CTA
 // per model order, one warp per pole; MAC over the l mode-shape components.
 #include "rsvd.cuh"
+#include "cluster.cuh"
 
 namespace ssi {
 namespace {
@@ -28,11 +29,18 @@ __device__ bool mac_ok(const double* a, const double* b, int l, double alpha) {
   return (1.0 - mac) <= alpha;
 }
 
-__global__ void __launch_bounds__(NT) stab_kernel(ssi_pole_table cur, ssi_pole_table prev,
-                                                  int has_prev, ssi_criteria c, uint8_t* flags,
+// One launch for every lag: CTA (order o, lag g = blockIdx.y); the tables travel by value in a
+// kernel-parameter TableSet (no host-to-device copy; at most SSI_MAX_LAGS lags per launch).
+__global__ void __launch_bounds__(NT) stab_kernel(TableSet ts, int g0, ssi_criteria c, uint8_t* flags,
                                                   int32_t* stable_count) {
   __shared__ int cnt;
   const int o = blockIdx.x;
+  const int gl = blockIdx.y, g = g0 + gl;
+  const ssi_pole_table& cur = ts.t[gl];
+  const ssi_pole_table& prev = ts.t[gl > 0 ? gl - 1 : SSI_MAX_LAGS - 1];   // slot MAX-1: lag g0 - 1
+  const int has_prev = g > 0;
+  flags += int64_t(gl) * cur.n_orders * cur.cap;
+  stable_count += int64_t(gl) * cur.n_orders;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cap = cur.cap, l = cur.l;
   if (threadIdx.x == 0) cnt = 0;
@@ -76,10 +84,14 @@ __global__ void __launch_bounds__(NT) stab_kernel(ssi_pole_table cur, ssi_pole_t
 ssi_status stab3d_run(const ssi_pole_table* tables, int n_lags, const ssi_criteria& crit,
                       uint8_t* flags, int32_t* stable_count, cudaStream_t s) {
   const int no = tables[0].n_orders, cap = tables[0].cap;
-  for (int g = 0; g < n_lags; ++g) {
-    const ssi_pole_table& prev = tables[g > 0 ? g - 1 : 0];
-    stab_kernel<<<no, NT, 0, s>>>(tables[g], prev, g > 0 ? 1 : 0, crit,
-                                  flags + int64_t(g) * no * cap, stable_count + int64_t(g) * no);
+  // lags in groups of SSI_MAX_LAGS - 1; the last slot carries the group's predecessor lag
+  for (int g0 = 0; g0 < n_lags; g0 += SSI_MAX_LAGS - 1) {
+    const int ng = n_lags - g0 < SSI_MAX_LAGS - 1 ? n_lags - g0 : SSI_MAX_LAGS - 1;
+    TableSet ts;
+    for (int j = 0; j < SSI_MAX_LAGS; ++j) ts.t[j] = tables[g0 + (j < ng ? j : 0)];
+    ts.t[SSI_MAX_LAGS - 1] = tables[g0 > 0 ? g0 - 1 : 0];
+    stab_kernel<<<dim3(unsigned(no), unsigned(ng)), NT, 0, s>>>(ts, g0, crit, flags + int64_t(g0) * no * cap,
+                                                                stable_count + int64_t(g0) * no);
     SSI_TRY(launch_check("stab_kernel"));
   }
   return SSI_OK;
