@@ -364,14 +364,27 @@ def batch_leg(api, drivers, synth, torch, dist, world, rank, dev, streams):
     torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
     a.record()
-    drivers.record_batch(recs, P, rank, world, n_streams=streams)
+    tabs = drivers.record_batch(recs, P, rank, world, n_streams=streams)
     b.record()
     torch.cuda.synchronize()
     ms = _max_over_ranks([a.elapsed_time(b)], world, dev)[0]
+    # monitoring step iii on the gathered tables: per-session two-stage clustering
+    # of the 2D diagram and tracking against the first session (every rank holds every table)
+    crit = api.CRITERIA_BRIDGE_2D
+    c = torch.cuda.Event(enable_timing=True); d = torch.cuda.Event(enable_timing=True)
+    c.record()
+    match, succ, ref_f, _ = drivers.track_campaign([tabs[j] for j in range(C5_RECORDS)], crit)
+    d.record()
+    torch.cuda.synchronize()
+    track = {"ms": c.elapsed_time(d), "sessions": C5_RECORDS, "reference_modes": int(ref_f.numel()),
+             "mean_success_pct": float(succ.mean().item()) if succ.numel() else None,
+             "note": "per-session ssi_stab3d + ssi_cluster_stage1/2 (one host read of the retained count "
+                     "each) + one ssi_track; 2 distinct records rotated, so success is ~100 % by construction"}
     return {"workload": f"c5: {C5_RECORDS} records x 180000 F32 samples, l=192, i=50, k=220, q=2, orders 2..200 "
                         "(2 distinct drifted records per rank rotated)",
             "ms_per_batch": ms, "records_per_s": C5_RECORDS / (ms / 1e3), "n_gpus": world, "scaling": "strong",
-            "records_per_rank": len(drivers.record_assignment(C5_RECORDS, world)[0])}
+            "records_per_rank": len(drivers.record_assignment(C5_RECORDS, world)[0]),
+            "campaign_clustering_tracking": track}
 
 
 def main():

@@ -442,3 +442,15 @@ def track_campaign(tables, crit: api.Criteria, max_modes: int = 64, df_max: floa
         ref_f, ref_shape = ref
     match, success = api.track(ref_f, ref_shape, f, sh, cnt, df_max, macd_max)
     return match, success, ref_f, ref_shape
+
+
+def identify_raw(raw: torch.Tensor, fs_in: float, fs_out: float, P: SweepParams, stream_id: int = 0,
+                 order: int = 8, rp_db: float = 0.05, engine: Engine | None = None):
+    """A raw acquisition file to its pole table (PAPER.md:482 then §2.1): ssi_preprocess (detrend,
+    zero-phase Chebyshev-I low-pass, rate change fs_in -> fs_out) into an FP32 record, then A1-A11.
+    P.fs must equal fs_out. Returns (table, preprocessed record)."""
+    if abs(P.fs - fs_out) > 1e-9 * fs_out:
+        raise ValueError("P.fs must be the output rate")
+    Y = api.preprocess(raw, fs_in, fs_out, order=order, rp_db=rp_db, out_dtype=torch.float32)
+    eng = engine or Engine(P, Y.shape[0], Y.device)
+    return eng.identify(Y, stream_id), Y

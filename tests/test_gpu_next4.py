@@ -125,9 +125,8 @@ def test_raw_record_through_preprocess_and_identification(api):
     identified (statistical band); the out-of-band ones are gone."""
     from paper_2411_05510_b200 import drivers
     Y, modes = make_raw_record(l=24, fs=125.0, N=450000, seed=9)
-    Z = api.preprocess(torch.from_numpy(Y).cuda(), 125.0, 40.0, out_dtype=torch.float32)
     P = drivers.SweepParams(l=24, i=40, n_max=60, p=20, q=2, fs=40.0, seed=1)
-    tab = drivers.Engine(P, Z.shape[0]).identify(Z, stream_id=1)
+    tab, Z = drivers.identify_raw(torch.from_numpy(Y).cuda(), 125.0, 40.0, P, stream_id=1)
     torch.cuda.synchronize()
     n = 2 * len(modes.f)
     o = (n - P.n_min) // P.n_step
