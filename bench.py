@@ -348,6 +348,44 @@ def sweep_leg(api, drivers, synth, torch, dist, Y, world, rank, dev, reps=3, war
             "lag_assignment": drivers.lpt_assign(list(C4_LAGS), world)}
 
 
+def _event_ms(torch, fn, reps=3):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
+        a.record(); fn(); b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def next_legs(api, synth, torch, R_c3, dev):
+    """Per-GPU legs of the paper's own settings (one GPU, device time, median of 3):
+    * NEXT-1: Algorithm 1 verbatim (q = p = 0) at the paper's rank rule k = ceil(kbar(T) % T)
+      (PAPER.md:367-371) on the c3 record: T = 11520, kbar = 25 %, k = 2880 (structured RSVD);
+    * NEXT-4: preprocessing of a 2-hour 114-channel 125 Hz acquisition to 40 Hz."""
+    from synth.raw import make_raw_record
+    cfg = synth.config("c3")
+    m = cfg.m
+    k = int(-(-max(30.0 - 0.00156 * m, 25.0) * m // 100))
+    ws = api._workspace(api.rsvd_toeplitz_ws_bytes(cfg.l, cfg.i, k, cfg.n_max), dev)
+    ms_rr = _event_ms(torch, lambda: api.rsvd_toeplitz(R_c3, cfg.i, k, 0, cfg.philox_key, cfg.i, cfg.n_max, ws=ws))
+    del ws
+    raw, _ = make_raw_record(l=114, fs=125.0, N=900000, seed=482)
+    rawd = torch.from_numpy(raw).to(dev)
+    wsp = api._workspace(api.preprocess_ws_bytes(900000, 114, 8), dev)
+    Z = torch.empty((288000, 114), dtype=torch.float32, device=dev)
+    ms_pp = _event_ms(torch, lambda: api.preprocess(rawd, 125.0, 40.0, out=Z, ws=wsp))
+    return {"rank_rule_rsvd_c3": {"workload": f"c3 record, T = {m}, Algorithm 1 verbatim (q = p = 0), k = {k} "
+                                              "(kbar(T) = 25 %), T through its block structure",
+                                  "ms_per_rsvd": ms_rr},
+            "preprocess_bridge_2h": {"workload": "114 ch x 900000 FP32 at 125 Hz -> 288000 at 40 Hz (L/M = 8/25), "
+                                                 "detrend + zero-phase 8th-order Chebyshev-I",
+                                     "ms": ms_pp, "hours_of_data_per_s": 2.0 / (ms_pp / 1e3)}}
+
+
 def batch_leg(api, drivers, synth, torch, dist, world, rank, dev, streams):
     """c5: 64 records of 180000 samples over all ranks (strong scaling), 8 in flight per rank,
     one packed all_gather of the 64 tables; device time, max over ranks."""
@@ -520,6 +558,8 @@ def main():
     if not args.no_legs:
         legs["lag_sweep_c4"] = sweep_leg(api, drivers, synth, torch, dist, Y_c3, world, rank, dev)
         legs["record_batch_c5"] = batch_leg(api, drivers, synth, torch, dist, world, rank, dev, args.streams)
+        if rank == 0:
+            legs["paper_settings"] = next_legs(api, synth, torch, eng.R, dev)
 
     # ---------------- roofline
     # The covariance stage alone (CUDA events around one record's A1 on the current stream) and
