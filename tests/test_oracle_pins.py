@@ -324,6 +324,27 @@ def test_p13_sketch_layout_and_moments():
     assert u1.min() > 0 and u1.max() < 1 and abs(u2.mean() - 0.5) < 0.005
 
 
+def test_p13_sketch_distribution_and_independence():
+    """Distributional pins of Ω independent of its construction: the Kolmogorov-Smirnov distance to
+    N(0, 1) (scipy.stats, not the oracle's Box-Muller), the two members of a Box-Muller pair and
+    neighbouring pairs uncorrelated, columns of Ω (distinct counters) uncorrelated, and a second
+    stream / seed giving an uncorrelated sketch; Ω^T Ω / m -> I (what the RSVD relies on)."""
+    from scipy import stats
+    m, k = 20000, 24
+    Om = oracle.gaussian_sketch(m, k, 0x5EED0003, 60)
+    z = Om.T.reshape(-1)                                 # element order e = col m + row
+    assert stats.kstest(z, "norm").pvalue > 1e-3
+    band = 4.5 / np.sqrt(z.size / 2)                     # ~4.5 sigma for a correlation estimate
+    assert abs(np.corrcoef(z[0::2], z[1::2])[0, 1]) < band           # cos / sin members of a pair
+    assert abs(np.corrcoef(z[:-2:2], z[2::2])[0, 1]) < band          # neighbouring pairs
+    G = Om.T @ Om / m
+    assert np.abs(G - np.eye(k)).max() < 6.0 / np.sqrt(m)            # columns ~ orthonormal
+    O2 = oracle.gaussian_sketch(m, k, 0x5EED0003, 61)
+    O3 = oracle.gaussian_sketch(m, k, 0x5EED0004, 60)
+    for other in (O2, O3):
+        assert np.abs(Om.T @ other / m).max() < 6.0 / np.sqrt(m)
+
+
 # ---------------------------------------------------------------- P14 indicators
 def test_p14_mac_mpc_mpd_special_cases():
     rng = np.random.default_rng(8)
