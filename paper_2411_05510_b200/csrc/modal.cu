@@ -347,7 +347,10 @@ __device__ __forceinline__ double* order_C(const EigArgs& g, int o) {
 // One CTA (1024 threads) per order: A <- Q_H^T A Q_H in place (global, L2-resident) and
 // C <- U[0:l, :n] Q_H. Left update: warp per column (coalesced, lanes over rows); right update:
 // 4 warps per 32-row block split the columns (coalesced, many loads in flight).
-constexpr int HT = 1024;
+#ifndef SSI_HESS_THREADS
+#define SSI_HESS_THREADS 1024
+#endif
+constexpr int HT = SSI_HESS_THREADS;   // threads of the Hessenberg CTA
 #ifndef SSI_HESS_QS
 #define SSI_HESS_QS 2
 #endif
