@@ -11,6 +11,7 @@ Multi-GPU (one process per GPU, torch.distributed over NCCL):
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 
 import torch
@@ -31,10 +32,21 @@ class SweepParams:
     seed: int = 0
     cov_mode: str = "spectral"
     structured: bool = True     # RSVD through the block structure of T (T never formed)
+    rank_rule: bool = False     # k = ceil(kbar(T) % T) per lag instead of n_max + p
 
     @property
     def k(self):
-        return self.n_max + self.p
+        return self.k_for(self.i)
+
+    def k_for(self, i: int) -> int:
+        """Sketch width at time-lag step i: n_max + p (north star), or the paper's rank rule
+        k = ceil(kbar(T) % * T), kbar(T) = max{30 - 0.00156 T; 25} % with T = l i (Eq.
+        empirical_formula, PAPER.md:367-371)."""
+        if not self.rank_rule:
+            return self.n_max + self.p
+        T = self.l * i
+        pct = max(30.0 - 0.00156 * T, 25.0)
+        return max(self.n_max, min(T, math.ceil(pct * T / 100.0 - 1e-9)))
 
     @property
     def m(self):
@@ -91,7 +103,7 @@ class Engine:
                 tab = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, out=self.table,
                                       ws=self.ws_modal)
             else:
-                U, S = api.rsvd_toeplitz(R, i, P.k, P.q, P.seed, stream_id, P.n_max, ws=self.ws_rsvd)
+                U, S = api.rsvd_toeplitz(R, i, P.k_for(i), P.q, P.seed, stream_id, P.n_max, ws=self.ws_rsvd)
                 tab = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=self.ws_modal)
             return tab, (U, S)
         if i == P.i:
@@ -102,7 +114,7 @@ class Engine:
                                   ws=self.ws_modal)
             return tab, (U, S)
         T = api.toeplitz(R, i, out=self.T.view(-1)[:m * m].view(m, m))
-        U, S = api.rsvd(T, P.k, P.q, P.seed, stream_id, P.n_max, ws=self.ws_rsvd)
+        U, S = api.rsvd(T, P.k_for(i), P.q, P.seed, stream_id, P.n_max, ws=self.ws_rsvd)
         return api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=self.ws_modal), (U, S)
 
     def workspaces(self):
@@ -329,11 +341,12 @@ def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank
     for j in range(ns):
         lag_max = max(mine[j::ns])                       # workspaces sized for the slot's largest lag
         m_max = P.l * lag_max
+        k_max = max(P.k_for(i) for i in mine[j::ns])
         if P.structured:
-            ws_r = api._workspace(api.rsvd_toeplitz_ws_bytes(P.l, lag_max, P.k, P.n_max), dev)
+            ws_r = api._workspace(max(api.rsvd_toeplitz_ws_bytes(P.l, i, P.k_for(i), P.n_max) for i in mine[j::ns]), dev)
             tb = None
         else:
-            ws_r = api._workspace(api.rsvd_ws_bytes(m_max, P.k, P.n_max), dev)
+            ws_r = api._workspace(api.rsvd_ws_bytes(m_max, k_max, P.n_max), dev)
             tb = torch.empty(m_max * m_max, dtype=torch.float64, device=dev)
         ws_m = api._workspace(max(api.modal_sweep_ws_bytes(P.l, i, P.n_min, P.n_max, P.n_step)
                                   for i in mine[j::ns]), dev)
@@ -347,10 +360,10 @@ def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank
         with torch.cuda.stream(st):
             m = P.l * i
             if P.structured:
-                U, S = api.rsvd_toeplitz(R, i, P.k, P.q, P.seed, i, P.n_max, ws=ws_r)
+                U, S = api.rsvd_toeplitz(R, i, P.k_for(i), P.q, P.seed, i, P.n_max, ws=ws_r)
             else:
                 T = api.toeplitz(R, i, out=tb[:m * m].view(m, m))
-                U, S = api.rsvd(T, P.k, P.q, P.seed, i, P.n_max, ws=ws_r)
+                U, S = api.rsvd(T, P.k_for(i), P.q, P.seed, i, P.n_max, ws=ws_r)
             local[i] = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=ws_m)
     for st in streams:
         cur.wait_stream(st)
@@ -454,3 +467,31 @@ def identify_raw(raw: torch.Tensor, fs_in: float, fs_out: float, P: SweepParams,
     Y = api.preprocess(raw, fs_in, fs_out, order=order, rp_db=rp_db, out_dtype=torch.float32)
     eng = engine or Engine(P, Y.shape[0], Y.device)
     return eng.identify(Y, stream_id), Y
+
+
+# ------------------------------------------------------------------ the paper's bridge workload
+def bridge_params(i: int = 76) -> SweepParams:
+    """The San Faustino settings: 114 channels at 40 Hz, j_b = 76 (T = 8664), orders
+    250..400 step 2, Algorithm 1 verbatim (q = 0) with the rank rule (25 % of T, k = 2166)."""
+    return SweepParams(l=114, i=i, n_max=400, p=0, q=0, fs=40.0, n_min=250, n_step=2, rank_rule=True)
+
+
+def bridge_identify_2d(raw: torch.Tensor, P: SweepParams | None = None, min_size: int | None = None):
+    """One record, 2D diagram: preprocessing 125 -> 40 Hz, covariances, RSVD,
+    modal sweep over orders 250..400, hard + soft criteria along the order axis (2 %, 3 %, 2 %)
+    and the two-stage clustering. Returns (table, flags, Clustering)."""
+    P = P or bridge_params()
+    tab, Y = identify_raw(raw, 125.0, P.fs, P)
+    crit = api.CRITERIA_BRIDGE_2D
+    flags, _ = api.stab3d([tab], crit)
+    ms = min_size if min_size is not None else max(1, int(0.2 * tab.n_orders))
+    return tab, flags, api.cluster3d([tab], flags, crit, min_size=ms)
+
+
+def bridge_identify_3d(raw: torch.Tensor, lags=tuple(range(69, 105, 5)), min_size: int | None = None,
+                       timing: dict | None = None):
+    """One record, 3D diagram: preprocessing, then 8 time lags j_b = 69..104 (rank
+    rule per lag), the 3D soft criteria (2.5 %, 5 %, 3 %) and the two-stage clustering."""
+    P = bridge_params(max(lags))
+    Y = api.preprocess(raw, 125.0, P.fs, out_dtype=torch.float32)
+    return identify_3d(Y, P, lags, api.CRITERIA_BRIDGE_3D, min_size=min_size, timing=timing)

@@ -100,3 +100,33 @@ def test_c3_rank_rule_full_size(api):
     U, S = api.rsvd_toeplitz(_dev(R), cfg.i, k, 0, cfg.philox_key, cfg.i, cfg.n_max, check=True)
     torch.cuda.synchronize()
     _svd_parity(U.cpu().numpy(), S.cpu().numpy(), Uo, So, cfg.n_max, k)
+
+
+def test_bridge_record_2d_full_size(api):
+    """The paper's bridge workload at its own sizes: a 2-hour 114-channel record,
+    j_b = 76 (T = 8664), Algorithm 1 verbatim with k = 25 % of T = 2166, orders 250..400. GPU chain
+    (covariances -> structured RSVD -> modal sweep) against the oracle chain on the same
+    preprocessed record (uploaded from the GPU's preprocessing, itself parity-tested in
+    test_gpu_next4.py: the oracle cannot run the 2-hour filter at 1 kHz in a test's time):
+    singular values and the poles of a sample of orders."""
+    from paper_2411_05510_b200 import drivers
+    from synth.raw import make_bridge_raw
+    from tests.parity import gpu_cells, compare_tables
+    raw, modes = make_bridge_raw()
+    P = drivers.bridge_params()
+    Yd = api.preprocess(torch.from_numpy(raw).cuda(), 125.0, 40.0, out_dtype=torch.float32)
+    Y = Yd.cpu().numpy()
+    assert P.k == 2166 and Y.shape == (288000, 114)
+    R = api.covariances(Yd, 2 * P.i - 1, 1, "spectral", check=True)
+    U, S = api.rsvd_toeplitz(R, P.i, P.k, 0, P.seed, P.i, P.n_max, check=True)
+    Ro = oracle.covariances(Y, 2 * P.i - 1)
+    assert np.linalg.norm(R.cpu().numpy() - Ro) / np.linalg.norm(Ro) <= 1e-12
+    Uo, So, _ = oracle.rsvd(oracle.toeplitz(Ro, P.i), P.k, 0, P.seed, P.i, P.n_max)
+    _svd_parity(U.cpu().numpy(), S.cpu().numpy(), Uo, So, P.n_max, P.k)
+    orders = [250, 300, 350, 400]
+    cells = oracle.modal_sweep(Uo, So, P.l, P.i, orders, P.dt)
+    for n, c in zip(orders, cells):
+        tab = api.modal_sweep(U, S, P.l, P.i, n, n, 2, P.dt, check=True)
+        st = compare_tables(gpu_cells(tab), [c])
+        assert st["count_mismatch"] == [], n
+        assert st["max_df_all"] <= 1e-6 and st["max_dxi_all"] <= 1e-5, (n, st)
