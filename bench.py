@@ -378,7 +378,21 @@ def next_legs(api, synth, torch, R_c3, dev):
     wsp = api._workspace(api.preprocess_ws_bytes(900000, 114, 8), dev)
     Z = torch.empty((288000, 114), dtype=torch.float32, device=dev)
     ms_pp = _event_ms(torch, lambda: api.preprocess(rawd, 125.0, 40.0, out=Z, ws=wsp))
-    return {"rank_rule_rsvd_c3": {"workload": f"c3 record, T = {m}, Algorithm 1 verbatim (q = p = 0), k = {k} "
+    # the paper's own end-to-end bridge workload: one synthetic 2-hour
+    # 114-channel 125 Hz acquisition, preprocessing to 40 Hz, 2D (j_b = 76) and 3D (j_b = 69..104)
+    from paper_2411_05510_b200 import drivers
+    from synth.raw import make_bridge_raw
+    braw = torch.from_numpy(make_bridge_raw()[0]).to(dev)
+    ms_b2 = _event_ms(torch, lambda: drivers.bridge_identify_2d(braw), reps=1)
+    ms_b3 = _event_ms(torch, lambda: drivers.bridge_identify_3d(braw), reps=1)
+    bridge = {"workload": "synthetic San-Faustino-shaped acquisition: 114 ch x 900000 FP32 at 125 Hz (2 h) -> 40 Hz; "
+                          "Algorithm 1 verbatim at the rank rule (j_b = 76: T = 8664, k = 2166), orders 250..400, "
+                          "HC + SC + two-stage clustering",
+              "identify_2d_ms": ms_b2, "identify_3d_8_lags_ms": ms_b3,
+              "paper_cpu_s": {"rsvd_2d": 204, "rsvd_3d": 512, "svd_2d": 449,
+                              "hardware": "i7-8750H (PAPER.md:544), other hardware: context only"}}
+    return {"bridge_record": bridge,
+            "rank_rule_rsvd_c3": {"workload": f"c3 record, T = {m}, Algorithm 1 verbatim (q = p = 0), k = {k} "
                                               "(kbar(T) = 25 %), T through its block structure",
                                   "ms_per_rsvd": ms_rr},
             "preprocess_bridge_2h": {"workload": "114 ch x 900000 FP32 at 125 Hz -> 288000 at 40 Hz (L/M = 8/25), "
