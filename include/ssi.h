@@ -36,8 +36,10 @@
  *    decision is taken on the device (conditional launches), so it costs no host
  *    synchronisation; the status stays SSI_OK. Only a breakdown of the final pass, or a
  *    non-finite Gram matrix, sets SSI_ERR_NUMERIC. Sketch widths k > 512 (the paper's rank rule
- *    at bridge sizes, blocked whole-GPU Cholesky) have no shifted retry: any breakdown sets
- *    SSI_ERR_NUMERIC.
+ *    at bridge sizes, blocked whole-GPU Cholesky) take the same fallback through conditional
+ *    launches of the blocked kernels (the shift uses the trace of the unshifted Gram matrix),
+ *    with up to three shifted extra passes, each run only if the previous one shifted (an
+ *    exactly rank-deficient panel needs two or three; see linalg_big.cu).
  *  - Determinism: fixed inputs, seed and launch configuration give bit-identical
  *    outputs run to run (fixed reduction orders, no floating-point atomics).
  */

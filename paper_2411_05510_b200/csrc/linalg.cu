@@ -424,10 +424,13 @@ size_t cholqr_partial_elems(int64_t m, int k) {
 void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w) {
   if (k > kSvdMaxK) {   // blocked whole-GPU path (linalg_big.cu): no explicit inverses
     w.W = c.take<double>(size_t(k) * k);
+    w.W0 = c.take<double>(size_t(k) * k);
     w.L1 = c.take<double>(size_t(k) * k);
     w.L2 = c.take<double>(size_t(k) * k);
-    w.Linv1 = w.Linv2 = w.LinvT1 = w.LinvT2 = w.Lb = w.Linvb = w.LinvTb = nullptr;
-    w.flag = c.take<int>(1);
+    w.Lb = c.take<double>(size_t(k) * k);
+    w.La = c.take<double>(size_t(k) * k);
+    w.Linv1 = w.Linv2 = w.LinvT1 = w.LinvT2 = w.Linvb = w.LinvTb = nullptr;
+    w.flag = c.take<int>(1 + kCqExtraPasses);
     w.Q1 = c.take<double>(size_t(m) * k);
     w.chol_g = nullptr;
     w.partial = c.take<double>(cholqr_partial_elems(m, k) + 1);
@@ -437,6 +440,7 @@ void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w) {
     return;
   }
   w.Dp1 = w.Dp2 = nullptr;
+  w.W0 = w.La = nullptr;
   w.W = c.take<double>(size_t(k) * k);
   w.L1 = c.take<double>(size_t(k) * k);
   w.Linv1 = c.take<double>(size_t(k) * k);

@@ -16,13 +16,16 @@ struct CholQRWork {
   double* Lb;       // k x k factors of the fallback pass (shifted CholeskyQR3)
   double* Linvb;
   double* LinvTb;
-  int* flag;        // 1 when pass 1 needed the shift (device; read by the conditional launches)
+  int* flag;        // 1 when pass 1 needed the shift (device; read by the conditional launches);
+                    //   k > kSvdMaxK: one flag per pass (1 + kCqExtraPasses)
   double* Q1;       // m x k intermediate
   double* chol_g;   // packed triangle when k is too large for shared memory
   double* partial;  // split-K partials
   double* tallp;    // split-K partials of the tall-skinny kernels
   double* Dp1;      // k > kSvdMaxK (linalg_big.cu): 64 x 64 panel inverses of L1 / L2 and the
   double* Dp2;      //   original Gram diagonal
+  double* W0;       // k > kSvdMaxK: the unshifted Gram matrix of a pass (shifted retry)
+  double* La;       // k > kSvdMaxK: product of the extra passes' factors
 };
 size_t cholqr_partial_elems(int64_t m, int k);
 void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w);
@@ -45,6 +48,7 @@ ssi_status chol_inv(const double* W, int k, int64_t m, double* L, double* Linv, 
 // entry points reject larger k synchronously, before any launch.
 constexpr int kSvdMaxK = 512;
 constexpr int kBigMaxK = 4096;
+constexpr int kCqExtraPasses = 3;   // k > kSvdMaxK: shifted extra CholeskyQR passes at most
 
 // linalg_big.cu (k > kSvdMaxK)
 size_t cholqr_big_panel_elems(int k);

@@ -2,7 +2,8 @@
 // PAPER.md:360-373 Eq. (empirical_formula) and :513 — e.g. k = 2880 at T = 11520):
 //   * CholeskyQR2 with a blocked right-looking Cholesky (64-column panels: one CTA factors the
 //     diagonal block and inverts it, DMMA tiles form the panel and the trailing update) and a
-//     blocked right-looking triangular solve Q = Y L^{-T} (no explicit L^{-1});
+//     blocked right-looking triangular solve Q = Y L^{-T} (no explicit L^{-1}); the shifted
+//     CholeskyQR3 fallback on breakdown, decided on the device (conditional launches);
 //   * the small SVD of the k x k factor as a block one-sided (Hestenes) Jacobi over the whole GPU:
 //     16-column blocks, round-robin pairing of the blocks, one persistent CTA per block pair
 //     (grid barrier between rounds); per pair the 32 x 32 Gram matrix is formed on the FP64
@@ -30,7 +31,8 @@ constexpr int kNtThreads = 256;
 // the tile reads its A rows before it writes them). lower: skip tiles strictly above the diagonal.
 __global__ void __launch_bounds__(kNtThreads) gemm_nt_kernel(int64_t M, int64_t N, int K, const double* A, int64_t lda,
                                                              const double* B, int64_t ldb, double* C, int64_t ldc,
-                                                             double alpha, double beta, int lower) {
+                                                             double alpha, double beta, int lower, const int* run_if) {
+  if (!run_enabled(run_if)) return;
   if (lower && blockIdx.y > blockIdx.x) return;
   extern __shared__ double smb[];
   double* As = smb;             // [64][TLD]: As[r][k]
@@ -78,21 +80,26 @@ __global__ void __launch_bounds__(kNtThreads) gemm_nt_kernel(int64_t M, int64_t 
 }
 
 ssi_status gemm_nt(int64_t M, int64_t N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
-                   double* C, int64_t ldc, double alpha, double beta, bool lower, cudaStream_t s) {
+                   double* C, int64_t ldc, double alpha, double beta, bool lower, cudaStream_t s,
+                   const int* run_if = nullptr) {
   if (M <= 0 || N <= 0) return SSI_OK;
   const size_t smem = size_t(2) * TT * TLD * sizeof(double);
   cudaFuncSetAttribute(gemm_nt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   gemm_nt_kernel<<<dim3(unsigned((M + TT - 1) / TT), unsigned((N + TT - 1) / TT)), kNtThreads, smem, s>>>(
-      M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, lower ? 1 : 0);
+      M, N, K, A, lda, B, ldb, C, ldc, alpha, beta, lower ? 1 : 0, run_if);
   return launch_check("gemm_nt_kernel");
 }
 
 // Diagonal panel [j0, j0 + jb) of the trailing-updated W: L11 = chol(W11) into L, L11^{-1} into
 // D (jb x jb col-major, ld PB). A pivot below 64 k u times its original diagonal entry (the
 // breakdown test of the one-CTA kernels) sets SSI_ERR_NUMERIC (no shifted retry at this size).
+// probe != nullptr: a breakdown sets *probe (the first attempt of pass 1, which the shifted retry
+// may replace); otherwise it sets SSI_ERR_NUMERIC in the status word.
 __global__ void __launch_bounds__(256) chol_panel_kernel(const double* __restrict__ W, const double* __restrict__ W0diag,
                                                          int k, int j0, int jb, double* __restrict__ L,
-                                                         double* __restrict__ D, int32_t* status) {
+                                                         double* __restrict__ D, int32_t* status, const int* run_if,
+                                                         int* probe) {
+  if (!run_enabled(run_if)) return;
   extern __shared__ double psm[];
   double (*a)[PB + 1] = reinterpret_cast<double (*)[PB + 1]>(psm);
   double (*x)[PB + 1] = reinterpret_cast<double (*)[PB + 1]>(psm + PB * (PB + 1));
@@ -137,18 +144,53 @@ __global__ void __launch_bounds__(256) chol_panel_kernel(const double* __restric
     L[(j0 + r) + int64_t(j0 + c) * k] = r >= c ? a[r][c] : 0.0;
     D[r + c * PB] = x[r][c];
   }
-  if (tid == 0 && bad) set_status(status, SSI_ERR_NUMERIC);
+  if (tid == 0 && bad) {
+    if (probe) *probe = 1;
+    else set_status(status, SSI_ERR_NUMERIC);
+  }
 }
 
-__global__ void diag_copy_kernel(const double* __restrict__ W, int k, double* __restrict__ d) {
+__global__ void diag_copy_kernel(const double* __restrict__ W, int k, double* __restrict__ d, const int* run_if) {
+  if (!run_enabled(run_if)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < k) d[i] = W[i + int64_t(i) * k];
 }
 
 __global__ void copy_cols_kernel(const double* __restrict__ src, int64_t lds, int64_t m, int64_t k,
-                                 double* __restrict__ dst) {
+                                 double* __restrict__ dst, const int* run_if) {
+  if (!run_enabled(run_if)) return;
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < m * k; e += int64_t(gridDim.x) * blockDim.x)
     dst[e] = src[(e % m) + (e / m) * lds];
+}
+
+__global__ void zero_kernel(double* __restrict__ p, int64_t n, const int* run_if) {
+  if (!run_enabled(run_if)) return;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x)
+    p[e] = 0.0;
+}
+
+// Shifted CholeskyQR (the one-CTA kernels' shift): W <- W0 + s I with
+// s = 11 (m k + k (k + 1)) u tr(W0); one CTA.
+__global__ void shift_kernel(const double* __restrict__ W0, int k, int64_t m, double* __restrict__ W,
+                             const int* run_if) {
+  if (!run_enabled(run_if)) return;
+  __shared__ double red[32];
+  double t = 0.0;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) t += W0[i + int64_t(i) * k];
+  t = warp_sum(t);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double sh = 11.0 * (double(m) * k + double(k) * (k + 1)) * 1.1102230246251565e-16 * red[0];
+  for (int64_t e = threadIdx.x; e < int64_t(k) * k; e += blockDim.x) {
+    const int64_t r = e % k, c = e / k;
+    W[e] = W0[e] + (r == c ? sh : 0.0);
+  }
 }
 
 // ---------------------------------------------------------------- block one-sided Jacobi
@@ -431,60 +473,107 @@ constexpr size_t kPanelSmem = size_t(2) * PB * (PB + 1) * sizeof(double);
 size_t cholqr_big_panel_elems(int k) { return size_t((k + PB - 1) / PB) * PB * PB + size_t(k); }
 
 // Blocked right-looking Cholesky of W (k x k col-major, lower part; overwritten by the trailing
-// updates) into L (lower, zero upper) with the panel inverses in D.
-ssi_status chol_big(double* W, int k, double* L, double* D, int32_t* status, cudaStream_t s) {
+// updates) into L (lower, zero upper) with the panel inverses in D. run_if: conditional launch;
+// probe: breakdown flag instead of the status word (see chol_panel_kernel).
+ssi_status chol_big(double* W, int k, double* L, double* D, int32_t* status, cudaStream_t s,
+                    const int* run_if = nullptr, int* probe = nullptr) {
   double* d0 = D + size_t((k + PB - 1) / PB) * PB * PB;    // original diagonal (breakdown test)
   cudaFuncSetAttribute(chol_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmem));
-  diag_copy_kernel<<<(k + 255) / 256, 256, 0, s>>>(W, k, d0);
+  diag_copy_kernel<<<(k + 255) / 256, 256, 0, s>>>(W, k, d0, run_if);
   SSI_TRY(launch_check("diag_copy_kernel"));
-  if (cudaMemsetAsync(L, 0, sizeof(double) * size_t(k) * k, s) != cudaSuccess) return launch_check("memset L");
+  zero_kernel<<<148 * 4, 256, 0, s>>>(L, int64_t(k) * k, run_if);
+  SSI_TRY(launch_check("zero_kernel"));
   for (int j0 = 0; j0 < k; j0 += PB) {
     const int jb = k - j0 < PB ? k - j0 : PB;
     double* Dj = D + size_t(j0 / PB) * PB * PB;
-    chol_panel_kernel<<<1, 256, kPanelSmem, s>>>(W, d0, k, j0, jb, L, Dj, status);
+    chol_panel_kernel<<<1, 256, kPanelSmem, s>>>(W, d0, k, j0, jb, L, Dj, status, run_if, probe);
     SSI_TRY(launch_check("chol_panel_kernel"));
     const int rest = k - j0 - jb;
     if (rest <= 0) break;
     // L21 = W21 L11^{-T}
     SSI_TRY(gemm_nt(rest, jb, jb, W + (j0 + jb) + int64_t(j0) * k, k, Dj, PB, L + (j0 + jb) + int64_t(j0) * k, k,
-                    0.0, 1.0, false, s));
+                    0.0, 1.0, false, s, run_if));
     // W22 -= L21 L21^T (lower tiles)
     SSI_TRY(gemm_nt(rest, rest, jb, L + (j0 + jb) + int64_t(j0) * k, k, L + (j0 + jb) + int64_t(j0) * k, k,
-                    W + (j0 + jb) + int64_t(j0 + jb) * k, k, 1.0, -1.0, true, s));
+                    W + (j0 + jb) + int64_t(j0 + jb) * k, k, 1.0, -1.0, true, s, run_if));
   }
   return SSI_OK;
 }
 
 // In place X <- X L^{-T} (X m x k col-major, ld m): block column j: X_j <- X_j D_j^T, then
 // X_{j+} -= X_j L_{j+, j}^T.
-ssi_status trsm_big(double* X, int64_t m, int k, const double* L, const double* D, cudaStream_t s) {
+ssi_status trsm_big(double* X, int64_t m, int k, const double* L, const double* D, cudaStream_t s,
+                    const int* run_if = nullptr) {
   for (int j0 = 0; j0 < k; j0 += PB) {
     const int jb = k - j0 < PB ? k - j0 : PB;
     const double* Dj = D + size_t(j0 / PB) * PB * PB;
     double* Xj = X + int64_t(j0) * m;
-    SSI_TRY(gemm_nt(m, jb, jb, Xj, m, Dj, PB, Xj, m, 0.0, 1.0, false, s));
+    SSI_TRY(gemm_nt(m, jb, jb, Xj, m, Dj, PB, Xj, m, 0.0, 1.0, false, s, run_if));
     const int rest = k - j0 - jb;
     if (rest <= 0) break;
     SSI_TRY(gemm_nt(m, rest, jb, Xj, m, L + (j0 + jb) + int64_t(j0) * k, k, X + int64_t(j0 + jb) * m, m, 1.0, -1.0,
-                    false, s));
+                    false, s, run_if));
   }
   return SSI_OK;
 }
 
-// CholeskyQR2 for k > kSvdMaxK: Y = Q R with R^T = L1 L2 (factors in w.L1, w.L2).
+// Cholesky with the shifted retry of the one-CTA path, as conditional launches: the first
+// attempt (under run_if) only raises *flag on a breakdown; then W <- W0 + s I and a second
+// attempt run only if *flag is set (a breakdown of that one sets SSI_ERR_NUMERIC).
+static ssi_status chol_retry(double* W, double* W0, int k, int64_t m, double* L, double* D, int32_t* status,
+                             cudaStream_t s, const int* run_if, int* flag) {
+  copy_cols_kernel<<<148 * 4, 256, 0, s>>>(W, k, k, k, W0, run_if);
+  SSI_TRY(launch_check("copy_cols_kernel"));
+  SSI_TRY(chol_big(W, k, L, D, status, s, run_if, flag));
+  shift_kernel<<<1, 1024, 0, s>>>(W0, k, m, W, flag);
+  SSI_TRY(launch_check("shift_kernel"));
+  return chol_big(W, k, L, D, status, s, flag, nullptr);
+}
+
+// CholeskyQR2 for k > kSvdMaxK, with the shifted-CholeskyQR fallback decided on the device. Pass 1
+// retries its Cholesky on W0 + s I after a breakdown; then up to kCqExtraPasses extra passes run,
+// each only if the previous pass shifted, each shifting again on a breakdown; the final pass must
+// factor unshifted (else SSI_ERR_NUMERIC). Y = Q R with R^T = L1 (Lb_1 ... Lb_n) L2, the product
+// of the extra passes' factors accumulated in La and folded into L2.
+// Why more than one extra pass (unlike the one-CTA path's single pass, whose explicit inverses add
+// error of order u kappa(L)^2): on an exactly rank-deficient Y the columns beyond the rank are
+// rounding noise, which each shifted pass scales up by about 1 / sqrt(s) ~ 1e4 relative to the
+// signal; the accurate blocked solves keep that noise small, so it takes two or three shifted
+// passes before those columns are O(1) and the final pass completes an orthonormal basis.
 ssi_status cholqr2_big(const double* Y, int64_t ldy, int64_t m, int k, double* Q, CholQRWork& w, int32_t* status,
                        cudaStream_t s) {
   const int splits = gemm_pick_splits(k, k, m);
+  int* f = w.flag;   // f[0]: pass 1 shifted; f[j]: extra pass j shifted (gates extra pass j + 1)
+  if (cudaMemsetAsync(w.flag, 0, (1 + kCqExtraPasses) * sizeof(int), s) != cudaSuccess)
+    return launch_check("cholqr2_big flag");
   SSI_TRY(gemm_f64(k, k, m, 1.0, Operand{Y, ldy, 1}, Operand{Y, 1, ldy}, w.W, k, splits, w.partial, s));
-  SSI_TRY(chol_big(w.W, k, w.L1, w.Dp1, status, s));
-  copy_cols_kernel<<<148 * 8, 256, 0, s>>>(Y, ldy, m, k, w.Q1);
+  SSI_TRY(chol_retry(w.W, w.W0, k, m, w.L1, w.Dp1, status, s, nullptr, f));
+  copy_cols_kernel<<<148 * 8, 256, 0, s>>>(Y, ldy, m, k, w.Q1, nullptr);
   SSI_TRY(launch_check("copy_cols_kernel"));
   SSI_TRY(trsm_big(w.Q1, m, k, w.L1, w.Dp1, s));
+  for (int j = 1; j <= kCqExtraPasses; ++j) {   // extra pass j: Q1 <- Q1 Lb^{-T}, La <- La Lb
+    const int* run = f + j - 1;
+    SSI_TRY(gemm_f64(k, k, m, 1.0, Operand{w.Q1, m, 1}, Operand{w.Q1, 1, m}, w.W, k, splits, w.partial, s, run));
+    SSI_TRY(chol_retry(w.W, w.W0, k, m, w.Lb, w.Dp2, status, s, run, f + j));
+    SSI_TRY(trsm_big(w.Q1, m, k, w.Lb, w.Dp2, s, run));
+    if (j == 1) {
+      copy_cols_kernel<<<148 * 8, 256, 0, s>>>(w.Lb, k, k, k, w.La, run);
+    } else {
+      SSI_TRY(gemm_f64(k, k, k, 1.0, Operand{w.La, 1, k}, Operand{w.Lb, 1, k}, w.W, k, 1, nullptr, s, run));
+      copy_cols_kernel<<<148 * 8, 256, 0, s>>>(w.W, k, k, k, w.La, run);
+    }
+    SSI_TRY(launch_check("copy_cols_kernel"));
+  }
+  // final pass
   SSI_TRY(gemm_f64(k, k, m, 1.0, Operand{w.Q1, m, 1}, Operand{w.Q1, 1, m}, w.W, k, splits, w.partial, s));
   SSI_TRY(chol_big(w.W, k, w.L2, w.Dp2, status, s));
   if (cudaMemcpyAsync(Q, w.Q1, sizeof(double) * size_t(m) * k, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
     return launch_check("cholqr2_big copy");
-  return trsm_big(Q, m, k, w.L2, w.Dp2, s);
+  SSI_TRY(trsm_big(Q, m, k, w.L2, w.Dp2, s));
+  // fold: L2 <- La L2 (both lower triangular; only after a shift)
+  SSI_TRY(gemm_f64(k, k, k, 1.0, Operand{w.La, 1, k}, Operand{w.L2, 1, k}, w.W, k, 1, nullptr, s, f));
+  copy_cols_kernel<<<148 * 8, 256, 0, s>>>(w.W, k, k, k, w.L2, f);
+  return launch_check("copy_cols_kernel");
 }
 
 size_t jacobi_big_scratch_elems(int k) {

@@ -130,3 +130,38 @@ def test_bridge_record_2d_full_size(api):
         st = compare_tables(gpu_cells(tab), [c])
         assert st["count_mismatch"] == [], n
         assert st["max_df_all"] <= 1e-6 and st["max_dxi_all"] <= 1e-5, (n, st)
+
+
+def test_big_k_rank_deficient_sketch_takes_the_shifted_fallback(api):
+    """k = 600 > 512 columns on an operator of rank 100: the first Cholesky breaks down, the
+    blocked path's shifted CholeskyQR3 fallback runs (conditional launches), the call returns
+    SSI_OK and the 100 nonzero singular values equal the full SVD's."""
+    rng = np.random.default_rng(606)
+    m, r = 1200, 100
+    A = np.linalg.qr(rng.standard_normal((m, r)))[0] * np.logspace(0, -2, r)
+    T = A @ np.linalg.qr(rng.standard_normal((m, r)))[0].T
+    So = np.linalg.svd(T, compute_uv=False)
+    U, S = api.rsvd(_dev(T), 600, 0, 9, 1, 50, check=True)          # raises on a device failure
+    S = S.cpu().numpy()
+    np.testing.assert_allclose(S[:r], So[:r], rtol=1e-11)
+    assert np.abs(S[r:]).max() <= 1e-10 * So[0]
+
+
+def test_full_svd_as_k_equal_T_on_the_e3_frame(api):
+    """The classical CoV-SSI decomposition (Eq. 8) is the same path with the
+    sketch spanning all of T (k = T = 1890, q = 0): every singular value against the oracle's
+    dgesdd, and the leading 30 singular vectors (E3 setting, Table 1 frame)."""
+    from synth.records import _simulate
+    from tests.analytic import shear_frame_modes
+    modes = shear_frame_modes(200.0)
+    Y = _simulate(modes, 60000, 0.1, np.random.default_rng([27, 0xE3]))
+    R = oracle.covariances(Y, 2 * 189 - 1)
+    T = oracle.toeplitz(R, 189)
+    Uo, So = oracle.full_svd(T)
+    U, S = api.rsvd_toeplitz(_dev(R), 189, 1890, 0, 1, 189, 30, check=True)
+    S = S.cpu().numpy()
+    assert np.abs(S - So).max() <= 1e-12 * So[0]
+    np.testing.assert_allclose(S[:30], So[:30], rtol=1e-10)
+    d = np.abs(np.sum(U.cpu().numpy() * Uo[:, :30], axis=0))
+    gap = np.minimum(np.abs(np.diff(So[:31]))[:30], np.r_[np.inf, np.abs(np.diff(So[:30]))]) / So[0]
+    assert np.all(d[gap > 1e-6] > 1 - 1e-8)
