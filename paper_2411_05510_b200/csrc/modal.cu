@@ -494,6 +494,95 @@ struct Band {
   }
 };
 
+// Eigenvector of the quasi-triangular Schur form T for mu = wr + i wi (wi > 0) of the 2 x 2 block
+// at rows (j, j + 1), by column-oriented (axpy) back substitution on one warp: x_j = 1,
+// x_{j+1} = (wr - T_jj + i wi) / T_{j,j+1}, x_p = 0 beyond; the residual r_p = -sum_{q > i} T_pq x_q
+// of every row p above the current one lives in registers (row p on lane p % 32, slot p / 32) and
+// is updated as soon as x_i is known, so a row costs one shuffle, one complex division and one
+// FMA on the dependent path (the row-oriented form needs a warp reduction per row). 1 x 1 and 2 x 2
+// diagonal blocks as in LAPACK dtrevc (perturbed to smin when singular). x into xr / xim [0, j+1].
+template <int KM>
+__device__ __forceinline__ void eigvec_axpy(const Band& H, int j, double wr, double wi, double smin, double* xr,
+                                            double* xim, int lane) {
+  double rr[KM], ri[KM];
+  const double b = H(j, j + 1);
+  const double x1r = (wr - H(j, j)) / b, x1i = wi / b;
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    const int p = lane + 32 * k;
+    rr[k] = 0.0; ri[k] = 0.0;
+    if (p < j) {
+      const double h0 = H(p, j), h1 = H(p, j + 1);
+      rr[k] = -fma(h1, x1r, h0);
+      ri[k] = -(h1 * x1i);
+    }
+  }
+  if (lane == 0) { xr[j] = 1.0; xim[j] = 0.0; xr[j + 1] = x1r; xim[j + 1] = x1i; }
+  // r_p of the (uniform) row p from its owner lane
+  auto pick = [&](int p, double& vr, double& vi) {
+    const int k = p >> 5;
+    double sr = 0.0, si = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KM; ++kk)
+      if (kk == k) { sr = rr[kk]; si = ri[kk]; }
+    vr = __shfl_sync(0xffffffffu, sr, p & 31);
+    vi = __shfl_sync(0xffffffffu, si, p & 31);
+  };
+  int i = j - 1;
+  while (i >= 0) {
+    const bool two = (i >= 1) && (H(i, i - 1) != 0.0);
+    if (!two) {
+      double r2r, r2i;
+      pick(i, r2r, r2i);
+      double dr = H(i, i) - wr, di = -wi;
+      if (fma(dr, dr, di * di) < smin * smin) { dr = smin; di = 0.0; }
+      const double iden = fast_rcp(fma(dr, dr, di * di));
+      const double xir = (r2r * dr + r2i * di) * iden, xii = (r2i * dr - r2r * di) * iden;
+      if (lane == (i & 31)) { xr[i] = xir; xim[i] = xii; }
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        const int p = lane + 32 * k;
+        if (p < i) {
+          const double h = H(p, i);
+          rr[k] = fma(-h, xir, rr[k]);
+          ri[k] = fma(-h, xii, ri[k]);
+        }
+      }
+      i -= 1;
+    } else {
+      // [[m00, m01], [m10, m11]] [x_{i-1}; x_i] = [r_{i-1}; r_i]
+      double r1r, r1i, r2r, r2i;
+      pick(i - 1, r1r, r1i);
+      pick(i, r2r, r2i);
+      const double m00r = H(i - 1, i - 1) - wr, m00i = -wi, m01 = H(i - 1, i);
+      const double m10 = H(i, i - 1), m11r = H(i, i) - wr, m11i = -wi;
+      double detr = (m00r * m11r - m00i * m11i) - m01 * m10;
+      double deti = (m00r * m11i + m00i * m11r);
+      if (fma(detr, detr, deti * deti) < smin * smin) { detr = smin; deti = 0.0; }
+      const double iden = fast_rcp(fma(detr, detr, deti * deti));
+      const double n1r = (r1r * m11r - r1i * m11i) - m01 * r2r;
+      const double n1i = (r1r * m11i + r1i * m11r) - m01 * r2i;
+      const double n2r = (m00r * r2r - m00i * r2i) - m10 * r1r;
+      const double n2i = (m00r * r2i + m00i * r2r) - m10 * r1i;
+      const double ar = (n1r * detr + n1i * deti) * iden, ai = (n1i * detr - n1r * deti) * iden;
+      const double br = (n2r * detr + n2i * deti) * iden, bi = (n2i * detr - n2r * deti) * iden;
+      if (lane == ((i - 1) & 31)) { xr[i - 1] = ar; xim[i - 1] = ai; }
+      if (lane == (i & 31)) { xr[i] = br; xim[i] = bi; }
+#pragma unroll
+      for (int k = 0; k < KM; ++k) {
+        const int p = lane + 32 * k;
+        if (p < i - 1) {
+          const double h0 = H(p, i - 1), h1 = H(p, i);
+          rr[k] = fma(-h1, br, fma(-h0, ar, rr[k]));
+          ri[k] = fma(-h1, bi, fma(-h0, ai, ri[k]));
+        }
+      }
+      i -= 2;
+    }
+  }
+  __syncwarp();
+}
+
 #ifndef SSI_EIG_MINB
 #define SSI_EIG_MINB 1
 #endif
@@ -1027,35 +1116,59 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
     return;
   }
 
-  // ---------------- poles: complex pairs of the standardized Schur form
+  // ---------------- poles: complex pairs of the standardized Schur form. Thread 0 finds the 2 x 2
+  // block starts (top-down scan, as dlahqr leaves them); the eigenvalue -> (f, xi) conversions
+  // (log / atan2 / hypot) run one block per thread; the first `cap` valid poles in block order are
+  // kept and ranked by (f, xi), ties by block order (a stable sort), in parallel.
+  double* cand = s.x;                        // scratch (free after the QR): 6 arrays of n / 2
+  const int half = n / 2 + 1;
+  double *cb = cand, *cfv = cand + half, *cxv = cand + 2 * half, *crv = cand + 3 * half, *civ = cand + 4 * half,
+         *cok = cand + 5 * half;
   if (tid == 0) {
-    int nc = 0;
-    for (int i = 0; i < n;) {
-      if (i + 1 < n && H(i + 1, i) != 0.0) {
-        const double wr = H(i, i);
-        const double wi = sqrt(fabs(H(i, i + 1))) * sqrt(fabs(H(i + 1, i)));
-        // lambda = ln(mu)/dt (principal branch); f = |lambda|/2pi; xi = -Re/|lambda|
-        const double lr = log(hypot(wr, wi)) / g.dt, li = atan2(wi, wr) / g.dt;
-        const double al = hypot(lr, li);
-        const double f = al / (2.0 * 3.141592653589793), xi = -lr / al;
-        if (wi > 0.0 && xi > 0.0 && xi < 1.0 && nc < cap) {
-          int pos = nc;
-          while (pos > 0 && (s.cf[pos - 1] > f || (s.cf[pos - 1] == f && s.cxi[pos - 1] > xi))) {
-            s.cf[pos] = s.cf[pos - 1]; s.cxi[pos] = s.cxi[pos - 1];
-            s.cre[pos] = s.cre[pos - 1]; s.cim[pos] = s.cim[pos - 1]; s.cj[pos] = s.cj[pos - 1];
-            --pos;
-          }
-          s.cf[pos] = f; s.cxi[pos] = xi; s.cre[pos] = wr; s.cim[pos] = wi; s.cj[pos] = i;
-          ++nc;
-        }
-        i += 2;
-      } else {
-        i += 1;
-      }
+    int nb = 0;
+    for (int i = 0; i + 1 < n;) {
+      if (H(i + 1, i) != 0.0) { cb[nb++] = double(i); i += 2; }
+      else i += 1;
     }
-    sh_ncand = nc;
-    T.count[o] = nc;
+    sh_ncand = nb;
   }
+  __syncthreads();
+  const int nb = sh_ncand;
+  for (int t = tid; t < nb; t += NT) {
+    const int i = int(cb[t]);
+    const double wr = H(i, i);
+    const double wi = sqrt(fabs(H(i, i + 1))) * sqrt(fabs(H(i + 1, i)));
+    // lambda = ln(mu)/dt (principal branch); f = |lambda|/2pi; xi = -Re/|lambda|
+    const double lr = log(hypot(wr, wi)) / g.dt, li = atan2(wi, wr) / g.dt;
+    const double al = hypot(lr, li);
+    const double f = al / (2.0 * 3.141592653589793), xi = -lr / al;
+    cfv[t] = f; cxv[t] = xi; crv[t] = wr; civ[t] = wi;
+    cok[t] = (wi > 0.0 && xi > 0.0 && xi < 1.0) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  int kept_here = 0;
+  for (int t = tid; t < nb; t += NT) {
+    if (cok[t] == 0.0) continue;
+    int ord = 0;                                   // valid poles before t (block order)
+    for (int u = 0; u < t; ++u) ord += cok[u] != 0.0;
+    if (ord >= cap) continue;
+    const double f = cfv[t], xi = cxv[t];
+    int rank = 0, seen = 0;
+    for (int u = 0; u < nb && seen < cap; ++u) {
+      if (cok[u] == 0.0) continue;
+      ++seen;
+      const double fu = cfv[u], xu = cxv[u];
+      rank += (fu < f || (fu == f && (xu < xi || (xu == xi && u < t))));
+    }
+    s.cf[rank] = f; s.cxi[rank] = xi; s.cre[rank] = crv[t]; s.cim[rank] = civ[t]; s.cj[rank] = int(cb[t]);
+    ++kept_here;
+  }
+  __syncthreads();
+  if (tid == 0) sh_ncand = 0;
+  __syncthreads();
+  if (kept_here) atomicAdd(&sh_ncand, kept_here);
+  __syncthreads();
+  if (tid == 0) T.count[o] = sh_ncand;
   __syncthreads();
   const int nc = sh_ncand;
   if (tid == 0) sh_l = 0;               // reused as the pole counter of the vectors phase
@@ -1076,67 +1189,41 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
     const int j = s.cj[c];
     const double wr = s.cre[c], wi = s.cim[c];
     const double smin = fmax(kUlp * hypot(wr, wi), kSafeMin);
-    if (lane == 0) {
-      xr[j] = 1.0; xim[j] = 0.0;
-      const double b = H(j, j + 1);
-      xr[j + 1] = (wr - H(j, j)) / b; xim[j + 1] = wi / b;
-    }
-    __syncwarp();
-    int i = j - 1;
-    while (i >= 0) {
-      const bool two = (i >= 1) && (H(i, i - 1) != 0.0);
-      double r1r = 0.0, r1i = 0.0, r2r = 0.0, r2i = 0.0;
-      for (int p = i + 1 + lane; p <= j + 1; p += 32) {
-        const double h = H(i, p);
-        r2r -= h * xr[p]; r2i -= h * xim[p];
-        if (two) { const double h1 = H(i - 1, p); r1r -= h1 * xr[p]; r1i -= h1 * xim[p]; }
-      }
-      r2r = warp_sum(r2r); r2i = warp_sum(r2i);
-      if (two) { r1r = warp_sum(r1r); r1i = warp_sum(r1i); }
-      if (lane == 0) {
-        if (!two) {
-          double dr = H(i, i) - wr, di = -wi;
-          if (fma(dr, dr, di * di) < smin * smin) { dr = smin; di = 0.0; }
-          const double iden = fast_rcp(fma(dr, dr, di * di));     // inline reciprocal: no slow-path call
-          xr[i] = (r2r * dr + r2i * di) * iden;
-          xim[i] = (r2i * dr - r2r * di) * iden;
-        } else {
-          // [[m00, m01], [m10, m11]] [x_{i-1}; x_i] = [r1; r2]
-          const double m00r = H(i - 1, i - 1) - wr, m00i = -wi, m01 = H(i - 1, i);
-          const double m10 = H(i, i - 1), m11r = H(i, i) - wr, m11i = -wi;
-          double detr = (m00r * m11r - m00i * m11i) - m01 * m10;
-          double deti = (m00r * m11i + m00i * m11r);
-          if (fma(detr, detr, deti * deti) < smin * smin) { detr = smin; deti = 0.0; }
-          const double iden = fast_rcp(fma(detr, detr, deti * deti));
-          const double n1r = (r1r * m11r - r1i * m11i) - m01 * r2r;
-          const double n1i = (r1r * m11i + r1i * m11r) - m01 * r2i;
-          const double n2r = (m00r * r2r - m00i * r2i) - m10 * r1r;
-          const double n2i = (m00r * r2i + m00i * r2r) - m10 * r1i;
-          xr[i - 1] = (n1r * detr + n1i * deti) * iden; xim[i - 1] = (n1i * detr - n1r * deti) * iden;
-          xr[i] = (n2r * detr + n2i * deti) * iden;     xim[i] = (n2i * detr - n2r * deti) * iden;
-        }
-      }
-      __syncwarp();
-      i -= two ? 2 : 1;
-    }
+    if (g.n_max <= 256) eigvec_axpy<8>(H, j, wr, wi, smin, xr, xim, lane);
+    else eigvec_axpy<16>(H, j, wr, wi, smin, xr, xim, lane);
     // Phi = C x (C: l x n col-major), raw into the output slot
     double* shp = T.shape + (int64_t(o) * cap + c) * int64_t(l) * 2;
     double nrm2 = 0.0, best = -1.0;
     int besti = 0;
-    for (int a = lane; a < l; a += 32) {
-      double pr = 0.0, pi = 0.0, qr = 0.0, qi = 0.0;
-      int p = 0;
-      for (; p + 1 <= j + 1; p += 2) {
-        const double c0 = C[a + int64_t(p) * l], c1 = C[a + int64_t(p + 1) * l];
-        pr += c0 * xr[p]; pi += c0 * xim[p];
-        qr += c1 * xr[p + 1]; qi += c1 * xim[p + 1];
+    for (int a0 = 0; a0 < l; a0 += 32 * 8) {
+      // channels a0 + lane + 32 u, u < 8, accumulated together (independent chains, 8 loads of C
+      // in flight per column); x_p broadcast from shared memory
+      double pr[8], pi[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { pr[u] = 0.0; pi[u] = 0.0; }
+      const double* Ca = C + a0 + lane;
+      for (int p = 0; p <= j + 1; ++p) {
+        const double xpr = xr[p], xpi = xim[p];
+        const double* Cp = Ca + int64_t(p) * l;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (a0 + lane + 32 * u < l) {
+            const double cv = Cp[32 * u];
+            pr[u] = fma(cv, xpr, pr[u]);
+            pi[u] = fma(cv, xpi, pi[u]);
+          }
+        }
       }
-      if (p <= j + 1) { const double c0 = C[a + int64_t(p) * l]; pr += c0 * xr[p]; pi += c0 * xim[p]; }
-      pr += qr; pi += qi;
-      shp[2 * a] = pr; shp[2 * a + 1] = pi;
-      const double m2 = pr * pr + pi * pi;
-      nrm2 += m2;
-      if (m2 > best) { best = m2; besti = a; }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int a = a0 + lane + 32 * u;
+        if (a < l) {
+          shp[2 * a] = pr[u]; shp[2 * a + 1] = pi[u];
+          const double m2 = pr[u] * pr[u] + pi[u] * pi[u];
+          nrm2 += m2;
+          if (m2 > best) { best = m2; besti = a; }
+        }
+      }
     }
     nrm2 = warp_sum(nrm2);
 #pragma unroll
