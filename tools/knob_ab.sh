@@ -1,0 +1,10 @@
+#!/bin/bash
+# A/B of compile-time knobs on the headline: for each SSI_NVCC_EXTRA value (arguments; "" =
+# default) rebuild libssi and run the c3 bench twice (device records/s, no legs / e2e / CPU leg).
+for v in "$@"; do
+  SSI_NVCC_EXTRA="$v" python -m paper_2411_05510_b200.build --force > /dev/null 2>&1 || { echo "build failed: $v"; continue; }
+  for r in 1 2; do
+    python bench.py --steps 40 --warmup 8 --no-cpu-baseline --no-legs --no-e2e 2>/dev/null |
+      python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print('[$v]', round(d['value'], 2), 'rec/s', round(d['ms_per_step'], 3), 'ms', d['clocks']['reasons'])"
+  done
+done
