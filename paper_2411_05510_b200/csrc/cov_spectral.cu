@@ -12,8 +12,8 @@
 // both spectra (X = (Z(f) + conj Z(F-f))/2, Ye = (Z(f) - conj Z(F-f))/2i). The sum over
 // segments is, per frequency, three real products on the FP64 tensor cores (cross_spectral.cu):
 //   T1 = sum Xr Yr, T2 = sum Xi Yi, T3 = sum (Xr + Xi)(Yi - Yr); Re G = T1 + T2, Im G = T3 + T1 - T2
-// (6 lp^2 S flops per frequency; SSI_SPEC_STACKED=1 selects the 8 lp^2 S complex-stacked real
-// GEMM instead, for A/B measurement).
+// (6 lp^2 S flops per frequency; the spectra are stored [f][s][channel][Re, Im], so the FFT writes
+// 16-byte (Re, Im) pairs and the product reads them as 16-byte fragments).
 // The inverse DFT at the K needed lags (hermitian half spectrum, weights 1 / 2 / 1, 1/(N-k)
 // folded in) is a second GEMM R (l^2 x n_lags) = G (l^2 x (F+2)) W ((F+2) x n_lags).
 // Work: 3 l^2 N F/B (cross-spectra) + 2 l^2 n_lags (F+2) (inverse) flops against
@@ -188,12 +188,9 @@ __global__ void __launch_bounds__(kFftThreads, 3) spec_fft_kernel(FftArgs g) {
     if (ch >= g.lp) continue;   // ch = l < lp (odd l): the zero padding channel
     const double2 zf = z[c * FP + dif_pos(f, F, R2)];
     const double2 zm = z[c * FP + dif_pos((F - f) & (F - 1), F, R2)];
-    double* Af = g.A + f * sS + (2 * s) * g.lp + ch;
-    double* Bf = g.Bs + f * sS + (2 * s) * g.lp + ch;
-    __stcs(Af, 0.5 * (zf.x + zm.x));            // Re X
-    __stcs(Af + g.lp, 0.5 * (zf.y - zm.y));     // Im X
-    __stcs(Bf, 0.5 * (zf.y + zm.y));            // Re Ye
-    __stcs(Bf + g.lp, -0.5 * (zf.x - zm.x));    // Im Ye
+    const int64_t off = f * sS + (s * g.lp + ch) * 2;
+    __stcs(reinterpret_cast<double2*>(g.A + off), make_double2(0.5 * (zf.x + zm.x), 0.5 * (zf.y - zm.y)));    // X
+    __stcs(reinterpret_cast<double2*>(g.Bs + off), make_double2(0.5 * (zf.y + zm.y), -0.5 * (zf.x - zm.x)));  // Ye
   }
 }
 
@@ -355,15 +352,11 @@ __global__ void __launch_bounds__(kFftThreads, SEGS == 1 ? 3 : SSI_FFT_MINB) spe
     const int cq = tid & 3;
     const double2* zq = z + cq * kFP;
     const int64_t sS = 2 * g.S * g.lp;
-    double* Ab = g.A + (2 * s) * g.lp + c0 + cq;
-    double* Bb = g.Bs + (2 * s) * g.lp + c0 + cq;
+    double* Ab = g.A + (s * g.lp + c0 + cq) * 2;
+    double* Bb = g.Bs + (s * g.lp + c0 + cq) * 2;
     auto put = [&](int f, double2 zf, double2 zm) {
-      double* Af = Ab + f * sS;
-      double* Bf = Bb + f * sS;
-      __stcs(Af, 0.5 * (zf.x + zm.x));            // Re X
-      __stcs(Af + g.lp, 0.5 * (zf.y - zm.y));     // Im X
-      __stcs(Bf, 0.5 * (zf.y + zm.y));            // Re Ye
-      __stcs(Bf + g.lp, -0.5 * (zf.x - zm.x));    // Im Ye
+      __stcs(reinterpret_cast<double2*>(Ab + f * sS), make_double2(0.5 * (zf.x + zm.x), 0.5 * (zf.y - zm.y)));  // X
+      __stcs(reinterpret_cast<double2*>(Bb + f * sS), make_double2(0.5 * (zf.y + zm.y), -0.5 * (zf.x - zm.x)));  // Ye
     };
     auto group = [&](int d0, int d1, double2 (&y)[4]) {
       const int base = d0 * 64 + d1 * 4;
@@ -512,16 +505,8 @@ ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY,
       }
     }
     if (phases & 2) {
-      // C_f (2lp x lp) (+)= A_f (2lp x 2 nseg) * B_f (2 nseg x lp); imaginary half to G + lp^2
-#ifdef SSI_SPEC_STACKED   // complex-stacked single GEMM, kept for A/B measurement (SSI_NVCC_EXTRA)
-      if (true)
-#else
-      if (false)
-#endif
-        SSI_TRY(gemm_tall_batched_brow(2 * p.lp, p.lp, 2 * nseg, b.A, p.lp, 2 * p.Sc * p.lp, b.Bs, p.lp,
-                                       2 * p.Sc * p.lp, b.G, p.lp, 2 * lp2, int(nf), p.lp, lp2, s0 > 0, s));
-      else
-        SSI_TRY(cross_spectral_3m(b.A, b.Bs, 2 * p.Sc * p.lp, nseg, p.lp, int(nf), b.G, s0 > 0, s));
+      // G_f (+)= sum over the chunk's segments (Re G to G, Im G to G + lp^2)
+      SSI_TRY(cross_spectral_3m(b.A, b.Bs, 2 * p.Sc * p.lp, nseg, p.lp, int(nf), b.G, s0 > 0, s));
     }
   }
   if (t_end <= t_begin) {

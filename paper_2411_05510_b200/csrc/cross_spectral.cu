@@ -5,9 +5,10 @@
 //   Re G = T1 + T2,   Im G = T3 + T1 - T2
 // i.e. 6 lp^2 S flops per frequency instead of 8 lp^2 S for the complex-stacked real GEMM.
 // One CTA owns a 64 (b) x 64 (a) tile of one frequency and keeps the three accumulators in
-// registers (FP64 DMMA m8n8k4, 8 warps as 2 x 4, warp tile 32 x 16); the operand tiles (Re and
-// Im rows of 16 segments) are staged by cp.async in a 2-stage ring; the sums Xr + Xi and
-// Yi - Yr are formed on the fragments. The epilogue writes Re G and Im G (optionally adding to
+// registers (FP64 DMMA m8n8k4, 8 warps as 2 x 4, warp tile 32 x 16); the operand tiles (16
+// segments x 64 channels of interleaved (Re, Im) pairs) are staged by cp.async in a 2-stage ring
+// and read as 16-byte (Re, Im) fragments; the sums Xr + Xi and Yi - Yr are formed on the
+// fragments. The epilogue writes Re G and Im G (optionally adding to
 // them: segment chunks accumulate in a fixed order).
 #include "cov_spectral.cuh"
 
@@ -15,15 +16,17 @@ namespace ssi {
 namespace {
 
 constexpr int XT = 64;            // tile (b) x (a)
-constexpr int XS = 16;            // segments per stage (32 spectrum rows: Re, Im interleaved)
-constexpr int XP = XT + 2;        // smem row pitch (doubles): fragment reads conflict-free
+constexpr int XS = 16;            // segments per stage
+constexpr int XP = 2 * XT + 4;    // smem pitch of a segment's (Re, Im) x 64 channels: P = 4 (mod 16)
+                                  // puts the 8 lanes of a quarter-warp 16-byte fragment load on
+                                  // distinct bank groups
 constexpr int XNT = 256;
 constexpr int XST = 2;            // stages
-constexpr int XSTAGE = 2 * (2 * XS) * XP;   // A rows + B rows per stage
+constexpr int XSTAGE = 2 * XS * XP;   // A segments + B segments per stage
 
 struct XArgs {
-  const double* A;   // X spectra  [f][2S][lp] (row 2s = Re, 2s+1 = Im; channel b contiguous)
-  const double* B;   // Ye spectra [f][2S][lp] (channel a contiguous)
+  const double* A;   // X spectra  [f][s][lp][Re, Im]
+  const double* B;   // Ye spectra [f][s][lp][Re, Im]
   int64_t sF;        // per-frequency stride of A and B (2 S_capacity lp)
   int64_t nseg;      // segments in this chunk
   int lp;
@@ -36,21 +39,22 @@ __device__ __forceinline__ void cpa16(double* dst, const double* src, bool valid
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
 }
 
-// stage: rows kk in [2 s0, 2 s0 + 32) of A (channels b0..b0+63) and B (channels a0..a0+63)
+// stage: segments [s0, s0 + 16) of A (channels b0..b0+63) and B (channels a0..a0+63), one 16-byte
+// (Re, Im) piece per channel: 1 KB contiguous per segment and operand
 __device__ __forceinline__ void x_load(const XArgs& g, double* st, const double* Af, const double* Bf, int64_t s0,
                                        int b0, int a0) {
   const int tid = threadIdx.x;
   double* As = st;
-  double* Bs = st + (2 * XS) * XP;
+  double* Bs = st + XS * XP;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {           // 32 rows x 32 pieces of 16 B per operand
+  for (int q = 0; q < 4; ++q) {           // 16 segments x 64 pieces per operand
     const int p = tid + q * XNT;
-    const int kk = p >> 5, c = (p & 31) * 2;
-    const int64_t row = 2 * s0 + kk;
-    const bool rv = row < 2 * g.nseg;
+    const int sg = p >> 6, c = p & 63;
+    const int64_t seg = s0 + sg;
+    const bool rv = seg < g.nseg;
     const bool va = rv && b0 + c < g.lp, vb = rv && a0 + c < g.lp;
-    cpa16(As + kk * XP + c, va ? Af + row * g.lp + b0 + c : Af, va);
-    cpa16(Bs + kk * XP + c, vb ? Bf + row * g.lp + a0 + c : Bf, vb);
+    cpa16(As + sg * XP + 2 * c, va ? Af + (seg * g.lp + b0 + c) * 2 : Af, va);
+    cpa16(Bs + sg * XP + 2 * c, vb ? Bf + (seg * g.lp + a0 + c) * 2 : Bf, vb);
   }
 }
 
@@ -79,21 +83,21 @@ __global__ void __launch_bounds__(XNT, 2) cross3m_kernel(XArgs g) {
     if (it + 1 < nst) x_load(g, xs + ((it + 1) % XST) * XSTAGE, Af, Bf, int64_t(it + 1) * XS, b0, a0);
     asm volatile("cp.async.commit_group;" ::: "memory");
     const double* As = xs + (it % XST) * XSTAGE;
-    const double* Bs = As + (2 * XS) * XP;
+    const double* Bs = As + XS * XP;
 #pragma unroll
     for (int k4 = 0; k4 < XS; k4 += 4) {
       const int s = k4 + kq;                                  // this lane's segment (k index)
       double ar[4], ai[4], as[4], br[2], bi[2], bd[2];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        ar[i] = As[(2 * s) * XP + wm + 8 * i + r8];
-        ai[i] = As[(2 * s + 1) * XP + wm + 8 * i + r8];
+        const double2 v = *reinterpret_cast<const double2*>(As + s * XP + 2 * (wm + 8 * i + r8));
+        ar[i] = v.x; ai[i] = v.y;
         as[i] = ar[i] + ai[i];
       }
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        br[j] = Bs[(2 * s) * XP + wn + 8 * j + r8];
-        bi[j] = Bs[(2 * s + 1) * XP + wn + 8 * j + r8];
+        const double2 v = *reinterpret_cast<const double2*>(Bs + s * XP + 2 * (wn + 8 * j + r8));
+        br[j] = v.x; bi[j] = v.y;
         bd[j] = bi[j] - br[j];
       }
 #pragma unroll

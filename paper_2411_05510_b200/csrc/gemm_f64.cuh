@@ -64,9 +64,6 @@ ssi_status gemm_tall_triu(int64_t M, int64_t N, int64_t K, const double* A, int6
 ssi_status gemm_tall_batched(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
                              int64_t sA, const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc,
                              int64_t sC, int batch, cudaStream_t s);
-ssi_status gemm_tall_batched_brow(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int64_t sA,
-                                  const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
-                                  int batch, int64_t rsplit, int64_t roff, bool accumulate, cudaStream_t s);
 // max of gemm_tall_partial_elems(m, N, m) over m <= M (workspace for every smaller square size)
 size_t gemm_tall_partial_elems_upto(int64_t M, int64_t N);
 }  // namespace ssi

@@ -13,9 +13,6 @@ namespace {
 // N-tile widths: 224 (the RSVD panels, k <= 224), 128 and 64 (the narrow DFT products; a
 // smaller tile also fits 2-3 CTAs per SM).
 constexpr int BM = 64, BN = 224, BK = 16, NT = 256, STAGES = 3;
-#ifndef TALL_CST_ST
-#define TALL_CST_ST 2
-#endif
 #ifndef TALL64_ST
 #define TALL64_ST 3
 #endif
@@ -34,18 +31,15 @@ constexpr int BM = 64, BN = 224, BK = 16, NT = 256, STAGES = 3;
 #ifndef TALL224_MINB
 #define TALL224_MINB 2
 #endif
-#ifndef TALL_CST_MINB
-#define TALL_CST_MINB 2
-#endif
 constexpr int LDK = BK + 4;            // k-contiguous rows (A row-major, B): 20 doubles
 constexpr int LDM = BM + 4;            // m-contiguous rows (A col-major): 68 doubles
 // per-stage tile sizes: A is BM x BK (k-contiguous rows) or BK x BM (m-contiguous rows); B is
-// TBN x BK (k-contiguous) or BK x TBN (BROW: n-contiguous, row pitch TBN + 4)
+// TBN x BK (k-contiguous)
 template <bool AROW> constexpr int a_elems() { return AROW ? BM * LDK : BK * LDM; }
-template <bool BROW, int TBN> constexpr int b_elems() { return BROW ? BK * (TBN + 4) : TBN * LDK; }
-template <bool AROW, bool BROW, int TBN> constexpr int stage_elems() { return a_elems<AROW>() + b_elems<BROW, TBN>(); }
-template <bool AROW, bool BROW, int TBN, int ST> constexpr size_t tall_smem() {
-  return size_t(ST) * stage_elems<AROW, BROW, TBN>() * sizeof(double);
+template <int TBN> constexpr int b_elems() { return TBN * LDK; }
+template <bool AROW, int TBN> constexpr int stage_elems() { return a_elems<AROW>() + b_elems<TBN>(); }
+template <bool AROW, int TBN, int ST> constexpr size_t tall_smem() {
+  return size_t(ST) * stage_elems<AROW, TBN>() * sizeof(double);
 }
 
 __device__ __forceinline__ void cp16n(double* dst, const double* src, int nbytes) {
@@ -70,12 +64,10 @@ struct TallArgs {
   int mode;             // 0 plain / batched; 1 lower-triangular tiles of a square C (blockIdx.x
                         // = triangular tile index, TBN = BM); 2 upper-triangular B (N tile
                         // blockIdx.z only needs K rows [0, n0 + TBN))
-  int64_t rsplit, roff; // rsplit > 0: output rows r >= rsplit go to (r - rsplit) + c*ldo + roff
-  int accum;            // 1: out += product (chunked K, fixed order); 0: out = product
   const int* run_if;    // conditional launch (run_enabled), nullptr = always
 };
 
-template <bool AROW, bool BROW, int TBN, bool CST = false>
+template <bool AROW, int TBN>
 __device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_t m0, int64_t k0, int64_t ke) {
   const int tid = threadIdx.x;
   double* As = st;
@@ -93,37 +85,25 @@ __device__ __forceinline__ void load_stage(const TallArgs& g, double* st, int64_
       const int kk = p >> 5, i = (p & 31) * 2;
       const int64_t gi = m0 + i, gk = k0 + kk;
       const bool ok = gi < g.M && gk < ke;
-      if (CST) {   // complex-stacked A: row r >= rsplit is row r - rsplit of column k ^ 1 (sign in the fragment)
-        const bool lo = gi >= g.rsplit;
-        cp16(As + kk * LDM + i, ok ? g.A + (lo ? gi - g.rsplit : gi) + (lo ? (gk ^ 1) : gk) * g.lda : g.A, ok);
-      } else {
-        cp16(As + kk * LDM + i, ok ? g.A + gi + gk * g.lda : g.A, ok);
-      }
+      cp16(As + kk * LDM + i, ok ? g.A + gi + gk * g.lda : g.A, ok);
     }
   }
   // B: TBN columns x 16 k-contiguous doubles = 8 TBN pieces, TBN / 32 per thread
 #pragma unroll
   for (int q = 0; q < TBN / 32; ++q) {
     const int p = tid + q * NT;
-    if (BROW) {                      // k-row kk: TBN n-contiguous doubles = TBN / 2 pieces
-      const int kk = p / (TBN / 2), j = (p % (TBN / 2)) * 2;
-      const int64_t gk = k0 + kk;
-      const int nv = (gk < ke) ? (g.N - j >= 2 ? 2 : (g.N - j > 0 ? int(g.N - j) : 0)) : 0;
-      cp16n(Bs + kk * (TBN + 4) + j, nv ? g.B + gk * g.ldb + j : g.B, 8 * nv);
-    } else {
-      const int j = p >> 3, kk = (p & 7) * 2;
-      const int64_t gk = k0 + kk;
-      const bool ok = j < g.N && gk < ke;
-      cp16(Bs + j * LDK + kk, ok ? g.B + gk + int64_t(j) * g.ldb : g.B, ok);
-    }
+    const int j = p >> 3, kk = (p & 7) * 2;
+    const int64_t gk = k0 + kk;
+    const bool ok = j < g.N && gk < ke;
+    cp16(Bs + j * LDK + kk, ok ? g.B + gk + int64_t(j) * g.ldb : g.B, ok);
   }
 }
 
-template <bool AROW, bool BROW, int TBN, bool CST = false, int ST = STAGES, int MINB = 1>
+template <bool AROW, int TBN, int ST = STAGES, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
   constexpr int WN = TBN / 4;          // warp tile N (56 / 32 / 16)
   constexpr int NJ = WN / 8;           // m8n8k4 tiles per warp along N
-  constexpr int STAGE_ELEMS = stage_elems<AROW, BROW, TBN>();
+  constexpr int STAGE_ELEMS = stage_elems<AROW, TBN>();
   extern __shared__ __align__(16) double sm[];
   if (!run_enabled(g.run_if)) return;
   int64_t m0 = int64_t(blockIdx.x) * BM, n0 = 0;
@@ -157,13 +137,6 @@ __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
   const int64_t ke = kb + g.kchunk < g.K ? kb + g.kchunk : g.K;
   const int nst = int((ke - kb + BK - 1) / BK);
 
-  // CST: rows >= rsplit of the stacked operand carry [-Im, Re] of the complex column pair
-  // (2s, 2s+1): the loaded value is negated at even k (k = lane & 3 in the fragment).
-  // The sign flip is an integer XOR of the high word (keeps the FP64 pipe free for DMMA).
-  int negmask[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    negmask[i] = (CST && (m0 + wm + 8 * i + (lane >> 2) >= g.rsplit) && !(lane & 1)) ? int(0x80000000u) : 0;
   double acc[4][NJ][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -172,7 +145,7 @@ __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
 
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) {
-    if (s < nst) load_stage<AROW, BROW, TBN, CST>(g, sm + s * STAGE_ELEMS, m0, kb + s * BK, ke);
+    if (s < nst) load_stage<AROW, TBN>(g, sm + s * STAGE_ELEMS, m0, kb + s * BK, ke);
     cp_commit();
   }
   for (int it = 0; it < nst; ++it) {
@@ -180,7 +153,7 @@ __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
     __syncthreads();
     {
       const int nx = it + ST - 1;
-      if (nx < nst) load_stage<AROW, BROW, TBN, CST>(g, sm + (nx % ST) * STAGE_ELEMS, m0, kb + int64_t(nx) * BK, ke);
+      if (nx < nst) load_stage<AROW, TBN>(g, sm + (nx % ST) * STAGE_ELEMS, m0, kb + int64_t(nx) * BK, ke);
       cp_commit();
     }
     const double* As = sm + (it % ST) * STAGE_ELEMS;
@@ -190,12 +163,9 @@ __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
       double af[4], bf[NJ];
       const int kq = k4 + (lane & 3), r8 = lane >> 2;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        af[i] = AROW ? As[(wm + 8 * i + r8) * LDK + kq] : As[kq * LDM + wm + 8 * i + r8];
-        if (CST) af[i] = __hiloint2double(__double2hiint(af[i]) ^ negmask[i], __double2loint(af[i]));
-      }
+      for (int i = 0; i < 4; ++i) af[i] = AROW ? As[(wm + 8 * i + r8) * LDK + kq] : As[kq * LDM + wm + 8 * i + r8];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) bf[j] = BROW ? Bs[kq * (TBN + 4) + wn + 8 * j + r8] : Bs[(wn + 8 * j + r8) * LDK + kq];
+      for (int j = 0; j < NJ; ++j) bf[j] = Bs[(wn + 8 * j + r8) * LDK + kq];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -211,10 +181,7 @@ __global__ void __launch_bounds__(NT, MINB) gemm_tall_kernel(TallArgs g) {
       for (int e = 0; e < 2; ++e) {
         const int64_t r = m0 + wm + 8 * i + (lane >> 2);
         const int64_t c = wn + 8 * j + 2 * (lane & 3) + e;
-        if (r < g.M && c < g.N) {
-          double* o = (g.rsplit > 0 && r >= g.rsplit) ? out + (r - g.rsplit) + c * g.ldo + g.roff : out + r + c * g.ldo;
-          *o = g.accum ? *o + acc[i][j][e] : acc[i][j][e];
-        }
+        if (r < g.M && c < g.N) out[r + c * g.ldo] = acc[i][j][e];
       }
 }
 
@@ -229,24 +196,24 @@ __global__ void tall_reduce(int64_t M, int64_t N, int splits, const double* __re
   }
 }
 
-template <bool AROW, int TBN, bool BROW = false, bool CST = false, int ST = STAGES, int MINB = 1>
+template <bool AROW, int TBN, int ST = STAGES, int MINB = 1>
 ssi_status launch_one(dim3 grid, const TallArgs& g, cudaStream_t s) {
-  constexpr size_t smem = tall_smem<AROW, BROW, TBN, ST>();
-  cudaFuncSetAttribute(gemm_tall_kernel<AROW, BROW, TBN, CST, ST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  gemm_tall_kernel<AROW, BROW, TBN, CST, ST, MINB><<<grid, NT, smem, s>>>(g);
+  constexpr size_t smem = tall_smem<AROW, TBN, ST>();
+  cudaFuncSetAttribute(gemm_tall_kernel<AROW, TBN, ST, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  gemm_tall_kernel<AROW, TBN, ST, MINB><<<grid, NT, smem, s>>>(g);
   return launch_check("gemm_tall_kernel");
 }
 
 // narrowest N tile that covers N
 ssi_status launch_tall(bool arow, int64_t N, dim3 grid, const TallArgs& g, cudaStream_t s) {
   if (N <= 64)
-    return arow ? launch_one<true, 64, false, false, TALL64_ST, TALL64_MINB>(grid, g, s)
-                : launch_one<false, 64, false, false, TALL64_ST, TALL64_MINB>(grid, g, s);
+    return arow ? launch_one<true, 64, TALL64_ST, TALL64_MINB>(grid, g, s)
+                : launch_one<false, 64, TALL64_ST, TALL64_MINB>(grid, g, s);
   if (N <= 128)
-    return arow ? launch_one<true, 128, false, false, TALL128_ST, TALL128_MINB>(grid, g, s)
-                : launch_one<false, 128, false, false, TALL128_ST, TALL128_MINB>(grid, g, s);
-  return arow ? launch_one<true, 224, false, false, TALL224_ST, TALL224_MINB>(grid, g, s)
-              : launch_one<false, 224, false, false, TALL224_ST, TALL224_MINB>(grid, g, s);
+    return arow ? launch_one<true, 128, TALL128_ST, TALL128_MINB>(grid, g, s)
+                : launch_one<false, 128, TALL128_ST, TALL128_MINB>(grid, g, s);
+  return arow ? launch_one<true, 224, TALL224_ST, TALL224_MINB>(grid, g, s)
+              : launch_one<false, 224, TALL224_ST, TALL224_MINB>(grid, g, s);
 }
 
 int tall_splits(int64_t M, int64_t K) {
@@ -265,30 +232,6 @@ int tall_splits(int64_t M, int64_t K) {
 }
 
 }  // namespace
-
-// Cross-spectral product (SSI_COV_SPECTRAL): per frequency z, C_z (M x N, M = 2 rsplit) =
-// A_z (M x K) * B_z (K x N, ROW-major: B(k, j) = B[k*ldb + j]) with A_z complex-stacked: the
-// caller stores only rows [0, rsplit) (col-major, column pairs (2s, 2s+1) = Re, Im), rows
-// r >= rsplit read as (-Im, Re) of row r - rsplit; output rows r >= rsplit are written at
-// (r - rsplit) + c*ldc + roff (the imaginary half of the complex product).
-ssi_status gemm_tall_batched_brow(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int64_t sA,
-                                  const double* B, int64_t ldb, int64_t sB, double* C, int64_t ldc, int64_t sC,
-                                  int batch, int64_t rsplit, int64_t roff, bool accumulate, cudaStream_t s) {
-  if (N > 192 || batch < 1 || batch > 65535 || (ldb & 1) || (lda & 1)) {
-    set_last_error("gemm_tall_batched_brow: N = %lld > 192, bad batch %d or odd ld", (long long)N, batch);
-    return SSI_ERR_INVALID_ARG;
-  }
-  const int64_t kchunk = (K + BK - 1) / BK * BK;
-  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, sA, sB, sC, 0, rsplit, roff, accumulate ? 1 : 0};
-  const dim3 grid(unsigned((M + BM - 1) / BM), 1u, unsigned(batch));
-  if (M != 2 * rsplit || (K & 1)) {
-    set_last_error("gemm_tall_batched_brow: need M = 2 rsplit and even K");
-    return SSI_ERR_INVALID_ARG;
-  }
-  if (N <= 64) return launch_one<false, 64, true, true>(grid, g, s);
-  if (N <= 128) return launch_one<false, 128, true, true>(grid, g, s);
-  return launch_one<false, 192, true, true, TALL_CST_ST, TALL_CST_MINB>(grid, g, s);
-}
 
 size_t gemm_tall_partial_elems(int64_t M, int64_t N, int64_t K) {
   const int s = tall_splits(M, K);
@@ -344,9 +287,9 @@ ssi_status gemm_tall_syrk_lower(int64_t n, int64_t K, const double* A, int64_t l
   int64_t kchunk = (K + splits - 1) / splits;
   kchunk = (kchunk + BK - 1) / BK * BK;
   const int z = int((K + kchunk - 1) / kchunk);
-  TallArgs g{n, n, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? n : ldc, kchunk, 0, 0, 0, 1, 0, 0, 0, run_if};
+  TallArgs g{n, n, K, A, lda, B, ldb, z > 1 ? partial : C, z > 1 ? n : ldc, kchunk, 0, 0, 0, 1, run_if};
   {
-    const ssi_status st = launch_one<true, 64, false, false, TALL64_ST, TALL64_MINB>(dim3(unsigned(tiles), unsigned(z)), g, s);
+    const ssi_status st = launch_one<true, 64, TALL64_ST, TALL64_MINB>(dim3(unsigned(tiles), unsigned(z)), g, s);
     if (st != SSI_OK) return st;
   }
   if (z > 1) {
@@ -364,8 +307,8 @@ ssi_status gemm_tall_syrk_lower(int64_t n, int64_t K, const double* A, int64_t l
 ssi_status gemm_tall_triu(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
                           int64_t ldb, double* C, int64_t ldc, cudaStream_t s, const int* run_if) {
   const int64_t kchunk = (K + BK - 1) / BK * BK;
-  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, 0, 0, 0, 2, 0, 0, 0, run_if};
-  return launch_one<false, 64, false, false, TALL64_ST, TALL64_MINB>(dim3(unsigned((M + BM - 1) / BM), 1u, unsigned((N + 63) / 64)), g, s);
+  TallArgs g{M, N, K, A, lda, B, ldb, C, ldc, kchunk, 0, 0, 0, 2, run_if};
+  return launch_one<false, 64, TALL64_ST, TALL64_MINB>(dim3(unsigned((M + BM - 1) / BM), 1u, unsigned((N + 63) / 64)), g, s);
 }
 
 ssi_status gemm_tall_batched(int64_t M, int64_t N, int64_t K, bool a_rowmajor, const double* A, int64_t lda,
