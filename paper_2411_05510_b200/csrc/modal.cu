@@ -216,121 +216,6 @@ __device__ void dlanv2(double& a, double& b, double& c, double& d, double& cs, d
   }
 }
 
-// Eigenvalues of a small N x N upper Hessenberg block (the shifts of an N-shift sweep), one
-// thread: double-shift Francis iterations with deflation (dlahqr structure, no Schur vectors),
-// 2 x 2 blocks by dlanv2. Returns false when it does not converge (the caller falls back to one
-// double shift).
-template <int N>
-__device__ bool eig_small(double (&G)[N][N], double (&wr)[N], double (&wi)[N]) {
-  // every array index is a compile-time constant (loops over fixed ranges with predicates), so
-  // G stays in registers
-  int i = N - 1, its = 0;
-  while (i >= 0) {
-    int l = 0;
-#pragma unroll
-    for (int ll = N - 1; ll > 0; --ll) {
-      if (ll <= i && l == 0) {
-        const double h = fabs(G[ll][ll - 1]);
-        double tst = fabs(G[ll - 1][ll - 1]) + fabs(G[ll][ll]);
-        if (tst == 0.0) tst = 1.0;
-        if (h <= kUlp * tst) { l = ll; G[ll][ll - 1] = 0.0; }
-      }
-    }
-    if (l == i) {
-#pragma unroll
-      for (int q = 0; q < N; ++q) if (q == i) { wr[q] = G[q][q]; wi[q] = 0.0; }
-      --i; its = 0; continue;
-    }
-    if (l == i - 1) {
-#pragma unroll
-      for (int q = 1; q < N; ++q) {
-        if (q == i) {
-          // eigenvalues of the 2 x 2 block (shift values only; no standardised Schur form needed)
-          const double a = G[q - 1][q - 1], b = G[q - 1][q], c = G[q][q - 1], d = G[q][q];
-          const double hm = 0.5 * (a - d), disc = fma(hm, hm, b * c), mid = 0.5 * (a + d);
-          if (disc >= 0.0) {
-            const double r = disc > 0.0 ? disc * fast_rsqrt(disc) : 0.0;
-            const double big = mid + copysign(r, mid);             // larger magnitude root
-            const double det = a * d - b * c;
-            const double small = big != 0.0 ? det * fast_rcp(big) : mid - copysign(r, mid);
-            wr[q - 1] = big; wi[q - 1] = 0.0; wr[q] = small; wi[q] = 0.0;
-          } else {
-            const double im = -disc * fast_rsqrt(-disc);
-            wr[q - 1] = mid; wi[q - 1] = im; wr[q] = mid; wi[q] = -im;
-          }
-        }
-      }
-      i -= 2; its = 0; continue;
-    }
-    if (++its > 40) return false;
-    // one Francis double step on rows/cols l..i (shifts: trailing 2 x 2 of the active block)
-    double t11 = 0, t12 = 0, t21 = 0, t22 = 0, a00 = 0, a01 = 0, a10 = 0, a11 = 0, a21 = 0;
-#pragma unroll
-    for (int q = 1; q < N; ++q)
-      if (q == i) { t11 = G[q - 1][q - 1]; t12 = G[q - 1][q]; t21 = G[q][q - 1]; t22 = G[q][q]; }
-#pragma unroll
-    for (int q = 0; q < N - 1; ++q)
-      if (q == l) {
-        a00 = G[q][q]; a01 = G[q][q + 1]; a10 = G[q + 1][q]; a11 = G[q + 1][q + 1];
-        if (q + 2 < N) a21 = G[q + 2][q + 1];
-      }
-    const double tr = t11 + t22, det = t11 * t22 - t12 * t21;
-    double x = a00 * a00 + a01 * a10 - tr * a00 + det;
-    double y = a10 * (a00 + a11 - tr);
-    double z = (l + 2 <= i) ? a10 * a21 : 0.0;
-#pragma unroll
-    for (int k = 0; k < N - 1; ++k) {
-      if (k < l || k >= i) continue;
-      const bool three = (k + 2 <= i);
-      if (k > l) { x = G[k][k - 1]; y = G[k + 1][k - 1]; z = (three && k + 2 < N) ? G[k + 2 < N ? k + 2 : k][k - 1] : 0.0; }
-      const double yz = y * y + z * z;
-      if (yz == 0.0) continue;
-      const double ss = fma(x, x, yz);
-      // as in the bulge chase: rsqrt and the reciprocal estimated together, Goldschmidt refinement
-      double rs, r0;
-      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(ss));
-      asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(fabs(x) + ss * rs));
-      double gq = ss * rs, hq = 0.5 * rs;
-#pragma unroll
-      for (int it = 0; it < 3; ++it) {
-        const double rr = fma(-gq, hq, 0.5);
-        gq = fma(gq, rr, gq);
-        hq = fma(hq, rr, hq);
-      }
-      rs = hq + hq;
-      const double sq = gq;
-      const double beta = -copysign(sq, x);
-      const double tau = fma(fabs(x), rs, 1.0);
-      const double den = fabs(x) + sq;
-      r0 = fma(r0, fma(-den, r0, 1.0), r0);
-      r0 = fma(r0, fma(-den, r0, 1.0), r0);
-      const double inv = copysign(r0, x);
-      const double v1 = y * inv, v2 = z * inv;
-      if (k > l) {
-        G[k][k - 1] = beta; G[k + 1][k - 1] = 0.0;
-        if (three && k + 2 < N) G[k + 2 < N ? k + 2 : k][k - 1] = 0.0;
-      }
-#pragma unroll
-      for (int c = 0; c < N; ++c) {
-        if (c < k || c > i) continue;
-        const double g2 = (three && k + 2 < N) ? G[k + 2 < N ? k + 2 : k][c] : 0.0;
-        const double sum = (G[k][c] + v1 * G[k + 1][c] + v2 * g2) * tau;
-        G[k][c] -= sum; G[k + 1][c] -= sum * v1;
-        if (three && k + 2 < N) G[k + 2 < N ? k + 2 : k][c] = g2 - sum * v2;
-      }
-#pragma unroll
-      for (int r = 0; r < N; ++r) {
-        if (r < l || r > (k + 3 < i ? k + 3 : i)) continue;
-        const double g2 = (three && k + 2 < N) ? G[r][k + 2 < N ? k + 2 : k] : 0.0;
-        const double sum = (G[r][k] + v1 * G[r][k + 1] + v2 * g2) * tau;
-        G[r][k] -= sum; G[r][k + 1] -= sum * v1;
-        if (three && k + 2 < N) G[r][k + 2 < N ? k + 2 : k] = g2 - sum * v2;
-      }
-    }
-  }
-  return true;
-}
-
 __device__ __forceinline__ bool order_truncated(const EigArgs& g, int n) {
   // orders above the numerical rank are reported (count = -1), not solved
   return !(g.S[n - 1] >= 1e-12 * g.S[0]);
@@ -591,8 +476,7 @@ __device__ __forceinline__ void eigvec_axpy(const Band& H, int j, double wr, dou
 template <bool BG>
 __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) {
   extern __shared__ __align__(16) double dsm[];
-  __shared__ double sh_cs, sh_sn, sh_pt[NSH / 2], sh_pd[NSH / 2];
-  __shared__ int sh_ok4;
+  __shared__ double sh_cs, sh_sn;
   __shared__ int sh_l, sh_fail, sh_ncand;
 
   const int o = kOrderRev ? int(gridDim.x) - 1 - int(blockIdx.x) : int(blockIdx.x);   // largest order first
@@ -747,9 +631,8 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
       // element as applying each reflector in turn (dlahqr); only independent updates reorder.
       {
         // First column of the shift polynomial. Normally NSH shifts per sweep (one bulge of
-        // length BS = NSH + 1): the eigenvalues of the trailing NSH x NSH block, paired into real
-        // quadratics (H^2 - t H + d), w = prod_q (H^2 - t_q H + d_q) e_lo formed in factored form.
-        // Exceptional sweeps (its = 10, 20) and small active blocks use one double shift from the
+        // length BS = NSH + 1): the eigenvalues of the trailing NSH x NSH block, through its
+        // characteristic polynomial (below). Exceptional sweeps (its = 10, 20) and small active blocks use one double shift from the
         // trailing 2 x 2 (w has 3 nonzeros; the same chase code runs with the other v_j = 0).
         double w0v[BS];
         const long long tsh0 = clock64();
@@ -798,48 +681,58 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
           double u[BS];
 #pragma unroll
           for (int r = 0; r < BS; ++r) u[r] = r == 0 ? 1.0 : 0.0;
-          // NSH shifts = eigenvalues of the trailing NSH x NSH block, paired into real quadratics
-          // (conjugate pairs together, real shifts two by two)
-          bool okn = false;
+          // NSH = 4 shifts = the eigenvalues of the trailing 4 x 4 block G: the first column of
+          // prod_q (H - s_q) is p(H) e_lo with p the characteristic polynomial of G, so the shifts
+          // never need to be computed — every H thread forms p's coefficients (trace, principal
+          // minors, det) from the broadcast-read block and evaluates p(H) e_lo by Horner's rule
+          // with a running scale (no one-thread eigen-solve, no barrier).
+          static_assert(NSH == 4, "characteristic-polynomial shifts assume 4 shifts");
           if (four) {
-            if (htid == 0) {
-              double G[NSH][NSH], wr[NSH], wi[NSH];
-              for (int r = 0; r < NSH; ++r)
-                for (int c = 0; c < NSH; ++c)
-                  G[r][c] = (r <= c + 1) ? H(ihi - NSH + 1 + r, ihi - NSH + 1 + c) : 0.0;
-              int okk = eig_small<NSH>(G, wr, wi) ? 1 : 0;
-              if (okk) {
-                int np = 0, nrl = 0;
-                double rr[NSH];
-                for (int q = 0; q < NSH; ++q) {
-                  if (wi[q] > 0.0) { sh_pt[np] = 2.0 * wr[q]; sh_pd[np] = wr[q] * wr[q] + wi[q] * wi[q]; ++np; }
-                  else if (wi[q] == 0.0) rr[nrl++] = wr[q];
-                }
-                for (int q = 0; q + 1 < nrl; q += 2) { sh_pt[np] = rr[q] + rr[q + 1]; sh_pd[np] = rr[q] * rr[q + 1]; ++np; }
-                okk = (np == NSH / 2);
-              }
-              sh_ok4 = okk;
-            }
-            hsync();
-            okn = sh_ok4 != 0;
-          }
-          if (okn) {
-            for (int q = 0; q < NSH / 2; ++q) {
+            double G[4][4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+              for (int c = 0; c < 4; ++c) G[r][c] = (r <= c + 1) ? H(ihi - 3 + r, ihi - 3 + c) : 0.0;
+            auto m2 = [&](int a, int b) { return G[a][a] * G[b][b] - G[a][b] * G[b][a]; };
+            auto m3 = [&](int a, int b, int c) {   // principal minor on rows / columns {a, b, c}
+              return G[a][a] * (G[b][b] * G[c][c] - G[b][c] * G[c][b]) -
+                     G[a][b] * (G[b][a] * G[c][c] - G[b][c] * G[c][a]) +
+                     G[a][c] * (G[b][a] * G[c][b] - G[b][b] * G[c][a]);
+            };
+            const double a3 = -(G[0][0] + G[1][1] + G[2][2] + G[3][3]);
+            const double a2 = m2(0, 1) + m2(0, 2) + m2(0, 3) + m2(1, 2) + m2(1, 3) + m2(2, 3);
+            const double a1 = -(m3(1, 2, 3) + m3(0, 2, 3) + m3(0, 1, 3) + m3(0, 1, 2));
+            // det by the first column (G[2][0] = G[3][0] = 0: Hessenberg)
+            const double a0 = G[0][0] * m3(1, 2, 3) -
+                              G[1][0] * (G[0][1] * (G[2][2] * G[3][3] - G[2][3] * G[3][2]) -
+                                         G[0][2] * (G[2][1] * G[3][3] - G[2][3] * G[3][1]) +
+                                         G[0][3] * (G[2][1] * G[3][2] - G[2][2] * G[3][1]));
+            const double coef[4] = {a3, a2, a1, a0};
+            double sc_run = 1.0;                   // u = (true Horner vector) * sc_run
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
               double y[BS];
-              quad(u, sh_pt[q], sh_pd[q], y);
+#pragma unroll
+              for (int r = 0; r < BS; ++r) {
+                double acc = 0.0;
+#pragma unroll
+                for (int c = 0; c < NSH; ++c) acc = fma(hh[r][c], u[c], acc);
+                y[r] = acc;
+              }
+              y[0] = fma(coef[q], sc_run, y[0]);
               double sc = 0.0;
 #pragma unroll
               for (int r = 0; r < BS; ++r) sc += fabs(y[r]);
               const double isc = sc > 0.0 ? 1.0 / sc : 1.0;
 #pragma unroll
               for (int r = 0; r < BS; ++r) u[r] = y[r] * isc;
+              sc_run *= isc;
             }
 #pragma unroll
             for (int r = 0; r < BS; ++r) w0v[r] = u[r];
           } else {
             quad(u, t1, d1, w0v);
           }
-          if (four) hsync();            // sh_pt / sh_pd read before the next sweep rewrites them
           double sc = 0.0;
 #pragma unroll
           for (int r = 0; r < BS; ++r) sc += fabs(w0v[r]);
