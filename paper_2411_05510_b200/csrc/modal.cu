@@ -44,7 +44,7 @@ constexpr int CG_T = NT - CG_W0 * 32;
 #define SSI_EIG_NSLOT 8
 #endif
 constexpr int NSLOT = SSI_EIG_NSLOT;        // H -> C queue depth
-enum { QWIN = 0, QROT = 1, QEND = 2 };
+enum { QWIN = 0, QEND = 2 };
 struct QEntry {
   int type, w0, nw, nsteps;
   int chi;                      // columns > chi (deflated, never read again by the H group) are the C group's
@@ -151,6 +151,7 @@ struct Smem {
   int* rowoff;    // n+1
   double* x;      // NW * 2 * n: per-warp complex eigenvector
   int* cj;        // cap: block start of candidate
+  int* blk;       // n_max / 2 + 1: first rows of the deflated 2 x 2 blocks (standardized after the QR)
   QEntry* q;      // NSLOT queue entries (H group -> C group)
   uint64_t* q_full;
   uint64_t* q_empty;
@@ -476,7 +477,7 @@ __device__ __forceinline__ void eigvec_axpy(const Band& H, int j, double wr, dou
 template <bool BG>
 __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) {
   extern __shared__ __align__(16) double dsm[];
-  __shared__ double sh_cs, sh_sn;
+  __shared__ int sh_nblk;
   __shared__ int sh_l, sh_fail, sh_ncand;
 
   const int o = kOrderRev ? int(gridDim.x) - 1 - int(blockIdx.x) : int(blockIdx.x);   // largest order first
@@ -521,7 +522,8 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
     s.q_empty = reinterpret_cast<uint64_t*>(p); p += sizeof(uint64_t) * NSLOT;
     s.q_rdone = reinterpret_cast<uint64_t*>(p); p += sizeof(uint64_t) * NSLOT;
     s.rowoff = reinterpret_cast<int*>(p);    p += sizeof(int) * (nm + 1);
-    s.cj = reinterpret_cast<int*>(p);
+    s.cj = reinterpret_cast<int*>(p);        p += sizeof(int) * cap;
+    s.blk = reinterpret_cast<int*>(p);
   }
   if (tid == 0) {
     for (int i = 0; i < NSLOT; ++i) { mbar_init1(&s.q_full[i]); mbar_init1(&s.q_empty[i]); mbar_init1(&s.q_rdone[i]); }
@@ -547,6 +549,7 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
     int ihi = n - 1;
     int its = 0;
     int qslot = 0, quse = 0;          // next queue slot to fill and its use count
+    int nblk = 0;                     // deflated 2 x 2 blocks so far
     const int itmax = 30 * (n > 10 ? n : 10);
     // acquire the next queue slot (all H threads call; thread 0 waits for the C group)
     auto acquire = [&]() -> QEntry* {
@@ -598,24 +601,19 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
       t_scan += tb - ta;
       if (lo > 0 && htid == 0) H(lo, lo - 1) = 0.0;
       if (lo == ihi) { ihi -= 1; its = 0; hsync(); continue; }
-      drain();
       if (lo == ihi - 1) {
-        const int p = ihi - 1, q = ihi;
-        QEntry* e = acquire();
-        if (htid == 0) {
-          double a = H(p, p), b = H(p, q), c = H(q, p), d = H(q, q), cs, sn;
-          dlanv2(a, b, c, d, cs, sn);
-          H(p, p) = a; H(p, q) = b; H(q, p) = c; H(q, q) = d;
-          sh_cs = cs; sh_sn = sn;
-          e->type = QROT; e->w0 = p; e->nw = 2; e->nsteps = 0; e->chi = q; e->r[0] = cs; e->r[1] = sn;
-        }
-        hsync();
-        const double cs = sh_cs, sn = sh_sn;
-        publish();                     // (rows above p and columns > q are rotated by the C group)
+        // a deflated 2 x 2 block: its standardization (dlanv2) and the rotation of the rows beyond
+        // it, the columns above it and C are deferred to the end of the QR — rows p, q are frozen
+        // from here on, and the later sweeps only apply row operations to columns p, q (which
+        // commute with the deferred column rotation)
+        if (htid == 0) s.blk[nblk] = ihi - 1;
+        ++nblk;
         ihi -= 2; its = 0;
         t_2x2 += clock64() - tb;
+        hsync();                       // sh_l is read by every H thread before thread 0 resets it
         continue;
       }
+      drain();
       ++its; ++total_its;
       if (its > 100 || total_its > itmax) {
         if (htid == 0) sh_fail = 1;
@@ -915,6 +913,7 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
       t_chase += tc - tb;
       steps += ihi - lo;
     }
+    if (htid == 0) sh_nblk = nblk;
     // end of the queue
     acquire();
     if (htid == 0) s.q[qslot].type = QEND;
@@ -948,14 +947,6 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
 #pragma unroll
           for (int u = 0; u < WIN; ++u) if (u < nw) row[u] = seg[u];
         }
-      } else {
-        const double cs = e->r[0], sn = e->r[1];
-        for (int r = ctid; r < w0; r += CG_T) {
-          double* row = s.H + s.rowoff[r];
-          const double x = row[w0], y = row[w0 + 1];
-          row[w0] = cs * x + sn * y;
-          row[w0 + 1] = cs * y - sn * x;
-        }
       }
       csync();
       if (ctid == 0) mbar_arrive(&s.q_rdone[slot]);
@@ -978,19 +969,6 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
 #pragma unroll
           for (int u = 0; u < WIN; ++u) if (u < nw) s.H[s.rowoff[w0 + u] + c] = seg[u];
         }
-      } else {   // QROT: columns p = w0, q = w0 + 1 of C; rows p, q of H beyond q
-        const double cs = e->r[0], sn = e->r[1];
-        for (int a = ctid; a < l; a += CG_T) {
-          double* cr = C + a;
-          const double x = cr[int64_t(w0) * l], y = cr[int64_t(w0 + 1) * l];
-          cr[int64_t(w0) * l] = cs * x + sn * y;
-          cr[int64_t(w0 + 1) * l] = cs * y - sn * x;
-        }
-        for (int c = chi + 1 + ctid; c < n; c += CG_T) {
-          const double x = s.H[s.rowoff[w0] + c], y = s.H[s.rowoff[w0 + 1] + c];
-          s.H[s.rowoff[w0] + c] = cs * x + sn * y;
-          s.H[s.rowoff[w0 + 1] + c] = cs * y - sn * x;
-        }
       }
       csync();
       if (ctid == 0) mbar_arrive(&s.q_empty[slot]);
@@ -1007,6 +985,48 @@ __global__ void __launch_bounds__(NT, SSI_EIG_MINB) eig_order_kernel(EigArgs g) 
     if (tid == 0) T.count[o] = -1;
     zero_shapes(0);
     return;
+  }
+  // ---------------- the deferred 2 x 2 standardizations: dlanv2 per block (one thread each), then
+  // the rotations — rows p, q beyond q (left), then rows above p and the Schur vectors C in
+  // columns p, q (right); blocks are disjoint index pairs, so each phase is race-free
+  {
+    const int nbk = sh_nblk;
+    double* rcs = s.x;
+    double* rsn = s.x + (g.n_max / 2 + 1);
+    for (int t = tid; t < nbk; t += NT) {
+      const int p = s.blk[t], q = p + 1;
+      double a = H(p, p), b = H(p, q), c = H(q, p), d = H(q, q), cs, sn;
+      dlanv2(a, b, c, d, cs, sn);
+      H(p, p) = a; H(p, q) = b; H(q, p) = c; H(q, q) = d;
+      rcs[t] = cs; rsn[t] = sn;
+    }
+    __syncthreads();
+    for (int t = warp; t < nbk; t += NT / 32) {
+      const int p = s.blk[t], q = p + 1;
+      const double cs = rcs[t], sn = rsn[t];
+      for (int c = q + 1 + lane; c < n; c += 32) {
+        const double x = H(p, c), y = H(q, c);
+        H(p, c) = cs * x + sn * y;
+        H(q, c) = cs * y - sn * x;
+      }
+    }
+    __syncthreads();
+    for (int t = warp; t < nbk; t += NT / 32) {
+      const int p = s.blk[t], q = p + 1;
+      const double cs = rcs[t], sn = rsn[t];
+      for (int r = lane; r < p; r += 32) {
+        const double x = H(r, p), y = H(r, q);
+        H(r, p) = cs * x + sn * y;
+        H(r, q) = cs * y - sn * x;
+      }
+      for (int a = lane; a < l; a += 32) {
+        double* cr = C + a;
+        const double x = cr[int64_t(p) * l], y = cr[int64_t(q) * l];
+        cr[int64_t(p) * l] = cs * x + sn * y;
+        cr[int64_t(q) * l] = cs * y - sn * x;
+      }
+    }
+    __syncthreads();
   }
 
   // ---------------- poles: complex pairs of the standardized Schur form. Thread 0 finds the 2 x 2
@@ -1170,7 +1190,7 @@ size_t modal_smem_bytes(int n_max, int cap, bool band_global) {
   return sizeof(QEntry) * NSLOT + 3 * sizeof(uint64_t) * NSLOT +
          sizeof(double) * ((band_global ? 0 : band_elems(n_max)) + x_elems(n_max) +
                            4 * size_t(cap)) +
-         sizeof(int) * (size_t(n_max) + 1 + cap) + 64;
+         sizeof(int) * (size_t(n_max) + 1 + cap + size_t(n_max) / 2 + 1) + 64;
 }
 
 // Orders up to ~230 keep the banded Hessenberg/Schur matrix in shared memory; beyond that (the
