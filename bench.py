@@ -538,7 +538,7 @@ def main():
     if not args.no_e2e:
         ns = len(pipe.streams)
         pinned = [torch.from_numpy(h).pin_memory() for h in host[:2]]
-        Ydev = [torch.empty_like(Ys[0]) for _ in range(ns)]
+        pipe.reserve_host_inputs(pinned[0].shape, pinned[0].dtype)
         tab_host = [[torch.empty_like(t, device="cpu").pin_memory() for t in e.table.tensors()]
                     for e in pipe.engines]
         d2h = sum(t.numel() * t.element_size() for t in tab_host[0])
@@ -552,10 +552,9 @@ def main():
             st.wait_stream(stream)
         for j in range(args.steps):
             slot = pipe.j % ns
-            st = pipe.streams[slot]
-            with torch.cuda.stream(st):
-                Ydev[slot].copy_(pinned[j % 2], non_blocking=True)       # H2D inside the step
-                tab, _ = pipe.submit(Ydev[slot], (j << 32) | cfg.i)
+            # H2D of this step's record inside the timed region, on the pipeline's copy stream
+            # (submit_host: a ring of device input buffers, copies overlap the records in flight)
+            tab, st = pipe.submit_host(pinned[j % 2], (j << 32) | cfg.i)
             with torch.cuda.stream(st):
                 for hst, d in zip(tab_host[slot], tab.tensors()):      # D2H of the result
                     hst.copy_(d, non_blocking=True)

@@ -153,25 +153,74 @@ class RecordPipeline:
         self.cov_streams = ([torch.cuda.Stream(device=device, priority=lo) for _ in range(n_streams)]
                             if split_priority else self.streams)
         self.j = 0
+        self.device = torch.device(device)
+        # host records (submit_host): a ring of device input buffers filled on one copy stream
+        self._in_bufs, self._in_free, self._hb = [], [], 0
+        self.copy_stream = None
 
-    def submit(self, Y: torch.Tensor, stream_id: int, events=None):
+    def submit(self, Y: torch.Tensor, stream_id: int, events=None, ready: torch.cuda.Event | None = None):
+        tab, st, _ = self._submit(Y, stream_id, events, ready)
+        return tab, st
+
+    def _submit(self, Y, stream_id, events=None, ready=None):
         k = self.j % len(self.engines)
         e, st, cst = self.engines[k], self.streams[k], self.cov_streams[k]
         self.j += 1
-        st.wait_stream(torch.cuda.current_stream(Y.device))   # Y was produced on the caller's stream
+        if ready is None:
+            st.wait_stream(torch.cuda.current_stream(Y.device))   # Y was produced on the caller's stream
         if self.split:
-            cst.wait_stream(st)            # the engine's buffers are free; Y is ready on st
-        Y.record_stream(cst)               # the caching allocator must not reuse Y before A1 read it
+            cst.wait_stream(st)            # the engine's buffers are free (and Y is ready on st)
+        if ready is not None:
+            cst.wait_event(ready)          # Y arrives from the copy stream
+        else:
+            Y.record_stream(cst)           # the caching allocator must not reuse Y before A1 read it
         with torch.cuda.stream(cst):
             if events is not None:
                 events[0].record(cst)
             R = e.covariances(Y)
             if events is not None:
                 events[1].record(cst)
+            read = torch.cuda.Event()
+            read.record(cst)               # A1 is the only reader of Y
         if self.split:
             st.wait_stream(cst)
         with torch.cuda.stream(st):
             tab, _ = e.decompose(R, e.P.i, stream_id)
+        return tab, st, read
+
+    def reserve_host_inputs(self, shape, dtype):
+        """Allocate submit_host's device input ring (n_streams + 2 records) and copy stream now,
+        so that no allocation happens while records stream through."""
+        if not self._in_bufs:
+            self.copy_stream = torch.cuda.Stream(device=self.device)
+            self._in_bufs = [torch.empty(tuple(shape), dtype=dtype, device=self.device)
+                             for _ in range(len(self.engines) + 2)]
+            self._in_free = [None] * len(self._in_bufs)
+
+    def submit_host(self, Yh: torch.Tensor, stream_id: int, events=None):
+        """submit() for a record in (pinned) host memory. The host-to-device copy runs on the
+        pipeline's copy stream into a ring of n_streams + 2 device buffers, so the copy of the
+        next records overlaps the compute of the ones in flight; a buffer is refilled once the
+        covariances (A1, its only reader) of its previous record are done. Returns (table,
+        stream) like submit()."""
+        self.reserve_host_inputs(Yh.shape, Yh.dtype)
+        nbuf = len(self._in_bufs)
+        b = self._hb % nbuf
+        self._hb += 1
+        buf = self._in_bufs[b]
+        if buf.shape != Yh.shape or buf.dtype != Yh.dtype:
+            raise ValueError(f"submit_host: record {tuple(Yh.shape)} {Yh.dtype} differs from the pipeline's "
+                             f"{tuple(buf.shape)} {buf.dtype}")
+        cs = self.copy_stream
+        cs.wait_stream(torch.cuda.current_stream(self.device))    # Yh was produced before this call
+        if self._in_free[b] is not None:
+            cs.wait_event(self._in_free[b])
+        with torch.cuda.stream(cs):
+            buf.copy_(Yh, non_blocking=True)
+            ready = torch.cuda.Event()
+            ready.record(cs)
+        tab, st, read = self._submit(buf, stream_id, events, ready)
+        self._in_free[b] = read
         return tab, st
 
     def check(self):
@@ -184,6 +233,8 @@ class RecordPipeline:
         cur = stream or torch.cuda.current_stream()
         for st in self.streams:
             cur.wait_stream(st)
+        if self.copy_stream is not None:
+            cur.wait_stream(self.copy_stream)
         if self.split:
             for st in self.cov_streams:
                 cur.wait_stream(st)
@@ -386,10 +437,14 @@ def record_batch(records, P: SweepParams, rank: int = 0, world: int = 1, n_strea
     assign = record_assignment(n, world)
     fetch = records if callable(records) else (lambda j: records[j])
     first = fetch(assign[rank][0]) if assign[rank] else fetch(0)
-    pipe = RecordPipeline(P, first.shape[0], first.device, n_streams)
+    device = first.device if first.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    pipe = RecordPipeline(P, first.shape[0], device, n_streams)
     local = {}
     for j in assign[rank]:
-        tab, st = pipe.submit(fetch(j), (j << 32) | P.i)
+        Yj = fetch(j)
+        # host records (pinned) stream in through the pipeline's copy stream
+        tab, st = (pipe.submit(Yj, (j << 32) | P.i) if Yj.is_cuda
+                   else pipe.submit_host(Yj, (j << 32) | P.i))
         with torch.cuda.stream(st):
             local[j] = api.PoleTable(tab.n_min, tab.n_step, tab.l, tab.cap, *[t.clone() for t in tab.tensors()])
     pipe.join()
@@ -397,7 +452,7 @@ def record_batch(records, P: SweepParams, rank: int = 0, world: int = 1, n_strea
     pipe.check()
     if not gather:
         return local
-    return gather_tables(local, assign, lambda: api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, first.device),
+    return gather_tables(local, assign, lambda: api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, device),
                          rank, world, group)
 
 

@@ -168,3 +168,10 @@ def test_c5_batch_eight_records(mods):
         torch.cuda.synchronize()
         for a, b in zip(alone.tensors(), tabs[j].tensors()):
             assert torch.equal(a, b), j          # bit-identical: fixed reduction orders
+    # the same batch from pinned host records (RecordPipeline.submit_host: copy stream + input
+    # ring) gives bit-identical tables
+    host = [torch.from_numpy(y).pin_memory() for y in recs]
+    tabs_h = drivers.record_batch(host, P, n_streams=3)
+    for j in range(8):
+        for a, b in zip(tabs_h[j].tensors(), tabs[j].tensors()):
+            assert torch.equal(a, b), ("host record", j)
