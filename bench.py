@@ -78,8 +78,8 @@ def record_flops(cfg, api):
     """Algorithmic flops of one record through the path as built, by stage:
     A1 spectral: cross-spectral product 6 lp^2 S (F/2+1) + inverse DFT 2 lp^2 L (F+2);
     A4/A6/A7 (2q+2 passes through the block DFT): per pass 2 i (2l)^2 k (block products) +
-    2 x 2 l (2i) i k (forward and inverse DFT);  A5/A8: 2q+2 CholeskyQR2 + the one of B^T, each
-    2 x (m k^2) (symmetric Gram, triangular Y L^-T) + Cholesky/inverse (2 k^3/3), U = Q U~
+    2 x 2 l (2i) i k (forward and inverse DFT);  A5/A8: 2q + 4 CholeskyQR passes (one between the power-iteration products,
+    two for the last Q and for B^T), each m k^2 (symmetric Gram) + m k^2 (triangular Y L^-T) + k^3/3, U = Q U~
     (2 m k n_max), Jacobi (~9 sweeps x k^2/2 pairs x 6k); A9-A11: CholeskyQR2 of U^up + Q^T U^down
     (~6 m n_max^2) and per order n: Hessenberg (10/3 n^3) with C_n = U[0:l,:n] Q_H (2 l n^2), and
     the Francis QR (~10 n^3) with its l-row Schur vectors (~15 l n^2; LAPACK's 25 n^3 for an
@@ -88,8 +88,11 @@ def record_flops(cfg, api):
     f_prod, f_inv = api.cov_spectral_flops(cfg.N, l, 2 * i - 1)
     passes = 2 * q + 2                       # Y = T Omega, 2q power-iteration passes, B^T = T^T Q
     rsvd_passes = passes * (2 * i * (2 * l) ** 2 * k + 2 * 2 * l * (2 * i) * i * k)
-    nqr = 2 * q + 2                          # qr(Y), 2q in the power iterations, qr(B^T)
-    qr = nqr * (4.0 * m * k * k + 2.0 * k ** 3 / 3)
+    # CholeskyQR passes (Gram m k^2 + triangular Y L^-T m k^2 + Cholesky/inverse k^3/3 each):
+    # one per re-orthonormalisation between the power iterations' products (2q when q > 0),
+    # two for the Q entering B = Q^T T and two for qr(B^T) (reading A-12)
+    npass = 2 * q + 4
+    qr = npass * (2.0 * m * k * k + k ** 3 / 3)
     small = 2.0 * m * k * n_max + 9 * (k * k / 2) * 6 * k
     modal = 6.0 * m * n_max ** 2 + sum(10.0 / 3 * n ** 3 + 2.0 * l * n * n + 10.0 * n ** 3 + 15.0 * l * n * n
                                        for n in cfg.orders)

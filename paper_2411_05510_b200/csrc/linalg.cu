@@ -571,6 +571,25 @@ ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, Ch
   return launch_check("cq_fold_kernel");
 }
 
+// One CholeskyQR pass (with the shift on breakdown): the re-orthonormalisation between the
+// power iterations' passes, where only span(Q) matters (the next pass and the final CholeskyQR2
+// see the same subspace); its orthogonality error ~ kappa(Y)^2 u is removed by the next QR.
+ssi_status cholqr1(const double* Y, int64_t ldy, int64_t m, int k, double* Q, CholQRWork& w,
+                   int32_t* status, cudaStream_t s) {
+  if (k > kSvdMaxK) return cholqr2_big(Y, ldy, m, k, Q, w, status, s);
+  const bool tall = k <= kTallMaxN && ldy % 2 == 0 && m % 2 == 0 && k % 2 == 0 &&
+                    (reinterpret_cast<uintptr_t>(Y) & 15) == 0 && (reinterpret_cast<uintptr_t>(Q) & 15) == 0;
+  if (tall) {
+    SSI_TRY(gemm_tall_syrk_lower(k, m, Y, ldy, Y, ldy, w.W, k, w.tallp, s, nullptr));
+  } else {
+    SSI_TRY(gemm_f64(k, k, m, 1.0, Operand{Y, ldy, 1}, Operand{Y, 1, ldy}, w.W, k, gemm_pick_splits(k, k, m),
+                     w.partial, s, nullptr));
+  }
+  SSI_TRY(chol_inv(w.W, k, m, w.L1, w.Linv1, w.LinvT1, w.chol_g, status, s, nullptr, w.flag, 0));
+  if (tall) return gemm_tall_triu(m, k, k, Y, ldy, w.LinvT1, k, Q, m, s, nullptr);
+  return gemm_f64(m, k, k, 1.0, Operand{Y, 1, ldy}, Operand{w.Linv1, k, 1}, Q, m, 1, nullptr, s, nullptr);
+}
+
 template <int KPL, int JCT>
 static ssi_status jacobi_launch(double* G, int k, double* Ut, double* S, double* scratch, int32_t* status,
                                 cudaStream_t s) {

@@ -35,6 +35,8 @@ void cholqr_carve(Carver& c, int64_t m, int k, CholQRWork& w);
 // (ld m). When the first Cholesky breaks down (Y numerically rank-deficient) it is redone with a
 // diagonal shift and one extra CholeskyQR pass runs (shifted CholeskyQR3), decided on the device;
 // the returned factors then include that pass.
+ssi_status cholqr1(const double* Y, int64_t ldy, int64_t m, int k, double* Q, CholQRWork& w,
+                   int32_t* status, cudaStream_t s);
 ssi_status cholqr2(const double* Y, int64_t ldy, int64_t m, int k, double* Q, CholQRWork& w,
                    int32_t* status, cudaStream_t s);
 
