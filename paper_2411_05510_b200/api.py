@@ -84,10 +84,15 @@ def cov_spectral_plan(N, l, lag_hi, lag_lo=1):
 
 def cov_spectral_flops(N, l, lag_hi, lag_lo=1):
     """Algorithmic flops of SSI_COV_SPECTRAL: (cross-spectral product -- three real products per
-    complex one, 6 lp^2 S (F/2+1) -- and the inverse transform)."""
+    complex one, 6 lp^2 S (F/2+1) -- and the inverse transform: for F = 1024 one complex FFT per
+    two elements, 5 F log2 F lp^2 / 2; otherwise the GEMM 2 lp^2 n_lags (F + 2))."""
     F, S = cov_spectral_plan(N, l, lag_hi, lag_lo)
     lp = l + (l & 1)
-    return 6.0 * lp * lp * S * (F // 2 + 1), 2.0 * lp * lp * (lag_hi - lag_lo + 1) * (F + 2)
+    if F == 1024 and lag_hi < F:
+        inv = 5.0 * F * 10 * lp * lp / 2
+    else:
+        inv = 2.0 * lp * lp * (lag_hi - lag_lo + 1) * (F + 2)
+    return 6.0 * lp * lp * S * (F // 2 + 1), inv
 
 
 def covariances(Y: torch.Tensor, lag_hi: int, lag_lo: int = 1, mode: str = "fp64",

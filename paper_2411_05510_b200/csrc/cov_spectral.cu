@@ -402,6 +402,100 @@ __global__ void __launch_bounds__(kFftThreads, SEGS == 1 ? 3 : SSI_FFT_MINB) spe
   }
 }
 
+// ---------------------------------------------------------------- inverse transform, F = 1024
+// R_k(e) = (1/den_k) Re sum_{f=0}^{F-1} G^_f(e) e^{+2 pi i f k / F}, G^ the hermitian extension of
+// the half spectrum G_0..G_{F/2} (Im G_0 and Im G_{F/2} taken as 0, the weights 1 / 2 / 1 of the
+// GEMM form), den_k = F (N - k) or F: the same sum as the GEMM R = G W, evaluated by an FFT
+// (5 F log2 F / 2 flop per element pair instead of 2 (F + 2) n_lags). Two real outputs per
+// complex transform: z_f = G^_f(e1) + i G^_f(e2) gives x(e1) + i x(e2); the inverse is the
+// forward transform of conj(z), conjugated. One CTA: 4 transforms = 8 consecutive elements e
+// (= (b, a) at b + a lp) of every frequency; the three in-register DIF passes of the forward
+// kernel, and only the groups holding the wanted lags are finished (radix 4) and written.
+#ifndef SSI_SPEC_IFFT
+#define SSI_SPEC_IFFT 1   // 0: the inverse as the GEMM R = G W for every F (A/B)
+#endif
+struct IfftArgs {
+  const double* G;     // [F/2+1][2][lp2]
+  int64_t lp2;
+  int lag_lo, n_lags;
+  int64_t N;
+  int normalize;
+  const double2* tw;
+  double* R;           // R[(k - lag_lo) lp2 + e]
+};
+
+__global__ void __launch_bounds__(kFftThreads, 2) spec_ifft1024_kernel(IfftArgs g) {
+  constexpr int CH = 4;
+  extern __shared__ __align__(16) double2 z[];     // [CH][kFP]
+  const int tid = threadIdx.x;
+  const int64_t e0 = int64_t(blockIdx.x) * (2 * CH);
+  // ---- conj(z_f) for f = 0..F-1 from G_f (f <= F/2) and its hermitian extension
+  {
+    constexpr int NF = kF / 2 + 1;
+    const int c = tid & 3;
+    const int64_t e = e0 + 2 * c;
+    const bool ok = e < g.lp2;                     // lp2 even: e + 1 < lp2 too
+    double2* zc = z + c * kFP;
+#pragma unroll 3
+    for (int f = tid >> 2; f < NF; f += kFftThreads / 4) {
+      double2 re = make_double2(0.0, 0.0), im = make_double2(0.0, 0.0);   // (a1, a2), (b1, b2)
+      if (ok) {
+        const double* src = g.G + int64_t(f) * 2 * g.lp2 + e;
+        re = __ldcs(reinterpret_cast<const double2*>(src));
+        im = __ldcs(reinterpret_cast<const double2*>(src + g.lp2));
+      }
+      if (f == 0 || f == kF / 2) im = make_double2(0.0, 0.0);
+      // z_f = (a1 - b2) + i (b1 + a2);  z_{F-f} = (a1 + b2) + i (a2 - b1)
+      zc[pad16(f)] = make_double2(re.x - im.y, -(im.x + re.y));
+      if (f != 0 && f != kF / 2) zc[pad16(kF - f)] = make_double2(re.x + im.y, -(re.y - im.x));
+    }
+  }
+  __syncthreads();
+  const int c = tid >> 6, b = tid & 63;
+  double2* zc = z + c * kFP;
+  // ---- pass 1: radix 16 over L = 1024 (q = 64), butterfly n = b
+  {
+    const double2 w1 = __ldg(&g.tw[b]), w4 = __ldg(&g.tw[4 * b]);
+    double2 x[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) x[m] = zc[pad16(b + 64 * m)];
+    dft_dif<16>(x);
+    store_twiddled(zc, b, 64, x, w1, w4);
+  }
+  __syncthreads();
+  // ---- pass 2: radix 16 over L = 64 (q = 4): block b >> 2, n = b & 3
+  {
+    const int n = b & 3, base = (b >> 2) * 64 + n;
+    const double2 w1 = __ldg(&g.tw[16 * n]), w4 = __ldg(&g.tw[64 * n]);
+    double2 x[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) x[m] = zc[pad16(base + 4 * m)];
+    dft_dif<16>(x);
+    store_twiddled(zc, base, 4, x, w1, w4);
+  }
+  __syncthreads();
+  // ---- pass 3 (radix 4) only for the wanted lags: lag k = d0 + 16 d1 + 256 r is output r of the
+  // group at d0 * 64 + d1 * 4; y_r = sum_m x_m w_4^{rm}; x(e1) = Re y, x(e2) = -Im y
+  for (int it = tid; it < g.n_lags * CH; it += kFftThreads) {
+    const int cq = it & 3, kk = it >> 2;
+    const int k = g.lag_lo + kk;
+    const int64_t e = e0 + 2 * cq;
+    if (e >= g.lp2) continue;
+    const int d0 = k & 15, d1 = (k >> 4) & 15, r = (k >> 8) & 3;
+    const double2* zq = z + cq * kFP;
+    const int base = d0 * 64 + d1 * 4;
+    const double2 x0 = zq[pad16(base)], x1 = zq[pad16(base + 1)], x2 = zq[pad16(base + 2)],
+                  x3 = zq[pad16(base + 3)];
+    double2 y;
+    if (r == 0) y = make_double2((x0.x + x2.x) + (x1.x + x3.x), (x0.y + x2.y) + (x1.y + x3.y));
+    else if (r == 2) y = make_double2((x0.x + x2.x) - (x1.x + x3.x), (x0.y + x2.y) - (x1.y + x3.y));
+    else if (r == 1) y = make_double2((x0.x - x2.x) + (x1.y - x3.y), (x0.y - x2.y) - (x1.x - x3.x));   // -i x1, +i x3
+    else y = make_double2((x0.x - x2.x) - (x1.y - x3.y), (x0.y - x2.y) + (x1.x - x3.x));
+    const double den = double(kF) * (g.normalize ? double(g.N - k) : 1.0);   // as spec_tables_kernel
+    __stcs(reinterpret_cast<double2*>(g.R + int64_t(kk) * g.lp2 + e), make_double2(y.x / den, -y.y / den));
+  }
+}
+
 // R[lag][a][b] (l x l blocks) <- Rp[lag][a][b] (lp x lp blocks) for odd l
 __global__ void spec_compact_kernel(const double* __restrict__ Rp, int l, int lp, int n_lags, double* __restrict__ R) {
   const int64_t total = int64_t(n_lags) * l * l;
@@ -516,7 +610,13 @@ ssi_status cov_spectral(const void* Y, int dtype, int64_t N, int l, int64_t ldY,
   // R (lp^2 x n_lags) = G (lp^2 x (F+2), col-major, ld lp^2) * W ((F+2) x n_lags)
   if (!(phases & 4)) return SSI_OK;
   double* Rout = b.Rp ? b.Rp : R;
-  for (int c0 = 0; c0 < p.n_lags; c0 += kTallMaxN) {
+  if (SSI_SPEC_IFFT && p.F == kF && lag_hi < kF) {
+    const size_t smem = size_t(4) * kFP * sizeof(double2);
+    cudaFuncSetAttribute(spec_ifft1024_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    const IfftArgs ia{b.G, lp2, lag_lo, p.n_lags, N, normalize, b.tw, Rout};
+    spec_ifft1024_kernel<<<unsigned((lp2 + 7) / 8), kFftThreads, smem, s>>>(ia);
+    SSI_TRY(launch_check("spec_ifft1024_kernel"));
+  } else for (int c0 = 0; c0 < p.n_lags; c0 += kTallMaxN) {
     const int nc = p.n_lags - c0 < kTallMaxN ? p.n_lags - c0 : kTallMaxN;
     SSI_TRY(gemm_tall(lp2, nc, p.F + 2, false, b.G, lp2, b.W + int64_t(c0) * (p.F + 2), p.F + 2,
                       Rout + int64_t(c0) * lp2, lp2, b.partial, s));

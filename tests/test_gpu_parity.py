@@ -159,6 +159,24 @@ def test_covariance_spectral_edge_cases(ssi):
     assert _rel_scale(R, oracle.covariances(Ywide[:, :9], 11)) <= 1e-12
 
 
+def test_covariance_spectral_inverse_fft(ssi):
+    """The F = 1024 inverse transform (spec_ifft1024_kernel): odd channel counts (padding channel,
+    a partial last CTA of 8 elements), lag_lo > 1, and lags in every radix-4 output quarter
+    (k >= 256, 512, 768), against the oracle's direct sums; normalised and raw sums."""
+    api, _ = ssi
+    rng = np.random.default_rng(35)
+    for (N, l, lo, hi) in ((200000, 9, 3, 300), (100000, 6, 1, 600), (50000, 3, 1, 850),
+                           (30000, 2, 1, 800), (200000, 11, 1, 119)):
+        assert api.cov_spectral_plan(N, l, hi, lo)[0] == 1024, (N, l, lo, hi)
+        Y = rng.standard_normal((N, l)).astype(np.float32)
+        R = api.covariances(_dev(Y), hi, lo, mode="spectral", check=True).cpu().numpy()
+        Ro = oracle.covariances(Y, hi, lo)
+        assert _rel_scale(R, Ro) <= 1e-12, (N, l, lo, hi)
+        S = api.covariances(_dev(Y), hi, lo, mode="spectral", normalize=False).cpu().numpy()
+        So = oracle.covariance_partial_sums(Y, lo, hi)
+        assert np.max(np.abs(S - So)) <= 1e-12 * np.max(np.abs(So)), (N, l, lo, hi)
+
+
 def test_covariance_spectral_long_record_chunks(ssi):
     """A record long enough that its segments are processed in several chunks (the product
     accumulates over chunks in a fixed order), against the oracle."""
