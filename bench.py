@@ -608,7 +608,7 @@ def main():
         prod_ms = float(np.median(pt))
         f_main, f_inv = api.cov_spectral_flops(cfg.N, cfg.l, 2 * cfg.i - 1)
         F, S_ = api.cov_spectral_plan(cfg.N, cfg.l, 2 * cfg.i - 1)
-        stage_cov = {"stage_ms": iso_ms, "plan": {"F": F, "S": S_}, "stage_dmma_flop": f_main + f_inv,
+        stage_cov = {"stage_ms": iso_ms, "plan": {"F": F, "S": S_}, "stage_flop": f_main + f_inv,
                      "stage_tflops": (f_main + f_inv) / (iso_ms / 1e3) / 1e12,
                      "stage_frac": (f_main + f_inv) / (iso_ms / 1e3) / 1e12 / dgemm,
                      "direct_sum_flop_equiv": cov_flops(cfg)}
@@ -658,6 +658,19 @@ def main():
         roof["sm_time_share"] = {"source": sm.get("source", "profiles/smtime_spectral_latest.json"),
                                  "top_kernels": {k.split("(")[0].replace("ssi::<unnamed>::", ""):
                                                  round(v["share_sm_time"], 4) for k, v in top}}
+        # the RSVD's tensor-core kernels (every gemm_tall launch of a record: the block-DFT passes
+        # of A4/A6/A7, the CholeskyQR Gram and Y L^-T products, the modal sweep's CholeskyQR2 of
+        # U^up) by their SM-time: algorithmic flops / GPU-ms equivalent against the DGEMM peak
+        if rf is not None:
+            l_, i_, k_, nm_, m_, q_ = cfg.l, cfg.i, cfg.k, cfg.n_max, cfg.m, cfg.q
+            g_flop = (rf["A4_A6_A7"] + (2 * q_ + 4) * 2.0 * m_ * k_ * k_ + 2 * 2.0 * (m_ - l_) * nm_ * nm_)
+            g_ms = sum(v["gpu_ms_equiv"] for kname, v in sm["kernels"].items() if "gemm_tall_kernel" in kname)
+            if g_ms > 0:
+                ach = g_flop / (g_ms / 1e3) / 1e12
+                roof["rsvd_tensor_kernels"] = {
+                    "kernels": "gemm_tall_kernel (all launches of one record)", "algorithmic_flop": g_flop,
+                    "gpu_ms_equiv": g_ms, "achieved": ach, "peak": dgemm, "unit": "TFLOP/s",
+                    "frac": ach / dgemm, "note": "rate while resident (SM-time from the committed ncu pass)"}
         # the kernel with the largest SM-time share: the per-order Francis QR (A10), one CTA per
         # order, a latency-bound bulge chase; its algorithmic flops (~10 n^3 per order, LAPACK's
         # count for the eigenvalues) over its SM-time, against the FP64 ALU peak

@@ -357,33 +357,13 @@ def gather_tables(local: dict, assignment, make_empty, rank: int, world: int, gr
     return out
 
 
-def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank: int = 0, world: int = 1,
-                 group=None, n_streams: int = 8, timing: dict | None = None):
-    """3D stabilization diagram (PAPER.md:278-291, steps i-ii) for the time-lag steps `lags`:
-    covariances once up to lag 2 max(i) - 1 (time-sharded over ranks + one all-reduce),
-    Toeplitz + RSVD + modal sweep per lag (lags assigned by LPT; on a rank the lags are
-    independent and run on `n_streams` CUDA streams, largest first, each stream with its own
-    workspaces), all tables gathered, ssi_stab3d over the lag axis.
-    timing: optional dict that receives CUDA events recorded on the current stream at the phase
-    boundaries ("start", "cov" = covariances + all-reduce + normalisation, "lags", "gather",
-    "stab").
-    Returns ({i: PoleTable}, flags, stable_count)."""
-    lags = sorted(lags)
-    lag_hi = 2 * lags[-1] - 1
-    dev = Y.device
-
-    def mark(name):
-        if timing is not None:
-            ev = torch.cuda.Event(enable_timing=True)
-            ev.record(torch.cuda.current_stream(dev))
-            timing[name] = ev
-
-    mark("start")
-    ws_c = api._workspace(api.covariances_ws_bytes(Y.shape[0], P.l, lag_hi, 1, P.cov_mode), dev)
-    R = sharded_covariances(Y, lag_hi, rank, world, P.cov_mode, group, ws=ws_c)
-    mark("cov")
-    assign = lpt_assign(lags, world)
-    mine = sorted(assign[rank], reverse=True)            # largest lags first (longest chains)
+def run_lags(R: torch.Tensor, P: SweepParams, mine, n_streams: int = 8):
+    """Toeplitz + RSVD + modal sweep for the time-lag steps `mine` from covariances R (lags
+    independent: n_streams high-priority CUDA streams, largest lag first, each stream with its
+    own workspaces). The streams are returned; the caller joins them. Returns (tables by lag,
+    per-stream workspaces, streams)."""
+    dev = R.device
+    mine = sorted(mine, reverse=True)                    # largest lags first (longest chains)
     ns = min(n_streams, len(mine))                       # 0 when this rank got no lag
     cur = torch.cuda.current_stream(dev)
     lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
@@ -416,6 +396,37 @@ def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank
                 T = api.toeplitz(R, i, out=tb[:m * m].view(m, m))
                 U, S = api.rsvd(T, P.k_for(i), P.q, P.seed, i, P.n_max, ws=ws_r)
             local[i] = api.modal_sweep(U, S, P.l, i, P.n_min, P.n_max, P.n_step, P.dt, ws=ws_m)
+    return local, slots, streams
+
+
+def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank: int = 0, world: int = 1,
+                 group=None, n_streams: int = 8, timing: dict | None = None):
+    """3D stabilization diagram (PAPER.md:278-291, steps i-ii) for the time-lag steps `lags`:
+    covariances once up to lag 2 max(i) - 1 (time-sharded over ranks + one all-reduce),
+    Toeplitz + RSVD + modal sweep per lag (lags assigned by LPT; on a rank the lags are
+    independent and run on `n_streams` CUDA streams, largest first, each stream with its own
+    workspaces), all tables gathered, ssi_stab3d over the lag axis.
+    timing: optional dict that receives CUDA events recorded on the current stream at the phase
+    boundaries ("start", "cov" = covariances + all-reduce + normalisation, "lags", "gather",
+    "stab").
+    Returns ({i: PoleTable}, flags, stable_count)."""
+    lags = sorted(lags)
+    lag_hi = 2 * lags[-1] - 1
+    dev = Y.device
+
+    def mark(name):
+        if timing is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(torch.cuda.current_stream(dev))
+            timing[name] = ev
+
+    mark("start")
+    ws_c = api._workspace(api.covariances_ws_bytes(Y.shape[0], P.l, lag_hi, 1, P.cov_mode), dev)
+    R = sharded_covariances(Y, lag_hi, rank, world, P.cov_mode, group, ws=ws_c)
+    mark("cov")
+    assign = lpt_assign(lags, world)
+    local, slots, streams = run_lags(R, P, assign[rank], n_streams)
+    cur = torch.cuda.current_stream(dev)
     for st in streams:
         cur.wait_stream(st)
     mark("lags")
