@@ -34,24 +34,37 @@ def rank_work(W, r):
     e[0].record(cur)
     api.covariances(Yd, lag_hi, 1, P.cov_mode, t_begin=tb, t_end=te, normalize=False, out=Rraw, ws=ws_c)
     e[1].record(cur)
+    keep = None
     if mine:
-        _, _, streams = drivers.run_lags(R, P, mine, 8)
-        for st in streams:
+        keep = drivers.run_lags(R, P, mine, 8)
+        for st in keep[2]:
             cur.wait_stream(st)
     e[2].record(cur)
     torch.cuda.synchronize()
+    del keep                                             # workspaces freed after the streams finished
     return e[0].elapsed_time(e[1]), e[1].elapsed_time(e[2]), mine
 
 
-rank_work(1, 0)                                          # warm-up (workspaces, first launches)
+for _ in range(2):
+    rank_work(1, 0)                                      # warm-up (workspaces, first launches)
+# the whole single-GPU sweep through the product driver, for comparison with rank_work(1, 0)
+crit = api.CRITERIA_BRIDGE_3D
+full = []
+for _ in range(3):
+    tm = {}
+    drivers.lag_sweep_3d(Yd, P, LAGS, crit, timing=tm)
+    torch.cuda.synchronize()
+    full.append(tm["start"].elapsed_time(tm["stab"]))
+print("lag_sweep_3d (1 GPU):", [round(x, 1) for x in full])
 out = {"how": __doc__.split("\n    python")[0], "workload": "c4: c3 record, i = 20..80 step 4 (16 lags)",
-       "table_bytes": None, "by_world": {}}
+       "table_bytes": None, "by_world": {}, "lag_sweep_3d_1gpu_ms": full}
 tab_bytes = sum(t.numel() * t.element_size() for t in api.PoleTable.empty(P.n_min, P.n_max, P.n_step, P.l, "cuda").tensors())
 out["table_bytes"] = tab_bytes
 for W in (1, 2, 4, 8):
     ranks = []
     for r in range(W):
         reps = [rank_work(W, r) for _ in range(3)]
+        print(W, r, [round(x[0] + x[1], 1) for x in reps])
         cov = float(np.median([x[0] for x in reps]))
         lag = float(np.median([x[1] for x in reps]))
         ranks.append({"rank": r, "lags": reps[0][2], "cov_shard_ms": cov, "lags_ms": lag, "total_ms": cov + lag})
