@@ -32,10 +32,16 @@ __device__ __forceinline__ int tri(int r) { return r * (r + 1) / 2; }
 // One warp, register-resident right-looking Cholesky of the 32 x 32 diagonal block at (j0, j0)
 // of the packed P (lane i holds row i; every index is a compile-time constant, so the row stays
 // in registers): per column one shuffle of the pivot, an inline rsqrt, and the rank-1 update
-// with the column entries broadcast lane to lane.
+// with the scaled column broadcast through a 2 x 32 shared-memory buffer `cb` (one store per
+// lane, broadcast loads: a single warp issues a shuffle only every ~15 cycles, and the 496
+// shuffled column entries made this 3x slower). The two halves of cb alternate by column, so a
+// lane's store of column j + 2 cannot overtake another lane's loads of column j.
 // Breakdown test: pivot j must exceed thr_j = tau * (diagonal of the Gram matrix at row j), lane j
 // holding thr_j; a smaller pivot means column j is numerically in the span of the previous ones.
-__device__ __noinline__ void chol32(double* P, int j0, int lane, double thr, int& bad) {
+#ifndef SSI_CHOL32_SHFL
+#define SSI_CHOL32_SHFL 0   // 1: the column broadcast by shuffles (round 1; A/B)
+#endif
+__device__ __noinline__ void chol32(double* P, int j0, int lane, double thr, int& bad, double* cb) {
   double* Li = P + tri(j0 + lane) + j0;
   double a[CB];
 #pragma unroll
@@ -47,9 +53,14 @@ __device__ __noinline__ void chol32(double* P, int j0, int lane, double thr, int
     if (!(d > tj) || !isfinite(d)) { bad = 1; d = 1.0; }
     const double r = fast_rsqrt(d);
     a[j] = (lane == j) ? d * r : a[j] * r;          // lanes < j hold 0 in a[j]
+    double* col = cb + (j & 1) * CB;
+    if (!SSI_CHOL32_SHFL) {
+      col[lane] = a[j];
+      __syncwarp();
+    }
 #pragma unroll
     for (int c = j + 1; c < CB; ++c) {
-      const double lcj = __shfl_sync(FULLM, a[j], c);
+      const double lcj = SSI_CHOL32_SHFL ? __shfl_sync(FULLM, a[j], c) : col[c];
       if (lane >= c) a[c] = fma(-a[j], lcj, a[c]);
     }
   }
@@ -138,7 +149,7 @@ __global__ void __launch_bounds__(kCholBlkThreads, 1) chol_blk_kernel(const doub
     if (warp == 0) {
       int bad = 0;
       const int r = j0 + lane;
-      chol32(P, j0, lane, tau * (r < k ? W[r + int64_t(r) * k] + sh : 1.0), bad);
+      chol32(P, j0, lane, tau * (r < k ? W[r + int64_t(r) * k] + sh : 1.0), bad, Xd);   // Xd: column buffer
       if (bad && lane == 0) fail = 1;
       inv32(P, j0, Xd, lane);
       // keep L_JJ^{-1} for the inverse phase (L2-resident scratch; saves recomputing it)
