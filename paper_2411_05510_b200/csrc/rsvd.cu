@@ -135,7 +135,10 @@ ssi_status rsvd_bt_run(const double* R, int l, int i, int k, int q, uint64_t see
   rsvd_bt_carve(c, l, i, k, w);
   const int64_t m = int64_t(l) * i;
   // spectrum of the block sequence B_d = R_{i+d}, once per call
-  SSI_TRY(bt_spectrum(R, l, i, w.Bb, w.tables, s));
+  // the spectrum GEMM's l^2 x 2i output lives in Xh when it fits (Xh is first written by the
+  // first pass, after the spectrum is formed)
+  const bool zfit = bt_freq_elems(l, i, k) >= size_t(l) * l * 2 * i;
+  SSI_TRY(bt_spectrum(R, l, i, w.Bb, w.tables, s, zfit ? w.Xh : nullptr));
   auto pass = [&](bool trans, const double* X, double* out) -> ssi_status {
     return bt_apply(w.Bb, w.tables, l, i, k, trans, X, m, out, m, w.Xh, w.Yh, s);
   };

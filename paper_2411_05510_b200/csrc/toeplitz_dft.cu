@@ -15,6 +15,10 @@
 #include "gemm_f64.cuh"
 #include "toeplitz_dft.cuh"
 
+#ifndef SSI_BT_SPEC_GEMM
+#define SSI_BT_SPEC_GEMM 1   // 0: the direct-sum spectrum kernel for every shape (A/B)
+#endif
+
 namespace ssi {
 namespace {
 
@@ -166,17 +170,63 @@ __global__ void bt_tables_kernel(int i, int ldF, double* __restrict__ Ft, double
   }
 }
 
+// Spectrum as a GEMM (l even, k >= l): Z (l^2 x 2F, col-major) = R (l^2 x P) Wb (P x 2F),
+// Wb[dd][2f] = cos(2 pi t / P), Wb[dd][2f + 1] = -sin(2 pi t / P), t = f (dd - (i - 1)) mod P
+// (dd = d + i - 1 indexes R_{i+d}); ld P + 1 with a zero pad row (16-byte k pairs).
+__global__ void bt_wspec_kernel(int i, double* __restrict__ Wb) {
+  const int P = 2 * i - 1, F = i, ld = P + 1;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ld * 2 * F; e += gridDim.x * blockDim.x) {
+    const int dd = e % ld, kk = e / ld, f = kk >> 1;
+    double v = 0.0;
+    if (dd < P) {
+      const int t = int((int64_t(f) * (dd - (i - 1) + P)) % P);
+      double sn, cs;
+      sincospi(2.0 * double(t) / double(P), &sn, &cs);
+      v = (kk & 1) ? -sn : cs;
+    }
+    Wb[e] = v;
+  }
+}
+
+// Z (l^2 x 2F) -> the real 2l x 2l block form of bt_spectrum_kernel
+__global__ void bt_scatter_kernel(const double* __restrict__ Z, int l, int F, double* __restrict__ Bb) {
+  const int64_t ll = int64_t(l) * l, L2 = 2 * int64_t(l);
+  for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < ll * F; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t e = q % ll, f = q / ll;
+    const int a = int(e / l), b = int(e % l);
+    const double re = Z[e + 2 * f * ll], im = Z[e + (2 * f + 1) * ll];
+    double* blk = Bb + f * L2 * L2;
+    blk[int64_t(a) * L2 + b] = re;
+    blk[int64_t(l + a) * L2 + (l + b)] = re;
+    blk[int64_t(l + a) * L2 + b] = im;
+    blk[int64_t(a) * L2 + (l + b)] = -im;
+  }
+}
+
 }  // namespace
 
 size_t bt_spectrum_elems(int l, int i) { return size_t(i) * 4 * size_t(l) * l; }
 int bt_ldF(int i) { return (i + 1) & ~1; }
-size_t bt_table_elems(int i) { return size_t(bt_ldF(i)) * 2 * i + size_t(2 * i) * i; }
+size_t bt_table_elems(int i) { return size_t(bt_ldF(i)) * 2 * i + size_t(2 * i) * i + size_t(2 * i) * (2 * i); }
 size_t bt_freq_elems(int l, int i, int k) { return size_t(i) * 2 * size_t(l) * k; }
 
-ssi_status bt_spectrum(const double* R, int l, int i, double* Bb, double* tables, cudaStream_t s) {
+ssi_status bt_spectrum(const double* R, int l, int i, double* Bb, double* tables, cudaStream_t s, double* Z) {
   bt_tables_kernel<<<unsigned((i * i + 255) / 256), 256, 0, s>>>(i, bt_ldF(i), tables,
                                                               tables + size_t(bt_ldF(i)) * 2 * i);
   SSI_TRY(launch_check("bt_tables_kernel"));
+  if (SSI_BT_SPEC_GEMM && Z && l % 2 == 0 && 2 * i <= kTallMaxN && (reinterpret_cast<uintptr_t>(R) & 15) == 0) {
+    // Z (l^2 x 2F) = R (l^2 x P) Wb (P x 2F) on the DMMA pipe, then the block form
+    double* Wb = tables + size_t(bt_ldF(i)) * 2 * i + size_t(2 * i) * i;
+    const int P = 2 * i - 1, F = i;
+    const int64_t ll = int64_t(l) * l;
+    bt_wspec_kernel<<<unsigned((2 * i * 2 * i + 255) / 256), 256, 0, s>>>(i, Wb);
+    SSI_TRY(launch_check("bt_wspec_kernel"));
+    SSI_TRY(gemm_tall_batched(ll, 2 * F, P, false, R, ll, 0, Wb, P + 1, 0, Z, ll, 0, 1, s));
+    int blocks = int((ll * F + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    bt_scatter_kernel<<<blocks, 256, 0, s>>>(Z, l, F, Bb);
+    return launch_check("bt_scatter_kernel");
+  }
   const int P = 2 * i - 1;
   const size_t smem = smem_twiddle(i) + sizeof(double) * size_t(P) * 32;
   if (smem > 48 * 1024)
