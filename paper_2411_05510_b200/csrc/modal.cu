@@ -1220,7 +1220,11 @@ static void modal_carve(Carver& c, int l, int i, int n_min, int n_max, int n_ste
   w.C = c.take<double>(size_t(lin) * l);
   w.Qup = c.take<double>(size_t(mu) * n_max);
   w.band = modal_band_global(n_max) ? c.take<double>(size_t(no) * band_elems(n_max)) : nullptr;
-  w.partial = c.take<double>(gemm_partial_elems(n_max, n_max, gemm_pick_splits(n_max, n_max, mu)) + 1);
+  {
+    const size_t pg = gemm_partial_elems(n_max, n_max, gemm_pick_splits(n_max, n_max, mu));
+    const size_t pt = n_max <= kTallMaxN ? gemm_tall_partial_elems(n_max, n_max, mu) : 0;
+    w.partial = c.take<double>((pg > pt ? pg : pt) + 1);
+  }
   cholqr_carve(c, mu, n_max, w.cq);
 }
 
@@ -1244,9 +1248,15 @@ ssi_status modal_run(const double* U, int64_t ldU, const double* S, int l, int i
   SSI_TRY(gemm_f64(n_max, n_max, n_max, 1.0, Operand{w.cq.Linv1, n_max, 1},
                    Operand{w.cq.Linv2, n_max, 1}, w.Rinv, n_max, 1, nullptr, st));
   // W = Q^T U^down, U^down = U[l:m, :n_max]
-  const int splits = gemm_pick_splits(n_max, n_max, mu);
-  SSI_TRY(gemm_f64(n_max, n_max, mu, 1.0, Operand{w.Qup, mu, 1}, Operand{U + l, 1, ldU}, w.W,
-                   n_max, splits, w.partial, st));
+  // (tall-skinny DMMA kernel, split-K, when the shapes allow its 16-byte pieces)
+  if (n_max <= kTallMaxN && mu % 2 == 0 && l % 2 == 0 && ldU % 2 == 0 &&
+      (reinterpret_cast<uintptr_t>(U) & 15) == 0 && (reinterpret_cast<uintptr_t>(w.Qup) & 15) == 0) {
+    SSI_TRY(gemm_tall(n_max, n_max, mu, true, w.Qup, mu, U + l, ldU, w.W, n_max, w.partial, st));
+  } else {
+    const int splits = gemm_pick_splits(n_max, n_max, mu);
+    SSI_TRY(gemm_f64(n_max, n_max, mu, 1.0, Operand{w.Qup, mu, 1}, Operand{U + l, 1, ldU}, w.W,
+                     n_max, splits, w.partial, st));
+  }
   // M_n = Rinv[:n,:n] W[:n,:n] for every order
   SSI_TRY(gemm_f64_orders(no, n_min, n_step, w.Rinv, n_max, w.W, n_max, w.M, st));
   EigArgs g{w.M, w.C, U, ldU, S, l, n_min, n_step, no, n_max, tab.cap, dt, tab,

@@ -71,8 +71,14 @@ static ssi_status rsvd_core(Pass&& pass, int64_t m, int k, int q, uint64_t seed,
                    nullptr, s));
   SSI_TRY(jacobi_svd(w.G, k, w.Ut, w.Sk, w.jac, status, s));
   // line 6: U = Q U~ (Eq. 18), leading n_keep columns
-  SSI_TRY(gemm_f64(m, n_keep, k, 1.0, Operand{w.Q, 1, m}, Operand{w.Ut, 1, k}, U, ldU, 1,
-                   nullptr, s));
+  if (n_keep <= kTallMaxN && m % 2 == 0 && k % 2 == 0 && ldU % 2 == 0 &&
+      (reinterpret_cast<uintptr_t>(U) & 15) == 0) {
+    // tall-skinny DMMA kernel, one M tile per CTA (no split-K)
+    SSI_TRY(gemm_tall_batched(m, n_keep, k, false, w.Q, m, 0, w.Ut, k, 0, U, ldU, 0, 1, s));
+  } else {
+    SSI_TRY(gemm_f64(m, n_keep, k, 1.0, Operand{w.Q, 1, m}, Operand{w.Ut, 1, k}, U, ldU, 1,
+                     nullptr, s));
+  }
   if (cudaMemcpyAsync(S, w.Sk, sizeof(double) * k, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
     return launch_check("rsvd S copy");
   return SSI_OK;
