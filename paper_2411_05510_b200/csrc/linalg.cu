@@ -12,6 +12,9 @@ namespace {
 constexpr int kJacThreads = 512;
 constexpr int JC = 8;                // Jacobi cluster size (CTAs); 16 (non-portable) for k > 256
 constexpr int kJacMaxSweeps = 60;
+#ifndef SSI_JAC_RING
+#define SSI_JAC_RING 1   // 0: columns re-read from L2 every round, cluster barrier per round (A/B)
+#endif
 
 
 // Blocked variant (k <= 224): 32-wide block columns; the diagonal block is factored and
@@ -426,6 +429,270 @@ __global__ void __launch_bounds__(kJacThreads, 1) jacobi_kernel(double* __restri
   }
 }
 
+// Ring variant of jacobi_kernel (k <= 256): the same pairs, rounds, rotation formulas and
+// convergence test — bit-identical results — but the columns stay in the registers of the warp
+// that owns their pair: warp g owns positions g (top) and n-1-g (bottom) of the round-robin
+// ordering, and between rounds the positions shift by one (new[p] = old[p+1] for p in [1, n-2],
+// new[n-1] = old[1], position 0 fixed), so every warp sends its top column to warp g-1 (warp 1:
+// to warp 0's bottom) and its bottom column to warp g+1 (the middle warp: to its own top)
+// through a double-buffered mailbox in the receiving CTA's shared memory (DSMEM stores and a
+// remote mbarrier arrive with release semantics at cluster scope). A round costs one dot
+// product, the rotation and two 32-lane DSMEM hand-offs instead of two L2 column reads, two
+// writes and a cluster barrier (k = 220: 10.5M -> 7.7M cycles; st.async with complete_tx per
+// 16-byte piece measured 16.8M, one release-arrive per warp after a warp sync 12.8M). A mailbox buffer is rewritten only after its reader has
+// consumed it: the writer of round t has received the reader's own round t-1 output (the two
+// neighbours exchange in both directions). Column norms travel with their columns.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t map_rank(uint32_t a, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster2(uint32_t a, double v0, double v1) {
+  asm volatile("st.shared::cluster.v2.f64 [%0], {%1, %2};" ::"r"(a), "d"(v0), "d"(v1) : "memory");
+}
+__device__ __forceinline__ void st_cluster1(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t a) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
+// st.async: store to a CTA of the cluster and signal its mbarrier with the bytes (complete_tx)
+__device__ __forceinline__ void st_async2(uint32_t a, double v0, double v1, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               ::"r"(a), "d"(v0), "d"(v1), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void st_async1(uint32_t a, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];"
+               ::"r"(a), "d"(v), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+#ifndef SSI_JAC_STASYNC
+#define SSI_JAC_STASYNC 0
+#endif
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a), "r"(parity) : "memory");
+}
+
+template <int KPL, int JCT>
+__global__ void __launch_bounds__(kJacThreads, 1) jacobi_ring_kernel(double* __restrict__ G, int k,
+                                                                  double* __restrict__ Ut,
+                                                                  double* __restrict__ S,
+                                                                  int* __restrict__ gflag,
+                                                                  int32_t* status, int profile) {
+  constexpr int NWC = kJacThreads / 32;             // warps per CTA
+  constexpr int MB = KPL * 32 + 2;                   // mailbox: column + norm (+ pad to 16 bytes)
+  static_assert(KPL % 2 == 0, "16-byte pairs");
+  extern __shared__ __align__(16) double jsm[];      // [NWC][2 slots][2 buffers][MB]
+  __shared__ __align__(8) uint64_t mbar[NWC][2][2];
+  __shared__ int rot;
+  const int n = (k + 1) & ~1, np = n / 2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cr = int(cluster_rank());
+  const int g = cr * NWC + warp;                     // pair index
+  const bool active = g < np;
+  const double tol = sqrt(double(k)) * 1.1102230246251565e-16;
+  if (tid == 0) {
+    for (int w = 0; w < NWC; ++w)
+      for (int sl = 0; sl < 2; ++sl)
+        for (int b = 0; b < 2; ++b)
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(&mbar[w][sl][b])), "r"(SSI_JAC_STASYNC ? 1 : 32) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (cr == 0)
+    for (int i = tid; i < kJacMaxSweeps; i += blockDim.x) gflag[i] = 0;
+  cluster_sync_all();
+  // destinations of this warp's top / bottom column (pair index, slot 0 = top, 1 = bottom)
+  // and the sources of its own new columns
+  const int top_dst = g >= 2 ? g - 1 : (g == 1 ? 0 : -1), top_slot = g >= 2 ? 0 : 1;
+  const int bot_dst = g <= np - 2 ? g + 1 : -1;      // -1: the middle warp keeps it as its top
+  const bool top_in = g >= 1 && g <= np - 2;         // new top arrives in slot 0
+  const bool bot_in = (g >= 1) || (g == 0 && np >= 2);   // new bottom arrives in slot 1
+  auto mbox = [&](int pair, int slot, int buf) -> double* {
+    return jsm + ((size_t(pair % NWC) * 2 + slot) * 2 + buf) * MB;
+  };
+  double x[KPL], y[KPL];                             // top / bottom column
+  double nx = 0.0, ny = 0.0;
+  const int ct0 = g, cb0 = n - 1 - g;                // columns at round 0
+  if (active) {
+#pragma unroll
+    for (int u = 0; u < KPL; ++u) {
+      const int r = lane + 32 * u;
+      x[u] = (r < k && ct0 < k) ? __ldcg(G + int64_t(ct0) * k + r) : 0.0;
+      y[u] = (r < k && cb0 < k) ? __ldcg(G + int64_t(cb0) * k + r) : 0.0;
+    }
+  }
+  bool converged = false;
+  int sweeps = 0;
+  long long t = 0;                                   // global round counter (mailbox phases)
+  const long long c0 = clock64();
+  for (int sweep = 0; sweep < kJacMaxSweeps && !converged; ++sweep) {
+    ++sweeps;
+    if (tid == 0) rot = 0;
+    int myrot = 0;
+    if (active) {                                    // exact norms at the start of every sweep
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int u = 0; u < KPL; ++u) {
+        const int r = lane + 32 * u;
+        if (r < k) { a += x[u] * x[u]; b += y[u] * y[u]; }
+      }
+      nx = warp_sum(a);
+      ny = warp_sum(b);
+    }
+    for (int round = 0; round < n - 1; ++round, ++t) {
+      if (!active) continue;
+      const int ct = g == 0 ? 0 : 1 + (g - 1 + round) % (n - 1);
+      const int cb = 1 + (n - 2 - g + round) % (n - 1);
+      if (np >= 2 && ct < k && cb < k) {
+        const bool sw = ct > cb;                     // x must hold column p = min(ct, cb)
+        if (sw) {
+#pragma unroll
+          for (int u = 0; u < KPL; ++u) { const double tmp = x[u]; x[u] = y[u]; y[u] = tmp; }
+        }
+        const double al = sw ? ny : nx, be = sw ? nx : ny;
+        double ga = 0.0;
+#pragma unroll
+        for (int u = 0; u < KPL; ++u) ga += x[u] * y[u];
+        ga = warp_sum(ga);
+        double na = al, nb = be;
+        if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+#pragma unroll
+          for (int u = 0; u < KPL; ++u) {
+            const int r = lane + 32 * u;
+            if (r < k) {
+              const double xp = c * x[u] - sn * y[u], yq = sn * x[u] + c * y[u];
+              x[u] = xp;
+              y[u] = yq;
+            }
+          }
+          na = al - tt * ga;
+          nb = be + tt * ga;
+          myrot = 1;
+        }
+        if (sw) {
+#pragma unroll
+          for (int u = 0; u < KPL; ++u) { const double tmp = x[u]; x[u] = y[u]; y[u] = tmp; }
+          nx = nb; ny = na;
+        } else {
+          nx = na; ny = nb;
+        }
+      }
+      if (np < 2) continue;
+      // hand-off for round t + 1 (buffer (t + 1) & 1)
+      const int buf = int((t + 1) & 1);
+      // mailbox layout: pair j = (x[2j], x[2j+1]) of lane L at 16-byte slot j * 32 + L (a warp's
+      // store covers 512 contiguous bytes; lane-major 64-byte runs measured 1.7x slower), norm last
+      if (top_dst >= 0) {
+        const uint32_t rk = uint32_t(top_dst / NWC);
+        const uint32_t dst = map_rank(smem_addr(mbox(top_dst, top_slot, buf)), rk);
+        const uint32_t bar = map_rank(smem_addr(&mbar[top_dst % NWC][top_slot][buf]), rk);
+        if (SSI_JAC_STASYNC) {
+#pragma unroll
+          for (int u = 0; u < KPL; u += 2) st_async2(dst + 16u * ((u / 2) * 32 + lane), x[u], x[u + 1], bar);
+          if (lane == 0) st_async1(dst + 8u * (KPL * 32), nx, bar);
+        } else {
+#pragma unroll
+          for (int u = 0; u < KPL; u += 2) st_cluster2(dst + 16u * ((u / 2) * 32 + lane), x[u], x[u + 1]);
+          if (lane == 0) st_cluster1(dst + 8u * (KPL * 32), nx);
+          mbar_arrive_cluster(bar);                    // every lane releases its own stores (count 32;
+        }                                            // one lane's release after a warp sync measured slower)
+      }
+      if (bot_dst >= 0) {
+        const uint32_t rk = uint32_t(bot_dst / NWC);
+        const uint32_t dst = map_rank(smem_addr(mbox(bot_dst, 1, buf)), rk);
+        const uint32_t bar = map_rank(smem_addr(&mbar[bot_dst % NWC][1][buf]), rk);
+        if (SSI_JAC_STASYNC) {
+#pragma unroll
+          for (int u = 0; u < KPL; u += 2) st_async2(dst + 16u * ((u / 2) * 32 + lane), y[u], y[u + 1], bar);
+          if (lane == 0) st_async1(dst + 8u * (KPL * 32), ny, bar);
+        } else {
+#pragma unroll
+          for (int u = 0; u < KPL; u += 2) st_cluster2(dst + 16u * ((u / 2) * 32 + lane), y[u], y[u + 1]);
+          if (lane == 0) st_cluster1(dst + 8u * (KPL * 32), ny);
+          mbar_arrive_cluster(bar);
+        }
+      } else {                                       // middle warp: bottom becomes its top
+#pragma unroll
+        for (int u = 0; u < KPL; ++u) x[u] = y[u];
+        nx = ny;
+      }
+      const uint32_t ph = uint32_t((t >> 1) & 1);       // use (t >> 1) of buffer (t + 1) & 1
+      if (top_in) {
+        const uint32_t bar = smem_addr(&mbar[warp][0][buf]);
+        if (SSI_JAC_STASYNC && lane == 0) mbar_expect_tx(bar, (KPL * 32 + 1) * 8);
+        mbar_wait_cluster(bar, ph);
+        const double2* src = reinterpret_cast<const double2*>(mbox(g, 0, buf)) + lane;
+#pragma unroll
+        for (int u = 0; u < KPL; u += 2) { const double2 v = src[(u / 2) * 32]; x[u] = v.x; x[u + 1] = v.y; }
+        nx = mbox(g, 0, buf)[KPL * 32];
+      }
+      if (bot_in) {
+        const uint32_t bar = smem_addr(&mbar[warp][1][buf]);
+        if (SSI_JAC_STASYNC && lane == 0) mbar_expect_tx(bar, (KPL * 32 + 1) * 8);
+        mbar_wait_cluster(bar, ph);
+        const double2* src = reinterpret_cast<const double2*>(mbox(g, 1, buf)) + lane;
+#pragma unroll
+        for (int u = 0; u < KPL; u += 2) { const double2 v = src[(u / 2) * 32]; y[u] = v.x; y[u + 1] = v.y; }
+        ny = mbox(g, 1, buf)[KPL * 32];
+      }
+    }
+    if (myrot && lane == 0) rot = 1;
+    __syncthreads();
+    if (tid == 0 && rot) atomicAdd(gflag + sweep, 1);
+    cluster_sync_all();
+    converged = (__ldcg(gflag + sweep) == 0);
+  }
+  // the columns are back at their round-0 positions: write them out for the final phase
+  if (active) {
+#pragma unroll
+    for (int u = 0; u < KPL; ++u) {
+      const int r = lane + 32 * u;
+      if (r < k) {
+        if (ct0 < k) __stcg(G + int64_t(ct0) * k + r, x[u]);
+        if (cb0 < k) __stcg(G + int64_t(cb0) * k + r, y[u]);
+      }
+    }
+  }
+  cluster_sync_all();
+  if (cr != 0) return;
+  if (!converged && tid == 0) set_status(status, SSI_ERR_NUMERIC);
+  if (profile && tid == 0) printf("jacobi(ring) k=%d: %d sweeps, %lld cycles\n", k, sweeps, clock64() - c0);
+  double* nrm = jsm;                                 // the mailboxes are no longer used
+  int* rank = reinterpret_cast<int*>(jsm + k);
+  const int nw = blockDim.x >> 5;
+  for (int j = warp; j < k; j += nw) {
+    double a = 0.0;
+    for (int r = lane; r < k; r += 32) { const double v = __ldcg(G + int64_t(j) * k + r); a += v * v; }
+    a = warp_sum(a);
+    if (lane == 0) nrm[j] = sqrt(a);
+  }
+  __syncthreads();
+  for (int j = tid; j < k; j += blockDim.x) {
+    int rk = 0;
+    const double v = nrm[j];
+    for (int i = 0; i < k; ++i) rk += (nrm[i] > v) || (nrm[i] == v && i < j);
+    rank[j] = rk;
+    S[rk] = v;
+  }
+  __syncthreads();
+  for (int j = warp; j < k; j += nw) {
+    const double inv = nrm[j] > 0.0 ? 1.0 / nrm[j] : 0.0;
+    const int dst = rank[j];
+    for (int r = lane; r < k; r += 32) Ut[int64_t(dst) * k + r] = __ldcg(G + int64_t(j) * k + r) * inv;
+  }
+}
+
 }  // namespace
 
 size_t cholqr_partial_elems(int64_t m, int k) {
@@ -630,6 +897,17 @@ static ssi_status jacobi_launch(double* G, int k, double* Ut, double* S, double*
   }
   double* gnrm = scratch;
   int* gflag = reinterpret_cast<int*>(scratch + k);
+  if constexpr (SSI_JAC_RING && JCT == 8 && KPL <= 8) if (k >= 3) {
+    // ring variant: mailboxes for 16 warps x 2 slots x 2 buffers per CTA
+    const size_t rsmem = size_t(kJacThreads / 32) * 4 * (KPL * 32 + 2) * sizeof(double);
+    const size_t fsmem = size_t(k) * (sizeof(double) + sizeof(int));
+    cfg.dynamicSmemBytes = rsmem > fsmem ? rsmem : fsmem;
+    cudaFuncSetAttribute(jacobi_ring_kernel<KPL, JCT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(cfg.dynamicSmemBytes));
+    if (cudaLaunchKernelEx(&cfg, jacobi_ring_kernel<KPL, JCT>, G, k, Ut, S, gflag, status, profile) != cudaSuccess)
+      return launch_check("jacobi_ring_kernel (cluster launch)");
+    return SSI_OK;
+  }
   if (cudaLaunchKernelEx(&cfg, jacobi_kernel<KPL, JCT>, G, k, Ut, S, gnrm, gflag, status, profile) != cudaSuccess)
     return launch_check("jacobi_kernel (cluster launch)");
   return SSI_OK;
