@@ -290,6 +290,23 @@ def test_rsvd_edge_cases(ssi):
     assert abs(abs(U[:, 0] @ Uo[:, 0]) - 1) < 1e-10
 
 
+def test_rsvd_small_svd_widths(ssi):
+    """The small SVD (ring Jacobi on an 8-CTA cluster, k <= 256; 16-CTA L2 variant above) at odd,
+    even and tile-edge widths: a rank-r matrix with r <= k is captured exactly, so the leading r
+    singular values equal the full SVD's and U's leading columns are orthonormal."""
+    api, _ = ssi
+    rng = np.random.default_rng(36)
+    m = 600
+    for k in (3, 5, 33, 64, 65, 127, 129, 255, 256, 257):
+        r = min(k, 24)
+        A = rng.standard_normal((m, r)) @ (rng.standard_normal((r, m)) * np.logspace(0, -3, m))
+        Sf = np.linalg.svd(A, compute_uv=False)
+        U, S, Uo, So = _rsvd_case(api, A, k, 1, 7, k, r)
+        np.testing.assert_allclose(S[:r], Sf[:r], rtol=1e-9, err_msg=f"k = {k}")
+        np.testing.assert_allclose(S[:r], So[:r], rtol=1e-9, err_msg=f"k = {k}")
+        np.testing.assert_allclose(U.T @ U, np.eye(r), atol=1e-10, err_msg=f"k = {k}")
+
+
 # ------------------------------------------------------------------ A2-A8 structured RSVD
 @pytest.mark.parametrize("name", ["c1", "c2"])
 def test_rsvd_toeplitz_matches_oracle_same_sketch(ssi, name):
