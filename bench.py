@@ -663,7 +663,9 @@ def main():
         # U^up) by their SM-time: algorithmic flops / GPU-ms equivalent against the DGEMM peak
         if rf is not None:
             l_, i_, k_, nm_, m_, q_ = cfg.l, cfg.i, cfg.k, cfg.n_max, cfg.m, cfg.q
-            g_flop = (rf["A4_A6_A7"] + (2 * q_ + 4) * 2.0 * m_ * k_ * k_ + 2 * 2.0 * (m_ - l_) * nm_ * nm_)
+            g_flop = (rf["A4_A6_A7"] + (2 * q_ + 4) * 2.0 * m_ * k_ * k_ + 2 * 2.0 * (m_ - l_) * nm_ * nm_
+                      + 2.0 * l_ * l_ * (2 * i_ - 1) * 2 * i_          # block spectrum Z = R W
+                      + 2.0 * (m_ - l_) * nm_ * nm_ + 2.0 * m_ * k_ * nm_)   # W = Q^T U_down, U = Q U~
             g_ms = sum(v["gpu_ms_equiv"] for kname, v in sm["kernels"].items() if "gemm_tall_kernel" in kname)
             if g_ms > 0:
                 ach = g_flop / (g_ms / 1e3) / 1e12
