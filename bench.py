@@ -309,7 +309,7 @@ def _max_over_ranks(x, world, dev):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor(x, dtype=torch.float64, device=dev)
+    t = torch.tensor(x, dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.tolist()
 
@@ -454,8 +454,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SSI_DIST_BACKEND=gloo: a functional run of the N-rank path with several ranks sharing the
+    # GPUs there are (no timing claim; e.g. 2 ranks on one B200); the default is NCCL, one GPU per rank
+    backend = os.environ.get("SSI_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if rank == 0:

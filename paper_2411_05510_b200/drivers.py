@@ -287,7 +287,8 @@ def sharded_covariances(Y: torch.Tensor, lag_hi: int, rank: int, world: int, mod
     N = Y.shape[0]
     tb, te = time_shards(N, world)[rank]
     S = api.covariances(Y, lag_hi, 1, mode, t_begin=tb, t_end=te, normalize=False, out=out, ws=ws)
-    allreduce_sums(S, group)
+    if world > 1:                      # world = 1 is a local call even inside a process group
+        allreduce_sums(S, group)
     return api.cov_normalize(S, N, 1)
 
 

@@ -180,6 +180,11 @@ def _world_job(rank, world, port, q):
         btabs = drivers.record_batch(recs, P, rank, world, n_streams=2)
         match, succ, _, _ = drivers.track_campaign([btabs[j] for j in range(3)], api.CRITERIA_BRIDGE_3D)
         clus = (cl.labels.cpu().numpy(), cl.f.cpu().numpy(), cl.size.cpu().numpy())
+        if world > 1 and rank == 0:
+            # a world = 1 call on one rank inside the process group (bench.py's rank-0 legs) must
+            # run no collective (the other rank never joins one): it equals the world = 1 sweep
+            solo = drivers.lag_sweep_3d(Yd, P, LAGS, api.CRITERIA_BRIDGE_3D, rank=0, world=1)[2]
+            assert torch.equal(solo.cpu(), drivers.lag_sweep_3d(Yd, P, LAGS, api.CRITERIA_BRIDGE_3D)[2].cpu())
         q.put((rank, (_host_tables(tabs), flags.cpu().numpy(), counts.cpu().numpy(), _host_tables(btabs), clus,
                       match.cpu().numpy())))
     finally:
