@@ -197,7 +197,6 @@ __global__ void shift_kernel(const double* __restrict__ W0, int k, int64_t m, do
 constexpr int JB = 16;             // columns per block
 constexpr int JP = 2 * JB;         // columns per pair
 constexpr int JRC = 96;            // rows per staged chunk (static shared memory < 48 KB)
-constexpr int JLD = JP + 4;        // 36: conflict-free m8n8k4 fragments
 constexpr int kBjThreads = 256;
 constexpr int kBjMaxSweeps = 40;
 #ifndef SSI_BJ_INNER
