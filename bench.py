@@ -579,11 +579,12 @@ def main():
 
     # ---------------- the c4 sweep and the c5 batch at this N
     legs = {}
-    if not args.no_legs:
+    if not args.no_legs or args.workload == "c4":     # --workload c4 / c5 needs its leg
         legs["lag_sweep_c4"] = sweep_leg(api, drivers, synth, torch, dist, Y_c3, world, rank, dev)
+    if not args.no_legs or args.workload == "c5":
         legs["record_batch_c5"] = batch_leg(api, drivers, synth, torch, dist, world, rank, dev, args.streams)
-        if rank == 0:
-            legs["paper_settings"] = next_legs(api, synth, torch, eng.R, dev)
+    if not args.no_legs and rank == 0:
+        legs["paper_settings"] = next_legs(api, synth, torch, eng.R, dev)
 
     # ---------------- roofline
     # The covariance stage alone (CUDA events around one record's A1 on the current stream) and
@@ -724,11 +725,13 @@ def main():
             if args.workload == "c4":
                 lg = legs["lag_sweep_c4"]
                 line.update(metric="CoV-SSI 3D lag sweeps/sec (c4)", value=lg["sweeps_per_s"], unit="sweeps/s",
-                            ms_per_step=lg["ms_per_sweep"], scaling="strong")
+                            ms_per_step=lg["ms_per_sweep"], scaling="strong",
+                            config={**line["config"], "workload": lg["workload"]})
             else:
                 lg = legs["record_batch_c5"]
                 line.update(metric="CoV-SSI records/sec (c5 batch)", value=lg["records_per_s"], unit=UNIT,
-                            ms_per_step=lg["ms_per_batch"] / C5_RECORDS, scaling="strong")
+                            ms_per_step=lg["ms_per_batch"] / C5_RECORDS, scaling="strong",
+                            config={**line["config"], "workload": lg["workload"]})
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
