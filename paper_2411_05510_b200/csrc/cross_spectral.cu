@@ -10,7 +10,24 @@
 // and read as 16-byte (Re, Im) fragments; the sums Xr + Xi and Yi - Yr are formed on the
 // fragments. The epilogue writes Re G and Im G (optionally adding to
 // them: segment chunks accumulate in a fixed order).
+// Measured alternative (-DSSI_CROSS_TMA=1, cross3m_tma_kernel): the same tile and fragment order, but each stage's
+// 32 segment rows (1 KB each, contiguous in HBM) are moved by the bulk-copy engine
+// (cp.async.bulk ... mbarrier::complete_tx) into a 3-stage ring with a full / empty mbarrier
+// pair per slot: warp 0 refills the slot the CTA finished one iteration earlier, so two
+// stages are in flight behind the one the warps multiply, and no thread computes addresses
+// or issues per-16-byte copies. Segments past the chunk's end are not copied; warp 0 zeroes
+// their rows (both operands) before it posts the stage, so stale shared memory never reaches
+// the sums.
+// Parity-green, but 1.564 ms against the cp.async kernel's 1.513 ms per c3 launch (CUPTI, 4
+// alternating calls each) and 125.4 vs 126.9 records/s: its warps stall on the full barrier
+// (22 % of samples, profiles/cross3m_tma_r02.ncu-rep) because a slot is refilled only after the
+// slowest warp released it; the 2-stage cp.async ring with 16 warps per SM hides the same
+// latency. Kept for the A/B; DESIGN.md §6 A1.
 #include "cov_spectral.cuh"
+
+#ifndef SSI_CROSS_TMA
+#define SSI_CROSS_TMA 0
+#endif
 
 namespace ssi {
 namespace {
@@ -132,6 +149,150 @@ __global__ void __launch_bounds__(XNT, 2) cross3m_kernel(XArgs g) {
       }
 }
 
+// ---------------------------------------------------------------- bulk-copy (TMA) variant
+constexpr int XSTT = 3;           // ring depth
+constexpr int XBAR_OFF = XSTT * XSTAGE;   // barriers after the ring (doubles)
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "XW_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra XW_%=;\n}" ::"r"(su32(b)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(double* dst, const double* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(b)) : "memory");
+}
+
+// warp 0: stage st of the chunk into ring slot st % XSTT (lane j < 16 copies segment j of A,
+// lane 16 + j segment j of B); lane 0 posts the byte count first.
+__device__ __forceinline__ void x_issue(const XArgs& g, double* xs, uint64_t* full, const double* Af,
+                                        const double* Bf, int st, int b0, int a0, int lane) {
+  const int slot = st % XSTT;
+  const int64_t s0 = int64_t(st) * XS;
+  const int nv = int(g.nseg - s0 < XS ? g.nseg - s0 : XS);
+  const int wa = min(XT, g.lp - b0), wb = min(XT, g.lp - a0);
+  if (nv < XS) {   // the chunk's last stage: zero the rows past its end (both operands)
+    double* z = xs + slot * XSTAGE;
+    for (int r = nv; r < XS; ++r)
+      for (int c = lane; c < XT; c += 32) {
+        *reinterpret_cast<double2*>(z + r * XP + 2 * c) = make_double2(0.0, 0.0);
+        *reinterpret_cast<double2*>(z + XS * XP + r * XP + 2 * c) = make_double2(0.0, 0.0);
+      }
+  }
+  __syncwarp();
+  if (lane == 0) bar_expect(&full[slot], uint32_t(nv * (wa + wb) * 16));
+  __syncwarp();
+  const int sg = lane & 15;
+  if (sg < nv) {
+    double* dst = xs + slot * XSTAGE + (lane >> 4) * (XS * XP) + sg * XP;
+    const double* src = (lane < 16 ? Af + ((s0 + sg) * g.lp + b0) * 2 : Bf + ((s0 + sg) * g.lp + a0) * 2);
+    bulk_g2s(dst, src, uint32_t((lane < 16 ? wa : wb) * 16), &full[slot]);
+  }
+}
+
+__global__ void __launch_bounds__(XNT, 2) cross3m_tma_kernel(XArgs g) {
+  extern __shared__ __align__(16) double xs[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(xs + XBAR_OFF);
+  uint64_t* empty = full + XSTT;
+  const int b0 = blockIdx.x * XT, a0 = blockIdx.y * XT;
+  const int64_t f = blockIdx.z;
+  const double* Af = g.A + f * g.sF;
+  const double* Bf = g.B + f * g.sF;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int r8 = lane >> 2, kq = lane & 3;
+  const int nst = int((g.nseg + XS - 1) / XS);
+  if (tid == 0) {
+    for (int i = 0; i < XSTT; ++i) {
+      bar_init(&full[i], 1);
+      bar_init(&empty[i], XNT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (int st = 0; st < min(XSTT, nst); ++st) x_issue(g, xs, full, Af, Bf, st, b0, a0, lane);
+  double t1[4][2][2], t2[4][2][2], t3[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) t1[i][j][e] = t2[i][j][e] = t3[i][j][e] = 0.0;
+  for (int it = 0; it < nst; ++it) {
+    // refill the slot every warp released one iteration ago (stage it - 1 + XSTT)
+    if (warp == 0 && it > 0 && it - 1 + XSTT < nst) {
+      bar_wait(&empty[(it - 1) % XSTT], uint32_t(((it - 1) / XSTT) & 1));
+      x_issue(g, xs, full, Af, Bf, it - 1 + XSTT, b0, a0, lane);
+    }
+    const int slot = it % XSTT;
+    bar_wait(&full[slot], uint32_t((it / XSTT) & 1));
+    const double* As = xs + slot * XSTAGE;
+    const double* Bs = As + XS * XP;
+#pragma unroll
+    for (int k4 = 0; k4 < XS; k4 += 4) {
+      const int s = k4 + kq;
+      double ar[4], ai[4], as[4], br[2], bi[2], bd[2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double2 v = *reinterpret_cast<const double2*>(As + s * XP + 2 * (wm + 8 * i + r8));
+        ar[i] = v.x; ai[i] = v.y;
+        as[i] = ar[i] + ai[i];
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const double2 v = *reinterpret_cast<const double2*>(Bs + s * XP + 2 * (wn + 8 * j + r8));
+        br[j] = v.x; bi[j] = v.y;
+        bd[j] = bi[j] - br[j];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          dmma884(t1[i][j][0], t1[i][j][1], ar[i], br[j]);
+          dmma884(t2[i][j][0], t2[i][j][1], ai[i], bi[j]);
+          dmma884(t3[i][j][0], t3[i][j][1], as[i], bd[j]);
+        }
+    }
+    __syncwarp();
+    if (lane == 0) bar_arrive(&empty[slot]);
+  }
+  const int64_t lp2 = int64_t(g.lp) * g.lp;
+  double* Gre = g.G + f * 2 * lp2;
+  double* Gim = Gre + lp2;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int b = b0 + wm + 8 * i + r8;
+        const int a = a0 + wn + 8 * j + 2 * kq + e;
+        if (b < g.lp && a < g.lp) {
+          const double re = t1[i][j][e] + t2[i][j][e];
+          const double im = t3[i][j][e] + (t1[i][j][e] - t2[i][j][e]);
+          const int64_t o = b + int64_t(a) * g.lp;
+          Gre[o] = g.accum ? Gre[o] + re : re;
+          Gim[o] = g.accum ? Gim[o] + im : im;
+        }
+      }
+}
+
 }  // namespace
 
 ssi_status cross_spectral_3m(const double* A, const double* B, int64_t sF, int64_t nseg, int lp, int nfreq,
@@ -141,11 +302,23 @@ ssi_status cross_spectral_3m(const double* A, const double* B, int64_t sF, int64
     return SSI_ERR_INVALID_ARG;
   }
   XArgs g{A, B, sF, nseg, lp, G, accumulate ? 1 : 0};
+  const dim3 grid(unsigned((lp + XT - 1) / XT), unsigned((lp + XT - 1) / XT), unsigned(nfreq));
+#if !SSI_CROSS_TMA
   const size_t smem = sizeof(double) * XST * XSTAGE;
   cudaFuncSetAttribute(cross3m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  const dim3 grid(unsigned((lp + XT - 1) / XT), unsigned((lp + XT - 1) / XT), unsigned(nfreq));
   cross3m_kernel<<<grid, XNT, smem, s>>>(g);
   return launch_check("cross3m_kernel");
+#else
+  // bulk copies need 16-byte aligned global rows: (Re, Im) doubles at 16-byte aligned bases
+  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) {
+    set_last_error("cross_spectral_3m: spectra not 16-byte aligned");
+    return SSI_ERR_INVALID_ARG;
+  }
+  const size_t smem = sizeof(double) * XBAR_OFF + 2 * XSTT * sizeof(uint64_t);
+  cudaFuncSetAttribute(cross3m_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cross3m_tma_kernel<<<grid, XNT, smem, s>>>(g);
+  return launch_check("cross3m_tma_kernel");
+#endif
 }
 
 }  // namespace ssi
