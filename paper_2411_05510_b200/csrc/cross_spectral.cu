@@ -22,7 +22,8 @@
 // alternating calls each) and 125.4 vs 126.9 records/s: its warps stall on the full barrier
 // (22 % of samples, profiles/cross3m_tma_r02.ncu-rep) because a slot is refilled only after the
 // slowest warp released it; the 2-stage cp.async ring with 16 warps per SM hides the same
-// latency. Kept for the A/B; DESIGN.md §6 A1.
+// latency. Kept for the A/B; DESIGN.md §6 A1. -DSSI_CROSS_TMA=2: the warp whose release
+// completes a slot (a shared counter) refills it at once, so no warp waits on an empty barrier.
 #include "cov_spectral.cuh"
 
 #ifndef SSI_CROSS_TMA
@@ -205,10 +206,14 @@ __device__ __forceinline__ void x_issue(const XArgs& g, double* xs, uint64_t* fu
   }
 }
 
+// LASTW: the warp whose release completes a slot refills it (a shared counter per slot) instead
+// of warp 0 waiting on the slot's empty barrier
+template <bool LASTW>
 __global__ void __launch_bounds__(XNT, 2) cross3m_tma_kernel(XArgs g) {
   extern __shared__ __align__(16) double xs[];
   uint64_t* full = reinterpret_cast<uint64_t*>(xs + XBAR_OFF);
   uint64_t* empty = full + XSTT;
+  int* cnt = reinterpret_cast<int*>(empty + XSTT);
   const int b0 = blockIdx.x * XT, a0 = blockIdx.y * XT;
   const int64_t f = blockIdx.z;
   const double* Af = g.A + f * g.sF;
@@ -221,6 +226,7 @@ __global__ void __launch_bounds__(XNT, 2) cross3m_tma_kernel(XArgs g) {
     for (int i = 0; i < XSTT; ++i) {
       bar_init(&full[i], 1);
       bar_init(&empty[i], XNT / 32);
+      cnt[i] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(XNT, 2) cross3m_tma_kernel(XArgs g) {
       for (int e = 0; e < 2; ++e) t1[i][j][e] = t2[i][j][e] = t3[i][j][e] = 0.0;
   for (int it = 0; it < nst; ++it) {
     // refill the slot every warp released one iteration ago (stage it - 1 + XSTT)
-    if (warp == 0 && it > 0 && it - 1 + XSTT < nst) {
+    if (!LASTW && warp == 0 && it > 0 && it - 1 + XSTT < nst) {
       bar_wait(&empty[(it - 1) % XSTT], uint32_t(((it - 1) / XSTT) & 1));
       x_issue(g, xs, full, Af, Bf, it - 1 + XSTT, b0, a0, lane);
     }
@@ -270,7 +276,19 @@ __global__ void __launch_bounds__(XNT, 2) cross3m_tma_kernel(XArgs g) {
         }
     }
     __syncwarp();
-    if (lane == 0) bar_arrive(&empty[slot]);
+    if (LASTW) {
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&cnt[slot], 1) == XNT / 32 - 1;
+        if (last) cnt[slot] = 0;
+        __threadfence_block();
+      }
+      last = __shfl_sync(0xffffffffu, last, 0);
+      if (last && it + XSTT < nst) x_issue(g, xs, full, Af, Bf, it + XSTT, b0, a0, lane);
+    } else if (lane == 0) {
+      bar_arrive(&empty[slot]);
+    }
   }
   const int64_t lp2 = int64_t(g.lp) * g.lp;
   double* Gre = g.G + f * 2 * lp2;
@@ -314,9 +332,10 @@ ssi_status cross_spectral_3m(const double* A, const double* B, int64_t sF, int64
     set_last_error("cross_spectral_3m: spectra not 16-byte aligned");
     return SSI_ERR_INVALID_ARG;
   }
-  const size_t smem = sizeof(double) * XBAR_OFF + 2 * XSTT * sizeof(uint64_t);
-  cudaFuncSetAttribute(cross3m_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  cross3m_tma_kernel<<<grid, XNT, smem, s>>>(g);
+  const size_t smem = sizeof(double) * XBAR_OFF + 3 * XSTT * sizeof(uint64_t);
+  constexpr bool lastw = SSI_CROSS_TMA == 2;
+  cudaFuncSetAttribute(cross3m_tma_kernel<lastw>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  cross3m_tma_kernel<lastw><<<grid, XNT, smem, s>>>(g);
   return launch_check("cross3m_tma_kernel");
 #endif
 }
