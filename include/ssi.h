@@ -81,6 +81,8 @@ enum { SSI_F32 = 0, SSI_F64 = 1 };
  *                   EXACTLY in int32 on the 5th-gen tensor cores (tcgen05 kind::i8)
  *                   and promoted to FP64. Error is the slicing rounding only
  *                   (<= 2^-22 of the channel's max |y| per sample); see DESIGN.md.
+ *                   Channel counts: l % 64 == 0, or l % 16 == 0 and l <= 64; any other l
+ *                   -> SSI_ERR_DTYPE from ssi_covariances and ssi_covariances_ws.
  *  SSI_COV_SPECTRAL : the same sums through segment cross-spectra, FP64 throughout: the record
  *                   is cut into segments of B = F - lag_hi samples (F a power of two <= 2048
  *                   chosen by a flop model), one FFT per segment and channel gives the spectra

@@ -97,6 +97,9 @@ ssi_status ssi_covariances_ws(int64_t N, int32_t l, int32_t lag_lo, int32_t lag_
               "ssi_covariances_ws: unknown cov_mode %d", cov_mode);
   SSI_REQUIRE(cov_mode != SSI_COV_SPECTRAL || cov_spec_supported(lag_hi), SSI_ERR_DTYPE,
               "ssi_covariances_ws: SSI_COV_SPECTRAL needs lag_hi < %d", kSpecMaxF);
+  // the int8x3 plan tiles channels by pick_nb(l); an unsupported l has no plan (and no size)
+  SSI_REQUIRE(cov_mode != SSI_COV_INT8X3 || cov_i8_supported(l, lag_hi - lag_lo + 1, l, SSI_F32), SSI_ERR_DTYPE,
+              "ssi_covariances_ws: SSI_COV_INT8X3 needs l %% 64 == 0, or l %% 16 == 0 and l <= 64");
   *bytes = cov_ws(N, l, lag_lo, lag_hi, cov_mode, N);
   return SSI_OK;
 }
@@ -132,7 +135,7 @@ ssi_status ssi_covariances(const void* Y, int32_t dtype, int64_t N, int32_t l, i
   SSI_REQUIRE(cov_mode == SSI_COV_FP64 || cov_mode == SSI_COV_INT8X3 || cov_mode == SSI_COV_SPECTRAL, SSI_ERR_DTYPE,
               "ssi_covariances: unknown cov_mode %d", cov_mode);
   SSI_REQUIRE(cov_mode != SSI_COV_INT8X3 || cov_i8_supported(l, lag_hi - lag_lo + 1, ldY, dtype),
-              SSI_ERR_DTYPE, "ssi_covariances: SSI_COV_INT8X3 needs l %% 32 == 0 and l <= 256");
+              SSI_ERR_DTYPE, "ssi_covariances: SSI_COV_INT8X3 needs l %% 64 == 0, or l %% 16 == 0 and l <= 64");
   SSI_REQUIRE(cov_mode != SSI_COV_SPECTRAL || cov_spec_supported(lag_hi), SSI_ERR_DTYPE,
               "ssi_covariances: SSI_COV_SPECTRAL needs lag_hi < %d", kSpecMaxF);
   const size_t need = cov_ws(N, l, lag_lo, lag_hi, cov_mode, t_end - t_begin);

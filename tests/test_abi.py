@@ -128,3 +128,16 @@ def test_spectral_covariance_workspace_and_validation(lib):
     # segments are processed in chunks: a day-long record needs no more spectra workspace
     assert lib.ssi_covariances_ws(8_640_000, 192, 1, 119, 2, C.byref(b)) == 0
     assert b.value < 4 * full
+
+
+def test_int8x3_channel_counts_rejected_synchronously(lib):
+    """SSI_COV_INT8X3 (= 1) tiles channels by 64 (or one tile of 16..64): any other l is rejected
+    by the workspace query and by ssi_covariances with SSI_ERR_DTYPE (= 3), before any work —
+    the query used to divide by a zero tile width (SIGFPE) for l = 6."""
+    b = C.c_size_t(0)
+    for l in (6, 7, 33, 72, 100):
+        assert lib.ssi_covariances_ws(6000, l, 1, 39, 1, C.byref(b)) == 3, l
+    for l in (16, 48, 64, 192, 256):
+        assert lib.ssi_covariances_ws(6000, l, 1, 39, 1, C.byref(b)) == 0 and b.value > 0, l
+    dummy = C.c_void_p(16)
+    assert lib.ssi_covariances(dummy, 0, 6000, 6, 6, 1, 39, 1, 0, 6000, 1, dummy, dummy, 1 << 30, None) == 3

@@ -458,3 +458,28 @@ def test_stab3d_two_lags_vs_oracle(ssi, c2_chain):
     fg, cg = api.stab3d(tabs_g, api.Criteria(**crit.__dict__))
     assert np.array_equal(cg.cpu().numpy(), co)
     assert np.array_equal(fg.cpu().numpy(), fo)
+
+
+@pytest.mark.parametrize("which", ["c2"])      # c1 (l = 6) has no int8x3 plan (test_abi.py)
+def test_end_to_end_int8x3_covariances(ssi, which, c1_chain, c2_chain):
+    """The int8x3 covariance path (exact int8 slices on tcgen05, `--cov int8x3`) carried through
+    the whole chain to the pole table and stab3d flags, against the FP64 oracle path. Contract of
+    the north star: pole counts exact, stable poles |df|/f <= 1e-5 and |dxi| <= 1e-4, flags and
+    stable counts identical (int8x3 covariances are within ~4e-9 of FP64)."""
+    api, drivers = ssi
+    cfg, Y, T, U, S, cells = c1_chain if which == "c1" else c2_chain
+    P = drivers.SweepParams(l=cfg.l, i=cfg.i, n_max=cfg.n_max, p=cfg.p, q=cfg.q, fs=cfg.fs,
+                            seed=cfg.philox_key, cov_mode="int8x3")
+    eng = drivers.Engine(P, cfg.N)
+    tab = eng.identify(_dev(Y), stream_id=cfg.i)
+    crit = oracle.SC_10DOF_3D
+    flags_o, counts_o = oracle.stab3d([cells], crit, cfg.n_max // 2)
+    st = compare_tables(gpu_cells(tab), cells, flags_o[0])
+    print(f"{which} int8x3 end to end: stable {st['n_stable']}, max df {st['max_df_stable']:.1e}, "
+          f"max dxi {st['max_dxi_stable']:.1e}")
+    assert st["count_mismatch"] == []
+    assert st["n_stable"] > 0
+    assert st["max_df_stable"] <= 1e-5 and st["max_dxi_stable"] <= 1e-4
+    flags, counts = api.stab3d([tab], api.Criteria(**crit.__dict__))
+    assert np.array_equal(counts.cpu().numpy(), counts_o)
+    assert np.array_equal(flags.cpu().numpy()[0], flags_o[0])
