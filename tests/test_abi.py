@@ -83,6 +83,16 @@ def test_oracle_is_not_imported_by_the_product():
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower().replace("no oracle", ""), f
 
 
+def test_oracle_is_not_imported_by_the_tools():
+    """Only tests/, smoke() and bench.py's CPU legs may execute the oracle: the measurement scripts
+    under tools/ take their presets from the product (api.CRITERIA_*); scripts that compare with the
+    oracle live under tests/tools/."""
+    for f in sorted(os.listdir(os.path.join(ROOT, "tools"))):
+        if f.endswith(".py"):
+            txt = open(os.path.join(ROOT, "tools", f)).read()
+            assert not re.search(r"^\s*(import|from)\s+.*\boracle\b", txt, re.M), f
+
+
 def test_rsvd_workspace_is_monotone_in_m(lib):
     """A workspace sized for the largest lag of a sweep (c4: i = 20..80) serves every lag."""
     b = C.c_size_t(0)

@@ -1,6 +1,6 @@
 """Measured covariance error of the int8x3 split path vs the FP64 oracle on a full config record."""
 import os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import oracle, synth
 from paper_2411_05510_b200 import api

@@ -1,5 +1,5 @@
 import os, sys, numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2411_05510_b200 import api
 import oracle
 N, l, L = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])

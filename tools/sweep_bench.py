@@ -7,7 +7,6 @@ Prints one JSON line."""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
-import oracle
 import synth
 from paper_2411_05510_b200 import api, drivers
 
@@ -18,7 +17,7 @@ lags = list(cfg.lags)
 Y = torch.from_numpy(synth.make_record(cfg)[0]).cuda()
 P = drivers.SweepParams(l=cfg.l, i=max(lags), n_max=cfg.n_max, p=cfg.p, q=cfg.q, fs=cfg.fs, n_min=cfg.n_min,
                         n_step=cfg.n_step, seed=cfg.philox_key, cov_mode=os.environ.get("SSI_COV_MODE", "spectral"))
-crit = api.Criteria(**oracle.SC_BRIDGE_3D.__dict__)
+crit = api.CRITERIA_BRIDGE_3D
 drivers.lag_sweep_3d(Y, P, lags, crit)
 torch.cuda.synchronize()
 ts = []

@@ -1,6 +1,6 @@
 import os, sys, time
 sys.path.insert(0, "/root/repo")
-import torch, synth, oracle
+import torch, synth
 from paper_2411_05510_b200 import api, drivers
 cfg = synth.config("c4")
 lags = list(cfg.lags)
@@ -8,7 +8,7 @@ Y = torch.from_numpy(synth.make_record(cfg)[0]).cuda()
 for mode in ("spectral", "int8x3"):
     P = drivers.SweepParams(l=cfg.l, i=max(lags), n_max=cfg.n_max, p=cfg.p, q=cfg.q, fs=cfg.fs, n_min=cfg.n_min,
                             n_step=cfg.n_step, seed=cfg.philox_key, cov_mode=mode)
-    crit = api.Criteria(**oracle.SC_BRIDGE_3D.__dict__)
+    crit = api.CRITERIA_BRIDGE_3D
     for rep in range(3):
         torch.cuda.synchronize()
         a, b, c = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
