@@ -55,6 +55,9 @@ def parse():
                          "applying it through its block structure")
     ap.add_argument("--records", type=int, default=2)
     ap.add_argument("--streams", type=int, default=8, help="records in flight (one engine per stream)")
+    ap.add_argument("--tail", type=int, default=0,
+                    help="the last TAIL records of the timed batch are submitted with the pipeline's tail hint "
+                         "(covariances at high priority: nothing follows them)")
     ap.add_argument("--no-priority", action="store_true",
                     help="one stream per record (no low-priority covariance streams)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -487,8 +490,8 @@ def main():
     eng = pipe.engines[0]
     stream = torch.cuda.current_stream()
 
-    def step(j, ev=None):
-        tab, _ = pipe.submit(Ys[j % len(Ys)], (j << 32) | cfg.i, ev)
+    def step(j, ev=None, tail=False):
+        tab, _ = pipe.submit(Ys[j % len(Ys)], (j << 32) | cfg.i, ev, tail=tail)
         return tab
 
     for j in range(args.warmup):
@@ -531,7 +534,7 @@ def main():
     for st in pipe.streams:
         st.wait_stream(stream)
     for j in range(args.steps):
-        step(j, cov_ev[j])
+        step(j, cov_ev[j], tail=j >= args.steps - args.tail)
     pipe.join(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
@@ -565,7 +568,7 @@ def main():
             slot = pipe.j % ns
             # H2D of this step's record inside the timed region, on the pipeline's copy stream
             # (submit_host: a ring of device input buffers, copies overlap the records in flight)
-            tab, st = pipe.submit_host(pinned[j % 2], (j << 32) | cfg.i)
+            tab, st = pipe.submit_host(pinned[j % 2], (j << 32) | cfg.i, tail=j >= args.steps - args.tail)
             with torch.cuda.stream(st):
                 for hst, d in zip(tab_host[slot], tab.tensors()):      # D2H of the result
                     hst.copy_(d, non_blocking=True)

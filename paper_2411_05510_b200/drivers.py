@@ -158,17 +158,23 @@ class RecordPipeline:
         self._in_bufs, self._in_free, self._hb = [], [], 0
         self.copy_stream = None
 
-    def submit(self, Y: torch.Tensor, stream_id: int, events=None, ready: torch.cuda.Event | None = None):
-        tab, st, _ = self._submit(Y, stream_id, events, ready)
+    def submit(self, Y: torch.Tensor, stream_id: int, events=None, ready: torch.cuda.Event | None = None,
+               tail: bool = False):
+        """tail: no record will follow this one soon (the end of a batch). Its covariances then run
+        on the engine's high-priority stream: with nothing behind it to fill the gaps, a low-priority
+        A1 would only delay the start of this record's latency-bound chain (same kernels, same
+        results; scheduling only)."""
+        tab, st, _ = self._submit(Y, stream_id, events, ready, tail)
         return tab, st
 
-    def _submit(self, Y, stream_id, events=None, ready=None):
+    def _submit(self, Y, stream_id, events=None, ready=None, tail=False):
         k = self.j % len(self.engines)
-        e, st, cst = self.engines[k], self.streams[k], self.cov_streams[k]
+        e, st = self.engines[k], self.streams[k]
+        cst = st if tail else self.cov_streams[k]
         self.j += 1
         if ready is None:
             st.wait_stream(torch.cuda.current_stream(Y.device))   # Y was produced on the caller's stream
-        if self.split:
+        if cst is not st:
             cst.wait_stream(st)            # the engine's buffers are free (and Y is ready on st)
         if ready is not None:
             cst.wait_event(ready)          # Y arrives from the copy stream
@@ -182,7 +188,7 @@ class RecordPipeline:
                 events[1].record(cst)
             read = torch.cuda.Event()
             read.record(cst)               # A1 is the only reader of Y
-        if self.split:
+        if cst is not st:
             st.wait_stream(cst)
         with torch.cuda.stream(st):
             tab, _ = e.decompose(R, e.P.i, stream_id)
@@ -197,7 +203,7 @@ class RecordPipeline:
                              for _ in range(len(self.engines) + 2)]
             self._in_free = [None] * len(self._in_bufs)
 
-    def submit_host(self, Yh: torch.Tensor, stream_id: int, events=None):
+    def submit_host(self, Yh: torch.Tensor, stream_id: int, events=None, tail: bool = False):
         """submit() for a record in (pinned) host memory. The host-to-device copy runs on the
         pipeline's copy stream into a ring of n_streams + 2 device buffers, so the copy of the
         next records overlaps the compute of the ones in flight; a buffer is refilled once the
@@ -219,7 +225,7 @@ class RecordPipeline:
             buf.copy_(Yh, non_blocking=True)
             ready = torch.cuda.Event()
             ready.record(cs)
-        tab, st, read = self._submit(buf, stream_id, events, ready)
+        tab, st, read = self._submit(buf, stream_id, events, ready, tail)
         self._in_free[b] = read
         return tab, st
 
@@ -441,10 +447,11 @@ def lag_sweep_3d(Y: torch.Tensor, P: SweepParams, lags, crit: api.Criteria, rank
 
 
 def record_batch(records, P: SweepParams, rank: int = 0, world: int = 1, n_streams: int = 3, group=None,
-                 gather: bool = True):
+                 gather: bool = True, tail: int = 0):
     """Continuous monitoring: records (a list of device tensors, or a
     callable j -> device tensor) processed on this rank by a RecordPipeline; tables gathered
-    on every rank when `gather`. No data-path collective (records are independent)."""
+    on every rank when `gather`. No data-path collective (records are independent). The last
+    `tail` records of this rank are submitted with the pipeline's tail hint (scheduling only)."""
     n = len(records) if not callable(records) else records.n
     assign = record_assignment(n, world)
     fetch = records if callable(records) else (lambda j: records[j])
@@ -452,11 +459,12 @@ def record_batch(records, P: SweepParams, rank: int = 0, world: int = 1, n_strea
     device = first.device if first.is_cuda else torch.device("cuda", torch.cuda.current_device())
     pipe = RecordPipeline(P, first.shape[0], device, n_streams)
     local = {}
-    for j in assign[rank]:
+    for n_done, j in enumerate(assign[rank]):
         Yj = fetch(j)
+        last = n_done >= len(assign[rank]) - tail
         # host records (pinned) stream in through the pipeline's copy stream
-        tab, st = (pipe.submit(Yj, (j << 32) | P.i) if Yj.is_cuda
-                   else pipe.submit_host(Yj, (j << 32) | P.i))
+        tab, st = (pipe.submit(Yj, (j << 32) | P.i, tail=last) if Yj.is_cuda
+                   else pipe.submit_host(Yj, (j << 32) | P.i, tail=last))
         with torch.cuda.stream(st):
             local[j] = api.PoleTable(tab.n_min, tab.n_step, tab.l, tab.cap, *[t.clone() for t in tab.tensors()])
     pipe.join()

@@ -175,3 +175,9 @@ def test_c5_batch_eight_records(mods):
     for j in range(8):
         for a, b in zip(tabs_h[j].tensors(), tabs[j].tensors()):
             assert torch.equal(a, b), ("host record", j)
+    # the tail hint (last records' covariances on the high-priority streams) is scheduling only
+    for src, ns in ((dev, 8), (host, 3)):
+        tabs_t = drivers.record_batch(src, P, n_streams=ns, tail=3)
+        for j in range(8):
+            for a, b in zip(tabs_t[j].tensors(), tabs[j].tensors()):
+                assert torch.equal(a, b), ("tail hint", ns, j)
